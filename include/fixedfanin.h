@@ -1,0 +1,190 @@
+/*
+ * fixedfanin.h — C ABI of the B200-native fixed fan-in (uniform sparsity) sparse
+ * output layer of arXiv 2306.03725 ("Towards Memory-Efficient Training for
+ * Extremely Large Output Spaces", §3.2 "uniform sparsity").
+ *
+ * Citations: P:n = line n of the paper's LaTeX source (reference PAPER.md);
+ * S:n = line n of the reference SPEC.md; readings R1..R23 are listed in DESIGN.md.
+ *
+ * Notation: L_global labels; this handle owns the contiguous
+ * label rows [row_begin, row_begin + L_local) ("label shard"); every label has
+ * exactly k connections ("fan-in", the paper's s) into a layer of width m
+ * (the paper's feature/intermediate dimension); B = mini-batch.
+ *
+ * Layouts (all row-major, C order):
+ *   W   float   [L_local][k]   weights        (the paper's `weights`  s x L, transposed; R2)
+ *   idx int32_t [L_local][k]   source columns (the paper's `indices`  s x L, transposed; R2)
+ *   bias, mb, vb float [L_local];  mW, vW float [L_local][k]  (Adam moments)
+ *   h   float [B][m]  input of the sparse layer (`features`)
+ *   y   float [B][L_local]   scores (`output`)
+ *   dh  float [B][m]  gradient w.r.t. h (Alg. 2), THIS SHARD's partial sum
+ *   labels: CSR over the batch — lbl_ptr int32 [B+1], lbl_ids int32 [lbl_ptr[B]] GLOBAL
+ *           label ids of the positives of each instance (y in {0,1}^L stored sparse,
+ *           P:92-97).  Ids outside this shard's rows are ignored (that is what makes
+ *           label sharding transparent); ids outside [0, L_global) -> FF_ERR_RANGE
+ *           (reported asynchronously, see fixedfanin_check).
+ *
+ * Memory ownership: the caller owns every buffer, including the workspace (one
+ * device allocation of fixedfanin_workspace_size() bytes that holds all layer state
+ * and scratch).  The library never allocates or frees device memory.
+ * Pointers are DEVICE pointers unless the name ends in _host.
+ * Asynchrony: every call enqueues its work on `stream` and returns without
+ * synchronizing, except get_params/set_params/check (documented below).  Host-side
+ * argument validation is synchronous and returns an error code before any work is
+ * enqueued.  Not thread-safe per handle; distinct handles are independent.
+ * Errors: status codes only (no exceptions cross the ABI); fixedfanin_last_error()
+ * returns a thread-local message for the last non-OK status.
+ */
+#ifndef FIXEDFANIN_H
+#define FIXEDFANIN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ff_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
+typedef struct ff_layer ff_layer;
+
+typedef enum {
+    FF_OK = 0,
+    FF_ERR_ARG = 1,        /* null pointer, bad shape, B > max_batch, K > max_topk, K > L_global   */
+    FF_ERR_CONFIG = 2,     /* invalid ff_config (k > m, k > FF_MAX_FANIN, prune count < 1 or
+                              m - k < prune count when redistribution is requested, ...)          */
+    FF_ERR_RANGE = 3,      /* idx outside [0,m) or duplicate idx in a row (set_params);
+                              label id outside [0, L_global) (reported by fixedfanin_check)       */
+    FF_ERR_NONFINITE = 4,  /* non-finite score/gradient seen with FF_FLAG_CHECK_FINITE           */
+    FF_ERR_CUDA = 5,       /* a CUDA runtime error (launch failure, async fault)                 */
+    FF_ERR_STATE = 6       /* call order violated (adam_step without a preceding backward, ...)  */
+} ff_status;
+
+/* Compile-time limits of this build (checked at create). */
+#define FF_MAX_FANIN 32     /* k <= 32: one label row = one warp-wide 128-B line per array   */
+#define FF_MAX_BATCH 128    /* B <= 128: processed as ceil(B/32) 32-sample lane groups        */
+#define FF_MAX_TOPK 8       /* K <= 8 (the paper reports P@1/3/5)                  */
+
+/* ff_config.flags */
+#define FF_FLAG_CHECK_FINITE 1u  /* raise FF_ERR_NONFINITE on a non-finite score/gradient     */
+#define FF_FLAG_STORE_GRADS 2u   /* fused train_step also stores dW/db (for get_grads/tests)  */
+
+/* ff_config.dh_mode */
+#define FF_DH_ATOMIC 0           /* dh by coalesced red.global.add (Alg. 2 with atomics) */
+#define FF_DH_CSC 1              /* dh by a transposed (CSC) index gather, rebuilt after redistribution */
+
+typedef struct {
+    int64_t L_global;    /* total labels, 1 <= L_global < 2^31 (32-bit label ids)   */
+    int64_t row_begin;   /* first global label row owned by this handle                         */
+    int64_t L_local;     /* rows owned, 0 <= L_local, row_begin + L_local <= L_global           */
+    int32_t m;           /* width of h, 1 <= m < 2^31                                           */
+    int32_t k;           /* connections per label, 1 <= k <= min(m, FF_MAX_FANIN)               */
+    int32_t max_batch;   /* largest B that will be passed, 1..FF_MAX_BATCH                      */
+    int32_t max_topk;    /* largest K that will be passed to predict_topk, 1..FF_MAX_TOPK       */
+    int32_t max_nnz;     /* largest lbl_ptr[B] for the *_host entry points (0 -> 64*max_batch)  */
+    int32_t dh_mode;     /* FF_DH_ATOMIC or FF_DH_CSC                                           */
+    uint64_t seed;       /* Philox key for init and redistribution (R13)                        */
+    float init_scale;    /* W init U(-a, a); 0 -> a = fp32(1/sqrt(k)) (R17)                     */
+    float beta1, beta2, eps;   /* Adam; 0 -> 0.9 / 0.999 / 1e-8 (R6)                            */
+    float prune_frac;    /* SET fraction alpha, p = floor(alpha*k) per row; 0 -> 0.1    */
+    uint32_t flags;      /* FF_FLAG_*                                                           */
+} ff_config;
+
+/* Bytes of device workspace the layer needs for `cfg` (host-only, no CUDA calls). */
+ff_status fixedfanin_workspace_size(const ff_config* cfg, size_t* bytes_host);
+
+/* Carve `workspace` (device, >= workspace_size bytes, 256-B aligned) and initialize the
+ * layer on `stream`: idx rows = k distinct uniform draws from [0,m) and W ~ U(-a,a) from
+ * the Philox streams keyed (seed, global row) (R13, R17); bias, moments = 0;
+ * t = 0.  *out_host receives the handle (host memory, freed by destroy).               */
+ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
+                            ff_stream_t stream, ff_layer** out_host);
+
+/* Free the host handle.  Does not touch the workspace (the caller owns it). */
+ff_status fixedfanin_destroy(ff_layer* layer);
+
+/* Overwrite the state from device arrays (any pointer may be NULL = keep).  Synchronizes
+ * `stream`, validates idx (range, no duplicates within a row) -> FF_ERR_RANGE (state is
+ * left modified but invalid in that case).  t_host: new Adam step count (NULL = keep). */
+ff_status fixedfanin_set_params(ff_layer* layer, const float* W, const int32_t* idx,
+                                const float* bias, const float* mW, const float* vW,
+                                const float* mb, const float* vb, const int64_t* t_host,
+                                ff_stream_t stream);
+
+/* Copy the state into device arrays (any pointer may be NULL = skip); *t_host = Adam t. */
+ff_status fixedfanin_get_params(ff_layer* layer, float* W, int32_t* idx, float* bias,
+                                float* mW, float* vW, float* mb, float* vb, int64_t* t_host,
+                                ff_stream_t stream);
+
+/* Alg. 1 + bias: y[b][j] = bias[j] + sum_i W[j][i] * h[b][idx[j][i]],
+ * for b < B, j < L_local.  0 <= B <= max_batch (B = 0 is a no-op).                   */
+ff_status fixedfanin_forward(ff_layer* layer, const float* h, int32_t B, float* y,
+                             ff_stream_t stream);
+
+/* BCE-with-logits gradient g = grad_scale*(sigmoid(y) - t) (R4, R5), then
+ * Alg. 3 dW[j][i] = sum_b g[b][j] h[b][idx[j][i]], db[j] = sum_b g[b][j]
+ * (kept in the workspace for adam_step/get_grads), and Alg. 2
+ * dh[b][c] = sum_{(j,i): idx[j][i]=c} W[j][i] g[b][j] (overwritten).  `y` must be the
+ * scores of the same h (e.g. from fixedfanin_forward).  loss (device float[1] or NULL)
+ * = grad_scale * sum_{b,j} softplus(y) - t*y.                                        */
+ff_status fixedfanin_backward(ff_layer* layer, const float* h, const float* y, int32_t B,
+                              const int32_t* lbl_ptr, const int32_t* lbl_ids,
+                              float grad_scale, float* dh, float* loss, ff_stream_t stream);
+
+/* Copy the gradients of the last backward (or train_step with FF_FLAG_STORE_GRADS). */
+ff_status fixedfanin_get_grads(ff_layer* layer, float* dW, float* db, ff_stream_t stream);
+
+/* t += 1; Adam (R6, R7) over W (with dW) and bias (with db). FF_ERR_STATE if
+ * no backward ran since the last adam_step.                                          */
+ff_status fixedfanin_adam_step(ff_layer* layer, float lr, ff_stream_t stream);
+
+/* The fused training step: forward, BCE gradient, dW, db, dh (pre-update W) and Adam
+ * (t += 1) in one pass over the label rows; y, g, dW are never written to HBM.
+ * dh (device [B][m]) overwritten; loss as in backward (NULL = skip).                */
+ff_status fixedfanin_train_step(ff_layer* layer, const float* h, int32_t B,
+                                const int32_t* lbl_ptr, const int32_t* lbl_ids,
+                                float grad_scale, float lr, float* dh, float* loss,
+                                ff_stream_t stream);
+
+/* Same as train_step with HOST inputs/outputs (end-to-end path): copies h_host [B][m]
+ * and the label CSR (host) into workspace staging, runs the fused step, then copies the
+ * loss (and dh if dh_host != NULL) back.  Use pinned host memory for asynchrony; the
+ * host outputs are valid after `stream` is synchronized.  lbl_ptr_host[B] <= max_nnz. */
+ff_status fixedfanin_train_step_host(ff_layer* layer, const float* h_host, int32_t B,
+                                     const int32_t* lbl_ptr_host, const int32_t* lbl_ids_host,
+                                     float grad_scale, float lr, float* dh_host,
+                                     float* loss_host, ff_stream_t stream);
+
+/* SET prune/regrow, per row (R8): the p = floor(prune_frac*k)
+ * slots of smallest (|W|, slot) are replaced by p distinct indices drawn uniformly from
+ * [0,m) minus the row's current set, from the Philox stream keyed (seed, step, global
+ * row) (R10-R13); W = mW = vW = 0 in those slots (R11).  The CSC index (dh_mode 1) is
+ * rebuilt.  FF_ERR_CONFIG if p < 1 or m - k < p.                                       */
+ff_status fixedfanin_redistribute(ff_layer* layer, uint64_t step, ff_stream_t stream);
+
+/* Top-K prediction: per instance the K labels of this shard with the largest
+ * scores, ordered by (score desc, global id asc) (R15).  scores [B][K] float,
+ * ids [B][K] int32 GLOBAL ids.  1 <= K <= min(max_topk, L_local).                      */
+ff_status fixedfanin_predict_topk(ff_layer* layer, const float* h, int32_t B, int32_t K,
+                                  float* scores, int32_t* ids, ff_stream_t stream);
+
+/* Merge per-shard top-K lists: in_scores/in_ids [P][B][K] (device) -> out [B][K] under
+ * the same total order.  Stateless.  1 <= K <= FF_MAX_TOPK, 1 <= P <= 1024.            */
+ff_status fixedfanin_merge_topk(const float* in_scores, const int32_t* in_ids, int32_t P,
+                                int32_t B, int32_t K, float* out_scores, int32_t* out_ids,
+                                ff_stream_t stream);
+
+/* Synchronize `stream` and report asynchronous errors raised by earlier calls
+ * (FF_ERR_RANGE for bad label ids, FF_ERR_NONFINITE, FF_ERR_CUDA); clears them.       */
+ff_status fixedfanin_check(ff_layer* layer, ff_stream_t stream);
+
+/* Number of kernel launches the last API call enqueued (host counter, for benchmarks). */
+int32_t fixedfanin_last_launch_count(void);
+
+/* Thread-local message of the last non-OK status ("" if none). */
+const char* fixedfanin_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIXEDFANIN_H */
