@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the fixed fan-in sparse output layer (arXiv 2306.03725) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--shape S]
+
+A "step" is one training step of the hot path on one synthetic batch (B = 32):
+the fused forward / BCE gradient / dW / db / dh / Adam kernel (+ its h-transpose and dh
+epilogue kernels), with the SET redistribution run inside the timed region whenever the
+global step count reaches a multiple of 1000 — so it is amortised exactly as in
+training.  Inference (top-K prediction, row a8) is timed in the same run ("predict").
+
+N = 1 runs in-process; N > 1 is launched by torchrun (one rank per GPU, NCCL): each rank
+owns a contiguous label shard, h is broadcast from rank 0 and dh is all-reduced every
+step (strong scaling of a fixed global batch).  Rank 0 prints one JSON line.
+
+--impl reference times the fp64 CPU oracle (the reference arm of this tier) on a
+bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train samples/sec & HBM GB/s fraction, Amazon-670K shape, 1/2/4/8 B200"
+REDIST_EVERY = 1000          # P:683 "Every 1000 training steps"
+N_BATCHES = 8                # distinct synthetic batches cycled through
+LR = 1e-3                    # P:678 initial learning rate
+
+
+def args_():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=1000)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--shape", default="amazon-670k")
+    p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(key):
+    """dram bytes per launch of `key` from the committed ncu --set full summary, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for ln in (self.out or "").splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- byte models
+def alg_bytes_train_kernel(L, k):
+    """Algorithmic HBM bytes of one fused-step kernel launch:
+    read W, idx, mW, vW and write W, mW, vW (28 B per connection); read+write bias, mb, vb
+    (24 B per label)."""
+    return 28 * L * k + 24 * L
+
+
+def alg_bytes_step(L, k, B, m, nnz):
+    """Algorithmic HBM bytes of one whole step: the kernel's state traffic + read h and
+    write dh (8 B per h element) + the labels, + the redistribution amortised over 1000
+    steps (read W, idx, mW, vW; write <= 4 arrays in the pruned slots ~ 0.024 L k)."""
+    return alg_bytes_train_kernel(L, k) + 8 * B * m + 4 * (B + 1 + nnz) + 0.024 * L * k
+
+
+def alg_bytes_predict(L, k, B, m):
+    return 8 * L * k + 4 * L + 4 * B * m
+
+
+# ----------------------------------------------------------------------------- cpu baseline
+def oracle_sample_rate(shape, rows, steps, data):
+    """Time the fp64 oracle (as it stands, single thread) on the first `rows` label rows of
+    the workload; return samples/s scaled to the full label count."""
+    import oracle
+    st = oracle.State.create(rows, shape.m, shape.k, seed=42)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        h, ptr, ids = data[s % len(data)]
+        oracle.train_step(st, h, ptr, ids, 1.0 / shape.B, LR)
+    dt = (time.perf_counter() - t0) / steps
+    return shape.B / (dt * shape.L / rows), dt
+
+
+def run_reference(a, shape, world, rank):
+    if rank != 0:
+        return
+    from paper_2306_03725_b200 import synth
+    rows = max(1, shape.L // 64)
+    data = [(synth.hidden_batch(shape.B, shape.m, step=s), *synth.label_batch(shape.B, shape.L, shape.avg_pos, step=s))
+            for s in range(N_BATCHES)]
+    import oracle
+    oracle.build()
+    if a.warmup:
+        oracle_sample_rate(shape, rows, max(1, min(a.warmup, 3)), data)
+    v, dt = oracle_sample_rate(shape, rows, a.steps, data)
+    sample = (f"first {rows} of {shape.L} label rows (1/64), m={shape.m}, k={shape.k}, B={shape.B}; "
+              f"{a.steps} oracle steps of {dt * 1e3:.1f} ms, scaled x{shape.L / rows:.1f} to all rows")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3 * shape.L / rows,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": shape.name, "L": shape.L, "m": shape.m, "k": shape.k,
+                                              "B": shape.B},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(a, shape, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2306_03725_b200 import synth
+    from paper_2306_03725_b200.layer import last_launch_count
+    from paper_2306_03725_b200.sharded import ShardedLayer
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B = shape.B
+    data = [(synth.hidden_batch(B, shape.m, step=s), *synth.label_batch(B, shape.L, shape.avg_pos, step=s))
+            for s in range(N_BATCHES)]
+    max_nnz = max(int(d[1][-1]) for d in data)
+    layer = ShardedLayer(shape.L, shape.m, shape.k, rank=rank, world=world, device=dev, max_batch=B,
+                         seed=synth.PARAM_SEED, max_nnz=max_nnz)
+    eng = layer.engine
+    L_local = layer.row_end - layer.row_begin
+    stream = torch.cuda.current_stream()
+
+    h_dev = [torch.from_numpy(d[0]).to(dev) for d in data]
+    ptr_dev = [torch.from_numpy(d[1]).to(dev) for d in data]
+    ids_dev = [torch.from_numpy(d[2]).to(dev) for d in data]
+    dh = torch.empty((B, shape.m), device=dev)
+    loss = torch.zeros(1, device=dev)
+    t_global = 0
+    launches = 0
+
+    def step(s):
+        nonlocal t_global, launches
+        i = s % N_BATCHES
+        layer.broadcast_h(h_dev[i])
+        layer.train_step(h_dev[i], ptr_dev[i], ids_dev[i], LR, dh=dh, loss=loss)
+        launches += last_launch_count()
+        t_global += 1
+        if t_global % REDIST_EVERY == 0:
+            layer.redistribute(t_global)
+            launches += last_launch_count()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for s in range(a.warmup):
+        step(s)
+    barrier()
+    launches = 0
+    eng.profile_begin(a.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for s in range(a.steps):
+            step(a.warmup + s)
+        e1.record(stream)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    k_ms, k_n = eng.profile_end()
+    k_avg_ms = max_over_ranks(k_ms / max(k_n, 1))
+    gpu_launches = launches
+
+    # ---- end to end through the public API with host buffers (H2D inputs, D2H loss)
+    n_e2e = a.e2e_steps or a.steps
+    h_pin = [torch.from_numpy(d[0]).pin_memory() for d in data]
+    ptr_pin = [torch.from_numpy(d[1]).pin_memory() for d in data]
+    ids_pin = [torch.from_numpy(d[2]).pin_memory() for d in data]
+    loss_pin = torch.zeros(1).pin_memory()
+    h2d = B * shape.m * 4 + int(np.mean([4 * (B + 1 + len(d[2])) for d in data]))
+    d2h = 4
+
+    def step_e2e(s):
+        nonlocal t_global
+        i = s % N_BATCHES
+        if world == 1:
+            eng.train_step_host(h_pin[i], ptr_pin[i], ids_pin[i], LR, loss_host=loss_pin)
+        else:
+            h_dev[i].copy_(h_pin[i], non_blocking=True)
+            ptr_dev[i].copy_(ptr_pin[i], non_blocking=True)
+            ids_dev[i].copy_(ids_pin[i], non_blocking=True)
+            layer.broadcast_h(h_dev[i])
+            layer.train_step(h_dev[i], ptr_dev[i], ids_dev[i], LR, dh=dh, loss=loss)
+            loss_pin.copy_(loss, non_blocking=True)
+        t_global += 1
+        if t_global % REDIST_EVERY == 0:
+            layer.redistribute(t_global)
+
+    for s in range(3):
+        step_e2e(s)
+    with ClockSampler(local_rank) as clk2:
+        barrier()
+        e0.record(stream)
+        for s in range(n_e2e):
+            step_e2e(s)
+        e1.record(stream)
+        barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+
+    # ---- inference: fused forward + top-K (row a8), K = 5 (P@1/3/5)
+    K = 5
+    for s in range(3):
+        layer.predict_topk(h_dev[s % N_BATCHES], K)
+    n_pred = 100
+    barrier()
+    e0.record(stream)
+    for s in range(n_pred):
+        layer.predict_topk(h_dev[s % N_BATCHES], K)
+    e1.record(stream)
+    barrier()
+    ms_pred = max_over_ranks(e0.elapsed_time(e1))
+
+    if rank != 0:
+        return
+    peak, peak_src = peaks()
+    samples_per_s = B * a.steps / (ms * 1e-3)
+    kb = alg_bytes_train_kernel(L_local, shape.k)
+    achieved = kb / (k_avg_ms * 1e-3) / 1e9
+    nnz_mean = float(np.mean([len(d[2]) for d in data]))
+    step_bytes = alg_bytes_step(shape.L, shape.k, B, shape.m, nnz_mean)
+    traffic = ncu_traffic(f"{shape.name}/train_kernel")
+    onchip = 2 * 128 * L_local * shape.k * ((B + 31) // 32)   # hT line gathers + dhT line reductions
+    pred_bytes = alg_bytes_predict(shape.L, shape.k, B, shape.m)
+    c1, c2 = clk.summary(), clk2.summary()
+    line = {
+        "metric": METRIC, "value": samples_per_s, "unit": "samples/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: h = ReLU(N(0,1)), Zipf(1.0) sparse labels, Philox-initialized W/idx (no dataset)",
+        "config": {"workload": shape.name, "L": shape.L, "m": shape.m, "k": shape.k, "B": B, "global_batch": B,
+                   "avg_pos": shape.avg_pos, "parallelism": f"label-shard x{world}",
+                   "redistribution": f"every {REDIST_EVERY} steps inside the timed region (global step counter)",
+                   "l2": "no flush: per-step state stream 617 MB >> 126 MB L2 (inputs larger than L2)"},
+        "clocks": {"sm_mhz": c1["sm_mhz"], "sm_max_mhz": c1["sm_max_mhz"], "reasons": c1["reasons"],
+                   "samples": c1["samples"]},
+        "hbm_step": {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / a.steps * 1e-3) / 1e9,
+                     "frac": step_bytes / (ms / a.steps * 1e-3) / 1e9 / peak},
+        "e2e": {"value": B * n_e2e / (ms_e2e * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ms_e2e / n_e2e,
+                "path": "fixedfanin_train_step_host (C ABI, pinned host buffers)" if world == 1 else
+                        "torch H2D + ShardedLayer.train_step + D2H loss", "clocks_sm_mhz": c2["sm_mhz"]},
+        "gpu_launches": gpu_launches,
+        "roofline": {"bound": "hbm", "kernel": "k_rows<train> (fused fwd/BCE/dW/db/dh/Adam)", "achieved": achieved,
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "alg_bytes_per_launch": kb, "avg_launch_ms": k_avg_ms,
+                     "kernel_share_of_step": k_avg_ms / (ms / a.steps)},
+        "onchip": {"l2_bytes_per_launch": onchip, "l2_gbs": onchip / (k_avg_ms * 1e-3) / 1e9,
+                   "note": "hT 128-B line gathers + dhT 128-B red.v4 per connection; measured ceilings "
+                           "(profiles/r01_l2bench.txt): gather ~19.9 TB/s, red ~6.3-6.6 TB/s"},
+        "predict": {"value": B * n_pred / (ms_pred * 1e-3), "unit": "samples/s", "K": K,
+                    "ms_per_batch": ms_pred / n_pred,
+                    "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,
+                    "frac": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9 / peak},
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        rows = shape.L // 8
+        v, dt = oracle_sample_rate(shape, rows, 2, data)
+        line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+                                "sample": f"first {rows} of {shape.L} label rows (1/8), m={shape.m}, k={shape.k}, "
+                                          f"B={B}; 2 fp64 oracle steps of {dt:.2f} s, scaled x8 to all rows"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = args_()
+    from paper_2306_03725_b200 import synth
+    shape = synth.SHAPES[a.shape]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, shape, world, rank)
+        return
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build_lib()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.barrier()
+    run_ours(a, shape, world, rank, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -178,6 +178,13 @@ ff_status fixedfanin_merge_topk(const float* in_scores, const int32_t* in_ids, i
  * (FF_ERR_RANGE for bad label ids, FF_ERR_NONFINITE, FF_ERR_CUDA); clears them.       */
 ff_status fixedfanin_check(ff_layer* layer, ff_stream_t stream);
 
+/* Kernel timing for benchmarks: between profile_begin and profile_end every train_step
+ * (and train_step_host) records a CUDA event pair around its fused row kernel on the
+ * call's stream (at most max_launches pairs).  profile_end synchronizes on the last event
+ * and returns the summed kernel milliseconds and the number of timed launches.        */
+ff_status fixedfanin_profile_begin(ff_layer* layer, int32_t max_launches);
+ff_status fixedfanin_profile_end(ff_layer* layer, double* kernel_ms_host, int32_t* launches_host);
+
 /* Number of kernel launches the last API call enqueued (host counter, for benchmarks). */
 int32_t fixedfanin_last_launch_count(void);
 

@@ -1,0 +1,536 @@
+// fixedfanin.cu — host side of the C ABI declared in include/fixedfanin.h: argument
+// validation, workspace carving, kernel launches.  No device memory is allocated here
+// (the caller owns the workspace) and no call synchronizes except set/get_params/check.
+#include "fixedfanin.h"
+#include "ff_kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace ff;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int32_t g_launches = 0;
+
+ff_status fail(ff_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+ff_status fail(ff_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define FF_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) return fail(FF_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define FF_LAUNCHED()                                                                   \
+  do {                                                                                  \
+    ++g_launches;                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess) return fail(FF_ERR_CUDA, "launch: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+constexpr int kMaxCandBlocks = 1024;    // predict grid cap (candidate buffer rows)
+
+size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {   // byte offsets into the workspace
+  size_t W, idx, mW, vW, dW, bias, mb, vb, db, posmask, hd, cand_s, cand_i,
+      h_stage, lbl_stage, dh_stage, scalars, total;
+};
+
+int nb_of(int B) { return (B + 31) / 32; }
+
+Layout layout_of(const ff_config& c) {
+  Layout o{};
+  const size_t Lk = (size_t)c.L_local * (size_t)c.k, L = (size_t)c.L_local;
+  const size_t nbm = (size_t)nb_of(c.max_batch), ldh = 32 * nbm, m = (size_t)c.m;
+  const size_t nnz = c.max_nnz > 0 ? (size_t)c.max_nnz : 64 * (size_t)c.max_batch;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t r = off; off += up(bytes); return r; };
+  o.W = take(4 * Lk); o.idx = take(4 * Lk); o.mW = take(4 * Lk); o.vW = take(4 * Lk); o.dW = take(4 * Lk);
+  o.bias = take(4 * L); o.mb = take(4 * L); o.vb = take(4 * L); o.db = take(4 * L);
+  o.posmask = take(4 * L * nbm);
+  o.hd = take(8 * m * ldh);         // [m][nb][h 32 | dh 32]
+  o.cand_s = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
+  o.cand_i = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
+  o.h_stage = take(4 * (size_t)c.max_batch * m);
+  o.lbl_stage = take(4 * ((size_t)c.max_batch + 1 + nnz));
+  o.dh_stage = take(4 * (size_t)c.max_batch * m);
+  o.scalars = take(kAlign);       // [0] int err, [1] float loss
+  o.total = off;
+  return o;
+}
+
+ff_status validate(const ff_config* c) {
+  if (!c) return fail(FF_ERR_ARG, "cfg is NULL");
+  if (c->L_global < 1 || c->L_global >= (int64_t(1) << 31))
+    return fail(FF_ERR_CONFIG, "L_global=%lld outside [1, 2^31)", (long long)c->L_global);
+  if (c->row_begin < 0 || c->L_local < 0 || c->row_begin + c->L_local > c->L_global)
+    return fail(FF_ERR_CONFIG, "shard rows [%lld, %lld) outside [0, L_global=%lld)", (long long)c->row_begin,
+                (long long)(c->row_begin + c->L_local), (long long)c->L_global);
+  if (c->m < 1) return fail(FF_ERR_CONFIG, "m=%d < 1", c->m);
+  if (c->k < 1 || c->k > FF_MAX_FANIN || c->k > c->m)
+    return fail(FF_ERR_CONFIG, "k=%d outside [1, min(m=%d, %d)]", c->k, c->m, FF_MAX_FANIN);
+  if (c->max_batch < 1 || c->max_batch > FF_MAX_BATCH)
+    return fail(FF_ERR_CONFIG, "max_batch=%d outside [1, %d]", c->max_batch, FF_MAX_BATCH);
+  if (c->max_topk < 1 || c->max_topk > FF_MAX_TOPK)
+    return fail(FF_ERR_CONFIG, "max_topk=%d outside [1, %d]", c->max_topk, FF_MAX_TOPK);
+  if (c->max_nnz < 0) return fail(FF_ERR_CONFIG, "max_nnz < 0");
+  if (c->dh_mode != FF_DH_ATOMIC)
+    return fail(FF_ERR_CONFIG, "dh_mode=%d not supported by this build (only FF_DH_ATOMIC)", c->dh_mode);
+  if (c->prune_frac < 0.0f || c->prune_frac >= 1.0f) return fail(FF_ERR_CONFIG, "prune_frac outside [0, 1)");
+  if (c->beta1 < 0.0f || c->beta1 >= 1.0f || c->beta2 < 0.0f || c->beta2 >= 1.0f || c->eps < 0.0f)
+    return fail(FF_ERR_CONFIG, "Adam hyper-parameters out of range");
+  return FF_OK;
+}
+
+ff_config with_defaults(const ff_config& in) {
+  ff_config c = in;
+  if (c.beta1 == 0.0f) c.beta1 = 0.9f;
+  if (c.beta2 == 0.0f) c.beta2 = 0.999f;
+  if (c.eps == 0.0f) c.eps = 1e-8f;
+  if (c.prune_frac == 0.0f) c.prune_frac = 0.1f;
+  if (c.init_scale == 0.0f) c.init_scale = (float)(1.0 / std::sqrt((double)c.k));
+  if (c.max_nnz == 0) c.max_nnz = 64 * c.max_batch;
+  return c;
+}
+
+}  // namespace
+
+struct ff_layer {
+  ff_config cfg;
+  Layout lay;
+  char* ws;
+  float *W, *mW, *vW, *dW, *bias, *mb, *vb, *db, *hd, *cand_s, *h_stage, *dh_stage;
+  int *idx, *cand_i, *lbl_stage, *err;
+  float* loss_scratch;
+  uint32_t* posmask;
+  int64_t t;
+  bool grads_valid;
+  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows;
+  int nsm;
+  std::vector<cudaEvent_t> prof_ev;   // pairs (before, after) of the fused row kernel
+  int prof_used = 0;
+};
+
+namespace {
+
+template <typename T>
+T* at(char* base, size_t off) { return reinterpret_cast<T*>(base + off); }
+
+ff_status launch_prep(ff_layer* l, const float* h, int B, bool zero_dh, const int* lbl_ptr,
+                      const int* lbl_ids, float* loss, cudaStream_t st) {
+  const int nb = nb_of(B);
+  dim3 grid((l->cfg.m + 31) / 32), block(32, 8);
+  k_prep<<<grid, block, 0, st>>>(h, B, l->cfg.m, nb, l->hd, zero_dh ? 1 : 0, lbl_ptr, lbl_ids, l->posmask,
+                                 l->cfg.L_local, l->cfg.row_begin, l->cfg.L_global, loss, l->err);
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
+ff_status launch_dh_out(ff_layer* l, int B, float* dh, cudaStream_t st) {
+  const int nb = nb_of(B);
+  dim3 grid((l->cfg.m + 31) / 32, nb), block(32, 8);
+  k_dh_out<<<grid, block, 0, st>>>(l->hd, B, l->cfg.m, nb, dh);
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
+AdamArgs adam_args(const ff_layer* l, float lr, int64_t t) {
+  AdamArgs a;
+  a.lr = lr;
+  a.beta1 = l->cfg.beta1;
+  a.beta2 = l->cfg.beta2;
+  a.one_minus_b1 = 1.0f - l->cfg.beta1;
+  a.one_minus_b2 = 1.0f - l->cfg.beta2;
+  a.rbc1 = (float)(1.0 / (1.0 - std::pow((double)l->cfg.beta1, (double)t)));
+  a.rbc2 = (float)(1.0 / (1.0 - std::pow((double)l->cfg.beta2, (double)t)));
+  a.eps = l->cfg.eps;
+  return a;
+}
+
+RowArgs row_args(ff_layer* l, int B) {
+  RowArgs a{};
+  a.W = l->W; a.idx = l->idx; a.bias = l->bias; a.mW = l->mW; a.vW = l->vW; a.mb = l->mb; a.vb = l->vb;
+  a.dW = l->dW; a.db = l->db; a.posmask = l->posmask; a.hd = l->hd;
+  a.L = l->cfg.L_local; a.k = l->cfg.k; a.B = B; a.nb = nb_of(B); a.cstride = 64 * a.nb;
+  a.err = l->err;
+  a.check_finite = (l->cfg.flags & FF_FLAG_CHECK_FINITE) ? 1u : 0u;
+  return a;
+}
+
+// Row kernels are specialized on NG = number of 4-connection groups a lane walks:
+// 4 for k <= 16, 8 for k <= 32.
+template <int MODE, bool SG>
+const void* row_kernel(int k) {
+  return k <= 16 ? (const void*)k_rows<MODE, SG, 4> : (const void*)k_rows<MODE, SG, 8>;
+}
+const void* predict_kernel(int k) {
+  return k <= 16 ? (const void*)k_predict<4> : (const void*)k_predict<8>;
+}
+
+ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st) {
+  void* args[] = {&a};
+  FF_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kRowThreads), args, 0, st));
+  ++g_launches;
+  return FF_OK;
+}
+
+int occupancy_grid(const void* fn, int nsm, int threads) {
+  int per = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0) != cudaSuccess || per < 1) per = 1;
+  return nsm * per;
+}
+
+bool ptr_ok(const void* p, int64_t n) { return n == 0 || p != nullptr; }
+
+ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t* lbl_ptr, const int32_t* lbl_ids,
+                          float grad_scale, float lr, float* dh, float* loss, cudaStream_t st) {
+  if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
+  if (!ptr_ok(h, B) || !ptr_ok(dh, B) || lbl_ptr == nullptr) return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
+  ff_status s = launch_prep(l, h, B, true, lbl_ptr, lbl_ids, loss, st);
+  if (s != FF_OK) return s;
+  l->t += 1;
+  RowArgs a = row_args(l, B);
+  a.grad_scale = grad_scale;
+  a.loss = loss;
+  a.adam = adam_args(l, lr, l->t);
+  const bool timed = l->cfg.L_local > 0 && 2 * (l->prof_used + 1) <= (int)l->prof_ev.size();
+  if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used], st));
+  if (l->cfg.L_local > 0) {
+    const void* fn = (l->cfg.flags & FF_FLAG_STORE_GRADS) ? row_kernel<kModeTrain, true>(l->cfg.k)
+                                                          : row_kernel<kModeTrain, false>(l->cfg.k);
+    ff_status s2 = launch_rows(fn, l->grid_train, a, st);
+    if (s2 != FF_OK) return s2;
+  }
+  if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used++ + 1], st));
+  l->grads_valid = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
+  if (B > 0) return launch_dh_out(l, B, dh, st);
+  return FF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fixedfanin_last_error(void) { return g_err.c_str(); }
+int32_t fixedfanin_last_launch_count(void) { return g_launches; }
+
+ff_status fixedfanin_workspace_size(const ff_config* cfg, size_t* bytes) {
+  g_launches = 0;
+  ff_status s = validate(cfg);
+  if (s != FF_OK) return s;
+  if (!bytes) return fail(FF_ERR_ARG, "bytes is NULL");
+  *bytes = layout_of(with_defaults(*cfg)).total;
+  return FF_OK;
+}
+
+ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes, ff_stream_t stream,
+                            ff_layer** out) {
+  g_launches = 0;
+  ff_status s = validate(cfg);
+  if (s != FF_OK) return s;
+  if (!out || !workspace) return fail(FF_ERR_ARG, "out/workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(FF_ERR_ARG, "workspace not 256-B aligned");
+  const ff_config c = with_defaults(*cfg);
+  const Layout lay = layout_of(c);
+  if (bytes < lay.total) return fail(FF_ERR_ARG, "workspace %zu B < required %zu B", bytes, lay.total);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  FF_CUDA(cudaGetLastError());
+  ff_layer* l = new (std::nothrow) ff_layer();
+  if (!l) return fail(FF_ERR_ARG, "host allocation failed");
+  l->cfg = c; l->lay = lay;
+  char* ws = static_cast<char*>(workspace);
+  l->ws = ws;
+  l->W = at<float>(ws, lay.W); l->idx = at<int>(ws, lay.idx); l->mW = at<float>(ws, lay.mW);
+  l->vW = at<float>(ws, lay.vW); l->dW = at<float>(ws, lay.dW); l->bias = at<float>(ws, lay.bias);
+  l->mb = at<float>(ws, lay.mb); l->vb = at<float>(ws, lay.vb); l->db = at<float>(ws, lay.db);
+  l->posmask = at<uint32_t>(ws, lay.posmask); l->hd = at<float>(ws, lay.hd);
+  l->cand_s = at<float>(ws, lay.cand_s); l->cand_i = at<int>(ws, lay.cand_i);
+  l->h_stage = at<float>(ws, lay.h_stage); l->lbl_stage = at<int>(ws, lay.lbl_stage);
+  l->dh_stage = at<float>(ws, lay.dh_stage);
+  l->err = at<int>(ws, lay.scalars); l->loss_scratch = at<float>(ws, lay.scalars + 4);
+  l->t = 0; l->grads_valid = false;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&l->nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) { delete l; return fail(FF_ERR_CUDA, "device query: %s", cudaGetErrorString(e)); }
+  l->grid_train = occupancy_grid(row_kernel<kModeTrain, false>(c.k), l->nsm, kRowThreads);
+  l->grid_fwd = occupancy_grid(row_kernel<kModeForward, false>(c.k), l->nsm, kRowThreads);
+  l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k), l->nsm, kRowThreads);
+  l->grid_pred = std::min(kMaxCandBlocks, occupancy_grid(predict_kernel(c.k), l->nsm, kRowThreads));
+  l->grid_rows = l->nsm * 8;
+  // zero everything that must start at zero (moments, masks, dW/db, dhT, scalars)
+  e = cudaMemsetAsync(ws, 0, lay.total, st);
+  if (e != cudaSuccess) { delete l; return fail(FF_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); }
+  if (c.L_local > 0) {
+    k_init<<<l->grid_rows, 256, 0, st>>>(l->W, l->idx, l->bias, l->mW, l->vW, l->mb, l->vb, c.L_local, c.row_begin,
+                                         c.m, c.k, (uint32_t)c.seed, (uint32_t)(c.seed >> 32), c.init_scale);
+    ++g_launches;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { delete l; return fail(FF_ERR_CUDA, "init launch: %s", cudaGetErrorString(e)); }
+  }
+  *out = l;
+  return FF_OK;
+}
+
+ff_status fixedfanin_destroy(ff_layer* l) {
+  if (l) for (cudaEvent_t e : l->prof_ev) cudaEventDestroy(e);
+  delete l;
+  return FF_OK;
+}
+
+ff_status fixedfanin_set_params(ff_layer* l, const float* W, const int32_t* idx, const float* bias, const float* mW,
+                                const float* vW, const float* mb, const float* vb, const int64_t* t,
+                                ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t Lk = (size_t)l->cfg.L_local * l->cfg.k * 4, L4 = (size_t)l->cfg.L_local * 4;
+  auto cp = [&](void* dst, const void* src, size_t n) -> cudaError_t {
+    return (src && n) ? cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  };
+  FF_CUDA(cp(l->W, W, Lk)); FF_CUDA(cp(l->idx, idx, Lk)); FF_CUDA(cp(l->bias, bias, L4));
+  FF_CUDA(cp(l->mW, mW, Lk)); FF_CUDA(cp(l->vW, vW, Lk)); FF_CUDA(cp(l->mb, mb, L4)); FF_CUDA(cp(l->vb, vb, L4));
+  if (t) l->t = *t;
+  l->grads_valid = false;
+  if (idx && l->cfg.L_local > 0) {
+    FF_CUDA(cudaMemsetAsync(l->err, 0, sizeof(int), st));
+    k_validate_idx<<<l->grid_rows, 256, 0, st>>>(l->idx, l->cfg.L_local, l->cfg.m, l->cfg.k, l->err);
+    FF_LAUNCHED();
+    int herr = 0;
+    FF_CUDA(cudaMemcpyAsync(&herr, l->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FF_CUDA(cudaStreamSynchronize(st));
+    if (herr & kErrIdxRange) return fail(FF_ERR_RANGE, "set_params: idx outside [0, m=%d)", l->cfg.m);
+    if (herr & kErrIdxDup) return fail(FF_ERR_RANGE, "set_params: duplicate idx within a row");
+  }
+  FF_CUDA(cudaStreamSynchronize(st));
+  return FF_OK;
+}
+
+ff_status fixedfanin_get_params(ff_layer* l, float* W, int32_t* idx, float* bias, float* mW, float* vW, float* mb,
+                                float* vb, int64_t* t, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t Lk = (size_t)l->cfg.L_local * l->cfg.k * 4, L4 = (size_t)l->cfg.L_local * 4;
+  auto cp = [&](void* dst, const void* src, size_t n) -> cudaError_t {
+    return (dst && n) ? cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  };
+  FF_CUDA(cp(W, l->W, Lk)); FF_CUDA(cp(idx, l->idx, Lk)); FF_CUDA(cp(bias, l->bias, L4));
+  FF_CUDA(cp(mW, l->mW, Lk)); FF_CUDA(cp(vW, l->vW, Lk)); FF_CUDA(cp(mb, l->mb, L4)); FF_CUDA(cp(vb, l->vb, L4));
+  if (t) *t = l->t;
+  FF_CUDA(cudaStreamSynchronize(st));
+  return FF_OK;
+}
+
+ff_status fixedfanin_forward(ff_layer* l, const float* h, int32_t B, float* y, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
+  if (B == 0) return FF_OK;
+  if (!h || (!y && l->cfg.L_local > 0)) return fail(FF_ERR_ARG, "null h/y");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ff_status s = launch_prep(l, h, B, false, nullptr, nullptr, nullptr, st);
+  if (s != FF_OK) return s;
+  if (l->cfg.L_local == 0) return FF_OK;
+  RowArgs a = row_args(l, B);
+  a.y_out = y;
+  return launch_rows(row_kernel<kModeForward, false>(l->cfg.k), l->grid_fwd, a, st);
+}
+
+ff_status fixedfanin_backward(ff_layer* l, const float* h, const float* y, int32_t B, const int32_t* lbl_ptr,
+                              const int32_t* lbl_ids, float grad_scale, float* dh, float* loss, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
+  if (!ptr_ok(h, B) || !ptr_ok(dh, B) || lbl_ptr == nullptr || (B > 0 && l->cfg.L_local > 0 && !y))
+    return fail(FF_ERR_ARG, "null h/y/dh/lbl_ptr");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ff_status s = launch_prep(l, h, B, true, lbl_ptr, lbl_ids, loss, st);
+  if (s != FF_OK) return s;
+  if (l->cfg.L_local > 0) {
+    RowArgs a = row_args(l, B);
+    a.y_in = y; a.grad_scale = grad_scale; a.loss = loss;
+    s = launch_rows(row_kernel<kModeBackward, false>(l->cfg.k), l->grid_bwd, a, st);
+    if (s != FF_OK) return s;
+  }
+  l->grads_valid = true;
+  if (B > 0) return launch_dh_out(l, B, dh, st);
+  return FF_OK;
+}
+
+ff_status fixedfanin_get_grads(ff_layer* l, float* dW, float* db, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (!l->grads_valid) return fail(FF_ERR_STATE, "no gradients: run backward (or train_step with FF_FLAG_STORE_GRADS)");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t Lk = (size_t)l->cfg.L_local * l->cfg.k * 4, L4 = (size_t)l->cfg.L_local * 4;
+  if (dW && Lk) FF_CUDA(cudaMemcpyAsync(dW, l->dW, Lk, cudaMemcpyDeviceToDevice, st));
+  if (db && L4) FF_CUDA(cudaMemcpyAsync(db, l->db, L4, cudaMemcpyDeviceToDevice, st));
+  return FF_OK;
+}
+
+ff_status fixedfanin_adam_step(ff_layer* l, float lr, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (!l->grads_valid) return fail(FF_ERR_STATE, "adam_step without a preceding backward");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  l->t += 1;
+  const int64_t n = l->cfg.L_local * l->cfg.k;
+  if (n > 0) {
+    k_adam<<<l->nsm * 8, 256, 0, st>>>(l->W, l->mW, l->vW, l->dW, n, l->bias, l->mb, l->vb, l->db, l->cfg.L_local,
+                                       adam_args(l, lr, l->t));
+    FF_LAUNCHED();
+  }
+  l->grads_valid = false;
+  return FF_OK;
+}
+
+ff_status fixedfanin_train_step(ff_layer* l, const float* h, int32_t B, const int32_t* lbl_ptr,
+                                const int32_t* lbl_ids, float grad_scale, float lr, float* dh, float* loss,
+                                ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  return train_step_impl(l, h, B, lbl_ptr, lbl_ids, grad_scale, lr, dh, loss, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ff_status fixedfanin_train_step_host(ff_layer* l, const float* h_host, int32_t B, const int32_t* lbl_ptr_host,
+                                     const int32_t* lbl_ids_host, float grad_scale, float lr, float* dh_host,
+                                     float* loss_host, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
+  if (!lbl_ptr_host || (B > 0 && !h_host)) return fail(FF_ERR_ARG, "null host input");
+  const int nnz = lbl_ptr_host[B];
+  if (nnz < 0 || nnz > l->cfg.max_nnz) return fail(FF_ERR_ARG, "lbl_ptr[B]=%d outside [0, max_nnz=%d]", nnz, l->cfg.max_nnz);
+  if (nnz > 0 && !lbl_ids_host) return fail(FF_ERR_ARG, "null lbl_ids_host");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t hb = (size_t)B * l->cfg.m * 4;
+  if (hb) FF_CUDA(cudaMemcpyAsync(l->h_stage, h_host, hb, cudaMemcpyHostToDevice, st));
+  FF_CUDA(cudaMemcpyAsync(l->lbl_stage, lbl_ptr_host, 4 * (size_t)(B + 1), cudaMemcpyHostToDevice, st));
+  if (nnz) FF_CUDA(cudaMemcpyAsync(l->lbl_stage + B + 1, lbl_ids_host, 4 * (size_t)nnz, cudaMemcpyHostToDevice, st));
+  ff_status s = train_step_impl(l, l->h_stage, B, l->lbl_stage, l->lbl_stage + B + 1, grad_scale, lr, l->dh_stage,
+                                l->loss_scratch, st);
+  const int32_t launches = g_launches;
+  if (s != FF_OK) return s;
+  if (loss_host) FF_CUDA(cudaMemcpyAsync(loss_host, l->loss_scratch, 4, cudaMemcpyDeviceToHost, st));
+  if (dh_host && hb) FF_CUDA(cudaMemcpyAsync(dh_host, l->dh_stage, hb, cudaMemcpyDeviceToHost, st));
+  g_launches = launches;
+  return FF_OK;
+}
+
+ff_status fixedfanin_redistribute(ff_layer* l, uint64_t step, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  const int p = (int)std::floor((double)l->cfg.prune_frac * (double)l->cfg.k);
+  if (p < 1) return fail(FF_ERR_CONFIG, "prune count floor(%g*%d) = %d < 1", l->cfg.prune_frac, l->cfg.k, p);
+  if (l->cfg.m - l->cfg.k < p) return fail(FF_ERR_CONFIG, "m - k = %d < prune count %d", l->cfg.m - l->cfg.k, p);
+  if (l->cfg.L_local == 0) return FF_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_redistribute<<<l->grid_rows, 256, 0, st>>>(l->W, l->idx, l->mW, l->vW, l->cfg.L_local, l->cfg.row_begin, l->cfg.m,
+                                               l->cfg.k, p, (uint32_t)step, (uint32_t)l->cfg.seed,
+                                               (uint32_t)(l->cfg.seed >> 32));
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
+ff_status fixedfanin_predict_topk(ff_layer* l, const float* h, int32_t B, int32_t K, float* scores, int32_t* ids,
+                                  ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
+  if (K < 1 || K > l->cfg.max_topk || K > l->cfg.L_local)
+    return fail(FF_ERR_ARG, "K=%d outside [1, min(max_topk=%d, L_local=%lld)]", K, l->cfg.max_topk,
+                (long long)l->cfg.L_local);
+  if (B == 0) return FF_OK;
+  if (!h || !scores || !ids) return fail(FF_ERR_ARG, "null h/scores/ids");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ff_status s = launch_prep(l, h, B, false, nullptr, nullptr, nullptr, st);
+  if (s != FF_OK) return s;
+  const int nb = nb_of(B), ldh = 32 * nb;
+  {
+    const float* W = l->W; const int* idx = l->idx; const float* bias = l->bias; const float* hd = l->hd;
+    int64_t L = l->cfg.L_local, rb = l->cfg.row_begin; int k = l->cfg.k, BB = B, nbb = nb;
+    float* cs = l->cand_s; int* ci = l->cand_i;
+    void* args[] = {&W, &idx, &bias, &hd, &L, &k, &BB, &nbb, &rb, &cs, &ci};
+    FF_CUDA(cudaLaunchKernel(predict_kernel(l->cfg.k), dim3(l->grid_pred), dim3(kRowThreads), args, 0, st));
+    ++g_launches;
+  }
+  k_merge_topk<<<(B + 7) / 8, 256, 0, st>>>(l->cand_s, l->cand_i, l->grid_pred, (int64_t)ldh * kTopkMax, kTopkMax, K,
+                                           B, K, scores, ids);
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
+ff_status fixedfanin_merge_topk(const float* in_s, const int32_t* in_i, int32_t P, int32_t B, int32_t K, float* out_s,
+                                int32_t* out_i, ff_stream_t stream) {
+  g_launches = 0;
+  if (P < 1 || P > 1024 || B < 0 || K < 1 || K > FF_MAX_TOPK) return fail(FF_ERR_ARG, "bad P/B/K");
+  if (B == 0) return FF_OK;
+  if (!in_s || !in_i || !out_s || !out_i) return fail(FF_ERR_ARG, "null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_merge_topk<<<(B + 7) / 8, 256, 0, st>>>(in_s, in_i, P, (int64_t)B * K, K, K, B, K, out_s, out_i);
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
+ff_status fixedfanin_profile_begin(ff_layer* l, int32_t max_launches) {
+  g_launches = 0;
+  if (!l || max_launches < 1) return fail(FF_ERR_ARG, "layer NULL or max_launches < 1");
+  for (cudaEvent_t e : l->prof_ev) cudaEventDestroy(e);
+  l->prof_ev.assign(2 * (size_t)max_launches, nullptr);
+  for (auto& e : l->prof_ev) FF_CUDA(cudaEventCreate(&e));
+  l->prof_used = 0;
+  return FF_OK;
+}
+
+ff_status fixedfanin_profile_end(ff_layer* l, double* ms, int32_t* launches) {
+  g_launches = 0;
+  if (!l || !ms || !launches) return fail(FF_ERR_ARG, "null argument");
+  double total = 0.0;
+  if (l->prof_used > 0) FF_CUDA(cudaEventSynchronize(l->prof_ev[2 * l->prof_used - 1]));
+  for (int i = 0; i < l->prof_used; ++i) {
+    float t = 0.0f;
+    FF_CUDA(cudaEventElapsedTime(&t, l->prof_ev[2 * i], l->prof_ev[2 * i + 1]));
+    total += t;
+  }
+  *ms = total;
+  *launches = l->prof_used;
+  for (cudaEvent_t e : l->prof_ev) cudaEventDestroy(e);
+  l->prof_ev.clear();
+  l->prof_used = 0;
+  return FF_OK;
+}
+
+ff_status fixedfanin_check(ff_layer* l, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int herr = 0;
+  FF_CUDA(cudaMemcpyAsync(&herr, l->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FF_CUDA(cudaStreamSynchronize(st));
+  FF_CUDA(cudaGetLastError());
+  if (herr) FF_CUDA(cudaMemsetAsync(l->err, 0, sizeof(int), st));
+  if (herr & kErrLabelRange) return fail(FF_ERR_RANGE, "a label id was outside [0, L_global=%lld)", (long long)l->cfg.L_global);
+  if (herr & kErrNonFinite) return fail(FF_ERR_NONFINITE, "non-finite score seen (FF_FLAG_CHECK_FINITE)");
+  return FF_OK;
+}
+
+}  // extern "C"

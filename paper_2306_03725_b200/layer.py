@@ -1,0 +1,271 @@
+"""Thin ctypes binding of ``libfixedfanin.so`` (C ABI in include/fixedfanin.h).
+
+Argument marshalling only: every step of the hot path runs in the library's sm_100a
+kernels.  PyTorch provides device memory (the workspace, inputs, outputs) and streams.
+There is no CPU fallback: if the library is missing, loading raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("FIXEDFANIN_LIB") or os.path.join(_HERE, "libfixedfanin.so")   # env: dev sweeps only
+
+FF_OK, FF_ERR_ARG, FF_ERR_CONFIG, FF_ERR_RANGE, FF_ERR_NONFINITE, FF_ERR_CUDA, FF_ERR_STATE = range(7)
+FF_FLAG_CHECK_FINITE = 1
+FF_FLAG_STORE_GRADS = 2
+FF_DH_ATOMIC, FF_DH_CSC = 0, 1
+FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 32, 128, 8
+_STATUS = {1: "FF_ERR_ARG", 2: "FF_ERR_CONFIG", 3: "FF_ERR_RANGE", 4: "FF_ERR_NONFINITE", 5: "FF_ERR_CUDA",
+           6: "FF_ERR_STATE"}
+
+EXPORTS = [
+    "fixedfanin_workspace_size", "fixedfanin_create", "fixedfanin_destroy", "fixedfanin_set_params",
+    "fixedfanin_get_params", "fixedfanin_forward", "fixedfanin_backward", "fixedfanin_get_grads",
+    "fixedfanin_adam_step", "fixedfanin_train_step", "fixedfanin_train_step_host", "fixedfanin_redistribute",
+    "fixedfanin_predict_topk", "fixedfanin_merge_topk", "fixedfanin_check", "fixedfanin_profile_begin",
+    "fixedfanin_profile_end", "fixedfanin_last_launch_count",
+    "fixedfanin_last_error",
+]
+
+
+class FFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ff_config(ctypes.Structure):
+    _fields_ = [
+        ("L_global", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("L_local", ctypes.c_int64),
+        ("m", ctypes.c_int32), ("k", ctypes.c_int32), ("max_batch", ctypes.c_int32),
+        ("max_topk", ctypes.c_int32), ("max_nnz", ctypes.c_int32), ("dh_mode", ctypes.c_int32),
+        ("seed", ctypes.c_uint64), ("init_scale", ctypes.c_float), ("beta1", ctypes.c_float),
+        ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("prune_frac", ctypes.c_float),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the CUDA library (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not found: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64, u64, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
+        sig = {
+            "fixedfanin_workspace_size": [P, P],
+            "fixedfanin_create": [P, P, ctypes.c_size_t, P, P],
+            "fixedfanin_destroy": [P],
+            "fixedfanin_set_params": [P, P, P, P, P, P, P, P, P, P],
+            "fixedfanin_get_params": [P, P, P, P, P, P, P, P, P, P],
+            "fixedfanin_forward": [P, P, i32, P, P],
+            "fixedfanin_backward": [P, P, P, i32, P, P, f32, P, P, P],
+            "fixedfanin_get_grads": [P, P, P, P],
+            "fixedfanin_adam_step": [P, f32, P],
+            "fixedfanin_train_step": [P, P, i32, P, P, f32, f32, P, P, P],
+            "fixedfanin_train_step_host": [P, P, i32, P, P, f32, f32, P, P, P],
+            "fixedfanin_redistribute": [P, u64, P],
+            "fixedfanin_predict_topk": [P, P, i32, i32, P, P, P],
+            "fixedfanin_merge_topk": [P, P, i32, i32, i32, P, P, P],
+            "fixedfanin_check": [P, P],
+            "fixedfanin_profile_begin": [P, i32],
+            "fixedfanin_profile_end": [P, P, P],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.fixedfanin_last_launch_count.argtypes = []
+        L.fixedfanin_last_launch_count.restype = i32
+        L.fixedfanin_last_error.argtypes = []
+        L.fixedfanin_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != FF_OK:
+        raise FFError(status, lib().fixedfanin_last_error().decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "device tensors must be contiguous CUDA tensors"
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(t):
+    if t is None:
+        return None
+    assert (not t.is_cuda) and t.is_contiguous()
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def last_launch_count() -> int:
+    return int(lib().fixedfanin_last_launch_count())
+
+
+@dataclass
+class LayerConfig:
+    L_global: int
+    m: int
+    k: int
+    row_begin: int = 0
+    L_local: int | None = None
+    max_batch: int = 32
+    max_topk: int = 8
+    max_nnz: int = 0
+    dh_mode: int = FF_DH_ATOMIC
+    seed: int = 42
+    init_scale: float = 0.0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    prune_frac: float = 0.1
+    flags: int = 0
+
+    def c(self) -> ff_config:
+        L_local = self.L_global - self.row_begin if self.L_local is None else self.L_local
+        return ff_config(self.L_global, self.row_begin, L_local, self.m, self.k, self.max_batch, self.max_topk,
+                         self.max_nnz, self.dh_mode, self.seed, self.init_scale, self.beta1, self.beta2, self.eps,
+                         self.prune_frac, self.flags)
+
+
+def workspace_size(cfg: LayerConfig) -> int:
+    n = ctypes.c_size_t(0)
+    c = cfg.c()
+    _check(lib().fixedfanin_workspace_size(ctypes.byref(c), ctypes.byref(n)))
+    return int(n.value)
+
+
+class FixedFanInLayer:
+    """One label shard [row_begin, row_begin + L_local) of the fixed fan-in layer on one GPU."""
+
+    def __init__(self, cfg: LayerConfig, device=None, stream=None):
+        self.cfg = cfg
+        self._c = cfg.c()
+        self.L_local = int(self._c.L_local)
+        self.device = torch.device(device if device is not None else "cuda")
+        nbytes = workspace_size(cfg)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self._h = ctypes.c_void_p()
+        _check(lib().fixedfanin_create(ctypes.byref(self._c), _ptr(self.workspace), nbytes, _stream(stream),
+                                       ctypes.byref(self._h)))
+        self.m, self.k = cfg.m, cfg.k
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().fixedfanin_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------------ state
+    def get_params(self, stream=None):
+        L, k, d = self.L_local, self.k, self.device
+        W = torch.empty((L, k), dtype=torch.float32, device=d)
+        idx = torch.empty((L, k), dtype=torch.int32, device=d)
+        bias, mb, vb = (torch.empty(L, dtype=torch.float32, device=d) for _ in range(3))
+        mW, vW = torch.empty_like(W), torch.empty_like(W)
+        t = ctypes.c_int64(0)
+        _check(lib().fixedfanin_get_params(self._h, _ptr(W), _ptr(idx), _ptr(bias), _ptr(mW), _ptr(vW), _ptr(mb),
+                                           _ptr(vb), ctypes.byref(t), _stream(stream)))
+        return dict(W=W, idx=idx, bias=bias, mW=mW, vW=vW, mb=mb, vb=vb, t=int(t.value))
+
+    def set_params(self, W=None, idx=None, bias=None, mW=None, vW=None, mb=None, vb=None, t=None, stream=None):
+        tt = ctypes.c_int64(int(t)) if t is not None else None
+        _check(lib().fixedfanin_set_params(self._h, _ptr(W), _ptr(idx), _ptr(bias), _ptr(mW), _ptr(vW), _ptr(mb),
+                                           _ptr(vb), ctypes.byref(tt) if tt is not None else None, _stream(stream)))
+
+    # ------------------------------------------------------------------ path
+    def forward(self, h, y=None, stream=None):
+        B = h.shape[0]
+        if y is None:
+            y = torch.empty((B, self.L_local), dtype=torch.float32, device=self.device)
+        _check(lib().fixedfanin_forward(self._h, _ptr(h), B, _ptr(y), _stream(stream)))
+        return y
+
+    def backward(self, h, y, lbl_ptr, lbl_ids, grad_scale=None, dh=None, loss=None, stream=None):
+        B = h.shape[0]
+        gs = 1.0 / max(B, 1) if grad_scale is None else grad_scale
+        if dh is None:
+            dh = torch.empty((B, self.m), dtype=torch.float32, device=self.device)
+        if loss is None:
+            loss = torch.empty(1, dtype=torch.float32, device=self.device)
+        _check(lib().fixedfanin_backward(self._h, _ptr(h), _ptr(y), B, _ptr(lbl_ptr), _ptr(lbl_ids), gs, _ptr(dh),
+                                         _ptr(loss), _stream(stream)))
+        return dh, loss
+
+    def get_grads(self, stream=None):
+        dW = torch.empty((self.L_local, self.k), dtype=torch.float32, device=self.device)
+        db = torch.empty(self.L_local, dtype=torch.float32, device=self.device)
+        _check(lib().fixedfanin_get_grads(self._h, _ptr(dW), _ptr(db), _stream(stream)))
+        return dW, db
+
+    def adam_step(self, lr, stream=None):
+        _check(lib().fixedfanin_adam_step(self._h, lr, _stream(stream)))
+
+    def train_step(self, h, lbl_ptr, lbl_ids, lr, grad_scale=None, dh=None, loss=None, stream=None):
+        B = h.shape[0]
+        gs = 1.0 / max(B, 1) if grad_scale is None else grad_scale
+        if dh is None:
+            dh = torch.empty((B, self.m), dtype=torch.float32, device=self.device)
+        _check(lib().fixedfanin_train_step(self._h, _ptr(h), B, _ptr(lbl_ptr), _ptr(lbl_ids), gs, lr, _ptr(dh),
+                                           _ptr(loss), _stream(stream)))
+        return dh, loss
+
+    def train_step_host(self, h_host, lbl_ptr_host, lbl_ids_host, lr, grad_scale=None, dh_host=None,
+                        loss_host=None, stream=None):
+        B = h_host.shape[0]
+        gs = 1.0 / max(B, 1) if grad_scale is None else grad_scale
+        _check(lib().fixedfanin_train_step_host(self._h, _hptr(h_host), B, _hptr(lbl_ptr_host), _hptr(lbl_ids_host),
+                                                gs, lr, _hptr(dh_host), _hptr(loss_host), _stream(stream)))
+
+    def redistribute(self, step, stream=None):
+        _check(lib().fixedfanin_redistribute(self._h, int(step), _stream(stream)))
+
+    def predict_topk(self, h, K, stream=None):
+        B = h.shape[0]
+        scores = torch.empty((B, K), dtype=torch.float32, device=self.device)
+        ids = torch.empty((B, K), dtype=torch.int32, device=self.device)
+        _check(lib().fixedfanin_predict_topk(self._h, _ptr(h), B, K, _ptr(scores), _ptr(ids), _stream(stream)))
+        return scores, ids
+
+    def profile_begin(self, max_launches: int):
+        _check(lib().fixedfanin_profile_begin(self._h, int(max_launches)))
+
+    def profile_end(self):
+        """-> (summed fused-kernel milliseconds, number of timed launches)"""
+        ms, n = ctypes.c_double(0), ctypes.c_int32(0)
+        _check(lib().fixedfanin_profile_end(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return float(ms.value), int(n.value)
+
+    def check(self, stream=None):
+        _check(lib().fixedfanin_check(self._h, _stream(stream)))
+
+
+def merge_topk(scores, ids, stream=None):
+    """Merge per-shard top-K lists [P][B][K] -> [B][K] on the device (exact total order)."""
+    P, B, K = scores.shape
+    out_s = torch.empty((B, K), dtype=torch.float32, device=scores.device)
+    out_i = torch.empty((B, K), dtype=torch.int32, device=scores.device)
+    _check(lib().fixedfanin_merge_topk(_ptr(scores.contiguous()), _ptr(ids.contiguous()), P, B, K, _ptr(out_s),
+                                       _ptr(out_i), _stream(stream)))
+    return out_s, out_i

@@ -1,0 +1,80 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol the header
+declares, sizes workspaces and rejects bad configurations — no compute calls (no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2306_03725_b200 import layer as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__ as g
+    g.build_lib()
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "fixedfanin.h")).read()
+    return sorted(set(re.findall(r"\b(fixedfanin_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 15
+    lib = L.lib()
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(L.EXPORTS)
+
+
+def test_no_torch_types_in_header():
+    txt = open(os.path.join(ROOT, "include", "fixedfanin.h")).read()
+    assert "torch" not in txt.lower().replace("pytorch", "") and "at::" not in txt
+
+
+def test_workspace_size_matches_layout_model():
+    cfg = L.LayerConfig(L_global=670091, m=32768, k=32, max_batch=32)
+    n = L.workspace_size(cfg)
+    Lk = 670091 * 32
+    state = 5 * 4 * Lk + 4 * 4 * 670091 + 4 * 670091          # W idx mW vW dW, bias mb vb db, posmask
+    scratch = 2 * 4 * 32768 * 32 + 2 * 4 * 1024 * 32 * 8 + 2 * 4 * 32 * 32768 + 4 * (33 + 64 * 32)
+    assert state <= n <= state + scratch + 32 * 256
+    assert n % 256 == 0
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(L_global=10, m=8, k=9), "k="),            # k > m
+    (dict(L_global=10, m=64, k=33), "k="),          # k > FF_MAX_FANIN
+    (dict(L_global=10, m=64, k=8, row_begin=5, L_local=6), "shard"),
+    (dict(L_global=10, m=64, k=8, max_batch=129), "max_batch"),
+    (dict(L_global=10, m=64, k=8, max_topk=9), "max_topk"),
+    (dict(L_global=2 ** 31, m=64, k=8), "L_global"),
+    (dict(L_global=10, m=64, k=8, prune_frac=1.0), "prune_frac"),
+])
+def test_bad_configs_rejected(kw, msg):
+    with pytest.raises(L.FFError) as e:
+        L.workspace_size(L.LayerConfig(**kw))
+    assert e.value.status == L.FF_ERR_CONFIG and msg in str(e.value)
+
+
+def test_create_without_gpu_fails_loudly():
+    """No CPU fallback: creating a layer on a machine without a usable GPU is an error."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = L.LayerConfig(L_global=100, m=64, k=8).c()
+    buf = (ctypes.c_char * (1 << 20))()
+    aligned = (ctypes.addressof(buf) + 255) // 256 * 256
+    out = ctypes.c_void_p()
+    st = L.lib().fixedfanin_create(ctypes.byref(cfg), ctypes.c_void_p(aligned), 1 << 19, None, ctypes.byref(out))
+    assert st != L.FF_OK
+
+
+def test_merge_topk_argument_validation():
+    st = L.lib().fixedfanin_merge_topk(None, None, 0, 1, 1, None, None, None)
+    assert st == L.FF_ERR_ARG
+    assert b"P" in L.lib().fixedfanin_last_error()

@@ -1,0 +1,380 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the fp64 oracle.
+
+Tolerances (R19/R20): floats compare with
+    err = |x_gpu - x_ref| / max(|x_ref|, A_ref)  <= 1e-4
+where A_ref is the oracle's sum of |terms| of that output; indices, redistribution and
+top-K label sets are bit-exact.  Lockstep protocol: the oracle step is evaluated on the
+GPU's state (fp32 widened exactly to fp64), so |W| orders and scores are comparable.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2306_03725_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+F32 = lambda x: float(np.float32(x))       # the GPU's fp32 hyper-parameters, widened exactly
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__ as g
+    g.build_lib()
+
+
+def L_():
+    from paper_2306_03725_b200 import layer
+    return layer
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def make(L, m, k, B=32, **kw):
+    layer = L_()
+    return layer.FixedFanInLayer(layer.LayerConfig(L_global=kw.pop("L_global", L), m=m, k=k, max_batch=B, **kw),
+                                 device=dev())
+
+
+def tens(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
+
+
+def rel_err(x, ref, A):
+    x = np.asarray(x, dtype=np.float64)
+    return np.abs(x - ref) / np.maximum(np.maximum(np.abs(ref), A), 1e-300)
+
+
+def assert_close(x, ref, A, what, rtol=RTOL):
+    e = rel_err(x, ref, A)
+    assert e.max() <= rtol, f"{what}: max err {e.max():.3e} at {np.unravel_index(e.argmax(), e.shape)}"
+
+
+def state_of(lay):
+    p = lay.get_params()
+    return {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in p.items()}
+
+
+ADAM = dict(beta1=F32(0.9), beta2=F32(0.999), eps=F32(1e-8))
+
+
+# ------------------------------------------------------------------ init (bit-exact)
+@pytest.mark.parametrize("L,m,k,row_begin,Lg", [(1000, 256, 16, 0, 1000), (777, 4096, 32, 123, 5000),
+                                                  (50, 37, 13, 0, 50), (40, 5, 5, 10, 50), (3, 1, 1, 0, 3)])
+def test_init_bit_exact(L, m, k, row_begin, Lg):
+    lay = make(L, m, k, L_global=Lg, row_begin=row_begin, L_local=L, seed=42)
+    s = state_of(lay)
+    idx, W = oracle.init(L, m, k, seed=42, row_begin=row_begin)
+    assert (s["idx"] == idx).all()
+    assert (s["W"].view(np.uint32) == W.view(np.uint32)).all()
+    assert (s["bias"] == 0).all() and (s["mW"] == 0).all() and (s["vW"] == 0).all() and s["t"] == 0
+
+
+def test_init_full_amazon_670k_sampled_rows():
+    L, m, k = 670091, 32768, 32
+    lay = make(L, m, k, seed=42)
+    s = state_of(lay)
+    rng = np.random.default_rng(0)
+    for j in list(rng.choice(L, 64, replace=False)) + [0, L - 1]:
+        idx, W = oracle.init(1, m, k, seed=42, row_begin=int(j))
+        assert (s["idx"][j] == idx[0]).all() and (s["W"][j].view(np.uint32) == W[0].view(np.uint32)).all()
+    assert all(len(set(r)) == k for r in s["idx"][::997])
+
+
+# --------------------------------------------------------------- forward / backward
+CASES = [(1000, 256, 16, 32), (1000, 256, 16, 5), (333, 100, 13, 37), (2000, 512, 32, 100), (97, 64, 1, 1),
+         (64, 32, 32, 128)]
+
+
+@pytest.mark.parametrize("L,m,k,B", CASES)
+def test_forward_parity(L, m, k, B):
+    lay = make(L, m, k, B=B, seed=7)
+    W, idx, bias = synth.random_params(L, m, k, seed=L + B)
+    lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    h = synth.hidden_batch(B, m, step=3)
+    y = lay.forward(tens(h)).cpu().numpy()
+    yr, Ay = oracle.forward(W, idx, bias, h)
+    assert_close(y, yr, Ay, "y")
+
+
+@pytest.mark.parametrize("L,m,k,B", CASES)
+def test_backward_and_adam_parity(L, m, k, B):
+    lay = make(L, m, k, B=B, seed=8)
+    W, idx, bias = synth.random_params(L, m, k, seed=L + 2 * B, scale=0.5)
+    lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    h = synth.hidden_batch(B, m, step=4)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=4)
+    y = lay.forward(tens(h))
+    loss = torch.zeros(1, device=dev())
+    dh, _ = lay.backward(tens(h), y, tens(ptr), tens(ids), loss=loss)
+    dW, db = lay.get_grads()
+    yn = y.cpu().numpy().astype(np.float64)
+    g, lr_ = oracle.bce_grad(yn, ptr, ids, F32(1.0 / B))
+    dWr, AdW, dbr, Adb = oracle.weight_grad(idx, h, g)
+    dhr, Adh = oracle.input_grad(W, idx, g, m)
+    assert_close(dW.cpu().numpy(), dWr, AdW, "dW")
+    assert_close(db.cpu().numpy(), dbr, Adb, "db")
+    assert_close(dh.cpu().numpy(), dhr, Adh, "dh")
+    assert abs(loss.item() - lr_) <= RTOL * abs(lr_)
+    # Adam on the GPU's gradients (lockstep): elementwise fp32 vs fp64
+    lay.adam_step(1e-3)
+    s = state_of(lay)
+    dWg, dbg = dW.cpu().numpy(), db.cpu().numpy()
+    lr32 = F32(1e-3)
+    Wr, mr, vr = oracle.adam(W, dWg, np.zeros_like(dWg), np.zeros_like(dWg), 1, lr32, **ADAM)
+    br, mbr, vbr = oracle.adam(bias, dbg, np.zeros(L), np.zeros(L), 1, lr32, **ADAM)
+    assert_close(s["W"], Wr, 0, "W'")
+    assert_close(s["mW"], mr, 0, "mW'")
+    assert_close(s["vW"], vr, 1e-30, "vW'")
+    assert_close(s["bias"], br, 0, "bias'")
+    assert s["t"] == 1
+
+
+@pytest.mark.parametrize("L,m,k,B", [(1000, 256, 16, 32), (333, 100, 13, 37), (2000, 512, 32, 100)])
+def test_fused_step_equals_unfused_path(L, m, k, B):
+    """train_step (one fused kernel) = forward + backward + adam_step: dW, db and the
+    updated state are bit-identical (same device arithmetic), dh equal up to atomic order."""
+    layer = L_()
+    W, idx, bias = synth.random_params(L, m, k, seed=5, scale=0.5)
+    a = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS)
+    b = make(L, m, k, B=B)
+    for x in (a, b):
+        x.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    for step in range(3):
+        h = tens(synth.hidden_batch(B, m, step=step))
+        ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        la, lb = torch.zeros(1, device=dev()), torch.zeros(1, device=dev())
+        dha, _ = a.train_step(h, tens(ptr), tens(ids), 1e-2, loss=la)
+        dWa, dba = a.get_grads()
+        y = b.forward(h)
+        dhb, _ = b.backward(h, y, tens(ptr), tens(ids), loss=lb)
+        dWb, dbb = b.get_grads()
+        b.adam_step(1e-2)
+        assert torch.equal(dWa, dWb) and torch.equal(dba, dbb)
+        sa, sb = state_of(a), state_of(b)
+        for key in ("W", "mW", "vW", "bias", "mb", "vb", "idx"):
+            assert (sa[key] == sb[key]).all(), key
+        assert torch.allclose(dha, dhb, rtol=1e-5, atol=1e-7)
+        assert abs(la.item() - lb.item()) <= 1e-5 * abs(lb.item())
+
+
+def test_fused_step_lockstep_vs_oracle():
+    L, m, k, B = 1000, 256, 16, 32
+    layer = L_()
+    lay = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, seed=42)
+    for step in range(5):
+        s0 = state_of(lay)
+        st = oracle.State(s0["W"].astype(np.float64), s0["idx"], s0["bias"].astype(np.float64),
+                          s0["mW"].astype(np.float64), s0["vW"].astype(np.float64), s0["mb"].astype(np.float64),
+                          s0["vb"].astype(np.float64), s0["t"])
+        h = synth.hidden_batch(B, m, step=step)
+        ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        loss = torch.zeros(1, device=dev())
+        dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3), loss=loss)
+        dW, db = lay.get_grads()
+        r = oracle.train_step(st, h, ptr, ids, F32(1.0 / B), F32(1e-3), **ADAM)
+        assert_close(dh.cpu().numpy(), r.dh, r.Adh, f"dh step {step}")
+        assert_close(dW.cpu().numpy(), r.dW, r.AdW, f"dW step {step}")
+        assert_close(db.cpu().numpy(), r.db, r.Adb, f"db step {step}")
+        assert abs(loss.item() - r.loss) <= RTOL * r.loss
+        # Adam applied by the oracle to the GPU's gradient: tight elementwise parity
+        s1 = state_of(lay)
+        Wr, mr, vr = oracle.adam(s0["W"], dW.cpu().numpy(), s0["mW"], s0["vW"], s0["t"] + 1, F32(1e-3), **ADAM)
+        assert_close(s1["W"], Wr, 0, "W'"); assert_close(s1["mW"], mr, 0, "m'"); assert_close(s1["vW"], vr, 1e-30, "v'")
+        assert s1["t"] == step + 1
+
+
+def test_free_running_tiny_run_matches_oracle():
+    """tiny config of BASELINE.json: 5 Adam steps + 1 redistribution, then predict K = 5.
+    The oracle evolves its own fp64 state from the same Philox init."""
+    L, m, k, B = 1000, 256, 16, 32
+    lay = make(L, m, k, B=B, seed=42)
+    st = oracle.State.create(L, m, k, seed=42)
+    for step in range(5):
+        h = synth.hidden_batch(B, m, step=step)
+        ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
+        oracle.train_step(st, h, ptr, ids, F32(1.0 / B), F32(1e-3), **ADAM)
+    s = state_of(lay)
+    A = np.abs(st.W) + 5 * F32(1e-3)            # 5 steps of at most ~lr each
+    assert_close(s["W"], st.W, A, "W after 5 steps")
+    lay.redistribute(5)
+    p = int(np.floor(F32(0.1) * k))
+    # redistribution is bit-exact given the state: run the oracle on the GPU's pre-call state
+    W2, idx2, m2, v2 = oracle.redistribute(s["W"], s["idx"], s["mW"], s["vW"], m, p, seed=42, step=5)
+    s2 = state_of(lay)
+    assert (s2["idx"] == idx2).all() and (s2["W"] == W2).all() and (s2["mW"] == m2).all() and (s2["vW"] == v2).all()
+    # and the free-running oracle state agrees except at near-ties of |W|
+    Wf, idxf, _, _ = oracle.redistribute(st.W, st.idx, st.mW, st.vW, m, p, seed=42, step=5)
+    assert (idxf == s2["idx"]).mean() > 0.999
+    h = synth.hidden_batch(B, m, step=99)
+    sc, ids_ = lay.predict_topk(tens(h), 5)
+    y = lay.forward(tens(h)).cpu().numpy().astype(np.float64)
+    _, oid = oracle.topk(y, 5)
+    assert (ids_.cpu().numpy() == oid).all()
+
+
+# ------------------------------------------------------------------- redistribution
+@pytest.mark.parametrize("L,m,k,frac,step", [(1000, 256, 16, 0.1, 1000), (3000, 4096, 32, 0.1, 7),
+                                              (500, 40, 32, 0.25, 3), (64, 3, 2, 0.5, 1)])
+def test_redistribution_bit_exact(L, m, k, frac, step):
+    lay = make(L, m, k, seed=11, prune_frac=frac)
+    W, idx, _ = synth.random_params(L, m, k, seed=3)
+    W[::3, 1] = W[::3, 0]            # ties
+    W[::4, 2 % k] = -W[::4, 0]       # ties across sign
+    W[::5, 0] = 0.0
+    rng = np.random.default_rng(1)
+    mW, vW = rng.random((L, k)).astype(np.float32), rng.random((L, k)).astype(np.float32)
+    lay.set_params(W=tens(W), idx=tens(idx), mW=tens(mW), vW=tens(vW))
+    lay.redistribute(step)
+    s = state_of(lay)
+    p = int(np.floor(F32(frac) * k))
+    W2, idx2, m2, v2 = oracle.redistribute(W, idx, mW, vW, m, p, seed=11, step=step)
+    assert (s["idx"] == idx2).all()
+    assert (s["W"] == W2).all() and (s["mW"] == m2).all() and (s["vW"] == v2).all()
+    assert all(len(set(r)) == k for r in s["idx"])
+
+
+def test_redistribution_config_errors():
+    layer = L_()
+    lay = make(100, 64, 8, prune_frac=0.05)          # floor(0.05*8) = 0
+    with pytest.raises(layer.FFError) as e:
+        lay.redistribute(1)
+    assert e.value.status == layer.FF_ERR_CONFIG
+    lay = make(100, 10, 10, prune_frac=0.2)          # m - k = 0 < p = 2
+    with pytest.raises(layer.FFError):
+        lay.redistribute(1)
+
+
+# ------------------------------------------------------------------------- top-K
+@pytest.mark.parametrize("L,m,k,B,K", [(1000, 256, 16, 32, 5), (5000, 512, 32, 70, 8), (9, 16, 4, 3, 1),
+                                        (8, 16, 4, 3, 8)])
+def test_predict_topk_bit_exact(L, m, k, B, K):
+    lay = make(L, m, k, B=B, seed=3)
+    h = tens(synth.hidden_batch(B, m, step=1))
+    sc, ids = lay.predict_topk(h, K)
+    y = lay.forward(h).cpu().numpy().astype(np.float64)
+    rs, rid = oracle.topk(y, K)
+    assert (ids.cpu().numpy() == rid).all()
+    assert (sc.cpu().numpy() == rs).all()
+
+
+def test_predict_topk_ties_resolved_by_lower_id():
+    L, m, k, B = 300, 64, 8, 4
+    lay = make(L, m, k, B=B)
+    W = np.zeros((L, k), np.float32)
+    bias = np.zeros(L, np.float32); bias[[17, 5, 250, 100]] = 1.0
+    lay.set_params(W=tens(W), bias=tens(bias))
+    sc, ids = lay.predict_topk(tens(synth.hidden_batch(B, m)), 6)
+    assert (ids.cpu().numpy() == np.array([5, 17, 100, 250, 0, 1])).all()
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_sharded_layers_are_p_invariant(P):
+    """Virtual sharding on one GPU: P handles with row offsets reproduce the unsharded
+    state, scores and (after merge) top-K bit-exactly (rows are independent)."""
+    layer = L_()
+    L, m, k, B, K = 2003, 512, 32, 32, 5
+    full = make(L, m, k, B=B, seed=9)
+    bounds = [L * r // P for r in range(P + 1)]
+    shards = [make(bounds[r + 1] - bounds[r], m, k, B=B, seed=9, L_global=L, row_begin=bounds[r],
+                   L_local=bounds[r + 1] - bounds[r]) for r in range(P)]
+    for step in range(2):
+        h = tens(synth.hidden_batch(B, m, step=step))
+        ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        dh_full, _ = full.train_step(h, tens(ptr), tens(ids), 1e-3)
+        dh_sum = sum(s.train_step(h, tens(ptr), tens(ids), 1e-3)[0] for s in shards)
+        assert torch.allclose(dh_full, dh_sum, rtol=1e-5, atol=1e-7)
+    full.redistribute(1000)
+    for s in shards:
+        s.redistribute(1000)
+    sf = state_of(full)
+    cat = [state_of(s) for s in shards]
+    for key in ("W", "idx", "bias", "mW", "vW"):
+        assert (np.concatenate([c[key] for c in cat]) == sf[key]).all(), key
+    h = tens(synth.hidden_batch(B, m, step=5))
+    fs, fi = full.predict_topk(h, K)
+    parts = [s.predict_topk(h, K) for s in shards]
+    ms, mi = layer.merge_topk(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]))
+    assert torch.equal(mi, fi) and torch.equal(ms, fs)
+
+
+# ------------------------------------------------------------------- edge cases
+def test_label_id_out_of_range_reported():
+    layer = L_()
+    lay = make(100, 64, 8, B=2)
+    h = tens(synth.hidden_batch(2, 64))
+    ptr = np.array([0, 1, 2], np.int32); ids = np.array([5, 100], np.int32)
+    lay.train_step(h, tens(ptr), tens(ids), 1e-3)
+    with pytest.raises(layer.FFError) as e:
+        lay.check()
+    assert e.value.status == layer.FF_ERR_RANGE
+    lay.check()                                           # cleared
+
+
+def test_set_params_rejects_bad_idx():
+    layer = L_()
+    lay = make(10, 64, 4)
+    idx = np.tile(np.arange(4, dtype=np.int32), (10, 1)); idx[3, 2] = idx[3, 0]
+    with pytest.raises(layer.FFError) as e:
+        lay.set_params(idx=tens(idx))
+    assert e.value.status == layer.FF_ERR_RANGE
+    idx[3, 2] = 64
+    with pytest.raises(layer.FFError):
+        lay.set_params(idx=tens(idx))
+
+
+def test_empty_batch_and_empty_shard():
+    L, m, k = 50, 32, 4
+    lay = make(L, m, k, B=8, seed=1)
+    s0 = state_of(lay)
+    h = torch.zeros((0, m), device=dev())
+    y = lay.forward(h)
+    assert y.shape == (0, L)
+    ptr = tens(np.zeros(1, np.int32)); ids = tens(np.zeros(1, np.int32))
+    lay.train_step(h, ptr, ids, 1e-3)                     # no samples: zero gradients, Adam still steps
+    s1 = state_of(lay)
+    Wr, _, _ = oracle.adam(s0["W"], np.zeros((L, k)), s0["mW"], s0["vW"], 1, F32(1e-3), **ADAM)
+    assert_close(s1["W"], Wr, 0, "W' with B=0")
+    assert s1["t"] == 1
+    empty = make(0, m, k, B=8, L_global=10, row_begin=10, L_local=0)
+    hb = tens(synth.hidden_batch(3, m))
+    dh, _ = empty.train_step(hb, tens(np.array([0, 0, 0, 0], np.int32)), ids, 1e-3)
+    assert (dh == 0).all()
+
+
+def test_full_fan_in_is_dense():
+    L, m, B = 40, 16, 8
+    lay = make(L, m, m, B=B)
+    rng = np.random.default_rng(0)
+    idx = np.stack([rng.permutation(m) for _ in range(L)]).astype(np.int32)
+    Wd = rng.standard_normal((m, L)).astype(np.float32)
+    W = np.take_along_axis(Wd.T, idx, axis=1)
+    lay.set_params(W=tens(np.ascontiguousarray(W)), idx=tens(idx), bias=tens(np.zeros(L, np.float32)))
+    h = synth.hidden_batch(B, m)
+    y = lay.forward(tens(h)).cpu().numpy()
+    ref = h.astype(np.float64) @ Wd.astype(np.float64)
+    assert np.abs(y - ref).max() <= 1e-4 * np.abs(h).sum(1).max() * np.abs(Wd).max()
+
+
+def test_host_entry_point_equals_device_entry_point():
+    L, m, k, B = 1000, 256, 16, 32
+    a, b = make(L, m, k, B=B, seed=4), make(L, m, k, B=B, seed=4)
+    h = synth.hidden_batch(B, m, step=2)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=2)
+    dh_host = torch.empty((B, m)).pin_memory(); loss_host = torch.empty(1).pin_memory()
+    a.train_step_host(torch.from_numpy(h).pin_memory(), torch.from_numpy(ptr), torch.from_numpy(ids), 1e-3,
+                      dh_host=dh_host, loss_host=loss_host)
+    loss = torch.zeros(1, device=dev())
+    dh, _ = b.train_step(tens(h), tens(ptr), tens(ids), 1e-3, loss=loss)
+    torch.cuda.synchronize()
+    assert torch.allclose(dh_host, dh.cpu(), rtol=1e-5, atol=1e-7)
+    assert abs(loss_host.item() - loss.item()) <= 1e-5 * loss.item()
+    sa, sb = state_of(a), state_of(b)
+    assert (sa["W"] == sb["W"]).all() and (sa["bias"] == sb["bias"]).all()
