@@ -46,6 +46,8 @@ def args_():
     p.add_argument("--shape", default="amazon-670k")
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dh-mode", default="csc", choices=["atomic", "csc"],
+                   help="dh scatter: red.global atomics or the CSC pull (DESIGN.md §6; chosen by measurement)")
     return p.parse_args()
 
 
@@ -188,8 +190,10 @@ def run_ours(a, shape, world, rank, local_rank):
     data = [(synth.hidden_batch(B, shape.m, step=s), *synth.label_batch(B, shape.L, shape.avg_pos, step=s))
             for s in range(N_BATCHES)]
     max_nnz = max(int(d[1][-1]) for d in data)
+    from paper_2306_03725_b200.layer import FF_DH_ATOMIC, FF_DH_CSC
+    dh_mode = FF_DH_CSC if a.dh_mode == "csc" else FF_DH_ATOMIC
     layer = ShardedLayer(shape.L, shape.m, shape.k, rank=rank, world=world, device=dev, max_batch=B,
-                         seed=synth.PARAM_SEED, max_nnz=max_nnz)
+                         seed=synth.PARAM_SEED, max_nnz=max_nnz, dh_mode=dh_mode)
     eng = layer.engine
     L_local = layer.row_end - layer.row_begin
     stream = torch.cuda.current_stream()
@@ -229,7 +233,7 @@ def run_ours(a, shape, world, rank, local_rank):
         step(s)
     barrier()
     launches = 0
-    eng.profile_begin(a.steps)
+    eng.profile_begin(a.steps * 16)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         barrier()
@@ -240,7 +244,8 @@ def run_ours(a, shape, world, rank, local_rank):
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     k_ms, k_n = eng.profile_end()
-    k_avg_ms = max_over_ranks(k_ms / max(k_n, 1))
+    k_step_ms = max_over_ranks(k_ms / a.steps)          # fused row kernel time per step (all its launches)
+    launches_per_step = k_n / a.steps
     gpu_launches = launches
 
     # ---- end to end through the public API with host buffers (H2D inputs, D2H loss)
@@ -296,11 +301,11 @@ def run_ours(a, shape, world, rank, local_rank):
         return
     peak, peak_src = peaks()
     samples_per_s = B * a.steps / (ms * 1e-3)
-    kb = alg_bytes_train_kernel(L_local, shape.k)
-    achieved = kb / (k_avg_ms * 1e-3) / 1e9
+    kb = alg_bytes_train_kernel(L_local, shape.k)        # per step = per launch x launches_per_step
+    achieved = kb / (k_step_ms * 1e-3) / 1e9
     nnz_mean = float(np.mean([len(d[2]) for d in data]))
     step_bytes = alg_bytes_step(shape.L, shape.k, B, shape.m, nnz_mean)
-    traffic = ncu_traffic(f"{shape.name}/train_kernel")
+    traffic = ncu_traffic(f"{shape.name}/{a.dh_mode}/train_kernel")
     onchip = 2 * 128 * L_local * shape.k * ((B + 31) // 32)   # hT line gathers + dhT line reductions
     pred_bytes = alg_bytes_predict(shape.L, shape.k, B, shape.m)
     c1, c2 = clk.summary(), clk2.summary()
@@ -310,7 +315,7 @@ def run_ours(a, shape, world, rank, local_rank):
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: h = ReLU(N(0,1)), Zipf(1.0) sparse labels, Philox-initialized W/idx (no dataset)",
         "config": {"workload": shape.name, "L": shape.L, "m": shape.m, "k": shape.k, "B": B, "global_batch": B,
-                   "avg_pos": shape.avg_pos, "parallelism": f"label-shard x{world}",
+                   "avg_pos": shape.avg_pos, "parallelism": f"label-shard x{world}", "dh_mode": a.dh_mode,
                    "redistribution": f"every {REDIST_EVERY} steps inside the timed region (global step counter)",
                    "l2": "no flush: per-step state stream 617 MB >> 126 MB L2 (inputs larger than L2)"},
         "clocks": {"sm_mhz": c1["sm_mhz"], "sm_max_mhz": c1["sm_max_mhz"], "reasons": c1["reasons"],
@@ -322,13 +327,16 @@ def run_ours(a, shape, world, rank, local_rank):
                 "path": "fixedfanin_train_step_host (C ABI, pinned host buffers)" if world == 1 else
                         "torch H2D + ShardedLayer.train_step + D2H loss", "clocks_sm_mhz": c2["sm_mhz"]},
         "gpu_launches": gpu_launches,
-        "roofline": {"bound": "hbm", "kernel": "k_rows<train> (fused fwd/BCE/dW/db/dh/Adam)", "achieved": achieved,
-                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "alg_bytes_per_launch": kb, "avg_launch_ms": k_avg_ms,
-                     "kernel_share_of_step": k_avg_ms / (ms / a.steps)},
-        "onchip": {"l2_bytes_per_launch": onchip, "l2_gbs": onchip / (k_avg_ms * 1e-3) / 1e9,
-                   "note": "hT 128-B line gathers + dhT 128-B red.v4 per connection; measured ceilings "
-                           "(profiles/r01_l2bench.txt): gather ~19.9 TB/s, red ~6.3-6.6 TB/s"},
+        "roofline": {"bound": "hbm", "kernel": "k_train_pipe (fused fwd/BCE/dW/db/dh-or-g/Adam row pass)",
+                     "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": kb / launches_per_step, "launches_per_step": launches_per_step,
+                     "avg_launch_ms": k_step_ms / launches_per_step,
+                     "kernel_share_of_step": k_step_ms / (ms / a.steps)},
+        "onchip": {"l2_bytes_per_step": onchip, "l2_gbs": onchip / (ms / a.steps * 1e-3) / 1e9,
+                   "note": ("h 128-B line gather + dh 128-B red.v4 per connection" if a.dh_mode == "atomic" else
+                            "h 128-B line gather (row pass) + g 128-B line gather (CSC column pass) per connection")
+                           + "; measured ceilings (profiles/r01_l2bench.txt): gather ~19.9 TB/s, red ~6.3-6.6 TB/s"},
         "predict": {"value": B * n_pred / (ms_pred * 1e-3), "unit": "samples/s", "K": K,
                     "ms_per_batch": ms_pred / n_pred,
                     "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,

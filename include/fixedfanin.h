@@ -68,6 +68,8 @@ typedef enum {
 /* ff_config.flags */
 #define FF_FLAG_CHECK_FINITE 1u  /* raise FF_ERR_NONFINITE on a non-finite score/gradient     */
 #define FF_FLAG_STORE_GRADS 2u   /* fused train_step also stores dW/db (for get_grads/tests)  */
+#define FF_FLAG_NO_PIPE 4u       /* use the generic fused kernel even where the pipelined one
+                                    applies (k = 32, B <= 32); same results, for A/B tests     */
 
 /* ff_config.dh_mode */
 #define FF_DH_ATOMIC 0           /* dh by coalesced red.global.add (Alg. 2 with atomics) */
@@ -179,8 +181,9 @@ ff_status fixedfanin_merge_topk(const float* in_scores, const int32_t* in_ids, i
 ff_status fixedfanin_check(ff_layer* layer, ff_stream_t stream);
 
 /* Kernel timing for benchmarks: between profile_begin and profile_end every train_step
- * (and train_step_host) records a CUDA event pair around its fused row kernel on the
- * call's stream (at most max_launches pairs).  profile_end synchronizes on the last event
+ * (and train_step_host, backward) records a CUDA event pair around each launch of its
+ * fused row kernel on the call's stream (one launch per step, or one per label tile in
+ * FF_DH_CSC mode; at most max_launches pairs).  profile_end synchronizes on the last event
  * and returns the summed kernel milliseconds and the number of timed launches.        */
 ff_status fixedfanin_profile_begin(ff_layer* layer, int32_t max_launches);
 ff_status fixedfanin_profile_end(ff_layer* layer, double* kernel_ms_host, int32_t* launches_host);

@@ -59,6 +59,30 @@ __device__ __forceinline__ int ld_stream_ro(const int* a, uint64_t pol) {
 __device__ __forceinline__ void st_stream(float* a, float v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(a), "f"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void st_hint(float* a, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(a), "f"(v), "l"(pol) : "memory");
+}
+// Plain (no L2 policy operand) variants for the hot loops: every `.L2::cache_hint` access
+// costs two R2UR moves of the policy into a fresh uniform descriptor pair in SASS.
+__device__ __forceinline__ float ld_na(const float* a) {
+  float v; asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(a)); return v;
+}
+__device__ __forceinline__ int ld_na_ro(const int* a) {
+  int v; asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(a)); return v;
+}
+__device__ __forceinline__ void st_na(float* a, float v) {
+  asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" :: "l"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ float4 ld_line4_plain(const float* a) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a));
+  return v;
+}
+__device__ __forceinline__ void red_add4_plain(float* a, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
 // one 16-B segment of an hT line (4 samples), L2-resident
 __device__ __forceinline__ float4 ld_line4(const float* a, uint64_t pol) {
   float4 v;
@@ -71,6 +95,27 @@ __device__ __forceinline__ void red_add4(float* a, float4 v, uint64_t pol) {
   asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
                :: "l"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
 }
+
+// ---------------------------------------------------------------- packed fp32x2 (sm_100)
+// fma.rn.f32x2 / mul.rn.f32x2: two independent IEEE fp32 FMAs/MULs per instruction (FFMA2);
+// each half rounds exactly like the scalar op.  A scalar operand broadcast into both halves
+// folds into the instruction (no packing moves).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 a, b, c, d; mov.b64 a, {%2,%3}; mov.b64 b, {%4,%5}; mov.b64 c, {%6,%7};"
+      " fma.rn.f32x2 d, a, b, c; mov.b64 {%0,%1}, d;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d; mov.b64 a, {%2,%3}; mov.b64 b, {%4,%5}; mul.rn.f32x2 d, a, b; mov.b64 {%0,%1}, d;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
 
 // ---------------------------------------------------------------- warp helpers
 __device__ __forceinline__ float warp_sum(float v) {
@@ -110,7 +155,9 @@ __device__ __forceinline__ void adam_update(float& p, float& mo, float& ve, floa
   ve = __fadd_rn(__fmul_rn(a.beta2, ve), __fmul_rn(a.one_minus_b2, __fmul_rn(q, q)));
   const float mhat = __fmul_rn(mo, a.rbc1);
   const float vhat = __fmul_rn(ve, a.rbc2);
-  p = __fsub_rn(p, __fdividef(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
+  float sq;                                  // MUFU.SQRT, rel. error ~2^-23 (sqrt(0) = 0)
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(vhat));
+  p = __fsub_rn(p, __fdividef(__fmul_rn(a.lr, mhat), __fadd_rn(sq, a.eps)));
 }
 
 }  // namespace ff

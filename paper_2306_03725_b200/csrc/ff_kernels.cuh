@@ -37,6 +37,10 @@ struct RowArgs {
   float* dW; float* db;
   uint32_t* posmask;          // [nb][L] bit (b & 31) of word [b>>5][j]: is row_begin+j a positive of b
   float* hd;                  // [m][nb][64]: h line | dh line per column and 32-sample chunk
+  const int* pos;             // CSC mode: CSC position of connection e = j*k + i
+  float* wcsc;                // CSC mode: pre-update W in CSC order
+  float* gT;                  // CSC mode: g[j - j_begin][nb][32] (per-label gradient lines of the tile)
+  int64_t j_begin, j_end;     // label rows processed by this launch (a tile; multiple of 32)
   int64_t L; int k; int B; int nb; int cstride;   // cstride = 64*nb floats per column
   float grad_scale;
   float* y_out;               // forward: y[B][L]
@@ -68,38 +72,58 @@ __device__ __forceinline__ void block_atomic_add(float v, float* dst) {
 // ---- shared pieces of the row kernels (forward / fused step / predict use the SAME
 // arithmetic, so their scores are bit-identical: the top-K parity relies on it)
 
-// Broadcast each connection's weight and hd column offset to the lanes that gather it:
-// lane (gq, bq) handles connections s = 4q + gq, q < NG.
+// Broadcast each connection's weight and hd column BYTE offset to the lanes that gather
+// it: lane (gq, bq) handles connections s = 4q + gq, q < NG.  cbytes = 4*cstride.
 template <int NG>
-__device__ __forceinline__ void row_spread(float w, int c, int cstride, int gq, float (&ws)[NG], uint32_t (&cs)[NG]) {
+__device__ __forceinline__ void row_spread(float w, int c, uint32_t cbytes, int gq, float (&ws)[NG], uint32_t (&cs)[NG]) {
 #pragma unroll
   for (int q = 0; q < NG; ++q) {
     ws[q] = __shfl_sync(kFull, w, 4 * q + gq);
-    cs[q] = (uint32_t)__shfl_sync(kFull, c, 4 * q + gq) * (uint32_t)cstride;
+    cs[q] = (uint32_t)__shfl_sync(kFull, c, 4 * q + gq) * cbytes;
   }
 }
 
-// Gather the 16-B segment [lo, lo+4) of each connection's 128-B h line of chunk `base`.
-template <int NG>
+__device__ __forceinline__ const float* at_bytes(const float* base, uint32_t off) {
+  return reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + off);
+}
+__device__ __forceinline__ float* at_bytes(float* base, uint32_t off) {
+  return reinterpret_cast<float*>(reinterpret_cast<char*>(base) + off);
+}
+
+// Gather this lane's 16-B segment of each connection's 128-B h line (hb = the lane's
+// segment in column 0 of the chunk).  FULL: k == 4*NG, every slot exists (no guards).
+template <int NG, bool FULL>
 __device__ __forceinline__ void row_gather(const float* hb, const uint32_t (&cs)[NG], int k, int gq,
                                            uint64_t pol, float4 (&hv)[NG]) {
 #pragma unroll
   for (int q = 0; q < NG; ++q) {
-    hv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * q + gq < k) hv[q] = ld_line4(hb + cs[q], pol);
+    if (FULL) {
+      hv[q] = ld_line4(at_bytes(hb, cs[q]), pol);
+    } else {
+      hv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (4 * q + gq < k) hv[q] = ld_line4(at_bytes(hb, cs[q]), pol);
+    }
   }
+}
+
+// The same gather without the L2 policy operand (hot loop of the pipelined kernel).
+template <int NG>
+__device__ __forceinline__ void row_gather_plain(const float* hb, const uint32_t (&cs)[NG], float4 (&hv)[NG]) {
+#pragma unroll
+  for (int q = 0; q < NG; ++q) hv[q] = ld_line4_plain(at_bytes(hb, cs[q]));
 }
 
 // y for this lane's own sample lo + gq: per-lane FMAs over its connections, then a
 // reduce-scatter over the four connection groups (xor 16, xor 8), + bias.
 template <int NG>
 __device__ __forceinline__ float row_score_own(const float (&ws)[NG], const float4 (&hv)[NG], int gq, float bj) {
-  float4 yp = make_float4(0.f, 0.f, 0.f, 0.f);
+  float2 y01 = make_float2(0.f, 0.f), y23 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int q = 0; q < NG; ++q) {
-    yp.x = fmaf(ws[q], hv[q].x, yp.x); yp.y = fmaf(ws[q], hv[q].y, yp.y);
-    yp.z = fmaf(ws[q], hv[q].z, yp.z); yp.w = fmaf(ws[q], hv[q].w, yp.w);
+  for (int q = 0; q < NG; ++q) {                     // packed: same per-component FMA order
+    y01 = ffma2(bc2(ws[q]), lo2(hv[q]), y01);
+    y23 = ffma2(bc2(ws[q]), hi2(hv[q]), y23);
   }
+  const float4 yp = make_float4(y01.x, y01.y, y23.x, y23.y);
   const bool hi = gq & 2, odd = gq & 1;
   const float k0 = hi ? yp.z : yp.x, k1 = hi ? yp.w : yp.y;
   const float s0 = hi ? yp.x : yp.z, s1 = hi ? yp.y : yp.w;
@@ -107,6 +131,19 @@ __device__ __forceinline__ float row_score_own(const float (&ws)[NG], const floa
   const float a1 = k1 + __shfl_xor_sync(kFull, s1, 16);
   const float keep = odd ? a1 : a0, send = odd ? a0 : a1;
   return (keep + __shfl_xor_sync(kFull, send, 8)) + bj;
+}
+
+// Partial dW of connection q over this lane's 4 samples: (g0 h0 + g2 h2) + (g1 h1 + g3 h3)
+// (two packed FMAs and one add); shared by every kernel so their dW are bit-identical.
+__device__ __forceinline__ float dw_partial(const float4& g4, const float4& hv) {
+  float2 t = ffma2(lo2(g4), lo2(hv), make_float2(0.f, 0.f));
+  t = ffma2(hi2(g4), hi2(hv), t);
+  return t.x + t.y;
+}
+// W[j][i] * g[b][j] for this lane's 4 samples (the Alg. 2 contributions of one connection).
+__device__ __forceinline__ float4 dh_contrib(float w, const float4& g4) {
+  const float2 a = fmul2(bc2(w), lo2(g4)), b = fmul2(bc2(w), hi2(g4));
+  return make_float4(a.x, a.y, b.x, b.y);
 }
 
 // Reduce dwp[q] (partial dW of slot 4q+gq over this lane's 4 samples) over the 8 lanes of
@@ -153,32 +190,35 @@ __device__ __forceinline__ float row_dw_slot(const float (&dwp)[NG], int lane) {
 // blocks) and walks their rows one at a time, prefetching the next row's state.  Per-label
 // scalars (bias, its moments, the positive mask) are one coalesced vector per block
 // (lane i <-> row i) and the bias Adam update runs once per block, vectorized.
-template <int MODE, bool STORE_GRADS, int NG>
+template <int MODE, bool STORE_GRADS, int NG, bool CSC, bool FULL>
 __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) {
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol_s = policy_evict_first(), pol_l = policy_evict_last();
-  const int k = a.k, cstride = a.cstride, nb = a.nb, B = a.B;
-  const int64_t L = a.L, nblk = (L + 31) >> 5;
+  const int k = FULL ? 4 * NG : a.k, nb = a.nb, B = a.B;
+  const uint32_t cbytes = 4u * (uint32_t)a.cstride;
+  float* const hd_lane = a.hd + 4 * bq;            // this lane's segment, column 0, chunk 0
+  const int64_t L = a.L, jb = a.j_begin, nblk = (a.j_end - jb + 31) >> 5;
   const bool act = lane < k;
   float loss_acc = 0.0f;
 
   float w_n = 0.f, mw_n = 0.f, vw_n = 0.f;
-  int c_n = 0;
+  int c_n = 0, p_n = 0;
   auto prefetch_row = [&](int64_t jj) {
     const int64_t row = jj * k;
     if (act) {
       w_n = ld_stream(a.W + row + lane, pol_s);
       c_n = ld_stream_ro(a.idx + row + lane, pol_s);
+      if (CSC && MODE != kModeForward) p_n = ld_stream_ro(a.pos + row + lane, pol_s);
       if (MODE == kModeTrain) { mw_n = ld_stream(a.mW + row + lane, pol_s); vw_n = ld_stream(a.vW + row + lane, pol_s); }
     }
   };
   int64_t blk = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
-  if (blk < nblk) prefetch_row(blk * 32);
+  if (blk < nblk) prefetch_row(jb + blk * 32);
 
   for (; blk < nblk; blk += nw) {
-    const int64_t j0 = blk * 32;
-    const int nl = (int)min((int64_t)32, L - j0);
+    const int64_t j0 = jb + blk * 32;
+    const int nl = (int)min((int64_t)32, a.j_end - j0);
     const bool lv = lane < nl;                  // lane i <-> row j0 + i for the block vectors
     float bias_v = 0.f, mb_v = 0.f, vb_v = 0.f, db_v = 0.f;
     uint32_t pm_v = 0u;
@@ -190,15 +230,15 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
     for (int i = 0; i < nl; ++i) {
       const int64_t j = j0 + i;
       float w = w_n, mw = mw_n, vw = vw_n;
-      const int c = c_n;
+      const int c = c_n, pe = p_n;
       if (i + 1 < nl) prefetch_row(j + 1);
-      else if (blk + nw < nblk) prefetch_row((blk + nw) * 32);
+      else if (blk + nw < nblk) prefetch_row(jb + (blk + nw) * 32);
       const int64_t row = j * k;
       const float bj = __shfl_sync(kFull, bias_v, i);
       uint32_t pm = __shfl_sync(kFull, pm_v, i);
 
       float ws[NG]; uint32_t cs[NG];
-      row_spread<NG>(w, c, cstride, gq, ws, cs);
+      row_spread<NG>(w, c, cbytes, gq, ws, cs);
       float dwp[NG];
 #pragma unroll
       for (int q = 0; q < NG; ++q) dwp[q] = 0.0f;
@@ -207,9 +247,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
       for (int q2 = 0; q2 < nb; ++q2) {
         const int lo = q2 * 32 + 4 * bq;             // this lane's 4-sample segment
         const int b = lo + gq;                        // this lane's own sample
-        float* hb = a.hd + q2 * 64 + 4 * bq;          // h segment; its dh segment is +32 floats
+        float* hb = hd_lane + q2 * 64;                // h segment; its dh segment is +32 floats
         float4 hv[NG];
-        row_gather<NG>(hb, cs, k, gq, pol_l, hv);
+        row_gather<NG, FULL>(hb, cs, k, gq, pol_l, hv);
         float y;
         if (MODE != kModeBackward) {
           y = row_score_own<NG>(ws, hv, gq, bj);
@@ -237,21 +277,22 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
         g4.z = __shfl_sync(kFull, g, (2 << 3) | bq);
         g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
 #pragma unroll
-        for (int q = 0; q < NG; ++q) {
-          float t = dwp[q];
-          t = fmaf(g4.x, hv[q].x, t); t = fmaf(g4.y, hv[q].y, t);
-          t = fmaf(g4.z, hv[q].z, t); t = fmaf(g4.w, hv[q].w, t);
-          dwp[q] = t;
-        }
-        // Alg. 2 with the pre-update weights: dh[b][idx[j][i]] += W[j][i] g[b][j]
+        for (int q = 0; q < NG; ++q) dwp[q] += dw_partial(g4, hv[q]);
+        if (CSC) {
+          // CSC mode: publish g[., j] (one 128-B line per chunk); dh is pulled later (k_dh_csc)
+          st_hint(a.gT + ((j - jb) * nb + q2) * 32 + 4 * bq + gq, g, pol_l);
+        } else {
+          // Alg. 2 with the pre-update weights: dh[b][idx[j][i]] += W[j][i] g[b][j]
 #pragma unroll
-        for (int q = 0; q < NG; ++q) {
-          if (4 * q + gq < k)
-            red_add4(hb + cs[q] + 32, make_float4(ws[q] * g4.x, ws[q] * g4.y, ws[q] * g4.z, ws[q] * g4.w), pol_l);
+          for (int q = 0; q < NG; ++q) {
+            if (FULL || 4 * q + gq < k)
+              red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
+          }
         }
       }
       if (MODE == kModeForward) continue;
 
+      if (CSC && act) a.wcsc[pe] = w;                 // pre-update W in CSC order (for k_dh_csc)
       const float gW = row_dw_slot<NG>(dwp, lane);
       const float db = warp_sum(dbp);
       if (lane == i) db_v = db;
@@ -278,6 +319,424 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
     }
   }
   if (MODE != kModeForward && a.loss != nullptr) block_atomic_add(loss_acc * a.grad_scale, a.loss);
+}
+
+// ------------------------------------------------------------------ pipelined train step
+// The fused training step of k_rows<train> for the hot configuration (k = 32 connections,
+// B <= 32 samples), software-pipelined for memory-level parallelism: while row X is being
+// computed, the 32 h-line gathers of row X+1 are already in flight (two register buffers
+// A/B, alternating) and the state of row X+2 is being loaded.  Same arithmetic (the shared
+// row_* helpers, same order) as k_rows, so results are bit-identical to the generic kernel.
+#ifndef FF_PIPE_THREADS
+#define FF_PIPE_THREADS 128
+#endif
+#ifndef FF_PIPE_MINB
+#define FF_PIPE_MINB 3
+#endif
+constexpr int kPipeThreads = FF_PIPE_THREADS;
+constexpr int kPipeMinBlocks = FF_PIPE_MINB;
+
+struct PipeCursor {             // position of one row in this warp's sequence of rows
+  int64_t blk;                  // 32-row block index within [j_begin, j_end)
+  int i;                        // row within the block
+};
+
+template <bool STORE_GRADS, bool CSC>
+__global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(RowArgs a) {
+  constexpr int NG = 8;
+  constexpr uint32_t kColBytes = 256;                   // hd column stride at nb = 1 (h | dh lines)
+  const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
+  const int nwarp = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const uint64_t pol_l = policy_evict_last();
+  const int B = a.B;
+  float* const hb = a.hd + 4 * bq;
+  float* const W = a.W; float* const mW = a.mW; float* const vW = a.vW;
+  const int* const idx = a.idx; const int* const pos = a.pos;
+  const float grad_scale = a.grad_scale;
+  const bool want_loss = a.loss != nullptr, check = a.check_finite != 0;
+  const AdamArgs adam = a.adam;
+  const int64_t jb = a.j_begin, je = a.j_end;
+  const int nblk = (int)((je - jb + 31) >> 5);
+  const int b = 4 * bq + gq;                            // this lane's own sample
+  const bool bvalid = b < B;
+  float loss_acc = 0.0f;
+
+  // this warp's rows: blocks w, w + nwarp, ...; cursor = (block, row in block, rows in block)
+  struct Cur { int blk, i, nl; };
+  auto nl_of = [&](int blk) { return (int)min((int64_t)32, je - (jb + (int64_t)blk * 32)); };
+  auto adv = [&](Cur c) {
+    if (++c.i >= c.nl) { c.blk += nwarp; c.i = 0; c.nl = c.blk < nblk ? nl_of(c.blk) : 0; }
+    return c;
+  };
+  auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * 32 + c.i; };
+
+  struct St { float w, mw, vw; int c, pe; };
+  auto load_st = [&](const Cur& cu, St& st) {
+    if (cu.blk < nblk) {
+      const int64_t row = row_of(cu) * 32 + lane;
+      st.w = ld_na(W + row);
+      st.c = ld_na_ro(idx + row);
+      st.mw = ld_na(mW + row);
+      st.vw = ld_na(vW + row);
+      if (CSC) st.pe = ld_na_ro(pos + row);
+    }
+  };
+  struct Bv { float bias, mb, vb; uint32_t pm; };
+  auto load_bv = [&](int blk, Bv& v) {
+    v.bias = v.mb = v.vb = 0.0f; v.pm = 0u;
+    if (blk < nblk && lane < nl_of(blk)) {
+      const int64_t j = jb + (int64_t)blk * 32 + lane;
+      v.bias = ld_na(a.bias + j); v.mb = ld_na(a.mb + j); v.vb = ld_na(a.vb + j); v.pm = a.posmask[j];
+    }
+  };
+
+  Cur X{(int)((((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5), 0, 0};
+  if (X.blk < nblk) {                                   // (no early return: block_atomic_add syncs)
+  X.nl = nl_of(X.blk);
+  Cur Y = adv(X), Z = adv(Y);
+  St sX{}, sY{}, sZ{};
+  Bv bv{}, bv_next{};
+  float db_v = 0.0f;
+  load_st(X, sX);
+  load_st(Y, sY);
+  load_bv(X.blk, bv);
+
+  float wsA[NG], wsB[NG]; uint32_t csA[NG], csB[NG]; float4 hvA[NG], hvB[NG];
+  auto issue = [&](const St& st, float (&ws)[NG], uint32_t (&cs)[NG], float4 (&hv)[NG]) {
+    row_spread<NG>(st.w, st.c, kColBytes, gq, ws, cs);
+    // atomic mode: keep hd (h and dh lines) evict_last against the state stream, else plain
+    if (CSC) row_gather_plain<NG>(hb, cs, hv);
+    else row_gather<NG, true>(hb, cs, 32, gq, pol_l, hv);
+  };
+  issue(sX, wsA, csA, hvA);
+  load_st(Z, sZ);
+
+  auto compute = [&](const Cur& cu, St& st, const float (&ws)[NG], const uint32_t (&cs)[NG],
+                     const float4 (&hv)[NG]) {
+    const int64_t j = row_of(cu);
+    const int i = cu.i;
+    const float bj = __shfl_sync(kFull, bv.bias, i);
+    const uint32_t pm = __shfl_sync(kFull, bv.pm, i);
+    const float y = row_score_own<NG>(ws, hv, gq, bj);
+    const bool pos_ = (pm >> b) & 1u;
+    float e;
+    float g = bce_grad(y, pos_, grad_scale, &e);
+    if (!bvalid) g = 0.0f;
+    if (want_loss && bvalid) loss_acc += bce_loss_term(y, pos_, e);
+    if (check && __any_sync(kFull, bvalid && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
+    float4 g4;
+    g4.x = __shfl_sync(kFull, g, (0 << 3) | bq);
+    g4.y = __shfl_sync(kFull, g, (1 << 3) | bq);
+    g4.z = __shfl_sync(kFull, g, (2 << 3) | bq);
+    g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
+    float dwp[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) dwp[q] = 0.0f + dw_partial(g4, hv[q]);
+    if (CSC) {
+      st_hint(a.gT + (j - jb) * 32 + b, g, pol_l);
+      a.wcsc[st.pe] = st.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < NG; ++q)
+        red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
+    }
+    const float gW = row_dw_slot<NG>(dwp, lane);
+    const float db = warp_sum(g);
+    if (lane == i) db_v = db;
+    const int64_t row = j * 32 + lane;
+    if (STORE_GRADS) a.dW[row] = gW;
+    adam_update(st.w, st.mw, st.vw, gW, adam);
+    st_na(W + row, st.w);
+    st_na(mW + row, st.mw);
+    st_na(vW + row, st.vw);
+    if (i == cu.nl - 1) {                                // block done: vectorized bias update
+      const int64_t jl = jb + (int64_t)cu.blk * 32 + lane;
+      if (lane <= i) {
+        if (bv.pm != 0u) a.posmask[jl] = 0u;
+        if (STORE_GRADS) a.db[jl] = db_v;
+        float p = bv.bias, mo = bv.mb, ve = bv.vb;
+        adam_update(p, mo, ve, db_v, adam);
+        st_na(a.bias + jl, p);
+        st_na(a.mb + jl, mo);
+        st_na(a.vb + jl, ve);
+      }
+      db_v = 0.0f;
+    }
+  };
+
+  // one pipeline step: issue Y's gathers into the free buffer, load the state of Z's
+  // successor, compute X; then X <- Y <- Z <- adv(Z).  Written twice so the A/B buffers
+  // swap roles without register moves.
+  auto step = [&](float (&wsC)[NG], uint32_t (&csC)[NG], float4 (&hvC)[NG],
+                  float (&wsN)[NG], uint32_t (&csN)[NG], float4 (&hvN)[NG]) -> bool {
+    if (Y.blk < nblk) {
+      issue(sY, wsN, csN, hvN);
+      if (Y.i == 0) load_bv(Y.blk, bv_next);
+    }
+    const Cur Zn = adv(Z);
+    St sZn{};
+    load_st(Zn, sZn);
+    compute(X, sX, wsC, csC, hvC);
+    X = Y; Y = Z; Z = Zn;
+    sX = sY; sY = sZ; sZ = sZn;
+    if (X.blk < nblk && X.i == 0) bv = bv_next;
+    return X.blk < nblk;
+  };
+  while (true) {
+    if (!step(wsA, csA, hvA, wsB, csB, hvB)) break;
+    if (!step(wsB, csB, hvB, wsA, csA, hvA)) break;
+  }
+  }
+  if (a.loss != nullptr) block_atomic_add(loss_acc * a.grad_scale, a.loss);
+}
+
+// Variant of k_train_pipe that keeps a single register buffer: the next row's h lines are
+// pulled into L1 with prefetch.global.L1 (no destination registers) and loaded from L1 when
+// the row is computed.  Fewer registers -> more resident warps; same arithmetic.
+__device__ __forceinline__ void prefetch_l1(const void* a) {
+  asm volatile("prefetch.global.L1 [%0];" :: "l"(a));
+}
+__device__ __forceinline__ float4 ld_line4_l1(const float* a) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a));
+  return v;
+}
+
+#ifndef FF_PF_THREADS
+#define FF_PF_THREADS 128
+#endif
+#ifndef FF_PF_MINB
+#define FF_PF_MINB 4
+#endif
+constexpr int kPfThreads = FF_PF_THREADS;
+constexpr int kPfMinBlocks = FF_PF_MINB;
+
+template <bool STORE_GRADS, bool CSC>
+__global__ void __launch_bounds__(kPfThreads, kPfMinBlocks) k_train_l1pf(RowArgs a) {
+  constexpr int NG = 8;
+  constexpr uint32_t kColBytes = 256;
+  const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
+  const int nwarp = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const uint64_t pol_l = policy_evict_last();
+  const int B = a.B;
+  float* const hb = a.hd + 4 * bq;
+  float* const W = a.W; float* const mW = a.mW; float* const vW = a.vW;
+  const int* const idx = a.idx; const int* const pos = a.pos;
+  const float grad_scale = a.grad_scale;
+  const bool want_loss = a.loss != nullptr, check = a.check_finite != 0;
+  const int64_t jb = a.j_begin, je = a.j_end;
+  const int nblk = (int)((je - jb + 31) >> 5);
+  const int b = 4 * bq + gq;
+  const bool bvalid = b < B;
+  float loss_acc = 0.0f;
+
+  struct Cur { int blk, i, nl; };
+  auto nl_of = [&](int blk) { return (int)min((int64_t)32, je - (jb + (int64_t)blk * 32)); };
+  auto adv = [&](Cur c) {
+    if (++c.i >= c.nl) { c.blk += nwarp; c.i = 0; c.nl = c.blk < nblk ? nl_of(c.blk) : 0; }
+    return c;
+  };
+  auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * 32 + c.i; };
+  struct St { float w, mw, vw; int c, pe; };
+  auto load_st = [&](const Cur& cu, St& st) {
+    if (cu.blk < nblk) {
+      const int64_t row = row_of(cu) * 32 + lane;
+      st.w = ld_na(W + row); st.c = ld_na_ro(idx + row); st.mw = ld_na(mW + row); st.vw = ld_na(vW + row);
+      if (CSC) st.pe = ld_na_ro(pos + row);
+    }
+  };
+  struct Bv { float bias, mb, vb; uint32_t pm; };
+  auto load_bv = [&](int blk, Bv& v) {
+    v.bias = v.mb = v.vb = 0.0f; v.pm = 0u;
+    if (blk < nblk && lane < nl_of(blk)) {
+      const int64_t j = jb + (int64_t)blk * 32 + lane;
+      v.bias = ld_na(a.bias + j); v.mb = ld_na(a.mb + j); v.vb = ld_na(a.vb + j); v.pm = a.posmask[j];
+    }
+  };
+  auto prefetch_row_lines = [&](const St& st) {
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+      const uint32_t off = (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq) * kColBytes;
+      prefetch_l1(at_bytes(hb, off));
+    }
+  };
+
+  Cur X{(int)((((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5), 0, 0};
+  if (X.blk < nblk) {
+  X.nl = nl_of(X.blk);
+  Cur Y = adv(X), Z = adv(Y);
+  St sX{}, sY{}, sZ{};
+  Bv bv{}, bv_next{};
+  float db_v = 0.0f;
+  load_st(X, sX);
+  load_st(Y, sY);
+  load_bv(X.blk, bv);
+  prefetch_row_lines(sX);
+  load_st(Z, sZ);
+  while (true) {
+    if (Y.blk < nblk) {
+      prefetch_row_lines(sY);
+      if (Y.i == 0) load_bv(Y.blk, bv_next);
+    }
+    const Cur Zn = adv(Z);
+    St sZn{};
+    load_st(Zn, sZn);
+    {   // compute X
+      float ws[NG]; uint32_t cs[NG]; float4 hv[NG];
+      row_spread<NG>(sX.w, sX.c, kColBytes, gq, ws, cs);
+#pragma unroll
+      for (int q = 0; q < NG; ++q) hv[q] = ld_line4_l1(at_bytes(hb, cs[q]));
+      const int64_t j = row_of(X);
+      const int i = X.i;
+      const float bj = __shfl_sync(kFull, bv.bias, i);
+      const uint32_t pm = __shfl_sync(kFull, bv.pm, i);
+      const float y = row_score_own<NG>(ws, hv, gq, bj);
+      const bool pos_ = (pm >> b) & 1u;
+      float e;
+      float g = bce_grad(y, pos_, grad_scale, &e);
+      if (!bvalid) g = 0.0f;
+      if (want_loss && bvalid) loss_acc += bce_loss_term(y, pos_, e);
+      if (check && __any_sync(kFull, bvalid && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
+      float4 g4;
+      g4.x = __shfl_sync(kFull, g, (0 << 3) | bq);
+      g4.y = __shfl_sync(kFull, g, (1 << 3) | bq);
+      g4.z = __shfl_sync(kFull, g, (2 << 3) | bq);
+      g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
+      float dwp[NG];
+#pragma unroll
+      for (int q = 0; q < NG; ++q) dwp[q] = 0.0f + dw_partial(g4, hv[q]);
+      if (CSC) {
+        st_hint(a.gT + (j - jb) * 32 + b, g, pol_l);
+        a.wcsc[sX.pe] = sX.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < NG; ++q)
+          red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
+      }
+      const float gW = row_dw_slot<NG>(dwp, lane);
+      const float db = warp_sum(g);
+      if (lane == i) db_v = db;
+      const int64_t row = j * 32 + lane;
+      if (STORE_GRADS) a.dW[row] = gW;
+      float w = sX.w, mw = sX.mw, vw = sX.vw;
+      adam_update(w, mw, vw, gW, a.adam);
+      st_na(W + row, w); st_na(mW + row, mw); st_na(vW + row, vw);
+      if (i == X.nl - 1) {
+        const int64_t jl = jb + (int64_t)X.blk * 32 + lane;
+        if (lane <= i) {
+          if (bv.pm != 0u) a.posmask[jl] = 0u;
+          if (STORE_GRADS) a.db[jl] = db_v;
+          float p = bv.bias, mo = bv.mb, ve = bv.vb;
+          adam_update(p, mo, ve, db_v, a.adam);
+          st_na(a.bias + jl, p); st_na(a.mb + jl, mo); st_na(a.vb + jl, ve);
+        }
+        db_v = 0.0f;
+      }
+    }
+    X = Y; Y = Z; Z = Zn;
+    sX = sY; sY = sZ; sZ = sZn;
+    if (X.blk >= nblk) break;
+    if (X.i == 0) bv = bv_next;
+  }
+  }
+  if (a.loss != nullptr) block_atomic_add(loss_acc * a.grad_scale, a.loss);
+}
+
+// ---------------------------------------------------------------------- CSC dh pull
+// Alg. 2 as a gather over the transposed (CSC) index: for every column c,
+//   dh[b][c] = sum_{p in col c} wcsc[p] * g[b][ent_row[p]]
+// with entries in (label tile, column, row) order — deterministic, no atomics.  The
+// transposed index is split by label tile so that the gT lines a launch gathers were
+// written by the row launch just before it (L2-resident).  Tile t covers col_ptr segments
+// [t*m + c]; tile 0 writes the dh half of hd, later tiles accumulate into it.
+// Warp per column (grid-stride); lane (gq, bq) takes entry 4u + gq of each 32-entry batch
+// and samples 4bq..4bq+3 (one 16-B slice of the 128-B g line).
+template <bool NB1>
+__global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr, const int* __restrict__ ent_row,
+                                                const float* __restrict__ wcsc, const float* __restrict__ gT,
+                                                int m, int nb_rt, int tile, int64_t j_begin, float* __restrict__ hd) {
+  const int nb = NB1 ? 1 : nb_rt;
+  const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol_l = policy_evict_last();
+  const int* cp = col_ptr + (int64_t)tile * m;
+  const int jb = (int)j_begin;
+  const uint32_t gstride = 128u * (uint32_t)nb;              // bytes per gT row
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < m; c += nw) {
+    const int p0 = cp[c], p1 = cp[c + 1];
+    for (int q2 = 0; q2 < nb; ++q2) {
+      const float* gb = gT + q2 * 32 + 4 * bq;                // this lane's slice of chunk q2
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      auto batch = [&](int p, bool tail) {
+        const bool ok = !tail || p + lane < p1;
+        const int jr = ok ? ld_na_ro(ent_row + p + lane) : jb;
+        const float wv = ok ? ld_na(wcsc + p + lane) : 0.0f;
+        float4 gv[8]; float ww[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t off = (uint32_t)(__shfl_sync(kFull, jr, 4 * u + gq) - jb) * gstride;
+          ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
+          if (tail) {
+            gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p + 4 * u + gq < p1) gv[u] = ld_line4(at_bytes(gb, off), pol_l);
+          } else {
+            gv[u] = ld_line4(at_bytes(gb, off), pol_l);
+          }
+        }
+        float2 a01 = lo2(acc), a23 = hi2(acc);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a01 = ffma2(bc2(ww[u]), lo2(gv[u]), a01);
+          a23 = ffma2(bc2(ww[u]), hi2(gv[u]), a23);
+        }
+        acc = make_float4(a01.x, a01.y, a23.x, a23.y);
+      };
+      int p = p0;
+      for (; p + 32 <= p1; p += 32) batch(p, false);
+      if (p < p1) batch(p, true);
+#pragma unroll
+      for (int o = 8; o <= 16; o <<= 1) {
+        acc.x += __shfl_xor_sync(kFull, acc.x, o); acc.y += __shfl_xor_sync(kFull, acc.y, o);
+        acc.z += __shfl_xor_sync(kFull, acc.z, o); acc.w += __shfl_xor_sync(kFull, acc.w, o);
+      }
+      if (gq == 0) {
+        float4* dst = reinterpret_cast<float4*>(hd + (int64_t)c * 64 * nb + q2 * 64 + 32 + 4 * bq);
+        if (tile > 0) {
+          const float4 o = *dst;
+          acc = make_float4(o.x + acc.x, o.y + acc.y, o.z + acc.z, o.w + acc.w);
+        }
+        *dst = acc;
+      }
+    }
+  }
+}
+
+// CSC build step 1: key = tile(row) * m + column, value = connection id e (row-major), so a
+// stable radix sort by key yields entries in (tile, column, row) order.
+__global__ void k_csc_keys(const int* __restrict__ idx, int64_t n, int k, int m, int64_t tile_rows,
+                           int* __restrict__ keys, int* __restrict__ vals) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = (e / k) / tile_rows;
+    keys[e] = (int)(tile * m + idx[e]);
+    vals[e] = (int)e;
+  }
+}
+// CSC build step 2: ent_row[p] = row of the p-th entry, pos[e] = p; col_ptr over the key
+// space [0, nkeys] from the sorted keys (col_ptr[q] = first p with key >= q).
+__global__ void k_csc_finish(const int* __restrict__ skeys, const int* __restrict__ svals, int64_t n, int k,
+                             int nkeys, int* __restrict__ ent_row, int* __restrict__ pos, int* __restrict__ col_ptr) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int e = svals[p];
+    const int key = skeys[p];
+    const int prev = p > 0 ? skeys[p - 1] : -1;
+    ent_row[p] = e / k;
+    pos[e] = (int)p;
+    for (int c = prev + 1; c <= key; ++c) col_ptr[c] = (int)p;
+    if (p == n - 1)
+      for (int c = key + 1; c <= nkeys; ++c) col_ptr[c] = (int)n;
+  }
+  if (n == 0 && blockIdx.x == 0)
+    for (int c = threadIdx.x; c <= nkeys; c += blockDim.x) col_ptr[c] = 0;
 }
 
 // ------------------------------------------------------------------------------ prep
@@ -487,7 +946,7 @@ __device__ __forceinline__ void topk_insert(float (&ts)[kTopkMax], int (&ti)[kTo
 // Fused forward + per-lane running top-K (y is never written).  For each 32-sample chunk
 // q2 every lane owns sample q2*32 + 4*bq + gq; a block merges its warps' lists and writes
 // candidates cand[blk][ldh][kTopkMax].
-template <int NG>
+template <int NG, bool FULL>
 __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict__ W, const int* __restrict__ idx,
                                                          const float* __restrict__ bias, const float* __restrict__ hd,
                                                          int64_t L, int k, int B, int nb, int64_t row_begin,
@@ -501,7 +960,7 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
   for (int q2 = 0; q2 < nb; ++q2) {
     const int lo = q2 * 32 + 4 * bq;
     const int b = lo + gq;
-    const int cstride = 64 * nb;
+    const uint32_t cbytes = 256u * (uint32_t)nb;
     const float* hb = hd + q2 * 64 + 4 * bq;
     float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll
@@ -520,8 +979,8 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
         bj_n = ld_stream(bias + jn, pol_s);
       }
       float ws[NG]; uint32_t cs[NG]; float4 hv[NG];
-      row_spread<NG>(w, c, cstride, gq, ws, cs);
-      row_gather<NG>(hb, cs, k, gq, pol_l, hv);
+      row_spread<NG>(w, c, cbytes, gq, ws, cs);
+      row_gather<NG, FULL>(hb, cs, k, gq, pol_l, hv);
       const float y = row_score_own<NG>(ws, hv, gq, bj);
       if (b < B) topk_insert(ts, ti, y, (int)(row_begin + j));
     }

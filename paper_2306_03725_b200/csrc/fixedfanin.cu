@@ -4,6 +4,8 @@
 #include "fixedfanin.h"
 #include "ff_kernels.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -51,10 +53,21 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {   // byte offsets into the workspace
   size_t W, idx, mW, vW, dW, bias, mb, vb, db, posmask, hd, cand_s, cand_i,
-      h_stage, lbl_stage, dh_stage, scalars, total;
+      h_stage, lbl_stage, dh_stage, scalars,
+      ent_row, pos, wcsc, gT, col_ptr, sort_keys, sort_tmp, sort_tmp_bytes,   // CSC mode only
+      total;
 };
 
 int nb_of(int B) { return (B + 31) / 32; }
+
+// CSC mode label tile: the g lines of one tile (tile_rows * 128 B * nb) stay L2-resident
+// between the row launch that writes them and the column launch that gathers them.
+constexpr size_t kCscTileBytes = size_t(32) << 20;
+size_t csc_tile_cap(const ff_config& c) {
+  const size_t nbm = (size_t)nb_of(c.max_batch);
+  const size_t cap = kCscTileBytes / (128 * nbm) / 32 * 32;
+  return std::max<size_t>(std::min<size_t>(cap, ((size_t)c.L_local + 31) / 32 * 32), 32);
+}
 
 Layout layout_of(const ff_config& c) {
   Layout o{};
@@ -73,6 +86,15 @@ Layout layout_of(const ff_config& c) {
   o.lbl_stage = take(4 * ((size_t)c.max_batch + 1 + nnz));
   o.dh_stage = take(4 * (size_t)c.max_batch * m);
   o.scalars = take(kAlign);       // [0] int err, [1] float loss
+  if (c.dh_mode == FF_DH_CSC) {
+    o.ent_row = take(4 * Lk); o.pos = take(4 * Lk); o.wcsc = take(4 * Lk); o.sort_keys = take(4 * Lk);
+    // tiles are >= cap/2 rows (create rounds the cap down to whole row-kernel waves, or keeps it)
+    const size_t lt = csc_tile_cap(c), ntile = (2 * L + lt - 1) / lt + 1;
+    o.gT = take(4 * lt * ldh);      // g lines of one label tile
+    o.col_ptr = take(4 * (std::max<size_t>(ntile, 1) * m + 1));
+    o.sort_tmp_bytes = (size_t(8) << 20) + 2 * Lk;
+    o.sort_tmp = take(o.sort_tmp_bytes);
+  }
   o.total = off;
   return o;
 }
@@ -92,8 +114,10 @@ ff_status validate(const ff_config* c) {
   if (c->max_topk < 1 || c->max_topk > FF_MAX_TOPK)
     return fail(FF_ERR_CONFIG, "max_topk=%d outside [1, %d]", c->max_topk, FF_MAX_TOPK);
   if (c->max_nnz < 0) return fail(FF_ERR_CONFIG, "max_nnz < 0");
-  if (c->dh_mode != FF_DH_ATOMIC)
-    return fail(FF_ERR_CONFIG, "dh_mode=%d not supported by this build (only FF_DH_ATOMIC)", c->dh_mode);
+  if (c->dh_mode != FF_DH_ATOMIC && c->dh_mode != FF_DH_CSC)
+    return fail(FF_ERR_CONFIG, "dh_mode=%d is neither FF_DH_ATOMIC nor FF_DH_CSC", c->dh_mode);
+  if (c->dh_mode == FF_DH_CSC && c->L_local * (int64_t)c->k >= (int64_t(1) << 31))
+    return fail(FF_ERR_CONFIG, "CSC mode needs L_local*k < 2^31");
   if (c->prune_frac < 0.0f || c->prune_frac >= 1.0f) return fail(FF_ERR_CONFIG, "prune_frac outside [0, 1)");
   if (c->beta1 < 0.0f || c->beta1 >= 1.0f || c->beta2 < 0.0f || c->beta2 >= 1.0f || c->eps < 0.0f)
     return fail(FF_ERR_CONFIG, "Adam hyper-parameters out of range");
@@ -119,11 +143,19 @@ struct ff_layer {
   char* ws;
   float *W, *mW, *vW, *dW, *bias, *mb, *vb, *db, *hd, *cand_s, *h_stage, *dh_stage;
   int *idx, *cand_i, *lbl_stage, *err;
+  int *ent_row, *pos, *col_ptr;     // CSC mode
+  float *wcsc, *gT;
+  int* sort_keys;
+  void* sort_tmp;
+  bool csc;
+  int grid_csc;
+  int64_t tile_rows;                // CSC mode: labels per tile (multiple of 32)
+  int ntiles;
   float* loss_scratch;
   uint32_t* posmask;
   int64_t t;
   bool grads_valid;
-  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows;
+  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_pipe;
   int nsm;
   std::vector<cudaEvent_t> prof_ev;   // pairs (before, after) of the fused row kernel
   int prof_used = 0;
@@ -171,23 +203,49 @@ RowArgs row_args(ff_layer* l, int B) {
   a.dW = l->dW; a.db = l->db; a.posmask = l->posmask; a.hd = l->hd;
   a.L = l->cfg.L_local; a.k = l->cfg.k; a.B = B; a.nb = nb_of(B); a.cstride = 64 * a.nb;
   a.err = l->err;
+  a.pos = l->pos; a.wcsc = l->wcsc; a.gT = l->gT;
+  a.j_begin = 0; a.j_end = l->cfg.L_local;
   a.check_finite = (l->cfg.flags & FF_FLAG_CHECK_FINITE) ? 1u : 0u;
   return a;
 }
 
 // Row kernels are specialized on NG = number of 4-connection groups a lane walks:
 // 4 for k <= 16, 8 for k <= 32.
+// FULL variants (k == 16 or k == 32: every slot of every group exists) drop the per-slot guards.
+template <int MODE, bool SG, bool CSC>
+const void* row_kernel_csc(int k) {
+  if (k == 32) return (const void*)k_rows<MODE, SG, 8, CSC, true>;
+  if (k == 16) return (const void*)k_rows<MODE, SG, 4, CSC, true>;
+  return k < 16 ? (const void*)k_rows<MODE, SG, 4, CSC, false> : (const void*)k_rows<MODE, SG, 8, CSC, false>;
+}
 template <int MODE, bool SG>
-const void* row_kernel(int k) {
-  return k <= 16 ? (const void*)k_rows<MODE, SG, 4> : (const void*)k_rows<MODE, SG, 8>;
+const void* row_kernel(int k, bool csc) {
+  return csc ? row_kernel_csc<MODE, SG, true>(k) : row_kernel_csc<MODE, SG, false>(k);
 }
 const void* predict_kernel(int k) {
-  return k <= 16 ? (const void*)k_predict<4> : (const void*)k_predict<8>;
+  if (k == 32) return (const void*)k_predict<8, true>;
+  if (k == 16) return (const void*)k_predict<4, true>;
+  return k < 16 ? (const void*)k_predict<4, false> : (const void*)k_predict<8, false>;
 }
 
-ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st) {
+// Pipelined fused step (k = 32, B <= 32): same arithmetic as k_rows<train>, more gathers in flight.
+#ifndef FF_PIPE_VARIANT
+#define FF_PIPE_VARIANT 0   // 0: register double buffer (k_train_pipe, default: measured faster), 1: L1 prefetch (k_train_l1pf)
+#endif
+const void* pipe_kernel(bool sg, bool csc) {
+#if FF_PIPE_VARIANT == 1
+  if (sg) return csc ? (const void*)k_train_l1pf<true, true> : (const void*)k_train_l1pf<true, false>;
+  return csc ? (const void*)k_train_l1pf<false, true> : (const void*)k_train_l1pf<false, false>;
+#else
+  if (sg) return csc ? (const void*)k_train_pipe<true, true> : (const void*)k_train_pipe<true, false>;
+  return csc ? (const void*)k_train_pipe<false, true> : (const void*)k_train_pipe<false, false>;
+#endif
+}
+constexpr int kPipeLaunchThreads = FF_PIPE_VARIANT == 1 ? kPfThreads : kPipeThreads;
+
+ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads = kRowThreads) {
   void* args[] = {&a};
-  FF_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kRowThreads), args, 0, st));
+  FF_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, st));
   ++g_launches;
   return FF_OK;
 }
@@ -200,29 +258,103 @@ int occupancy_grid(const void* fn, int nsm, int threads) {
 
 bool ptr_ok(const void* p, int64_t n) { return n == 0 || p != nullptr; }
 
+// CSC mode: dh of one label tile = pull over the transposed index (after the row kernel
+// published that tile's g lines and pre-update weights).
+ff_status launch_dh_csc(ff_layer* l, int B, int tile, cudaStream_t st) {
+  if (B <= 32)
+    k_dh_csc<true><<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent_row, l->wcsc, l->gT, l->cfg.m, 1, tile,
+                                                 (int64_t)tile * l->tile_rows, l->hd);
+  else
+    k_dh_csc<false><<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent_row, l->wcsc, l->gT, l->cfg.m, nb_of(B), tile,
+                                                  (int64_t)tile * l->tile_rows, l->hd);
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
+// One row-kernel launch, bracketed by a profiling event pair while profiling is on.
+ff_status timed_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads) {
+  const bool timed = 2 * (l->prof_used + 1) <= (int)l->prof_ev.size();
+  if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used], st));
+  ff_status s = launch_rows(fn, grid, a, st, threads);
+  if (s != FF_OK) return s;
+  if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used++ + 1], st));
+  return FF_OK;
+}
+
+// The row pass (+ the CSC column pass per label tile in CSC mode).
+ff_status run_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, int B, cudaStream_t st,
+                   int threads = kRowThreads) {
+  if (!l->csc) {
+    if (l->cfg.L_local == 0) return FF_OK;
+    return timed_rows(l, fn, grid, a, st, threads);
+  }
+  for (int t = 0; t < l->ntiles; ++t) {
+    a.j_begin = (int64_t)t * l->tile_rows;
+    a.j_end = std::min<int64_t>(a.j_begin + l->tile_rows, l->cfg.L_local);
+    ff_status s = timed_rows(l, fn, grid, a, st, threads);
+    if (s != FF_OK) return s;
+    if (B > 0) {
+      s = launch_dh_csc(l, B, t, st);
+      if (s != FF_OK) return s;
+    }
+  }
+  return FF_OK;
+}
+
+// Rebuild the transposed (CSC) index of idx: stable radix sort of (column, connection id)
+// pairs; the sort's ping-pong buffers borrow gT / wcsc / dW / ent_row, so it runs between
+// steps only (create, set_params, redistribute) and invalidates stored gradients.
+ff_status csc_rebuild(ff_layer* l, cudaStream_t st) {
+  const int64_t n = l->cfg.L_local * l->cfg.k;
+  int* keysA = l->sort_keys;
+  int* keysB = reinterpret_cast<int*>(l->wcsc);
+  int* valsA = reinterpret_cast<int*>(l->dW);
+  int* valsB = l->ent_row;
+  const int nkeys = l->ntiles * l->cfg.m;
+  int end_bit = 1;
+  while ((1ll << end_bit) < (long long)nkeys) ++end_bit;
+  if (n > 0) {
+    k_csc_keys<<<l->nsm * 8, 256, 0, st>>>(l->idx, n, l->cfg.k, l->cfg.m, l->tile_rows, keysA, valsA);
+    FF_LAUNCHED();
+  }
+  cub::DoubleBuffer<unsigned> dk(reinterpret_cast<unsigned*>(keysA), reinterpret_cast<unsigned*>(keysB));
+  cub::DoubleBuffer<int> dv(valsA, valsB);
+  if (n > 0) {
+    size_t need = 0;
+    FF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, (int)n, 0, end_bit, st));
+    if (need > l->lay.sort_tmp_bytes)
+      return fail(FF_ERR_CONFIG, "CSC sort needs %zu B of scratch > reserved %zu B", need, l->lay.sort_tmp_bytes);
+    size_t have = l->lay.sort_tmp_bytes;
+    FF_CUDA(cub::DeviceRadixSort::SortPairs(l->sort_tmp, have, dk, dv, (int)n, 0, end_bit, st));
+    ++g_launches;
+  }
+  k_csc_finish<<<l->nsm * 8, 256, 0, st>>>(reinterpret_cast<const int*>(dk.Current()), dv.Current(), n, l->cfg.k,
+                                           nkeys, l->ent_row, l->pos, l->col_ptr);
+  FF_LAUNCHED();
+  l->grads_valid = false;
+  return FF_OK;
+}
+
 ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t* lbl_ptr, const int32_t* lbl_ids,
                           float grad_scale, float lr, float* dh, float* loss, cudaStream_t st) {
   if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
   if (!ptr_ok(h, B) || !ptr_ok(dh, B) || lbl_ptr == nullptr) return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
-  ff_status s = launch_prep(l, h, B, true, lbl_ptr, lbl_ids, loss, st);
+  ff_status s = launch_prep(l, h, B, !l->csc, lbl_ptr, lbl_ids, loss, st);
   if (s != FF_OK) return s;
   l->t += 1;
   RowArgs a = row_args(l, B);
   a.grad_scale = grad_scale;
   a.loss = loss;
   a.adam = adam_args(l, lr, l->t);
-  const bool timed = l->cfg.L_local > 0 && 2 * (l->prof_used + 1) <= (int)l->prof_ev.size();
-  if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used], st));
-  if (l->cfg.L_local > 0) {
-    const void* fn = (l->cfg.flags & FF_FLAG_STORE_GRADS) ? row_kernel<kModeTrain, true>(l->cfg.k)
-                                                          : row_kernel<kModeTrain, false>(l->cfg.k);
-    ff_status s2 = launch_rows(fn, l->grid_train, a, st);
-    if (s2 != FF_OK) return s2;
-  }
-  if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used++ + 1], st));
+  const bool sg = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
+  const bool pipe = l->cfg.k == 32 && B <= 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE);
+  const void* fn = pipe ? pipe_kernel(sg, l->csc)
+                        : (sg ? row_kernel<kModeTrain, true>(l->cfg.k, l->csc) : row_kernel<kModeTrain, false>(l->cfg.k, l->csc));
+  s = run_rows(l, fn, pipe ? l->grid_pipe : l->grid_train, a, B, st, pipe ? kPipeLaunchThreads : kRowThreads);
+  if (s != FF_OK) return s;
   l->grads_valid = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
-  if (B > 0) return launch_dh_out(l, B, dh, st);
-  return FF_OK;
+  if (B == 0) return FF_OK;
+  return launch_dh_out(l, B, dh, st);
 }
 
 }  // namespace
@@ -266,14 +398,28 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->h_stage = at<float>(ws, lay.h_stage); l->lbl_stage = at<int>(ws, lay.lbl_stage);
   l->dh_stage = at<float>(ws, lay.dh_stage);
   l->err = at<int>(ws, lay.scalars); l->loss_scratch = at<float>(ws, lay.scalars + 4);
+  l->csc = c.dh_mode == FF_DH_CSC;
+  if (l->csc) {
+    l->ent_row = at<int>(ws, lay.ent_row); l->pos = at<int>(ws, lay.pos); l->wcsc = at<float>(ws, lay.wcsc);
+    l->gT = at<float>(ws, lay.gT); l->col_ptr = at<int>(ws, lay.col_ptr); l->sort_tmp = ws + lay.sort_tmp;
+    l->sort_keys = at<int>(ws, lay.sort_keys);
+  }
   l->t = 0; l->grads_valid = false;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&l->nsm, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) { delete l; return fail(FF_ERR_CUDA, "device query: %s", cudaGetErrorString(e)); }
-  l->grid_train = occupancy_grid(row_kernel<kModeTrain, false>(c.k), l->nsm, kRowThreads);
-  l->grid_fwd = occupancy_grid(row_kernel<kModeForward, false>(c.k), l->nsm, kRowThreads);
-  l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k), l->nsm, kRowThreads);
+  l->grid_train = occupancy_grid(row_kernel<kModeTrain, false>(c.k, l->csc), l->nsm, kRowThreads);
+  l->grid_fwd = occupancy_grid(row_kernel<kModeForward, false>(c.k, false), l->nsm, kRowThreads);
+  l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k, l->csc), l->nsm, kRowThreads);
+  l->grid_csc = occupancy_grid((const void*)k_dh_csc<true>, l->nsm, 256);
+  l->grid_pipe = occupancy_grid(pipe_kernel(false, l->csc), l->nsm, kPipeLaunchThreads);
+  if (l->csc) {
+    // tile = a whole number of row-kernel "waves" (warps x 32 labels) within the L2 budget
+    const int64_t cap = (int64_t)csc_tile_cap(c), wave = (int64_t)l->grid_train * (kRowThreads / 32) * 32;
+    l->tile_rows = cap >= wave ? cap / wave * wave : cap;
+    l->ntiles = (int)std::max<int64_t>(1, (c.L_local + l->tile_rows - 1) / l->tile_rows);
+  }
   l->grid_pred = std::min(kMaxCandBlocks, occupancy_grid(predict_kernel(c.k), l->nsm, kRowThreads));
   l->grid_rows = l->nsm * 8;
   // zero everything that must start at zero (moments, masks, dW/db, dhT, scalars)
@@ -285,6 +431,10 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
     ++g_launches;
     e = cudaGetLastError();
     if (e != cudaSuccess) { delete l; return fail(FF_ERR_CUDA, "init launch: %s", cudaGetErrorString(e)); }
+  }
+  if (l->csc) {
+    ff_status s2 = csc_rebuild(l, st);
+    if (s2 != FF_OK) { delete l; return s2; }
   }
   *out = l;
   return FF_OK;
@@ -319,6 +469,10 @@ ff_status fixedfanin_set_params(ff_layer* l, const float* W, const int32_t* idx,
     FF_CUDA(cudaStreamSynchronize(st));
     if (herr & kErrIdxRange) return fail(FF_ERR_RANGE, "set_params: idx outside [0, m=%d)", l->cfg.m);
     if (herr & kErrIdxDup) return fail(FF_ERR_RANGE, "set_params: duplicate idx within a row");
+    if (l->csc) {
+      ff_status s2 = csc_rebuild(l, st);
+      if (s2 != FF_OK) return s2;
+    }
   }
   FF_CUDA(cudaStreamSynchronize(st));
   return FF_OK;
@@ -352,7 +506,7 @@ ff_status fixedfanin_forward(ff_layer* l, const float* h, int32_t B, float* y, f
   if (l->cfg.L_local == 0) return FF_OK;
   RowArgs a = row_args(l, B);
   a.y_out = y;
-  return launch_rows(row_kernel<kModeForward, false>(l->cfg.k), l->grid_fwd, a, st);
+  return launch_rows(row_kernel<kModeForward, false>(l->cfg.k, false), l->grid_fwd, a, st);
 }
 
 ff_status fixedfanin_backward(ff_layer* l, const float* h, const float* y, int32_t B, const int32_t* lbl_ptr,
@@ -363,17 +517,15 @@ ff_status fixedfanin_backward(ff_layer* l, const float* h, const float* y, int32
   if (!ptr_ok(h, B) || !ptr_ok(dh, B) || lbl_ptr == nullptr || (B > 0 && l->cfg.L_local > 0 && !y))
     return fail(FF_ERR_ARG, "null h/y/dh/lbl_ptr");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  ff_status s = launch_prep(l, h, B, true, lbl_ptr, lbl_ids, loss, st);
+  ff_status s = launch_prep(l, h, B, !l->csc, lbl_ptr, lbl_ids, loss, st);
   if (s != FF_OK) return s;
-  if (l->cfg.L_local > 0) {
-    RowArgs a = row_args(l, B);
-    a.y_in = y; a.grad_scale = grad_scale; a.loss = loss;
-    s = launch_rows(row_kernel<kModeBackward, false>(l->cfg.k), l->grid_bwd, a, st);
-    if (s != FF_OK) return s;
-  }
+  RowArgs a = row_args(l, B);
+  a.y_in = y; a.grad_scale = grad_scale; a.loss = loss;
+  s = run_rows(l, row_kernel<kModeBackward, false>(l->cfg.k, l->csc), l->grid_bwd, a, B, st);
+  if (s != FF_OK) return s;
   l->grads_valid = true;
-  if (B > 0) return launch_dh_out(l, B, dh, st);
-  return FF_OK;
+  if (B == 0) return FF_OK;
+  return launch_dh_out(l, B, dh, st);
 }
 
 ff_status fixedfanin_get_grads(ff_layer* l, float* dW, float* db, ff_stream_t stream) {
@@ -448,6 +600,7 @@ ff_status fixedfanin_redistribute(ff_layer* l, uint64_t step, ff_stream_t stream
                                                l->cfg.k, p, (uint32_t)step, (uint32_t)l->cfg.seed,
                                                (uint32_t)(l->cfg.seed >> 32));
   FF_LAUNCHED();
+  if (l->csc) return csc_rebuild(l, st);
   return FF_OK;
 }
 

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("FIXEDFANIN_LIB") or os.path.join(_HERE, "libfixedfani
 FF_OK, FF_ERR_ARG, FF_ERR_CONFIG, FF_ERR_RANGE, FF_ERR_NONFINITE, FF_ERR_CUDA, FF_ERR_STATE = range(7)
 FF_FLAG_CHECK_FINITE = 1
 FF_FLAG_STORE_GRADS = 2
+FF_FLAG_NO_PIPE = 4
 FF_DH_ATOMIC, FF_DH_CSC = 0, 1
 FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 32, 128, 8
 _STATUS = {1: "FF_ERR_ARG", 2: "FF_ERR_CONFIG", 3: "FF_ERR_RANGE", 4: "FF_ERR_NONFINITE", 5: "FF_ERR_CUDA",

@@ -103,9 +103,13 @@ def test_forward_parity(L, m, k, B):
     assert_close(y, yr, Ay, "y")
 
 
+DH = pytest.mark.parametrize("dh_mode", [0, 1], ids=["atomic", "csc"])
+
+
+@DH
 @pytest.mark.parametrize("L,m,k,B", CASES)
-def test_backward_and_adam_parity(L, m, k, B):
-    lay = make(L, m, k, B=B, seed=8)
+def test_backward_and_adam_parity(L, m, k, B, dh_mode):
+    lay = make(L, m, k, B=B, seed=8, dh_mode=dh_mode)
     W, idx, bias = synth.random_params(L, m, k, seed=L + 2 * B, scale=0.5)
     lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
     h = synth.hidden_batch(B, m, step=4)
@@ -136,14 +140,16 @@ def test_backward_and_adam_parity(L, m, k, B):
     assert s["t"] == 1
 
 
-@pytest.mark.parametrize("L,m,k,B", [(1000, 256, 16, 32), (333, 100, 13, 37), (2000, 512, 32, 100)])
-def test_fused_step_equals_unfused_path(L, m, k, B):
+@DH
+@pytest.mark.parametrize("L,m,k,B", [(1000, 256, 16, 32), (333, 100, 13, 37), (2000, 512, 32, 100),
+                                     (3000, 512, 32, 32), (777, 300, 32, 7), (65, 40, 32, 1)])
+def test_fused_step_equals_unfused_path(L, m, k, B, dh_mode):
     """train_step (one fused kernel) = forward + backward + adam_step: dW, db and the
     updated state are bit-identical (same device arithmetic), dh equal up to atomic order."""
     layer = L_()
     W, idx, bias = synth.random_params(L, m, k, seed=5, scale=0.5)
-    a = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS)
-    b = make(L, m, k, B=B)
+    a = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, dh_mode=dh_mode)
+    b = make(L, m, k, B=B, dh_mode=dh_mode)
     for x in (a, b):
         x.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
     for step in range(3):
@@ -160,14 +166,18 @@ def test_fused_step_equals_unfused_path(L, m, k, B):
         sa, sb = state_of(a), state_of(b)
         for key in ("W", "mW", "vW", "bias", "mb", "vb", "idx"):
             assert (sa[key] == sb[key]).all(), key
-        assert torch.allclose(dha, dhb, rtol=1e-5, atol=1e-7)
+        if dh_mode == 1:
+            assert torch.equal(dha, dhb)          # CSC pull: fixed summation order
+        else:
+            assert torch.allclose(dha, dhb, rtol=1e-5, atol=1e-7)
         assert abs(la.item() - lb.item()) <= 1e-5 * abs(lb.item())
 
 
-def test_fused_step_lockstep_vs_oracle():
+@DH
+def test_fused_step_lockstep_vs_oracle(dh_mode):
     L, m, k, B = 1000, 256, 16, 32
     layer = L_()
-    lay = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, seed=42)
+    lay = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, seed=42, dh_mode=dh_mode)
     for step in range(5):
         s0 = state_of(lay)
         st = oracle.State(s0["W"].astype(np.float64), s0["idx"], s0["bias"].astype(np.float64),
@@ -190,11 +200,12 @@ def test_fused_step_lockstep_vs_oracle():
         assert s1["t"] == step + 1
 
 
-def test_free_running_tiny_run_matches_oracle():
+@DH
+def test_free_running_tiny_run_matches_oracle(dh_mode):
     """tiny config of BASELINE.json: 5 Adam steps + 1 redistribution, then predict K = 5.
     The oracle evolves its own fp64 state from the same Philox init."""
     L, m, k, B = 1000, 256, 16, 32
-    lay = make(L, m, k, B=B, seed=42)
+    lay = make(L, m, k, B=B, seed=42, dh_mode=dh_mode)
     st = oracle.State.create(L, m, k, seed=42)
     for step in range(5):
         h = synth.hidden_batch(B, m, step=step)
@@ -213,6 +224,16 @@ def test_free_running_tiny_run_matches_oracle():
     # and the free-running oracle state agrees except at near-ties of |W|
     Wf, idxf, _, _ = oracle.redistribute(st.W, st.idx, st.mW, st.vW, m, p, seed=42, step=5)
     assert (idxf == s2["idx"]).mean() > 0.999
+    # one more step after the redistribution: dh must use the new connections (CSC rebuilt)
+    s2 = state_of(lay)
+    st2 = oracle.State(s2["W"].astype(np.float64), s2["idx"], s2["bias"].astype(np.float64),
+                       s2["mW"].astype(np.float64), s2["vW"].astype(np.float64), s2["mb"].astype(np.float64),
+                       s2["vb"].astype(np.float64), s2["t"])
+    h = synth.hidden_batch(B, m, step=6)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=6)
+    dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
+    r = oracle.train_step(st2, h, ptr, ids, F32(1.0 / B), F32(1e-3), **ADAM)
+    assert_close(dh.cpu().numpy(), r.dh, r.Adh, "dh after redistribution")
     h = synth.hidden_batch(B, m, step=99)
     sc, ids_ = lay.predict_topk(tens(h), 5)
     y = lay.forward(tens(h)).cpu().numpy().astype(np.float64)
@@ -275,16 +296,17 @@ def test_predict_topk_ties_resolved_by_lower_id():
     assert (ids.cpu().numpy() == np.array([5, 17, 100, 250, 0, 1])).all()
 
 
+@DH
 @pytest.mark.parametrize("P", [2, 3, 8])
-def test_sharded_layers_are_p_invariant(P):
+def test_sharded_layers_are_p_invariant(P, dh_mode):
     """Virtual sharding on one GPU: P handles with row offsets reproduce the unsharded
     state, scores and (after merge) top-K bit-exactly (rows are independent)."""
     layer = L_()
     L, m, k, B, K = 2003, 512, 32, 32, 5
-    full = make(L, m, k, B=B, seed=9)
+    full = make(L, m, k, B=B, seed=9, dh_mode=dh_mode)
     bounds = [L * r // P for r in range(P + 1)]
     shards = [make(bounds[r + 1] - bounds[r], m, k, B=B, seed=9, L_global=L, row_begin=bounds[r],
-                   L_local=bounds[r + 1] - bounds[r]) for r in range(P)]
+                   L_local=bounds[r + 1] - bounds[r], dh_mode=dh_mode) for r in range(P)]
     for step in range(2):
         h = tens(synth.hidden_batch(B, m, step=step))
         ptr, ids = synth.label_batch(B, L, 5.0, step=step)
@@ -330,9 +352,10 @@ def test_set_params_rejects_bad_idx():
         lay.set_params(idx=tens(idx))
 
 
-def test_empty_batch_and_empty_shard():
+@DH
+def test_empty_batch_and_empty_shard(dh_mode):
     L, m, k = 50, 32, 4
-    lay = make(L, m, k, B=8, seed=1)
+    lay = make(L, m, k, B=8, seed=1, dh_mode=dh_mode)
     s0 = state_of(lay)
     h = torch.zeros((0, m), device=dev())
     y = lay.forward(h)
@@ -343,7 +366,7 @@ def test_empty_batch_and_empty_shard():
     Wr, _, _ = oracle.adam(s0["W"], np.zeros((L, k)), s0["mW"], s0["vW"], 1, F32(1e-3), **ADAM)
     assert_close(s1["W"], Wr, 0, "W' with B=0")
     assert s1["t"] == 1
-    empty = make(0, m, k, B=8, L_global=10, row_begin=10, L_local=0)
+    empty = make(0, m, k, B=8, L_global=10, row_begin=10, L_local=0, dh_mode=dh_mode)
     hb = tens(synth.hidden_batch(3, m))
     dh, _ = empty.train_step(hb, tens(np.array([0, 0, 0, 0], np.int32)), ids, 1e-3)
     assert (dh == 0).all()
@@ -363,9 +386,10 @@ def test_full_fan_in_is_dense():
     assert np.abs(y - ref).max() <= 1e-4 * np.abs(h).sum(1).max() * np.abs(Wd).max()
 
 
-def test_host_entry_point_equals_device_entry_point():
+@DH
+def test_host_entry_point_equals_device_entry_point(dh_mode):
     L, m, k, B = 1000, 256, 16, 32
-    a, b = make(L, m, k, B=B, seed=4), make(L, m, k, B=B, seed=4)
+    a, b = make(L, m, k, B=B, seed=4, dh_mode=dh_mode), make(L, m, k, B=B, seed=4, dh_mode=dh_mode)
     h = synth.hidden_batch(B, m, step=2)
     ptr, ids = synth.label_batch(B, L, 5.0, step=2)
     dh_host = torch.empty((B, m)).pin_memory(); loss_host = torch.empty(1).pin_memory()
@@ -378,3 +402,101 @@ def test_host_entry_point_equals_device_entry_point():
     assert abs(loss_host.item() - loss.item()) <= 1e-5 * loss.item()
     sa, sb = state_of(a), state_of(b)
     assert (sa["W"] == sb["W"]).all() and (sa["bias"] == sb["bias"]).all()
+
+
+def test_csc_dh_is_deterministic_and_matches_atomic():
+    L, m, k, B = 3000, 1024, 32, 32
+    a, b = make(L, m, k, B=B, seed=2, dh_mode=1), make(L, m, k, B=B, seed=2, dh_mode=0)
+    h = tens(synth.hidden_batch(B, m, step=1))
+    ptr, ids = synth.label_batch(B, L, 5.0, step=1)
+    W, idx, bias = synth.random_params(L, m, k, seed=3)
+    for x in (a, b):
+        x.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    y = a.forward(h)
+    d1, _ = a.backward(h, y, tens(ptr), tens(ids))
+    d2, _ = a.backward(h, y, tens(ptr), tens(ids))
+    assert torch.equal(d1, d2)
+    d3, _ = b.backward(h, y, tens(ptr), tens(ids))
+    assert torch.allclose(d1, d3, rtol=1e-5, atol=1e-7)
+
+
+def test_full_size_amazon_670k_sampled_parity():
+    """BASELINE.json's Amazon-670K shape in the bench's launch configuration: one fused
+    step (CSC and atomic dh), checked on sampled label rows (dW, db, W') and on full dh
+    (the oracle's Alg. 2 over all 21.4 M connections), lockstep (R20)."""
+    layer = L_()
+    shape = synth.SHAPES["amazon-670k"]
+    L, m, k, B = shape.L, shape.m, shape.k, shape.B
+    h = synth.hidden_batch(B, m, step=0)
+    ptr, ids = synth.label_batch(B, L, shape.avg_pos, step=0)
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(L, 256, replace=False))
+    for dh_mode in (1, 0):
+        lay = make(L, m, k, B=B, seed=42, flags=layer.FF_FLAG_STORE_GRADS, dh_mode=dh_mode)
+        s0 = state_of(lay)
+        y = lay.forward(tens(h)).cpu().numpy().astype(np.float64)
+        dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
+        dW, db = (x.cpu().numpy() for x in lay.get_grads())
+        s1 = state_of(lay)
+        # scores of sampled rows from the GPU state (Alg. 1) vs the GPU forward
+        yr, Ay = oracle.forward(s0["W"][rows], s0["idx"][rows], s0["bias"][rows], h)
+        assert_close(y[:, rows], yr, Ay, "y rows")
+        g, _ = oracle.bce_grad(y, ptr, ids, F32(1.0 / B))
+        dWr, AdW, dbr, Adb = oracle.weight_grad(s0["idx"][rows], h, g[:, rows])
+        assert_close(dW[rows], dWr, AdW, "dW rows")
+        assert_close(db[rows], dbr, Adb, "db rows")
+        Wr, mr, vr = oracle.adam(s0["W"][rows], dW[rows], s0["mW"][rows], s0["vW"][rows], 1, F32(1e-3), **ADAM)
+        assert_close(s1["W"][rows], Wr, 0, "W' rows")
+        dhr, Adh = oracle.input_grad(s0["W"], s0["idx"], g, m)
+        assert_close(dh.cpu().numpy(), dhr, Adh, f"dh full (mode {dh_mode})")
+        del lay
+        torch.cuda.empty_cache()
+
+
+def test_csc_multi_tile_dh_and_grads():
+    """CSC mode with several label tiles (B = 100 -> 4 sample chunks -> 65,536-row tiles):
+    the per-tile column passes accumulate dh across tiles; compared with the oracle."""
+    layer = L_()
+    L, m, k, B = 140000, 2048, 32, 100
+    lay = make(L, m, k, B=128, seed=6, dh_mode=1, flags=layer.FF_FLAG_STORE_GRADS)
+    s0 = state_of(lay)
+    h = synth.hidden_batch(B, m, step=2)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=2)
+    y = lay.forward(tens(h)).cpu().numpy().astype(np.float64)
+    dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
+    dW, db = (x.cpu().numpy() for x in lay.get_grads())
+    g, _ = oracle.bce_grad(y, ptr, ids, F32(1.0 / B))
+    dhr, Adh = oracle.input_grad(s0["W"], s0["idx"], g, m)
+    assert_close(dh.cpu().numpy(), dhr, Adh, "dh (3 tiles)")
+    rows = np.arange(0, L, 997)
+    dWr, AdW, dbr, Adb = oracle.weight_grad(s0["idx"][rows], h, g[:, rows])
+    assert_close(dW[rows], dWr, AdW, "dW rows")
+    assert_close(db[rows], dbr, Adb, "db rows")
+
+
+@DH
+@pytest.mark.parametrize("L,m,B", [(5000, 1024, 32), (1234, 700, 19), (31, 64, 32), (70000, 4096, 32)])
+def test_pipelined_step_equals_generic_step(L, m, B, dh_mode):
+    """k = 32, B <= 32 runs the software-pipelined fused kernel; FF_FLAG_NO_PIPE forces the
+    generic one.  Both implement the same arithmetic: state and gradients bit-identical."""
+    layer = L_()
+    k = 32
+    flags = layer.FF_FLAG_STORE_GRADS
+    a = make(L, m, k, B=B, seed=12, flags=flags, dh_mode=dh_mode)
+    b = make(L, m, k, B=B, seed=12, flags=flags | layer.FF_FLAG_NO_PIPE, dh_mode=dh_mode)
+    for step in range(3):
+        h = tens(synth.hidden_batch(B, m, step=step))
+        ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        la, lb = torch.zeros(1, device=dev()), torch.zeros(1, device=dev())
+        dha, _ = a.train_step(h, tens(ptr), tens(ids), 1e-2, loss=la)
+        dhb, _ = b.train_step(h, tens(ptr), tens(ids), 1e-2, loss=lb)
+        ga, gb = a.get_grads(), b.get_grads()
+        assert torch.equal(ga[0], gb[0]) and torch.equal(ga[1], gb[1])
+        sa, sb = state_of(a), state_of(b)
+        for key in ("W", "mW", "vW", "bias", "mb", "vb", "idx"):
+            assert (sa[key] == sb[key]).all(), key
+        if dh_mode == 1:
+            assert torch.equal(dha, dhb)
+        else:
+            assert torch.allclose(dha, dhb, rtol=1e-5, atol=1e-7)
+        assert abs(la.item() - lb.item()) <= 1e-5 * abs(lb.item())
