@@ -156,7 +156,7 @@ def run_reference(a, shape, world, rank):
     if rank != 0:
         return
     from paper_2306_03725_b200 import synth
-    rows = max(1, shape.L // 64)
+    rows = max(1, shape.L // 128)
     data = [(synth.hidden_batch(shape.B, shape.m, step=s), *synth.label_batch(shape.B, shape.L, shape.avg_pos, step=s))
             for s in range(N_BATCHES)]
     import oracle
@@ -164,7 +164,7 @@ def run_reference(a, shape, world, rank):
     if a.warmup:
         oracle_sample_rate(shape, rows, max(1, min(a.warmup, 3)), data)
     v, dt = oracle_sample_rate(shape, rows, a.steps, data)
-    sample = (f"first {rows} of {shape.L} label rows (1/64), m={shape.m}, k={shape.k}, B={shape.B}; "
+    sample = (f"first {rows} of {shape.L} label rows (1/128), m={shape.m}, k={shape.k}, B={shape.B}; "
               f"{a.steps} oracle steps of {dt * 1e3:.1f} ms, scaled x{shape.L / rows:.1f} to all rows")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3 * shape.L / rows,

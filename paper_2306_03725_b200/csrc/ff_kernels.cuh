@@ -334,6 +334,12 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
 #define FF_PIPE_MINB 3
 #endif
 constexpr int kPipeThreads = FF_PIPE_THREADS;
+#ifndef FF_WS_RECOMPUTE
+#define FF_WS_RECOMPUTE 1   // CSC mode: re-shuffle the row's weights at compute time (saves registers)
+#endif
+#ifndef FF_ABLATE
+#define FF_ABLATE 0      // dev-only ablation switches of k_train_pipe (timing experiments; wrong results)
+#endif
 constexpr int kPipeMinBlocks = FF_PIPE_MINB;
 
 struct PipeCursor {             // position of one row in this warp's sequence of rows
@@ -354,7 +360,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   const int* const idx = a.idx; const int* const pos = a.pos;
   const float grad_scale = a.grad_scale;
   const bool want_loss = a.loss != nullptr, check = a.check_finite != 0;
-  const AdamArgs adam = a.adam;
   const int64_t jb = a.j_begin, je = a.j_end;
   const int nblk = (int)((je - jb + 31) >> 5);
   const int b = 4 * bq + gq;                            // this lane's own sample
@@ -370,10 +375,15 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   };
   auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * 32 + c.i; };
 
-  struct St { float w, mw, vw; int c, pe; };
+  struct St { float w, mw, vw; int c, pe; int64_t row; };
   auto load_st = [&](const Cur& cu, St& st) {
     if (cu.blk < nblk) {
       const int64_t row = row_of(cu) * 32 + lane;
+      st.row = row - lane;
+      if (FF_ABLATE & 2) {                                  // ablation: no state loads
+        st.w = 0.01f * lane; st.c = (int)((row * 2654435761u) & 32767); st.mw = 0.f; st.vw = 0.f; st.pe = (int)row;
+        return;
+      }
       st.w = ld_na(W + row);
       st.c = ld_na_ro(idx + row);
       st.mw = ld_na(mW + row);
@@ -403,59 +413,89 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
 
   float wsA[NG], wsB[NG]; uint32_t csA[NG], csB[NG]; float4 hvA[NG], hvB[NG];
   auto issue = [&](const St& st, float (&ws)[NG], uint32_t (&cs)[NG], float4 (&hv)[NG]) {
+    if (FF_ABLATE & 64) {                                  // ablation: gather-layout loads, no spread shuffles
+      const float4 w0 = *reinterpret_cast<const float4*>(W + st.row + gq * 8);
+      const float4 w1 = *reinterpret_cast<const float4*>(W + st.row + gq * 8 + 4);
+      const int4 c0 = *reinterpret_cast<const int4*>(idx + st.row + gq * 8);
+      const int4 c1 = *reinterpret_cast<const int4*>(idx + st.row + gq * 8 + 4);
+      ws[0] = w0.x; ws[1] = w0.y; ws[2] = w0.z; ws[3] = w0.w; ws[4] = w1.x; ws[5] = w1.y; ws[6] = w1.z; ws[7] = w1.w;
+      cs[0] = c0.x * kColBytes; cs[1] = c0.y * kColBytes; cs[2] = c0.z * kColBytes; cs[3] = c0.w * kColBytes;
+      cs[4] = c1.x * kColBytes; cs[5] = c1.y * kColBytes; cs[6] = c1.z * kColBytes; cs[7] = c1.w * kColBytes;
+    } else
     row_spread<NG>(st.w, st.c, kColBytes, gq, ws, cs);
     // atomic mode: keep hd (h and dh lines) evict_last against the state stream, else plain
-    if (CSC) row_gather_plain<NG>(hb, cs, hv);
+    if (FF_ABLATE & 1) {                                   // ablation: no gathers
+#pragma unroll
+      for (int q = 0; q < NG; ++q) hv[q] = make_float4(__uint_as_float(cs[q] & 0x3fffff), 0.5f, 0.25f, 0.125f);
+    } else if (CSC) row_gather_plain<NG>(hb, cs, hv);
     else row_gather<NG, true>(hb, cs, 32, gq, pol_l, hv);
   };
   issue(sX, wsA, csA, hvA);
   load_st(Z, sZ);
 
-  auto compute = [&](const Cur& cu, St& st, const float (&ws)[NG], const uint32_t (&cs)[NG],
+  auto compute = [&](const Cur& cu, St& st, const float (&ws_in)[NG], const uint32_t (&cs)[NG],
                      const float4 (&hv)[NG]) {
+    float ws[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) ws[q] = (CSC && FF_WS_RECOMPUTE) ? __shfl_sync(kFull, st.w, 4 * q + gq) : ws_in[q];
     const int64_t j = row_of(cu);
     const int i = cu.i;
     const float bj = __shfl_sync(kFull, bv.bias, i);
     const uint32_t pm = __shfl_sync(kFull, bv.pm, i);
-    const float y = row_score_own<NG>(ws, hv, gq, bj);
+    float y;
+    if (FF_ABLATE & 128) {                                 // ablation: no score reduce-scatter shuffles
+      float2 y01 = make_float2(0.f, 0.f), y23 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < NG; ++q) { y01 = ffma2(bc2(ws[q]), lo2(hv[q]), y01); y23 = ffma2(bc2(ws[q]), hi2(hv[q]), y23); }
+      y = y01.x + y01.y + y23.x + y23.y + bj;
+    } else
+    y = row_score_own<NG>(ws, hv, gq, bj);
     const bool pos_ = (pm >> b) & 1u;
-    float e;
-    float g = bce_grad(y, pos_, grad_scale, &e);
+    float e = 0.5f;
+    float g = (FF_ABLATE & 8) ? y * grad_scale : bce_grad(y, pos_, grad_scale, &e);
     if (!bvalid) g = 0.0f;
     if (want_loss && bvalid) loss_acc += bce_loss_term(y, pos_, e);
     if (check && __any_sync(kFull, bvalid && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
     float4 g4;
+    if (FF_ABLATE & 128) { g4 = make_float4(g, g * 0.5f, g * 0.25f, g * 2.0f); } else {
     g4.x = __shfl_sync(kFull, g, (0 << 3) | bq);
     g4.y = __shfl_sync(kFull, g, (1 << 3) | bq);
     g4.z = __shfl_sync(kFull, g, (2 << 3) | bq);
     g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
+    }
     float dwp[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q) dwp[q] = 0.0f + dw_partial(g4, hv[q]);
     if (CSC) {
-      st_hint(a.gT + (j - jb) * 32 + b, g, pol_l);
-      a.wcsc[st.pe] = st.w;
+      if (!(FF_ABLATE & 32)) {                             // ablation: no g / W_old publication
+        st_hint(a.gT + (j - jb) * 32 + b, g, pol_l);
+        a.wcsc[st.pe] = st.w;
+      }
     } else {
 #pragma unroll
       for (int q = 0; q < NG; ++q)
         red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
     }
-    const float gW = row_dw_slot<NG>(dwp, lane);
-    const float db = warp_sum(g);
+    const float gW = (FF_ABLATE & 16) ? dwp[lane & 7] : row_dw_slot<NG>(dwp, lane);
+    const float db = (FF_ABLATE & 16) ? g : warp_sum(g);
     if (lane == i) db_v = db;
     const int64_t row = j * 32 + lane;
     if (STORE_GRADS) a.dW[row] = gW;
-    adam_update(st.w, st.mw, st.vw, gW, adam);
-    st_na(W + row, st.w);
-    st_na(mW + row, st.mw);
-    st_na(vW + row, st.vw);
+    if (FF_ABLATE & 4) {                                   // ablation: no Adam, one store
+      st_na(W + row, st.w + gW);
+    } else {
+      adam_update(st.w, st.mw, st.vw, gW, a.adam);
+      st_na(W + row, st.w);
+      st_na(mW + row, st.mw);
+      st_na(vW + row, st.vw);
+    }
     if (i == cu.nl - 1) {                                // block done: vectorized bias update
       const int64_t jl = jb + (int64_t)cu.blk * 32 + lane;
       if (lane <= i) {
         if (bv.pm != 0u) a.posmask[jl] = 0u;
         if (STORE_GRADS) a.db[jl] = db_v;
         float p = bv.bias, mo = bv.mb, ve = bv.vb;
-        adam_update(p, mo, ve, db_v, adam);
+        adam_update(p, mo, ve, db_v, a.adam);
         st_na(a.bias + jl, p);
         st_na(a.mb + jl, mo);
         st_na(a.vb + jl, ve);

@@ -56,6 +56,14 @@ def assert_close(x, ref, A, what, rtol=RTOL):
     assert e.max() <= rtol, f"{what}: max err {e.max():.3e} at {np.unravel_index(e.argmax(), e.shape)}"
 
 
+def dh_close(a, b):
+    """Two GPU dh results whose fp32 sums ran in different (atomic) orders: equal up to
+    rounding relative to the dh scale (R19/R21; elements with cancellation have no
+    meaningful plain relative error)."""
+    scale = float(torch.maximum(a.abs().max(), b.abs().max()))
+    return torch.allclose(a, b, rtol=1e-5, atol=1e-5 * scale + 1e-30)
+
+
 def state_of(lay):
     p = lay.get_params()
     return {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in p.items()}
@@ -169,7 +177,7 @@ def test_fused_step_equals_unfused_path(L, m, k, B, dh_mode):
         if dh_mode == 1:
             assert torch.equal(dha, dhb)          # CSC pull: fixed summation order
         else:
-            assert torch.allclose(dha, dhb, rtol=1e-5, atol=1e-7)
+            assert dh_close(dha, dhb)
         assert abs(la.item() - lb.item()) <= 1e-5 * abs(lb.item())
 
 
@@ -312,7 +320,7 @@ def test_sharded_layers_are_p_invariant(P, dh_mode):
         ptr, ids = synth.label_batch(B, L, 5.0, step=step)
         dh_full, _ = full.train_step(h, tens(ptr), tens(ids), 1e-3)
         dh_sum = sum(s.train_step(h, tens(ptr), tens(ids), 1e-3)[0] for s in shards)
-        assert torch.allclose(dh_full, dh_sum, rtol=1e-5, atol=1e-7)
+        assert dh_close(dh_full, dh_sum)
     full.redistribute(1000)
     for s in shards:
         s.redistribute(1000)
@@ -398,7 +406,7 @@ def test_host_entry_point_equals_device_entry_point(dh_mode):
     loss = torch.zeros(1, device=dev())
     dh, _ = b.train_step(tens(h), tens(ptr), tens(ids), 1e-3, loss=loss)
     torch.cuda.synchronize()
-    assert torch.allclose(dh_host, dh.cpu(), rtol=1e-5, atol=1e-7)
+    assert dh_close(dh_host, dh.cpu())
     assert abs(loss_host.item() - loss.item()) <= 1e-5 * loss.item()
     sa, sb = state_of(a), state_of(b)
     assert (sa["W"] == sb["W"]).all() and (sa["bias"] == sb["bias"]).all()
@@ -417,7 +425,7 @@ def test_csc_dh_is_deterministic_and_matches_atomic():
     d2, _ = a.backward(h, y, tens(ptr), tens(ids))
     assert torch.equal(d1, d2)
     d3, _ = b.backward(h, y, tens(ptr), tens(ids))
-    assert torch.allclose(d1, d3, rtol=1e-5, atol=1e-7)
+    assert dh_close(d1, d3)
 
 
 def test_full_size_amazon_670k_sampled_parity():
@@ -498,5 +506,5 @@ def test_pipelined_step_equals_generic_step(L, m, B, dh_mode):
         if dh_mode == 1:
             assert torch.equal(dha, dhb)
         else:
-            assert torch.allclose(dha, dhb, rtol=1e-5, atol=1e-7)
+            assert dh_close(dha, dhb)
         assert abs(la.item() - lb.item()) <= 1e-5 * abs(lb.item())
