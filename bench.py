@@ -46,6 +46,7 @@ def args_():
     p.add_argument("--shape", default="amazon-670k")
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--flags", type=int, default=0, help="extra ff_config.flags (A/B experiments)")
     p.add_argument("--dh-mode", default="csc", choices=["atomic", "csc"],
                    help="dh scatter: red.global atomics or the CSC pull (DESIGN.md §6; chosen by measurement)")
     return p.parse_args()
@@ -193,7 +194,7 @@ def run_ours(a, shape, world, rank, local_rank):
     from paper_2306_03725_b200.layer import FF_DH_ATOMIC, FF_DH_CSC
     dh_mode = FF_DH_CSC if a.dh_mode == "csc" else FF_DH_ATOMIC
     layer = ShardedLayer(shape.L, shape.m, shape.k, rank=rank, world=world, device=dev, max_batch=B,
-                         seed=synth.PARAM_SEED, max_nnz=max_nnz, dh_mode=dh_mode)
+                         seed=synth.PARAM_SEED, max_nnz=max_nnz, dh_mode=dh_mode, flags=a.flags)
     eng = layer.engine
     L_local = layer.row_end - layer.row_begin
     stream = torch.cuda.current_stream()

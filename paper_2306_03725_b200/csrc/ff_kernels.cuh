@@ -117,13 +117,19 @@ __device__ __forceinline__ void row_gather_plain(const float* hb, const uint32_t
 // reduce-scatter over the four connection groups (xor 16, xor 8), + bias.
 template <int NG>
 __device__ __forceinline__ float row_score_own(const float (&ws)[NG], const float4 (&hv)[NG], int gq, float bj) {
-  float2 y01 = make_float2(0.f, 0.f), y23 = make_float2(0.f, 0.f);
+  // packed FMAs in 4 independent chains (even / odd connections), then combined
+  float2 y01a = make_float2(0.f, 0.f), y23a = make_float2(0.f, 0.f);
+  float2 y01b = make_float2(0.f, 0.f), y23b = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int q = 0; q < NG; ++q) {                     // packed: same per-component FMA order
-    y01 = ffma2(bc2(ws[q]), lo2(hv[q]), y01);
-    y23 = ffma2(bc2(ws[q]), hi2(hv[q]), y23);
+  for (int q = 0; q < NG; q += 2) {
+    y01a = ffma2(bc2(ws[q]), lo2(hv[q]), y01a);
+    y23a = ffma2(bc2(ws[q]), hi2(hv[q]), y23a);
+    if (q + 1 < NG) {
+      y01b = ffma2(bc2(ws[q + 1]), lo2(hv[q + 1]), y01b);
+      y23b = ffma2(bc2(ws[q + 1]), hi2(hv[q + 1]), y23b);
+    }
   }
-  const float4 yp = make_float4(y01.x, y01.y, y23.x, y23.y);
+  const float4 yp = make_float4(y01a.x + y01b.x, y01a.y + y01b.y, y23a.x + y23b.x, y23a.y + y23b.y);
   const bool hi = gq & 2, odd = gq & 1;
   const float k0 = hi ? yp.z : yp.x, k1 = hi ? yp.w : yp.y;
   const float s0 = hi ? yp.x : yp.z, s1 = hi ? yp.y : yp.w;
@@ -182,6 +188,17 @@ __device__ __forceinline__ float row_dw_slot(const float (&dwp)[NG], int lane) {
   return __shfl_sync(kFull, v[0], ((lane & 3) << 3) | ((lane >> 2) & (NG > 4 ? 7 : 3)));
 }
 
+// Bias gradient of a 32-row block without a per-row warp reduction: row i's per-sample
+// gradients are parked in a per-warp shared buffer gb[i][sample]; at the end of the block
+// lane r sums row r over samples 0..31 in ascending order (fixed order, all kernels).
+struct DbBuf { float v[32][33]; };
+__device__ __forceinline__ float db_block_sum(const DbBuf& gb, int r) {
+  float s = 0.0f;
+#pragma unroll
+  for (int b = 0; b < 32; ++b) s += gb.v[r][b];
+  return s;
+}
+
 // The row kernel: forward (Alg. 1) for MODE forward; BCE gradient,
 // Alg. 3 weight gradient, bias gradient and Alg. 2 input-gradient scatter
 // for MODE backward; all of those plus Adam for MODE train — the
@@ -201,6 +218,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
   const int64_t L = a.L, jb = a.j_begin, nblk = (a.j_end - jb + 31) >> 5;
   const bool act = lane < k;
   float loss_acc = 0.0f;
+  __shared__ DbBuf dbbuf[kRowThreads / 32];
+  DbBuf& gbuf = dbbuf[threadIdx.x >> 5];
 
   float w_n = 0.f, mw_n = 0.f, vw_n = 0.f;
   int c_n = 0, p_n = 0;
@@ -294,8 +313,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
 
       if (CSC && act) a.wcsc[pe] = w;                 // pre-update W in CSC order (for k_dh_csc)
       const float gW = row_dw_slot<NG>(dwp, lane);
-      const float db = warp_sum(dbp);
-      if (lane == i) db_v = db;
+      gbuf.v[i][4 * bq + gq] = dbp;                   // this lane's sample (over all chunks)
       if (MODE == kModeBackward || STORE_GRADS) {
         if (act) a.dW[row + lane] = gW;
       }
@@ -307,6 +325,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
       }
     }
     if (MODE == kModeForward) continue;
+    __syncwarp();
+    if (lv) db_v = db_block_sum(gbuf, lane);
+    __syncwarp();
     if (lv) {
       if (pm_v != 0u) a.posmask[j0 + lane] = 0u;      // self-clearing mask (chunk 0)
       if (MODE == kModeBackward || STORE_GRADS) a.db[j0 + lane] = db_v;
@@ -365,6 +386,8 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   const int b = 4 * bq + gq;                            // this lane's own sample
   const bool bvalid = b < B;
   float loss_acc = 0.0f;
+  __shared__ DbBuf dbbuf[kPipeThreads / 32];
+  DbBuf& gbuf = dbbuf[threadIdx.x >> 5];
 
   // this warp's rows: blocks w, w + nwarp, ...; cursor = (block, row in block, rows in block)
   struct Cur { int blk, i, nl; };
@@ -477,8 +500,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
         red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
     }
     const float gW = (FF_ABLATE & 16) ? dwp[lane & 7] : row_dw_slot<NG>(dwp, lane);
-    const float db = (FF_ABLATE & 16) ? g : warp_sum(g);
-    if (lane == i) db_v = db;
+    gbuf.v[i][b] = g;
     const int64_t row = j * 32 + lane;
     if (STORE_GRADS) a.dW[row] = gW;
     if (FF_ABLATE & 4) {                                   // ablation: no Adam, one store
@@ -491,6 +513,9 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     }
     if (i == cu.nl - 1) {                                // block done: vectorized bias update
       const int64_t jl = jb + (int64_t)cu.blk * 32 + lane;
+      __syncwarp();
+      if (lane <= i) db_v = db_block_sum(gbuf, lane);
+      __syncwarp();
       if (lane <= i) {
         if (bv.pm != 0u) a.posmask[jl] = 0u;
         if (STORE_GRADS) a.db[jl] = db_v;
@@ -525,158 +550,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   while (true) {
     if (!step(wsA, csA, hvA, wsB, csB, hvB)) break;
     if (!step(wsB, csB, hvB, wsA, csA, hvA)) break;
-  }
-  }
-  if (a.loss != nullptr) block_atomic_add(loss_acc * a.grad_scale, a.loss);
-}
-
-// Variant of k_train_pipe that keeps a single register buffer: the next row's h lines are
-// pulled into L1 with prefetch.global.L1 (no destination registers) and loaded from L1 when
-// the row is computed.  Fewer registers -> more resident warps; same arithmetic.
-__device__ __forceinline__ void prefetch_l1(const void* a) {
-  asm volatile("prefetch.global.L1 [%0];" :: "l"(a));
-}
-__device__ __forceinline__ float4 ld_line4_l1(const float* a) {
-  float4 v;
-  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a));
-  return v;
-}
-
-#ifndef FF_PF_THREADS
-#define FF_PF_THREADS 128
-#endif
-#ifndef FF_PF_MINB
-#define FF_PF_MINB 4
-#endif
-constexpr int kPfThreads = FF_PF_THREADS;
-constexpr int kPfMinBlocks = FF_PF_MINB;
-
-template <bool STORE_GRADS, bool CSC>
-__global__ void __launch_bounds__(kPfThreads, kPfMinBlocks) k_train_l1pf(RowArgs a) {
-  constexpr int NG = 8;
-  constexpr uint32_t kColBytes = 256;
-  const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
-  const int nwarp = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const uint64_t pol_l = policy_evict_last();
-  const int B = a.B;
-  float* const hb = a.hd + 4 * bq;
-  float* const W = a.W; float* const mW = a.mW; float* const vW = a.vW;
-  const int* const idx = a.idx; const int* const pos = a.pos;
-  const float grad_scale = a.grad_scale;
-  const bool want_loss = a.loss != nullptr, check = a.check_finite != 0;
-  const int64_t jb = a.j_begin, je = a.j_end;
-  const int nblk = (int)((je - jb + 31) >> 5);
-  const int b = 4 * bq + gq;
-  const bool bvalid = b < B;
-  float loss_acc = 0.0f;
-
-  struct Cur { int blk, i, nl; };
-  auto nl_of = [&](int blk) { return (int)min((int64_t)32, je - (jb + (int64_t)blk * 32)); };
-  auto adv = [&](Cur c) {
-    if (++c.i >= c.nl) { c.blk += nwarp; c.i = 0; c.nl = c.blk < nblk ? nl_of(c.blk) : 0; }
-    return c;
-  };
-  auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * 32 + c.i; };
-  struct St { float w, mw, vw; int c, pe; };
-  auto load_st = [&](const Cur& cu, St& st) {
-    if (cu.blk < nblk) {
-      const int64_t row = row_of(cu) * 32 + lane;
-      st.w = ld_na(W + row); st.c = ld_na_ro(idx + row); st.mw = ld_na(mW + row); st.vw = ld_na(vW + row);
-      if (CSC) st.pe = ld_na_ro(pos + row);
-    }
-  };
-  struct Bv { float bias, mb, vb; uint32_t pm; };
-  auto load_bv = [&](int blk, Bv& v) {
-    v.bias = v.mb = v.vb = 0.0f; v.pm = 0u;
-    if (blk < nblk && lane < nl_of(blk)) {
-      const int64_t j = jb + (int64_t)blk * 32 + lane;
-      v.bias = ld_na(a.bias + j); v.mb = ld_na(a.mb + j); v.vb = ld_na(a.vb + j); v.pm = a.posmask[j];
-    }
-  };
-  auto prefetch_row_lines = [&](const St& st) {
-#pragma unroll
-    for (int q = 0; q < NG; ++q) {
-      const uint32_t off = (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq) * kColBytes;
-      prefetch_l1(at_bytes(hb, off));
-    }
-  };
-
-  Cur X{(int)((((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5), 0, 0};
-  if (X.blk < nblk) {
-  X.nl = nl_of(X.blk);
-  Cur Y = adv(X), Z = adv(Y);
-  St sX{}, sY{}, sZ{};
-  Bv bv{}, bv_next{};
-  float db_v = 0.0f;
-  load_st(X, sX);
-  load_st(Y, sY);
-  load_bv(X.blk, bv);
-  prefetch_row_lines(sX);
-  load_st(Z, sZ);
-  while (true) {
-    if (Y.blk < nblk) {
-      prefetch_row_lines(sY);
-      if (Y.i == 0) load_bv(Y.blk, bv_next);
-    }
-    const Cur Zn = adv(Z);
-    St sZn{};
-    load_st(Zn, sZn);
-    {   // compute X
-      float ws[NG]; uint32_t cs[NG]; float4 hv[NG];
-      row_spread<NG>(sX.w, sX.c, kColBytes, gq, ws, cs);
-#pragma unroll
-      for (int q = 0; q < NG; ++q) hv[q] = ld_line4_l1(at_bytes(hb, cs[q]));
-      const int64_t j = row_of(X);
-      const int i = X.i;
-      const float bj = __shfl_sync(kFull, bv.bias, i);
-      const uint32_t pm = __shfl_sync(kFull, bv.pm, i);
-      const float y = row_score_own<NG>(ws, hv, gq, bj);
-      const bool pos_ = (pm >> b) & 1u;
-      float e;
-      float g = bce_grad(y, pos_, grad_scale, &e);
-      if (!bvalid) g = 0.0f;
-      if (want_loss && bvalid) loss_acc += bce_loss_term(y, pos_, e);
-      if (check && __any_sync(kFull, bvalid && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
-      float4 g4;
-      g4.x = __shfl_sync(kFull, g, (0 << 3) | bq);
-      g4.y = __shfl_sync(kFull, g, (1 << 3) | bq);
-      g4.z = __shfl_sync(kFull, g, (2 << 3) | bq);
-      g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
-      float dwp[NG];
-#pragma unroll
-      for (int q = 0; q < NG; ++q) dwp[q] = 0.0f + dw_partial(g4, hv[q]);
-      if (CSC) {
-        st_hint(a.gT + (j - jb) * 32 + b, g, pol_l);
-        a.wcsc[sX.pe] = sX.w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < NG; ++q)
-          red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
-      }
-      const float gW = row_dw_slot<NG>(dwp, lane);
-      const float db = warp_sum(g);
-      if (lane == i) db_v = db;
-      const int64_t row = j * 32 + lane;
-      if (STORE_GRADS) a.dW[row] = gW;
-      float w = sX.w, mw = sX.mw, vw = sX.vw;
-      adam_update(w, mw, vw, gW, a.adam);
-      st_na(W + row, w); st_na(mW + row, mw); st_na(vW + row, vw);
-      if (i == X.nl - 1) {
-        const int64_t jl = jb + (int64_t)X.blk * 32 + lane;
-        if (lane <= i) {
-          if (bv.pm != 0u) a.posmask[jl] = 0u;
-          if (STORE_GRADS) a.db[jl] = db_v;
-          float p = bv.bias, mo = bv.mb, ve = bv.vb;
-          adam_update(p, mo, ve, db_v, a.adam);
-          st_na(a.bias + jl, p); st_na(a.mb + jl, mo); st_na(a.vb + jl, ve);
-        }
-        db_v = 0.0f;
-      }
-    }
-    X = Y; Y = Z; Z = Zn;
-    sX = sY; sY = sZ; sZ = sZn;
-    if (X.blk >= nblk) break;
-    if (X.i == 0) bv = bv_next;
   }
   }
   if (a.loss != nullptr) block_atomic_add(loss_acc * a.grad_scale, a.loss);

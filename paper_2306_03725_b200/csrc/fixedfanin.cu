@@ -229,19 +229,11 @@ const void* predict_kernel(int k) {
 }
 
 // Pipelined fused step (k = 32, B <= 32): same arithmetic as k_rows<train>, more gathers in flight.
-#ifndef FF_PIPE_VARIANT
-#define FF_PIPE_VARIANT 0   // 0: register double buffer (k_train_pipe, default: measured faster), 1: L1 prefetch (k_train_l1pf)
-#endif
 const void* pipe_kernel(bool sg, bool csc) {
-#if FF_PIPE_VARIANT == 1
-  if (sg) return csc ? (const void*)k_train_l1pf<true, true> : (const void*)k_train_l1pf<true, false>;
-  return csc ? (const void*)k_train_l1pf<false, true> : (const void*)k_train_l1pf<false, false>;
-#else
   if (sg) return csc ? (const void*)k_train_pipe<true, true> : (const void*)k_train_pipe<true, false>;
   return csc ? (const void*)k_train_pipe<false, true> : (const void*)k_train_pipe<false, false>;
-#endif
 }
-constexpr int kPipeLaunchThreads = FF_PIPE_VARIANT == 1 ? kPfThreads : kPipeThreads;
+constexpr int kPipeLaunchThreads = kPipeThreads;
 
 ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads = kRowThreads) {
   void* args[] = {&a};
