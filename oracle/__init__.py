@@ -42,6 +42,7 @@ def lib():
         i64, i32, u64, f64, f32 = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, ctypes.c_float
         L.oracle_forward.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P]
         L.oracle_bce_grad.argtypes = [i64, i64, i32, P, P, P, f64, P, P]
+        L.oracle_sqh_grad.argtypes = [i64, i64, i32, P, P, P, f64, P, P]
         L.oracle_weight_grad.argtypes = [i64, i32, i32, i32, P, P, P, P, P, P, P]
         L.oracle_input_grad.argtypes = [i64, i32, i32, i32, P, P, P, P, P]
         L.oracle_adam.argtypes = [i64, P, P, P, P, i64, f64, f64, f64, f64]
@@ -51,7 +52,7 @@ def lib():
         L.oracle_topk.argtypes = [i64, i64, i32, P, i32, P, P]
         L.oracle_precision_at_k.argtypes = [i32, i32, P, P, P]
         L.oracle_precision_at_k.restype = f64
-        for f in ("oracle_forward", "oracle_bce_grad", "oracle_weight_grad", "oracle_input_grad",
+        for f in ("oracle_forward", "oracle_bce_grad", "oracle_sqh_grad", "oracle_weight_grad", "oracle_input_grad",
                   "oracle_adam", "oracle_philox4x32_10", "oracle_init", "oracle_redistribute", "oracle_topk"):
             getattr(L, f).restype = None
         _lib = L
@@ -102,6 +103,22 @@ def bce_grad(y, lbl_ptr, lbl_ids, grad_scale, row_begin=0):
     lib().oracle_bce_grad(L, row_begin, B, _p(y), _p(lp), _p(li), float(grad_scale), _p(g),
                           ctypes.cast(ctypes.pointer(loss), ctypes.c_void_p))
     return g, loss.value
+
+
+def sqh_grad(y, lbl_ptr, lbl_ids, grad_scale, row_begin=0):
+    """Squared-hinge gradient and loss, exact zeros where y*yhat >= 1."""
+    y = _f64(y)
+    B, L = y.shape
+    g = np.empty_like(y)
+    loss = ctypes.c_double(0.0)
+    lp, li = _i32(lbl_ptr), _i32(lbl_ids if len(lbl_ids) else np.zeros(1, np.int32))
+    lib().oracle_sqh_grad(L, row_begin, B, _p(y), _p(lp), _p(li), float(grad_scale), _p(g),
+                          ctypes.cast(ctypes.pointer(loss), ctypes.c_void_p))
+    return g, loss.value
+
+
+def loss_grad(kind, y, lbl_ptr, lbl_ids, grad_scale, row_begin=0):
+    return (sqh_grad if kind == "sqh" else bce_grad)(y, lbl_ptr, lbl_ids, grad_scale, row_begin)
 
 
 def weight_grad(idx, h, g):
@@ -215,14 +232,15 @@ class StepResult:
 
 
 def train_step(st: State, h, lbl_ptr, lbl_ids, grad_scale, lr, row_begin=0,
-               beta1=0.9, beta2=0.999, eps=1e-8):
-    """One training step in the paper's order: Alg. 1 forward, BCE gradient, Alg. 3
-    weight gradient (+db), Alg. 2 input gradient with the PRE-update weights, then
-    Adam over W and bias with the incremented global t.  Mutates ``st``."""
+               beta1=0.9, beta2=0.999, eps=1e-8, loss="bce"):
+    """One training step in the paper's order: Alg. 1 forward, loss gradient (BCE, or the
+    squared hinge with loss="sqh"), Alg. 3 weight gradient (+db), Alg. 2 input gradient
+    with the PRE-update weights, then Adam over W and bias with the incremented global t.
+    Mutates ``st``."""
     h = _f64(h)
     m = h.shape[1]
     y, Ay = forward(st.W, st.idx, st.bias, h)
-    g, loss = bce_grad(y, lbl_ptr, lbl_ids, grad_scale, row_begin)
+    g, loss = loss_grad(loss, y, lbl_ptr, lbl_ids, grad_scale, row_begin)
     dW, AdW, db, Adb = weight_grad(st.idx, h, g)
     dh, Adh = input_grad(st.W, st.idx, g, m)
     st.t += 1

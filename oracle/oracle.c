@@ -96,6 +96,28 @@ void oracle_bce_grad(int64_t L, int64_t row_begin, int32_t B, const double* y,
     if (loss) *loss = s_g * total;
 }
 
+/* Squared hinge, the paper's main loss: l(y, yhat) = max(0, 1 - y yhat)^2 with
+ * y = +1 for positives and -1 for negatives; dl/dyhat = -2 y max(0, 1 - y yhat),
+ * "exactly zero whenever y yhat >= 1" — the implicit negative mining of §3.3.
+ * g = s_g * dl/dyhat, loss = s_g * sum_{b,j} l.                                            */
+void oracle_sqh_grad(int64_t L, int64_t row_begin, int32_t B, const double* y,
+                     const int32_t* lbl_ptr, const int32_t* lbl_ids, double s_g,
+                     double* g, double* loss)
+{
+    double total = 0.0;
+    for (int32_t b = 0; b < B; ++b) {
+        for (int64_t j = 0; j < L; ++j) {
+            double yy = y[(int64_t)b * L + j];
+            double t = is_positive(lbl_ptr, lbl_ids, b, row_begin + j) ? 1.0 : -1.0;
+            double margin = 1.0 - t * yy;
+            double hinge = margin > 0.0 ? margin : 0.0;
+            g[(int64_t)b * L + j] = s_g * (-2.0 * t * hinge);
+            total += hinge * hinge;
+        }
+    }
+    if (loss) *loss = s_g * total;
+}
+
 /* Alg. 3: gradient of one structural non-zero weight:
  *   source = indices[weight_idx, label]; result = 0
  *   for instance in range(batch_size): out = backward[instance, label];

@@ -382,3 +382,36 @@ def test_train_step_uses_pre_update_weights_for_dh_and_updates_bias():
     # t = 1 sign step: |dW| >> eps so every weight moved by ~lr
     moved = np.abs(st.W - W0)[np.abs(r.dW) > 1e-5]
     np.testing.assert_allclose(moved, 1e-2, rtol=1e-3)
+
+
+# ------------------------------------------------------ squared hinge (NEXT-1)
+def test_sqh_closed_forms_and_exact_zeros():
+    for ln in read_golden("spec_examples.txt"):
+        if ln.startswith("sqh:"):
+            yv, t, l_e, g_e = [p.strip() for p in ln.split(":", 1)[1].split("|")]
+            ptr = np.array([0, 1], np.int32); ids = np.array([0], np.int32)
+            assert int(t) == 1
+            g, loss = oracle.sqh_grad(np.array([[float(yv)]]), ptr, ids, 1.0)
+            assert loss == float(l_e) and g[0, 0] == float(g_e)
+    # negatives use y = -1: yhat = -2 meets the margin (zero), yhat = 0.25 -> grad 2*1.25, loss 1.5625
+    g, loss = oracle.sqh_grad(np.array([[-2.0, 0.25]]), np.array([0, 0], np.int32), np.zeros(0, np.int32), 1.0)
+    assert g[0, 0] == 0.0 and g[0, 1] == 2.5 and loss == 1.5625
+
+
+def test_sqh_zero_count_equals_margin_count_and_fd():
+    """the number of exact zeros in the gradient equals the number of (b, j) with
+    y*yhat >= 1; the gradient is the derivative of the loss (central differences)."""
+    rng = np.random.default_rng(3)
+    y = rng.standard_normal((6, 50)) * 2
+    ptr, ids = synth.random_labels_uniform(6, 50, 4, seed=5)
+    g, _ = oracle.sqh_grad(y, ptr, ids, 0.5)
+    t = -np.ones_like(y)
+    for b in range(6):
+        t[b, ids[ptr[b]:ptr[b + 1]]] = 1.0
+    assert (g == 0).sum() == (t * y >= 1).sum()
+    for pos in [(0, 0), (3, 17), (5, 49)]:
+        e = 1e-6
+        yp = y.copy(); yp[pos] += e
+        ym = y.copy(); ym[pos] -= e
+        num = (oracle.sqh_grad(yp, ptr, ids, 0.5)[1] - oracle.sqh_grad(ym, ptr, ids, 0.5)[1]) / (2 * e)
+        assert num == pytest.approx(g[pos], rel=1e-6, abs=1e-9)
