@@ -47,6 +47,11 @@ def args_():
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--flags", type=int, default=0, help="extra ff_config.flags (A/B experiments)")
+    p.add_argument("--loss", default="bce", choices=["bce", "sqh"],
+                   help="bce (north star) or the paper's squared hinge with implicit negative mining (P:526-551)")
+    p.add_argument("--margin-bias", type=float, default=0.0,
+                   help="sqh: start every label bias at -X so that a controlled fraction of negatives meets the "
+                        "margin (engineered-margin analog of a trained model, SURVEY §8(f) NEXT-1)")
     p.add_argument("--dh-mode", default="csc", choices=["atomic", "csc"],
                    help="dh scatter: red.global atomics or the CSC pull (DESIGN.md §6; chosen by measurement)")
     return p.parse_args()
@@ -191,10 +196,11 @@ def run_ours(a, shape, world, rank, local_rank):
     data = [(synth.hidden_batch(B, shape.m, step=s), *synth.label_batch(B, shape.L, shape.avg_pos, step=s))
             for s in range(N_BATCHES)]
     max_nnz = max(int(d[1][-1]) for d in data)
-    from paper_2306_03725_b200.layer import FF_DH_ATOMIC, FF_DH_CSC
+    from paper_2306_03725_b200.layer import FF_DH_ATOMIC, FF_DH_CSC, FF_LOSS_BCE, FF_LOSS_SQH
     dh_mode = FF_DH_CSC if a.dh_mode == "csc" else FF_DH_ATOMIC
     layer = ShardedLayer(shape.L, shape.m, shape.k, rank=rank, world=world, device=dev, max_batch=B,
-                         seed=synth.PARAM_SEED, max_nnz=max_nnz, dh_mode=dh_mode, flags=a.flags)
+                         seed=synth.PARAM_SEED, max_nnz=max_nnz, dh_mode=dh_mode, flags=a.flags,
+                         loss=FF_LOSS_SQH if a.loss == "sqh" else FF_LOSS_BCE)
     eng = layer.engine
     L_local = layer.row_end - layer.row_begin
     stream = torch.cuda.current_stream()
@@ -202,6 +208,20 @@ def run_ours(a, shape, world, rank, local_rank):
     h_dev = [torch.from_numpy(d[0]).to(dev) for d in data]
     ptr_dev = [torch.from_numpy(d[1]).to(dev) for d in data]
     ids_dev = [torch.from_numpy(d[2]).to(dev) for d in data]
+    skip_fraction = None
+    if a.margin_bias:
+        eng.set_params(bias=torch.full((L_local,), -a.margin_bias, dtype=torch.float32, device=dev))
+    if a.loss == "sqh":
+        # fraction of (sample, label) gradients that are exactly zero on the first batch (t' y >= 1)
+        y = eng.forward(h_dev[0])
+        t = -torch.ones_like(y)
+        p_, i_ = data[0][1], data[0][2]
+        for b in range(B):
+            loc = [int(x) - layer.row_begin for x in i_[p_[b]:p_[b + 1]] if layer.row_begin <= x < layer.row_end]
+            if loc:
+                t[b, loc] = 1.0
+        skip_fraction = float(((t * y) >= 1.0).float().mean().item())
+        del y, t
     dh = torch.empty((B, shape.m), device=dev)
     loss = torch.zeros(1, device=dev)
     t_global = 0
@@ -317,6 +337,7 @@ def run_ours(a, shape, world, rank, local_rank):
         "data": "synthetic: h = ReLU(N(0,1)), Zipf(1.0) sparse labels, Philox-initialized W/idx (no dataset)",
         "config": {"workload": shape.name, "L": shape.L, "m": shape.m, "k": shape.k, "B": B, "global_batch": B,
                    "avg_pos": shape.avg_pos, "parallelism": f"label-shard x{world}", "dh_mode": a.dh_mode,
+                   "loss": a.loss, "margin_bias": a.margin_bias, "grad_skip_fraction": skip_fraction,
                    "redistribution": f"every {REDIST_EVERY} steps inside the timed region (global step counter)",
                    "l2": "no flush: per-step state stream 617 MB >> 126 MB L2 (inputs larger than L2)"},
         "clocks": {"sm_mhz": c1["sm_mhz"], "sm_max_mhz": c1["sm_max_mhz"], "reasons": c1["reasons"],

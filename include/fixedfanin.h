@@ -71,6 +71,11 @@ typedef enum {
 #define FF_FLAG_NO_PIPE 4u       /* use the generic fused kernel even where the pipelined one
                                     applies (k = 32, B <= 32); same results, for A/B tests     */
 
+/* ff_config.loss: the one-vs-all binary loss whose gradient the backward pass consumes */
+#define FF_LOSS_BCE 0            /* binary cross-entropy with logits (the north star's) */
+#define FF_LOSS_SQH 1            /* squared hinge max(0, 1 - y yhat)^2, y = +-1, whose
+                                    exact zeros are skipped (implicit negative mining, §3.3)     */
+
 /* ff_config.dh_mode */
 #define FF_DH_ATOMIC 0           /* dh by coalesced red.global.add (Alg. 2 with atomics) */
 #define FF_DH_CSC 1              /* dh by a transposed (CSC) index gather, rebuilt after redistribution */
@@ -90,6 +95,7 @@ typedef struct {
     float beta1, beta2, eps;   /* Adam; 0 -> 0.9 / 0.999 / 1e-8 (R6)                            */
     float prune_frac;    /* SET fraction alpha, p = floor(alpha*k) per row; 0 -> 0.1    */
     uint32_t flags;      /* FF_FLAG_*                                                           */
+    int32_t loss;        /* FF_LOSS_BCE (default) or FF_LOSS_SQH                                */
 } ff_config;
 
 /* Bytes of device workspace the layer needs for `cfg` (host-only, no CUDA calls). */
@@ -123,12 +129,15 @@ ff_status fixedfanin_get_params(ff_layer* layer, float* W, int32_t* idx, float* 
 ff_status fixedfanin_forward(ff_layer* layer, const float* h, int32_t B, float* y,
                              ff_stream_t stream);
 
-/* BCE-with-logits gradient g = grad_scale*(sigmoid(y) - t) (R4, R5), then
+/* Loss gradient — BCE g = grad_scale*(sigmoid(y) - t) (R4, R5), or with
+ * FF_LOSS_SQH g = grad_scale*(-2 t' max(0, 1 - t' y)), t' = +-1 — then
  * Alg. 3 dW[j][i] = sum_b g[b][j] h[b][idx[j][i]], db[j] = sum_b g[b][j]
  * (kept in the workspace for adam_step/get_grads), and Alg. 2
  * dh[b][c] = sum_{(j,i): idx[j][i]=c} W[j][i] g[b][j] (overwritten).  `y` must be the
  * scores of the same h (e.g. from fixedfanin_forward).  loss (device float[1] or NULL)
- * = grad_scale * sum_{b,j} softplus(y) - t*y.                                        */
+ * = grad_scale * sum_{b,j} softplus(y) - t*y  (BCE)  or  max(0, 1 - t' y)^2  (SQH).
+ * Exact-zero gradients (SQH) are skipped: no dh reductions / CSC gathers for them
+ * (the paper's Alg. 2 early exit); results equal the unskipped sums.       */
 ff_status fixedfanin_backward(ff_layer* layer, const float* h, const float* y, int32_t B,
                               const int32_t* lbl_ptr, const int32_t* lbl_ids,
                               float grad_scale, float* dh, float* loss, ff_stream_t stream);

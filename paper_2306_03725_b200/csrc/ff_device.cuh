@@ -145,6 +145,16 @@ __device__ __forceinline__ float bce_loss_term(float y, bool pos, float e) {
   return fmaxf(y, 0.0f) - (pos ? y : 0.0f) + l1p;
 }
 
+// Squared hinge with t' = +1 for positives, -1 for negatives:
+// g = s * (-2 t' max(0, 1 - t' y)) — exactly zero when t' y >= 1 (the sign of 1 - t'y is
+// exact in fp32 since t'y is); *lterm = max(0, 1 - t' y)^2.
+__device__ __forceinline__ float sqh_grad(float y, bool pos, float s, float* lterm) {
+  const float t = pos ? 1.0f : -1.0f;
+  const float mg = fmaxf(0.0f, __fsub_rn(1.0f, t * y));
+  *lterm = mg * mg;
+  return s * (-2.0f * t * mg);
+}
+
 struct AdamArgs {
   float lr, beta1, beta2, one_minus_b1, one_minus_b2, rbc1, rbc2, eps;   // rbc = 1/(1 - beta^t)
 };

@@ -49,7 +49,17 @@ struct RowArgs {
   int* err;
   AdamArgs adam;
   uint32_t check_finite;
+  int sqh;                    // loss: 0 = BCE, 1 = squared hinge (exact zeros skipped)
 };
+
+// Loss gradient of one score and its loss term (BCE or squared hinge).
+__device__ __forceinline__ float loss_grad(float y, bool pos, float s, bool sqh, float* lterm) {
+  if (sqh) return sqh_grad(y, pos, s, lterm);
+  float e;
+  const float g = bce_grad(y, pos, s, &e);
+  *lterm = bce_loss_term(y, pos, e);
+  return g;
+}
 
 __device__ __forceinline__ float comp(const float4& v, int e) {
   return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
@@ -262,6 +272,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
 #pragma unroll
       for (int q = 0; q < NG; ++q) dwp[q] = 0.0f;
       float dbp = 0.0f;
+      bool gany = false;                               // any nonzero gradient in this row
 
       for (int q2 = 0; q2 < nb; ++q2) {
         const int lo = q2 * 32 + 4 * bq;             // this lane's 4-sample segment
@@ -284,10 +295,11 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
           if (lane == 0 && pm != 0u) a.posmask[(int64_t)q2 * L + j] = 0u;
         }
         const bool pos = (pm >> (4 * bq + gq)) & 1u;
-        float e;
-        float g = bce_grad(y, pos, a.grad_scale, &e);
+        float lt;
+        float g = loss_grad(y, pos, a.grad_scale, a.sqh != 0, &lt);
         if (b >= B) g = 0.0f;
-        if (a.loss != nullptr && b < B) loss_acc += bce_loss_term(y, pos, e);
+        if (a.loss != nullptr && b < B) loss_acc += lt;
+        gany |= __any_sync(kFull, g != 0.0f);
         if (a.check_finite && __any_sync(kFull, b < B && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
         dbp += g;
         float4 g4;
@@ -301,17 +313,21 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
           // CSC mode: publish g[., j] (one 128-B line per chunk); dh is pulled later (k_dh_csc)
           st_hint(a.gT + ((j - jb) * nb + q2) * 32 + 4 * bq + gq, g, pol_l);
         } else {
-          // Alg. 2 with the pre-update weights: dh[b][idx[j][i]] += W[j][i] g[b][j]
+          // Alg. 2 with the pre-update weights: dh[b][idx[j][i]] += W[j][i] g[b][j], skipping
+          // this lane's reductions when its 4 gradients are exactly zero
+          const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
           for (int q = 0; q < NG; ++q) {
-            if (FULL || 4 * q + gq < k)
+            if ((FULL || 4 * q + gq < k) && gnz)
               red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
           }
         }
       }
       if (MODE == kModeForward) continue;
 
-      if (CSC && act) a.wcsc[pe] = w;                 // pre-update W in CSC order (for k_dh_csc)
+      // pre-update W in CSC order for k_dh_csc; 0 when the row's gradient is all zero, so the
+      // column pass skips the gather (its contribution w*g is exactly zero anyway)
+      if (CSC && act) a.wcsc[pe] = gany ? w : 0.0f;
       const float gW = row_dw_slot<NG>(dwp, lane);
       gbuf.v[i][4 * bq + gq] = dbp;                   // this lane's sample (over all chunks)
       if (MODE == kModeBackward || STORE_GRADS) {
@@ -380,7 +396,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   float* const W = a.W; float* const mW = a.mW; float* const vW = a.vW;
   const int* const idx = a.idx; const int* const pos = a.pos;
   const float grad_scale = a.grad_scale;
-  const bool want_loss = a.loss != nullptr, check = a.check_finite != 0;
+  const bool want_loss = a.loss != nullptr, check = a.check_finite != 0, sqh = a.sqh != 0;
   const int64_t jb = a.j_begin, je = a.j_end;
   const int nblk = (int)((je - jb + 31) >> 5);
   const int b = 4 * bq + gq;                            // this lane's own sample
@@ -474,10 +490,11 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     } else
     y = row_score_own<NG>(ws, hv, gq, bj);
     const bool pos_ = (pm >> b) & 1u;
-    float e = 0.5f;
-    float g = (FF_ABLATE & 8) ? y * grad_scale : bce_grad(y, pos_, grad_scale, &e);
+    float lt = 0.0f;
+    float g = (FF_ABLATE & 8) ? y * grad_scale : loss_grad(y, pos_, grad_scale, sqh, &lt);
     if (!bvalid) g = 0.0f;
-    if (want_loss && bvalid) loss_acc += bce_loss_term(y, pos_, e);
+    if (want_loss && bvalid) loss_acc += lt;
+    const bool gany = __any_sync(kFull, g != 0.0f);
     if (check && __any_sync(kFull, bvalid && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
     float4 g4;
     if (FF_ABLATE & 128) { g4 = make_float4(g, g * 0.5f, g * 0.25f, g * 2.0f); } else {
@@ -492,12 +509,13 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     if (CSC) {
       if (!(FF_ABLATE & 32)) {                             // ablation: no g / W_old publication
         st_hint(a.gT + (j - jb) * 32 + b, g, pol_l);
-        a.wcsc[st.pe] = st.w;
+        a.wcsc[st.pe] = gany ? st.w : 0.0f;                // 0: column pass skips (w*g == 0)
       }
     } else {
+      const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
       for (int q = 0; q < NG; ++q)
-        red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
+        if (gnz) red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
     }
     const float gW = (FF_ABLATE & 16) ? dwp[lane & 7] : row_dw_slot<NG>(dwp, lane);
     gbuf.v[i][b] = g;
@@ -589,12 +607,11 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
         for (int u = 0; u < 8; ++u) {
           const uint32_t off = (uint32_t)(__shfl_sync(kFull, jr, 4 * u + gq) - jb) * gstride;
           ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
-          if (tail) {
-            gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (p + 4 * u + gq < p1) gv[u] = ld_line4(at_bytes(gb, off), pol_l);
-          } else {
-            gv[u] = ld_line4(at_bytes(gb, off), pol_l);
-          }
+          // entries with a zero weight contribute exactly zero: no gather (this is how the
+          // implicit negative mining reaches the column pass: the row pass publishes 0 for
+          // rows whose gradient is all zero)
+          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if ((!tail || p + 4 * u + gq < p1) && ww[u] != 0.0f) gv[u] = ld_line4(at_bytes(gb, off), pol_l);
         }
         float2 a01 = lo2(acc), a23 = hi2(acc);
 #pragma unroll

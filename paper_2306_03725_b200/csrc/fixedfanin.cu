@@ -119,6 +119,7 @@ ff_status validate(const ff_config* c) {
   if (c->dh_mode == FF_DH_CSC && c->L_local * (int64_t)c->k >= (int64_t(1) << 31))
     return fail(FF_ERR_CONFIG, "CSC mode needs L_local*k < 2^31");
   if (c->prune_frac < 0.0f || c->prune_frac >= 1.0f) return fail(FF_ERR_CONFIG, "prune_frac outside [0, 1)");
+  if (c->loss != FF_LOSS_BCE && c->loss != FF_LOSS_SQH) return fail(FF_ERR_CONFIG, "loss=%d unknown", c->loss);
   if (c->beta1 < 0.0f || c->beta1 >= 1.0f || c->beta2 < 0.0f || c->beta2 >= 1.0f || c->eps < 0.0f)
     return fail(FF_ERR_CONFIG, "Adam hyper-parameters out of range");
   return FF_OK;
@@ -206,6 +207,7 @@ RowArgs row_args(ff_layer* l, int B) {
   a.pos = l->pos; a.wcsc = l->wcsc; a.gT = l->gT;
   a.j_begin = 0; a.j_end = l->cfg.L_local;
   a.check_finite = (l->cfg.flags & FF_FLAG_CHECK_FINITE) ? 1u : 0u;
+  a.sqh = l->cfg.loss == FF_LOSS_SQH ? 1 : 0;
   return a;
 }
 

@@ -114,26 +114,34 @@ def test_forward_parity(L, m, k, B):
 DH = pytest.mark.parametrize("dh_mode", [0, 1], ids=["atomic", "csc"])
 
 
+LOSS = pytest.mark.parametrize("loss", ["bce", "sqh"])
+
+
+def loss_id(loss):
+    return L_().FF_LOSS_SQH if loss == "sqh" else L_().FF_LOSS_BCE
+
+
+@LOSS
 @DH
 @pytest.mark.parametrize("L,m,k,B", CASES)
-def test_backward_and_adam_parity(L, m, k, B, dh_mode):
-    lay = make(L, m, k, B=B, seed=8, dh_mode=dh_mode)
+def test_backward_and_adam_parity(L, m, k, B, dh_mode, loss):
+    lay = make(L, m, k, B=B, seed=8, dh_mode=dh_mode, loss=loss_id(loss))
     W, idx, bias = synth.random_params(L, m, k, seed=L + 2 * B, scale=0.5)
     lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
     h = synth.hidden_batch(B, m, step=4)
     ptr, ids = synth.label_batch(B, L, 5.0, step=4)
     y = lay.forward(tens(h))
-    loss = torch.zeros(1, device=dev())
-    dh, _ = lay.backward(tens(h), y, tens(ptr), tens(ids), loss=loss)
+    loss_t = torch.zeros(1, device=dev())
+    dh, _ = lay.backward(tens(h), y, tens(ptr), tens(ids), loss=loss_t)
     dW, db = lay.get_grads()
     yn = y.cpu().numpy().astype(np.float64)
-    g, lr_ = oracle.bce_grad(yn, ptr, ids, F32(1.0 / B))
+    g, lr_ = oracle.loss_grad(loss, yn, ptr, ids, F32(1.0 / B))
     dWr, AdW, dbr, Adb = oracle.weight_grad(idx, h, g)
     dhr, Adh = oracle.input_grad(W, idx, g, m)
     assert_close(dW.cpu().numpy(), dWr, AdW, "dW")
     assert_close(db.cpu().numpy(), dbr, Adb, "db")
     assert_close(dh.cpu().numpy(), dhr, Adh, "dh")
-    assert abs(loss.item() - lr_) <= RTOL * abs(lr_)
+    assert abs(loss_t.item() - lr_) <= RTOL * abs(lr_)
     # Adam on the GPU's gradients (lockstep): elementwise fp32 vs fp64
     lay.adam_step(1e-3)
     s = state_of(lay)
@@ -181,11 +189,13 @@ def test_fused_step_equals_unfused_path(L, m, k, B, dh_mode):
         assert abs(la.item() - lb.item()) <= 1e-5 * abs(lb.item())
 
 
+@LOSS
 @DH
-def test_fused_step_lockstep_vs_oracle(dh_mode):
-    L, m, k, B = 1000, 256, 16, 32
+@pytest.mark.parametrize("k", [16, 32])
+def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k):
+    L, m, B = 1000, 256, 32
     layer = L_()
-    lay = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, seed=42, dh_mode=dh_mode)
+    lay = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, seed=42, dh_mode=dh_mode, loss=loss_id(loss))
     for step in range(5):
         s0 = state_of(lay)
         st = oracle.State(s0["W"].astype(np.float64), s0["idx"], s0["bias"].astype(np.float64),
@@ -193,14 +203,14 @@ def test_fused_step_lockstep_vs_oracle(dh_mode):
                           s0["vb"].astype(np.float64), s0["t"])
         h = synth.hidden_batch(B, m, step=step)
         ptr, ids = synth.label_batch(B, L, 5.0, step=step)
-        loss = torch.zeros(1, device=dev())
-        dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3), loss=loss)
+        loss_t = torch.zeros(1, device=dev())
+        dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3), loss=loss_t)
         dW, db = lay.get_grads()
-        r = oracle.train_step(st, h, ptr, ids, F32(1.0 / B), F32(1e-3), **ADAM)
+        r = oracle.train_step(st, h, ptr, ids, F32(1.0 / B), F32(1e-3), loss=loss, **ADAM)
         assert_close(dh.cpu().numpy(), r.dh, r.Adh, f"dh step {step}")
         assert_close(dW.cpu().numpy(), r.dW, r.AdW, f"dW step {step}")
         assert_close(db.cpu().numpy(), r.db, r.Adb, f"db step {step}")
-        assert abs(loss.item() - r.loss) <= RTOL * r.loss
+        assert abs(loss_t.item() - r.loss) <= RTOL * r.loss
         # Adam applied by the oracle to the GPU's gradient: tight elementwise parity
         s1 = state_of(lay)
         Wr, mr, vr = oracle.adam(s0["W"], dW.cpu().numpy(), s0["mW"], s0["vW"], s0["t"] + 1, F32(1e-3), **ADAM)
@@ -482,16 +492,17 @@ def test_csc_multi_tile_dh_and_grads():
     assert_close(db[rows], dbr, Adb, "db rows")
 
 
+@LOSS
 @DH
 @pytest.mark.parametrize("L,m,B", [(5000, 1024, 32), (1234, 700, 19), (31, 64, 32), (70000, 4096, 32)])
-def test_pipelined_step_equals_generic_step(L, m, B, dh_mode):
+def test_pipelined_step_equals_generic_step(L, m, B, dh_mode, loss):
     """k = 32, B <= 32 runs the software-pipelined fused kernel; FF_FLAG_NO_PIPE forces the
     generic one.  Both implement the same arithmetic: state and gradients bit-identical."""
     layer = L_()
     k = 32
     flags = layer.FF_FLAG_STORE_GRADS
-    a = make(L, m, k, B=B, seed=12, flags=flags, dh_mode=dh_mode)
-    b = make(L, m, k, B=B, seed=12, flags=flags | layer.FF_FLAG_NO_PIPE, dh_mode=dh_mode)
+    a = make(L, m, k, B=B, seed=12, flags=flags, dh_mode=dh_mode, loss=loss_id(loss))
+    b = make(L, m, k, B=B, seed=12, flags=flags | layer.FF_FLAG_NO_PIPE, dh_mode=dh_mode, loss=loss_id(loss))
     for step in range(3):
         h = tens(synth.hidden_batch(B, m, step=step))
         ptr, ids = synth.label_batch(B, L, 5.0, step=step)
@@ -508,3 +519,36 @@ def test_pipelined_step_equals_generic_step(L, m, B, dh_mode):
         else:
             assert dh_close(dha, dhb)
         assert abs(la.item() - lb.item()) <= 1e-5 * abs(lb.item())
+
+
+
+@DH
+@pytest.mark.parametrize("k,B", [(32, 32), (32, 20), (16, 32), (13, 40)])
+def test_sqh_implicit_negative_mining_skips_are_exact(dh_mode, k, B):
+    """Engineered margins (bias = -3): most negatives meet the margin, so most of the
+    squared-hinge gradient is exactly zero and the kernels skip that work.
+    Skipping must not change anything: dW rows whose gradient column is all zero are
+    exactly 0, and dh / dW / W' match the oracle, which never skips."""
+    layer = L_()
+    L, m = 4000, 1024
+    lay = make(L, m, k, B=max(B, 32), seed=31, dh_mode=dh_mode, loss=layer.FF_LOSS_SQH,
+               flags=layer.FF_FLAG_STORE_GRADS)
+    W, idx, _ = synth.random_params(L, m, k, seed=4, scale=0.3)
+    bias = np.full(L, -3.0, np.float32)
+    lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    h = synth.hidden_batch(B, m, step=7)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=7)
+    y = lay.forward(tens(h)).cpu().numpy().astype(np.float64)
+    loss = torch.zeros(1, device=dev())
+    dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3), loss=loss)
+    dW, db = (x.cpu().numpy() for x in lay.get_grads())
+    g, lref = oracle.sqh_grad(y, ptr, ids, F32(1.0 / B))
+    zero_cols = (g == 0).all(axis=0)
+    assert zero_cols.mean() > 0.5                      # the skip really happens
+    assert (dW[zero_cols] == 0).all() and (db[zero_cols] == 0).all()
+    dWr, AdW, dbr, Adb = oracle.weight_grad(idx, h, g)
+    dhr, Adh = oracle.input_grad(W, idx, g, m)
+    assert_close(dW, dWr, AdW, "dW")
+    assert_close(db, dbr, Adb, "db")
+    assert_close(dh.cpu().numpy(), dhr, Adh, "dh")
+    assert abs(loss.item() - lref) <= RTOL * lref
