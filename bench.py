@@ -386,14 +386,15 @@ def main():
         run_reference(a, shape, world, rank)
         return
     import __graft_entry__
-    if rank == 0:
-        __graft_entry__.build_lib()
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        dist.barrier()
+    if rank == 0:
+        __graft_entry__.build_lib()          # no-op when the in-tree .so is current
+    if world > 1:
+        dist.barrier()                       # the other ranks load the library only after rank 0 built it
     run_ours(a, shape, world, rank, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -82,45 +82,47 @@ __device__ __forceinline__ void block_atomic_add(float v, float* dst) {
 // ---- shared pieces of the row kernels (forward / fused step / predict use the SAME
 // arithmetic, so their scores are bit-identical: the top-K parity relies on it)
 
-// Broadcast each connection's weight and hd column BYTE offset to the lanes that gather
-// it: lane (gq, bq) handles connections s = 4q + gq, q < NG.  cbytes = 4*cstride.
+// Broadcast each connection's weight and hd column to the lanes that gather it: lane
+// (gq, bq) handles connections s = 4q + gq, q < NG.  Columns stay raw 32-bit indices: the
+// line address base + c * cfloats is then one IMAD.WIDE.U32 at the load.
 template <int NG>
-__device__ __forceinline__ void row_spread(float w, int c, uint32_t cbytes, int gq, float (&ws)[NG], uint32_t (&cs)[NG]) {
+__device__ __forceinline__ void row_spread(float w, int c, int gq, float (&ws)[NG], uint32_t (&cs)[NG]) {
 #pragma unroll
   for (int q = 0; q < NG; ++q) {
     ws[q] = __shfl_sync(kFull, w, 4 * q + gq);
-    cs[q] = (uint32_t)__shfl_sync(kFull, c, 4 * q + gq) * cbytes;
+    cs[q] = (uint32_t)__shfl_sync(kFull, c, 4 * q + gq);
   }
 }
 
-__device__ __forceinline__ const float* at_bytes(const float* base, uint32_t off) {
-  return reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + off);
+__device__ __forceinline__ const float* col_line(const float* hb, uint32_t c, uint32_t cfloats) {
+  return hb + (size_t)c * cfloats;
 }
-__device__ __forceinline__ float* at_bytes(float* base, uint32_t off) {
-  return reinterpret_cast<float*>(reinterpret_cast<char*>(base) + off);
+__device__ __forceinline__ float* col_line(float* hb, uint32_t c, uint32_t cfloats) {
+  return hb + (size_t)c * cfloats;
 }
 
 // Gather this lane's 16-B segment of each connection's 128-B h line (hb = the lane's
 // segment in column 0 of the chunk).  FULL: k == 4*NG, every slot exists (no guards).
 template <int NG, bool FULL>
-__device__ __forceinline__ void row_gather(const float* hb, const uint32_t (&cs)[NG], int k, int gq,
+__device__ __forceinline__ void row_gather(const float* hb, const uint32_t (&cs)[NG], uint32_t cfloats, int k, int gq,
                                            uint64_t pol, float4 (&hv)[NG]) {
 #pragma unroll
   for (int q = 0; q < NG; ++q) {
     if (FULL) {
-      hv[q] = ld_line4(at_bytes(hb, cs[q]), pol);
+      hv[q] = ld_line4(col_line(hb, cs[q], cfloats), pol);
     } else {
       hv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (4 * q + gq < k) hv[q] = ld_line4(at_bytes(hb, cs[q]), pol);
+      if (4 * q + gq < k) hv[q] = ld_line4(col_line(hb, cs[q], cfloats), pol);
     }
   }
 }
 
 // The same gather without the L2 policy operand (hot loop of the pipelined kernel).
 template <int NG>
-__device__ __forceinline__ void row_gather_plain(const float* hb, const uint32_t (&cs)[NG], float4 (&hv)[NG]) {
+__device__ __forceinline__ void row_gather_plain(const float* hb, const uint32_t (&cs)[NG], uint32_t cfloats,
+                                                 float4 (&hv)[NG]) {
 #pragma unroll
-  for (int q = 0; q < NG; ++q) hv[q] = ld_line4_plain(at_bytes(hb, cs[q]));
+  for (int q = 0; q < NG; ++q) hv[q] = ld_line4_plain(col_line(hb, cs[q], cfloats));
 }
 
 // y for this lane's own sample lo + gq: per-lane FMAs over its connections, then a
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol_s = policy_evict_first(), pol_l = policy_evict_last();
   const int k = FULL ? 4 * NG : a.k, nb = a.nb, B = a.B;
-  const uint32_t cbytes = 4u * (uint32_t)a.cstride;
+  const uint32_t cfl = (uint32_t)a.cstride;
   float* const hd_lane = a.hd + 4 * bq;            // this lane's segment, column 0, chunk 0
   const int64_t L = a.L, jb = a.j_begin, nblk = (a.j_end - jb + 31) >> 5;
   const bool act = lane < k;
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
       uint32_t pm = __shfl_sync(kFull, pm_v, i);
 
       float ws[NG]; uint32_t cs[NG];
-      row_spread<NG>(w, c, cbytes, gq, ws, cs);
+      row_spread<NG>(w, c, gq, ws, cs);
       float dwp[NG];
 #pragma unroll
       for (int q = 0; q < NG; ++q) dwp[q] = 0.0f;
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
         const int b = lo + gq;                        // this lane's own sample
         float* hb = hd_lane + q2 * 64;                // h segment; its dh segment is +32 floats
         float4 hv[NG];
-        row_gather<NG, FULL>(hb, cs, k, gq, pol_l, hv);
+        row_gather<NG, FULL>(hb, cs, cfl, k, gq, pol_l, hv);
         float y;
         if (MODE != kModeBackward) {
           y = row_score_own<NG>(ws, hv, gq, bj);
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
 #pragma unroll
           for (int q = 0; q < NG; ++q) {
             if ((FULL || 4 * q + gq < k) && gnz)
-              red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
+              red_add4(col_line(hb, cs[q], cfl) + 32, dh_contrib(ws[q], g4), pol_l);
           }
         }
       }
@@ -387,7 +389,7 @@ struct PipeCursor {             // position of one row in this warp's sequence o
 template <bool STORE_GRADS, bool CSC>
 __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(RowArgs a) {
   constexpr int NG = 8;
-  constexpr uint32_t kColBytes = 256;                   // hd column stride at nb = 1 (h | dh lines)
+  constexpr uint32_t kColFloats = 64;                   // hd column stride at nb = 1 (h | dh lines)
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int nwarp = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   const uint64_t pol_l = policy_evict_last();
@@ -414,11 +416,10 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   };
   auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * 32 + c.i; };
 
-  struct St { float w, mw, vw; int c, pe; int64_t row; };
+  struct St { float w, mw, vw; int c, pe; };
   auto load_st = [&](const Cur& cu, St& st) {
     if (cu.blk < nblk) {
-      const int64_t row = row_of(cu) * 32 + lane;
-      st.row = row - lane;
+      const uint32_t row = (uint32_t)row_of(cu) * 32u + lane;   // L*k < 2^31: 32-bit indices
       if (FF_ABLATE & 2) {                                  // ablation: no state loads
         st.w = 0.01f * lane; st.c = (int)((row * 2654435761u) & 32767); st.mw = 0.f; st.vw = 0.f; st.pe = (int)row;
         return;
@@ -452,22 +453,13 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
 
   float wsA[NG], wsB[NG]; uint32_t csA[NG], csB[NG]; float4 hvA[NG], hvB[NG];
   auto issue = [&](const St& st, float (&ws)[NG], uint32_t (&cs)[NG], float4 (&hv)[NG]) {
-    if (FF_ABLATE & 64) {                                  // ablation: gather-layout loads, no spread shuffles
-      const float4 w0 = *reinterpret_cast<const float4*>(W + st.row + gq * 8);
-      const float4 w1 = *reinterpret_cast<const float4*>(W + st.row + gq * 8 + 4);
-      const int4 c0 = *reinterpret_cast<const int4*>(idx + st.row + gq * 8);
-      const int4 c1 = *reinterpret_cast<const int4*>(idx + st.row + gq * 8 + 4);
-      ws[0] = w0.x; ws[1] = w0.y; ws[2] = w0.z; ws[3] = w0.w; ws[4] = w1.x; ws[5] = w1.y; ws[6] = w1.z; ws[7] = w1.w;
-      cs[0] = c0.x * kColBytes; cs[1] = c0.y * kColBytes; cs[2] = c0.z * kColBytes; cs[3] = c0.w * kColBytes;
-      cs[4] = c1.x * kColBytes; cs[5] = c1.y * kColBytes; cs[6] = c1.z * kColBytes; cs[7] = c1.w * kColBytes;
-    } else
-    row_spread<NG>(st.w, st.c, kColBytes, gq, ws, cs);
+    row_spread<NG>(st.w, st.c, gq, ws, cs);
     // atomic mode: keep hd (h and dh lines) evict_last against the state stream, else plain
     if (FF_ABLATE & 1) {                                   // ablation: no gathers
 #pragma unroll
       for (int q = 0; q < NG; ++q) hv[q] = make_float4(__uint_as_float(cs[q] & 0x3fffff), 0.5f, 0.25f, 0.125f);
-    } else if (CSC) row_gather_plain<NG>(hb, cs, hv);
-    else row_gather<NG, true>(hb, cs, 32, gq, pol_l, hv);
+    } else if (CSC) row_gather_plain<NG>(hb, cs, kColFloats, hv);
+    else row_gather<NG, true>(hb, cs, kColFloats, 32, gq, pol_l, hv);
   };
   issue(sX, wsA, csA, hvA);
   load_st(Z, sZ);
@@ -508,18 +500,18 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     for (int q = 0; q < NG; ++q) dwp[q] = 0.0f + dw_partial(g4, hv[q]);
     if (CSC) {
       if (!(FF_ABLATE & 32)) {                             // ablation: no g / W_old publication
-        st_hint(a.gT + (j - jb) * 32 + b, g, pol_l);
-        a.wcsc[st.pe] = gany ? st.w : 0.0f;                // 0: column pass skips (w*g == 0)
+        st_hint(a.gT + (size_t)((uint32_t)(j - jb) * 32u + b), g, pol_l);
+        a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;      // 0: column pass skips (w*g == 0)
       }
     } else {
       const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
       for (int q = 0; q < NG; ++q)
-        if (gnz) red_add4(at_bytes(hb, cs[q]) + 32, dh_contrib(ws[q], g4), pol_l);
+        if (gnz) red_add4(col_line(hb, cs[q], kColFloats) + 32, dh_contrib(ws[q], g4), pol_l);
     }
     const float gW = (FF_ABLATE & 16) ? dwp[lane & 7] : row_dw_slot<NG>(dwp, lane);
     gbuf.v[i][b] = g;
-    const int64_t row = j * 32 + lane;
+    const uint32_t row = (uint32_t)j * 32u + lane;
     if (STORE_GRADS) a.dW[row] = gW;
     if (FF_ABLATE & 4) {                                   // ablation: no Adam, one store
       st_na(W + row, st.w + gW);
@@ -592,7 +584,7 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
   const uint64_t pol_l = policy_evict_last();
   const int* cp = col_ptr + (int64_t)tile * m;
   const int jb = (int)j_begin;
-  const uint32_t gstride = 128u * (uint32_t)nb;              // bytes per gT row
+  const uint32_t gstride = 32u * (uint32_t)nb;               // floats per gT row
   for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < m; c += nw) {
     const int p0 = cp[c], p1 = cp[c + 1];
     for (int q2 = 0; q2 < nb; ++q2) {
@@ -605,13 +597,13 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
         float4 gv[8]; float ww[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const uint32_t off = (uint32_t)(__shfl_sync(kFull, jr, 4 * u + gq) - jb) * gstride;
+          const uint32_t grow = (uint32_t)(__shfl_sync(kFull, jr, 4 * u + gq) - jb);
           ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
           // entries with a zero weight contribute exactly zero: no gather (this is how the
           // implicit negative mining reaches the column pass: the row pass publishes 0 for
           // rows whose gradient is all zero)
           gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if ((!tail || p + 4 * u + gq < p1) && ww[u] != 0.0f) gv[u] = ld_line4(at_bytes(gb, off), pol_l);
+          if ((!tail || p + 4 * u + gq < p1) && ww[u] != 0.0f) gv[u] = ld_line4(col_line(gb, grow, gstride), pol_l);
         }
         float2 a01 = lo2(acc), a23 = hi2(acc);
 #pragma unroll
@@ -890,7 +882,7 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
   for (int q2 = 0; q2 < nb; ++q2) {
     const int lo = q2 * 32 + 4 * bq;
     const int b = lo + gq;
-    const uint32_t cbytes = 256u * (uint32_t)nb;
+    const uint32_t cfl = 64u * (uint32_t)nb;
     const float* hb = hd + q2 * 64 + 4 * bq;
     float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll
@@ -909,8 +901,8 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
         bj_n = ld_stream(bias + jn, pol_s);
       }
       float ws[NG]; uint32_t cs[NG]; float4 hv[NG];
-      row_spread<NG>(w, c, cbytes, gq, ws, cs);
-      row_gather<NG, FULL>(hb, cs, k, gq, pol_l, hv);
+      row_spread<NG>(w, c, gq, ws, cs);
+      row_gather<NG, FULL>(hb, cs, cfl, k, gq, pol_l, hv);
       const float y = row_score_own<NG>(ws, hv, gq, bj);
       if (b < B) topk_insert(ts, ti, y, (int)(row_begin + j));
     }
