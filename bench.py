@@ -52,8 +52,9 @@ def args_():
     p.add_argument("--margin-bias", type=float, default=0.0,
                    help="sqh: start every label bias at -X so that a controlled fraction of negatives meets the "
                         "margin (engineered-margin analog of a trained model, SURVEY §8(f) NEXT-1)")
-    p.add_argument("--dh-mode", default="csc", choices=["atomic", "csc"],
-                   help="dh scatter: red.global atomics or the CSC pull (DESIGN.md §6; chosen by measurement)")
+    p.add_argument("--dh-mode", default="atomic", choices=["atomic", "csc"],
+                   help="dh scatter: red.global atomics (default: measured faster, DESIGN.md §6) or the "
+                        "deterministic CSC pull")
     return p.parse_args()
 
 
