@@ -191,7 +191,7 @@ def run_ours(a, shape, world, rank, local_rank):
     from paper_2306_03725_b200.layer import last_launch_count
     from paper_2306_03725_b200.sharded import ShardedLayer
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     B = shape.B
     data = [(synth.hidden_batch(B, shape.m, step=s), *synth.label_batch(B, shape.L, shape.avg_pos, step=s))
@@ -365,6 +365,18 @@ def run_ours(a, shape, world, rank, local_rank):
                     "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,
                     "frac": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9 / peak},
     }
+    # NEXT-4 memory report: this layer's device bytes vs the dense/COO formats of P:37-45
+    Lk = shape.L * shape.k
+    line["memory"] = {
+        "workspace_bytes_per_gpu": int(eng.workspace.numel()),
+        "peak_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
+        "uniform_params_bytes": 8 * Lk + 4 * shape.L,                 # W + idx (32-bit) + bias
+        "uniform_with_adam_bytes": 16 * Lk + 12 * shape.L,            # + mW, vW, mb, vb
+        "coo64_params_bytes": 20 * Lk,                                # 2 x int64 + fp32 per nnz
+        "dense_params_bytes": 4 * shape.m * shape.L,                  # the dense layer it replaces
+        "dense_with_adam_bytes": 12 * shape.m * shape.L,              # weights + two moments
+        "note": "dense figures for a dense m x L last layer of the same width (P:37-45 quotes 10.7 GiB "
+                "/ >40 GiB for Amazon-3M at 1024 hidden)"}
     if world == 1 and not a.no_cpu_baseline:
         import oracle
         oracle.build()
@@ -390,8 +402,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # NCCL (one rank per GPU) in production; FF_BENCH_BACKEND=gloo lets several ranks share
+        # one GPU to exercise the multi-rank path where only one GPU is available (tests only)
+        backend = os.environ.get("FF_BENCH_BACKEND", "nccl")
+        gpu = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     if rank == 0:
         __graft_entry__.build_lib()          # no-op when the in-tree .so is current
     if world > 1:

@@ -376,9 +376,6 @@ constexpr int kPipeThreads = FF_PIPE_THREADS;
 #ifndef FF_WS_RECOMPUTE
 #define FF_WS_RECOMPUTE 1   // CSC mode: re-shuffle the row's weights at compute time (saves registers)
 #endif
-#ifndef FF_ABLATE
-#define FF_ABLATE 0      // dev-only ablation switches of k_train_pipe (timing experiments; wrong results)
-#endif
 constexpr int kPipeMinBlocks = FF_PIPE_MINB;
 
 struct PipeCursor {             // position of one row in this warp's sequence of rows
@@ -420,10 +417,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   auto load_st = [&](const Cur& cu, St& st) {
     if (cu.blk < nblk) {
       const uint32_t row = (uint32_t)row_of(cu) * 32u + lane;   // L*k < 2^31: 32-bit indices
-      if (FF_ABLATE & 2) {                                  // ablation: no state loads
-        st.w = 0.01f * lane; st.c = (int)((row * 2654435761u) & 32767); st.mw = 0.f; st.vw = 0.f; st.pe = (int)row;
-        return;
-      }
       st.w = ld_na(W + row);
       st.c = ld_na_ro(idx + row);
       st.mw = ld_na(mW + row);
@@ -455,10 +448,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   auto issue = [&](const St& st, float (&ws)[NG], uint32_t (&cs)[NG], float4 (&hv)[NG]) {
     row_spread<NG>(st.w, st.c, gq, ws, cs);
     // atomic mode: keep hd (h and dh lines) evict_last against the state stream, else plain
-    if (FF_ABLATE & 1) {                                   // ablation: no gathers
-#pragma unroll
-      for (int q = 0; q < NG; ++q) hv[q] = make_float4(__uint_as_float(cs[q] & 0x3fffff), 0.5f, 0.25f, 0.125f);
-    } else if (CSC) row_gather_plain<NG>(hb, cs, kColFloats, hv);
+    if (CSC) row_gather_plain<NG>(hb, cs, kColFloats, hv);
     else row_gather<NG, true>(hb, cs, kColFloats, 32, gq, pol_l, hv);
   };
   issue(sX, wsA, csA, hvA);
@@ -473,54 +463,39 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     const int i = cu.i;
     const float bj = __shfl_sync(kFull, bv.bias, i);
     const uint32_t pm = __shfl_sync(kFull, bv.pm, i);
-    float y;
-    if (FF_ABLATE & 128) {                                 // ablation: no score reduce-scatter shuffles
-      float2 y01 = make_float2(0.f, 0.f), y23 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int q = 0; q < NG; ++q) { y01 = ffma2(bc2(ws[q]), lo2(hv[q]), y01); y23 = ffma2(bc2(ws[q]), hi2(hv[q]), y23); }
-      y = y01.x + y01.y + y23.x + y23.y + bj;
-    } else
-    y = row_score_own<NG>(ws, hv, gq, bj);
+    const float y = row_score_own<NG>(ws, hv, gq, bj);
     const bool pos_ = (pm >> b) & 1u;
     float lt = 0.0f;
-    float g = (FF_ABLATE & 8) ? y * grad_scale : loss_grad(y, pos_, grad_scale, sqh, &lt);
+    float g = loss_grad(y, pos_, grad_scale, sqh, &lt);
     if (!bvalid) g = 0.0f;
     if (want_loss && bvalid) loss_acc += lt;
     const bool gany = __any_sync(kFull, g != 0.0f);
     if (check && __any_sync(kFull, bvalid && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
     float4 g4;
-    if (FF_ABLATE & 128) { g4 = make_float4(g, g * 0.5f, g * 0.25f, g * 2.0f); } else {
     g4.x = __shfl_sync(kFull, g, (0 << 3) | bq);
     g4.y = __shfl_sync(kFull, g, (1 << 3) | bq);
     g4.z = __shfl_sync(kFull, g, (2 << 3) | bq);
     g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
-    }
     float dwp[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q) dwp[q] = 0.0f + dw_partial(g4, hv[q]);
     if (CSC) {
-      if (!(FF_ABLATE & 32)) {                             // ablation: no g / W_old publication
-        st_hint(a.gT + (size_t)((uint32_t)(j - jb) * 32u + b), g, pol_l);
-        a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;      // 0: column pass skips (w*g == 0)
-      }
+      st_hint(a.gT + (size_t)((uint32_t)(j - jb) * 32u + b), g, pol_l);
+      a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;        // 0: column pass skips (w*g == 0)
     } else {
       const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
       for (int q = 0; q < NG; ++q)
         if (gnz) red_add4(col_line(hb, cs[q], kColFloats) + 32, dh_contrib(ws[q], g4), pol_l);
     }
-    const float gW = (FF_ABLATE & 16) ? dwp[lane & 7] : row_dw_slot<NG>(dwp, lane);
+    const float gW = row_dw_slot<NG>(dwp, lane);
     gbuf.v[i][b] = g;
     const uint32_t row = (uint32_t)j * 32u + lane;
     if (STORE_GRADS) a.dW[row] = gW;
-    if (FF_ABLATE & 4) {                                   // ablation: no Adam, one store
-      st_na(W + row, st.w + gW);
-    } else {
-      adam_update(st.w, st.mw, st.vw, gW, a.adam);
-      st_na(W + row, st.w);
-      st_na(mW + row, st.mw);
-      st_na(vW + row, st.vw);
-    }
+    adam_update(st.w, st.mw, st.vw, gW, a.adam);
+    st_na(W + row, st.w);
+    st_na(mW + row, st.mw);
+    st_na(vW + row, st.vw);
     if (i == cu.nl - 1) {                                // block done: vectorized bias update
       const int64_t jl = jb + (int64_t)cu.blk * 32 + lane;
       __syncwarp();
