@@ -228,11 +228,12 @@ def run_ours(a, shape, world, rank, local_rank):
     t_global = 0
     launches = 0
 
+    from paper_2306_03725_b200.sharded import OverlappedTrainer
+    trainer = OverlappedTrainer(layer, h_dev, ptr_dev, ids_dev, LR, B, shape.m, dev, loss=loss)
+
     def step(s):
         nonlocal t_global, launches
-        i = s % N_BATCHES
-        layer.broadcast_h(h_dev[i])
-        layer.train_step(h_dev[i], ptr_dev[i], ids_dev[i], LR, dh=dh, loss=loss)
+        trainer.step(s % N_BATCHES, (s + 1) % N_BATCHES)     # h broadcast / dh all-reduce overlapped
         launches += last_launch_count()
         t_global += 1
         if t_global % REDIST_EVERY == 0:
@@ -253,6 +254,7 @@ def run_ours(a, shape, world, rank, local_rank):
 
     for s in range(a.warmup):
         step(s)
+    trainer.finish()
     barrier()
     launches = 0
     eng.profile_begin(a.steps * 16)
@@ -262,6 +264,7 @@ def run_ours(a, shape, world, rank, local_rank):
         e0.record(stream)
         for s in range(a.steps):
             step(a.warmup + s)
+        trainer.finish()                                     # every collective inside the timed region
         e1.record(stream)
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))

@@ -67,3 +67,57 @@ class ShardedLayer:
         dist.all_gather(ss, s, group=self.group)
         dist.all_gather(ii, i, group=self.group)
         return self.merge_fn(torch.stack(ss), torch.stack(ii))
+
+
+class OverlappedTrainer:
+    """Training loop helper that overlaps the per-step collectives with compute (P > 1):
+
+    * the h broadcast for step s+1 is issued (async) before step s computes;
+    * the dh all-reduce of step s runs (async) while step s+1 computes, into one of two
+      dh buffers, which is waited on before that buffer is overwritten two steps later.
+
+    ``step(i_cur, i_next)`` runs one step on batch slot ``i_cur`` of the caller's device
+    buffers ``h[i]``/``ptr[i]``/``ids[i]`` and prefetches slot ``i_next``; ``finish()`` waits
+    for every outstanding collective.  ``dh(s)`` is step s's reduced dh once ``finish()`` (or
+    the step two later) has run.  With P = 1 it degenerates to plain ``train_step`` calls.
+    """
+
+    def __init__(self, layer: ShardedLayer, h, ptr, ids, lr, B, m, device, loss=None):
+        self.layer, self.h, self.ptr, self.ids, self.lr = layer, h, ptr, ids, lr
+        self.dh = [torch.empty((B, m), device=device) for _ in range(2)]
+        self.loss = loss
+        self.bcast = [None] * len(h)
+        self.ar = [None, None]
+        self.s = 0
+
+    def prefetch(self, i):
+        if self.layer.world > 1 and self.bcast[i] is None:
+            self.bcast[i] = dist.broadcast(self.h[i], src=0, group=self.layer.group, async_op=True)
+
+    def step(self, i_cur, i_next):
+        L = self.layer
+        if self.bcast[i_cur] is not None:
+            self.bcast[i_cur].wait()
+            self.bcast[i_cur] = None
+        elif L.world > 1:
+            dist.broadcast(self.h[i_cur], src=0, group=L.group)
+        self.prefetch(i_next)
+        slot = self.s & 1
+        if self.ar[slot] is not None:
+            self.ar[slot].wait()
+            self.ar[slot] = None
+        L.engine.train_step(self.h[i_cur], self.ptr[i_cur], self.ids[i_cur], self.lr, dh=self.dh[slot], loss=self.loss)
+        if L.world > 1:
+            self.ar[slot] = dist.all_reduce(self.dh[slot], op=dist.ReduceOp.SUM, group=L.group, async_op=True)
+        self.s += 1
+        return self.dh[slot]
+
+    def finish(self):
+        for k in range(2):
+            if self.ar[k] is not None:
+                self.ar[k].wait()
+                self.ar[k] = None
+        for i in range(len(self.bcast)):
+            if self.bcast[i] is not None:
+                self.bcast[i].wait()
+                self.bcast[i] = None

@@ -141,3 +141,49 @@ def test_two_rank_gloo_matches_unsharded_oracle():
     for rank in range(world):
         assert (results[rank]["top_i"] == i_ref).all()
         np.testing.assert_array_equal(results[rank]["top_s"], s_ref)
+
+
+def _worker_overlap(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2306_03725_b200.sharded import OverlappedTrainer
+        rb, re_ = shard_rows(L, rank, world)
+        eng = OracleEngine(L, M, K_FAN, rb, re_, SEED)
+        lay = ShardedLayer(L, M, K_FAN, rank=rank, world=world, engine=eng, merge_fn=cpu_merge)
+        nb = 3
+        hs, ptrs, idss = [], [], []
+        for s in range(nb):
+            h = torch.from_numpy(synth.hidden_batch(B, M, step=s).astype(np.float64))
+            if rank != 0:
+                h = torch.zeros_like(h)                 # only the producer rank has the data
+            p_, i_ = synth.label_batch(B, L, 3.0, step=s)
+            hs.append(h); ptrs.append(torch.from_numpy(p_)); idss.append(torch.from_numpy(i_))
+        tr = OverlappedTrainer(lay, hs, ptrs, idss, 1e-2, B, M, "cpu")
+        tr.dh = [torch.empty((B, M), dtype=torch.float64) for _ in range(2)]
+        out = []
+        for s in range(nb):
+            out.append(tr.step(s, (s + 1) % nb))
+        tr.finish()
+        results[rank] = [d.numpy().copy() for d in out[-2:]]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlapped_trainer_two_ranks():
+    """Async h broadcast / dh all-reduce pipeline: after finish(), the last two steps' dh
+    buffers equal the unsharded oracle's dh of those steps."""
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker_overlap, args=(world, _free_port(), results), nprocs=world, join=True)
+    st = oracle.State.create(L, M, K_FAN, SEED)
+    ref = []
+    for s in range(3):
+        h = synth.hidden_batch(B, M, step=s).astype(np.float64)
+        ptr, ids = synth.label_batch(B, L, 3.0, step=s)
+        ref.append(oracle.train_step(st, h, ptr, ids, 1.0 / B, 1e-2).dh)
+    for rank in range(world):
+        np.testing.assert_allclose(results[rank][0], ref[1], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(results[rank][1], ref[2], rtol=1e-12, atol=1e-14)
