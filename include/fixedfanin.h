@@ -61,7 +61,8 @@ typedef enum {
 } ff_status;
 
 /* Compile-time limits of this build (checked at create). */
-#define FF_MAX_FANIN 32     /* k <= 32: one label row = one warp-wide 128-B line per array   */
+#define FF_MAX_FANIN 64     /* k <= 64 (the paper's largest, 64 nnz/label): a label
+                               row is one or two warp-wide 128-B lines per array               */
 #define FF_MAX_BATCH 128    /* B <= 128: processed as ceil(B/32) 32-sample lane groups        */
 #define FF_MAX_TOPK 8       /* K <= 8 (the paper reports P@1/3/5)                  */
 

@@ -93,6 +93,17 @@ __device__ __forceinline__ void row_spread(float w, int c, int gq, float (&ws)[N
     cs[q] = (uint32_t)__shfl_sync(kFull, c, 4 * q + gq);
   }
 }
+// k <= 64: lane owns slots lane (e = 0) and lane + 32 (e = 1); connection s = 4q + gq lives
+// in register e = q / 8 of lane 4*(q%8) + gq.
+template <int NG, int KPL>
+__device__ __forceinline__ void row_spread_k(const float (&w)[KPL], const int (&c)[KPL], int gq, float (&ws)[NG],
+                                             uint32_t (&cs)[NG]) {
+#pragma unroll
+  for (int q = 0; q < NG; ++q) {
+    ws[q] = __shfl_sync(kFull, w[q / 8], 4 * (q % 8) + gq);
+    cs[q] = (uint32_t)__shfl_sync(kFull, c[q / 8], 4 * (q % 8) + gq);
+  }
+}
 
 __device__ __forceinline__ const float* col_line(const float* hb, uint32_t c, uint32_t cfloats) {
   return hb + (size_t)c * cfloats;
@@ -211,6 +222,20 @@ __device__ __forceinline__ float db_block_sum(const DbBuf& gb, int r) {
   return s;
 }
 
+// dW of this lane's slots (lane, lane + 32 for k > 32).
+template <int NG>
+__device__ __forceinline__ void row_dw_slots(const float (&dwp)[NG], int lane, float (&gW)[(NG + 7) / 8]) {
+  if constexpr (NG <= 8) {
+    gW[0] = row_dw_slot<NG>(dwp, lane);
+  } else {
+    float lo[8], hi[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { lo[q] = dwp[q]; hi[q] = dwp[q + 8]; }
+    gW[0] = row_dw_slot<8>(lo, lane);
+    gW[1] = row_dw_slot<8>(hi, lane);
+  }
+}
+
 // The row kernel: forward (Alg. 1) for MODE forward; BCE gradient,
 // Alg. 3 weight gradient, bias gradient and Alg. 2 input-gradient scatter
 // for MODE backward; all of those plus Adam for MODE train — the
@@ -220,7 +245,8 @@ __device__ __forceinline__ float db_block_sum(const DbBuf& gb, int r) {
 // scalars (bias, its moments, the positive mask) are one coalesced vector per block
 // (lane i <-> row i) and the bias Adam update runs once per block, vectorized.
 template <int MODE, bool STORE_GRADS, int NG, bool CSC, bool FULL>
-__global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) {
+__global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_rows(RowArgs a) {
+  constexpr int KPL = (NG + 7) / 8;                 // slots per lane (k <= 32 * KPL)
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol_s = policy_evict_first(), pol_l = policy_evict_last();
@@ -228,20 +254,28 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
   const uint32_t cfl = (uint32_t)a.cstride;
   float* const hd_lane = a.hd + 4 * bq;            // this lane's segment, column 0, chunk 0
   const int64_t L = a.L, jb = a.j_begin, nblk = (a.j_end - jb + 31) >> 5;
-  const bool act = lane < k;
+  bool act[KPL];
+#pragma unroll
+  for (int e = 0; e < KPL; ++e) act[e] = lane + 32 * e < k;
   float loss_acc = 0.0f;
   __shared__ DbBuf dbbuf[kRowThreads / 32];
   DbBuf& gbuf = dbbuf[threadIdx.x >> 5];
 
-  float w_n = 0.f, mw_n = 0.f, vw_n = 0.f;
-  int c_n = 0, p_n = 0;
+  float w_n[KPL], mw_n[KPL], vw_n[KPL];
+  int c_n[KPL], p_n[KPL];
+#pragma unroll
+  for (int e = 0; e < KPL; ++e) { w_n[e] = mw_n[e] = vw_n[e] = 0.f; c_n[e] = p_n[e] = 0; }
   auto prefetch_row = [&](int64_t jj) {
     const int64_t row = jj * k;
-    if (act) {
-      w_n = ld_stream(a.W + row + lane, pol_s);
-      c_n = ld_stream_ro(a.idx + row + lane, pol_s);
-      if (CSC && MODE != kModeForward) p_n = ld_stream_ro(a.pos + row + lane, pol_s);
-      if (MODE == kModeTrain) { mw_n = ld_stream(a.mW + row + lane, pol_s); vw_n = ld_stream(a.vW + row + lane, pol_s); }
+#pragma unroll
+    for (int e = 0; e < KPL; ++e) {
+      if (act[e]) {
+        const int64_t r = row + lane + 32 * e;
+        w_n[e] = ld_stream(a.W + r, pol_s);
+        c_n[e] = ld_stream_ro(a.idx + r, pol_s);
+        if (CSC && MODE != kModeForward) p_n[e] = ld_stream_ro(a.pos + r, pol_s);
+        if (MODE == kModeTrain) { mw_n[e] = ld_stream(a.mW + r, pol_s); vw_n[e] = ld_stream(a.vW + r, pol_s); }
+      }
     }
   };
   int64_t blk = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
@@ -260,8 +294,10 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
     }
     for (int i = 0; i < nl; ++i) {
       const int64_t j = j0 + i;
-      float w = w_n, mw = mw_n, vw = vw_n;
-      const int c = c_n, pe = p_n;
+      float w[KPL], mw[KPL], vw[KPL];
+      int c[KPL], pe[KPL];
+#pragma unroll
+      for (int e = 0; e < KPL; ++e) { w[e] = w_n[e]; mw[e] = mw_n[e]; vw[e] = vw_n[e]; c[e] = c_n[e]; pe[e] = p_n[e]; }
       if (i + 1 < nl) prefetch_row(j + 1);
       else if (blk + nw < nblk) prefetch_row(jb + (blk + nw) * 32);
       const int64_t row = j * k;
@@ -269,7 +305,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
       uint32_t pm = __shfl_sync(kFull, pm_v, i);
 
       float ws[NG]; uint32_t cs[NG];
-      row_spread<NG>(w, c, gq, ws, cs);
+      row_spread_k<NG, KPL>(w, c, gq, ws, cs);
       float dwp[NG];
 #pragma unroll
       for (int q = 0; q < NG; ++q) dwp[q] = 0.0f;
@@ -329,17 +365,21 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) k_rows(RowArgs a) 
 
       // pre-update W in CSC order for k_dh_csc; 0 when the row's gradient is all zero, so the
       // column pass skips the gather (its contribution w*g is exactly zero anyway)
-      if (CSC && act) a.wcsc[pe] = gany ? w : 0.0f;
-      const float gW = row_dw_slot<NG>(dwp, lane);
+      float gW[KPL];
+      row_dw_slots<NG>(dwp, lane, gW);
       gbuf.v[i][4 * bq + gq] = dbp;                   // this lane's sample (over all chunks)
-      if (MODE == kModeBackward || STORE_GRADS) {
-        if (act) a.dW[row + lane] = gW;
-      }
-      if (MODE == kModeTrain && act) {
-        adam_update(w, mw, vw, gW, a.adam);
-        st_stream(a.W + row + lane, w, pol_s);
-        st_stream(a.mW + row + lane, mw, pol_s);
-        st_stream(a.vW + row + lane, vw, pol_s);
+#pragma unroll
+      for (int e = 0; e < KPL; ++e) {
+        if (!act[e]) continue;
+        const int64_t r = row + lane + 32 * e;
+        if (CSC) a.wcsc[pe[e]] = gany ? w[e] : 0.0f;
+        if (MODE == kModeBackward || STORE_GRADS) a.dW[r] = gW[e];
+        if (MODE == kModeTrain) {
+          adam_update(w[e], mw[e], vw[e], gW[e], a.adam);
+          st_stream(a.W + r, w[e], pol_s);
+          st_stream(a.mW + r, mw[e], pol_s);
+          st_stream(a.vW + r, vw[e], pol_s);
+        }
       }
     }
     if (MODE == kModeForward) continue;
@@ -720,6 +760,7 @@ __global__ void k_adam(float* __restrict__ W, float* __restrict__ mW, float* __r
 // Uniform random connections: row j's slot i gets the i-th accepted draw of
 // the init-idx stream (Lemire, rejecting duplicates); W[j][i] = a*(2*(u>>8)*2^-24 - 1) in
 // fp32 from word i of the init-W stream (R17).  Also zeroes bias and the moments.
+// Warp per row; lane owns slots lane and lane + 32 (k <= 64).
 __global__ void k_init(float* __restrict__ W, int* __restrict__ idx, float* __restrict__ bias,
                        float* __restrict__ mW, float* __restrict__ vW, float* __restrict__ mb,
                        float* __restrict__ vb, int64_t L, int64_t row_begin, int m, int k,
@@ -729,62 +770,80 @@ __global__ void k_init(float* __restrict__ W, int* __restrict__ idx, float* __re
   const uint32_t thr = (uint32_t)(0x100000000ull % (uint64_t)m);
   for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < L; j += nw) {
     const uint32_t grow = (uint32_t)(row_begin + j);
-    int mine = -1, count = 0;
+    int mine[2] = {-1, -1};
+    int count = 0;
     for (uint32_t n = 0; count < k; ++n) {
       const U4 v = philox(n, grow, 0u, kDomInitIdx, key0, key1);
 #pragma unroll
       for (int wi = 0; wi < 4; ++wi) {
         if (count < k) {
           const int cand = lemire_draw(word_of(v, wi), (uint32_t)m, thr);
-          if (cand >= 0 && __ballot_sync(kFull, lane < count && mine == cand) == 0u) {
-            if (lane == count) mine = cand;
+          if (cand >= 0 && __ballot_sync(kFull, (lane < count && mine[0] == cand) ||
+                                                  (lane + 32 < count && mine[1] == cand)) == 0u) {
+            if (lane == (count & 31)) mine[count >> 5] = cand;
             ++count;
           }
         }
       }
     }
-    if (lane < k) {
-      const U4 v = philox((uint32_t)(lane >> 2), grow, 0u, kDomInitW, key0, key1);
-      const uint32_t u = word_of(v, lane & 3);
-      const float unit = __fmul_rn((float)(u >> 8), 1.0f / 16777216.0f);
-      const float centered = __fsub_rn(__fmul_rn(2.0f, unit), 1.0f);
-      const int64_t e = j * k + lane;
-      idx[e] = mine;
-      W[e] = __fmul_rn(scale, centered);
-      mW[e] = 0.0f; vW[e] = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int slot = lane + 32 * e;
+      if (slot < k) {
+        const U4 v = philox((uint32_t)(slot >> 2), grow, 0u, kDomInitW, key0, key1);
+        const uint32_t u = word_of(v, slot & 3);
+        const float unit = __fmul_rn((float)(u >> 8), 1.0f / 16777216.0f);
+        const float centered = __fsub_rn(__fmul_rn(2.0f, unit), 1.0f);
+        const int64_t el = j * k + slot;
+        idx[el] = mine[e];
+        W[el] = __fmul_rn(scale, centered);
+        mW[el] = 0.0f; vW[el] = 0.0f;
+      }
     }
     if (lane == 0) { bias[j] = 0.0f; mb[j] = 0.0f; vb[j] = 0.0f; }
   }
 }
 
 // ---------------------------------------------------------------------- redistribution
-// SET prune/regrow per row (R8-R14).  Warp per row, lane = slot:
-// rank of (|W| bits, slot) among the row; the p lowest are pruned; the regrow stream
-// (domain 2, counter (n, global row, step, 2)) yields candidates uniform on [0,m) that
-// are accepted when not in the pre-call row set and not yet accepted; the q-th accepted
-// index goes to the q-th pruned slot in ascending slot order; W = mW = vW = 0 there.
+// SET prune/regrow per row (R8-R14).  Warp per row, lane owns slots
+// lane and lane + 32 (k <= 64): rank of (|W| bits, slot) among the row; the p lowest are
+// pruned; the regrow stream (domain 2, counter (n, global row, step, 2)) yields candidates
+// uniform on [0,m) that are accepted when not in the pre-call row set and not yet accepted;
+// the q-th accepted index goes to the q-th pruned slot in ascending slot order; W = mW =
+// vW = 0 there.
 __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, float* __restrict__ mW,
                                float* __restrict__ vW, int64_t L, int64_t row_begin, int m, int k,
                                int p, uint32_t step, uint32_t key0, uint32_t key1) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t thr = (uint32_t)(0x100000000ull % (uint64_t)m);
+  const int KPL = k > 32 ? 2 : 1;
   for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < L; j += nw) {
-    const int64_t e = j * k + lane;
-    const bool act = lane < k;
-    const float w = act ? W[e] : 0.0f;
-    const int c = act ? idx[e] : -1;
-    const uint32_t key = act ? (__float_as_uint(w) & 0x7fffffffu) : 0xffffffffu;
-    int rank = 0;
+    bool act[2]; int c[2]; uint32_t key[2]; int rank[2] = {0, 0};
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const uint32_t kq = __shfl_sync(kFull, key, q);
-      rank += (kq < key || (kq == key && q < lane)) ? 1 : 0;
+    for (int e = 0; e < 2; ++e) {
+      const int slot = lane + 32 * e;
+      act[e] = slot < k;
+      const float w = act[e] ? W[j * k + slot] : 0.0f;
+      c[e] = act[e] ? idx[j * k + slot] : -1;
+      key[e] = act[e] ? (__float_as_uint(w) & 0x7fffffffu) : 0xffffffffu;
     }
-    const bool pruned = act && rank < p;
-    const uint32_t pmask = __ballot_sync(kFull, pruned);
+    for (int e2 = 0; e2 < KPL; ++e2) {                 // compare with every slot q of the row
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const uint32_t kq = __shfl_sync(kFull, key[e2], q);
+        const int sq = q + 32 * e2;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int se = lane + 32 * e;
+          rank[e] += (kq < key[e] || (kq == key[e] && sq < se)) ? 1 : 0;
+        }
+      }
+    }
+    const bool pruned0 = act[0] && rank[0] < p, pruned1 = act[1] && rank[1] < p;
+    const uint32_t pm0 = __ballot_sync(kFull, pruned0), pm1 = __ballot_sync(kFull, pruned1);
     const uint32_t grow = (uint32_t)(row_begin + j);
-    int acc = -1, na = 0;
+    int acc = -1, na = 0;                              // accepted draws: lane q holds draw q (p <= 32)
     for (uint32_t n = 0; na < p; ++n) {
       const U4 v = philox(n, grow, step, kDomRegrow, key0, key1);
 #pragma unroll
@@ -792,7 +851,8 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
         if (na < p) {
           const int cand = lemire_draw(word_of(v, wi), (uint32_t)m, thr);
           if (cand >= 0) {
-            const bool taken = __ballot_sync(kFull, (act && c == cand) || (lane < na && acc == cand)) != 0u;
+            const bool taken = __ballot_sync(kFull, (act[0] && c[0] == cand) || (act[1] && c[1] == cand) ||
+                                                    (lane < na && acc == cand)) != 0u;
             if (!taken) {
               if (lane == na) acc = cand;
               ++na;
@@ -801,25 +861,33 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
         }
       }
     }
-    const int order = __popc(pmask & ((1u << lane) - 1u));
-    const int newc = __shfl_sync(kFull, acc, order & 31);
-    if (pruned) { idx[e] = newc; W[e] = 0.0f; mW[e] = 0.0f; vW[e] = 0.0f; }
+    const int order0 = __popc(pm0 & ((1u << lane) - 1u));
+    const int order1 = __popc(pm0) + __popc(pm1 & ((1u << lane) - 1u));
+    const int new0 = __shfl_sync(kFull, acc, order0 & 31);
+    const int new1 = __shfl_sync(kFull, acc, order1 & 31);
+    if (pruned0) { const int64_t el = j * k + lane; idx[el] = new0; W[el] = 0.0f; mW[el] = 0.0f; vW[el] = 0.0f; }
+    if (pruned1) { const int64_t el = j * k + lane + 32; idx[el] = new1; W[el] = 0.0f; mW[el] = 0.0f; vW[el] = 0.0f; }
   }
 }
 
-// Validation for set_params: idx in [0, m), distinct within each row.
+// Validation for set_params: idx in [0, m), distinct within each row (k <= 64).
 __global__ void k_validate_idx(const int* __restrict__ idx, int64_t L, int m, int k, int* err) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < L; j += nw) {
-    const bool act = lane < k;
-    const int c = act ? idx[j * k + lane] : -1 - lane;
-    if (act && (c < 0 || c >= m)) atomicOr(err, kErrIdxRange);
+    bool act[2]; int c[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      act[e] = lane + 32 * e < k;
+      c[e] = act[e] ? idx[j * k + lane + 32 * e] : -1 - lane - 32 * e;   // distinct sentinels
+      if (act[e] && (c[e] < 0 || c[e] >= m)) atomicOr(err, kErrIdxRange);
+    }
     bool dup = false;
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
-      const int cq = __shfl_sync(kFull, c, q);
-      dup |= act && q != lane && q < k && cq == c;
+      const int cq0 = __shfl_sync(kFull, c[0], q), cq1 = __shfl_sync(kFull, c[1], q);
+      dup |= act[0] && ((q != lane && cq0 == c[0]) || cq1 == c[0]);
+      dup |= act[1] && ((q != lane && cq1 == c[1]) || cq0 == c[1]);
     }
     if (dup) atomicOr(err, kErrIdxDup);
   }
@@ -853,7 +921,7 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7, wid = threadIdx.x >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol_s = policy_evict_first(), pol_l = policy_evict_last();
-  const bool act = lane < k;
+  constexpr int KPL = (NG + 7) / 8;
   for (int q2 = 0; q2 < nb; ++q2) {
     const int lo = q2 * 32 + 4 * bq;
     const int b = lo + gq;
@@ -863,20 +931,28 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
 #pragma unroll
     for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
     int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
-    float w_n = 0.f, bj_n = 0.f; int c_n = 0;
-    if (j < L) {
-      if (act) { w_n = ld_stream(W + j * k + lane, pol_s); c_n = ld_stream_ro(idx + j * k + lane, pol_s); }
-      bj_n = ld_stream(bias + j, pol_s);
-    }
-    for (; j < L; j += nw) {
-      const float w = w_n, bj = bj_n; const int c = c_n;
-      const int64_t jn = j + nw;
-      if (jn < L) {
-        if (act) { w_n = ld_stream(W + jn * k + lane, pol_s); c_n = ld_stream_ro(idx + jn * k + lane, pol_s); }
-        bj_n = ld_stream(bias + jn, pol_s);
+    float w_n[KPL], bj_n = 0.f; int c_n[KPL];
+    auto load = [&](int64_t jj) {
+#pragma unroll
+      for (int e = 0; e < KPL; ++e) {
+        w_n[e] = 0.f; c_n[e] = 0;
+        if (lane + 32 * e < k) {
+          w_n[e] = ld_stream(W + jj * k + lane + 32 * e, pol_s);
+          c_n[e] = ld_stream_ro(idx + jj * k + lane + 32 * e, pol_s);
+        }
       }
+      bj_n = ld_stream(bias + jj, pol_s);
+    };
+    if (j < L) load(j);
+    for (; j < L; j += nw) {
+      float w[KPL]; int c[KPL];
+#pragma unroll
+      for (int e = 0; e < KPL; ++e) { w[e] = w_n[e]; c[e] = c_n[e]; }
+      const float bj = bj_n;
+      const int64_t jn = j + nw;
+      if (jn < L) load(jn);
       float ws[NG]; uint32_t cs[NG]; float4 hv[NG];
-      row_spread<NG>(w, c, gq, ws, cs);
+      row_spread_k<NG, KPL>(w, c, gq, ws, cs);
       row_gather<NG, FULL>(hb, cs, cfl, k, gq, pol_l, hv);
       const float y = row_score_own<NG>(ws, hv, gq, bj);
       if (b < B) topk_insert(ts, ti, y, (int)(row_begin + j));

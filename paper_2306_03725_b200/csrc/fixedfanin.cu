@@ -216,8 +216,10 @@ RowArgs row_args(ff_layer* l, int B) {
 // FULL variants (k == 16 or k == 32: every slot of every group exists) drop the per-slot guards.
 template <int MODE, bool SG, bool CSC>
 const void* row_kernel_csc(int k) {
+  if (k == 64) return (const void*)k_rows<MODE, SG, 16, CSC, true>;
   if (k == 32) return (const void*)k_rows<MODE, SG, 8, CSC, true>;
   if (k == 16) return (const void*)k_rows<MODE, SG, 4, CSC, true>;
+  if (k > 32) return (const void*)k_rows<MODE, SG, 16, CSC, false>;
   return k < 16 ? (const void*)k_rows<MODE, SG, 4, CSC, false> : (const void*)k_rows<MODE, SG, 8, CSC, false>;
 }
 template <int MODE, bool SG>
@@ -225,8 +227,10 @@ const void* row_kernel(int k, bool csc) {
   return csc ? row_kernel_csc<MODE, SG, true>(k) : row_kernel_csc<MODE, SG, false>(k);
 }
 const void* predict_kernel(int k) {
+  if (k == 64) return (const void*)k_predict<16, true>;
   if (k == 32) return (const void*)k_predict<8, true>;
   if (k == 16) return (const void*)k_predict<4, true>;
+  if (k > 32) return (const void*)k_predict<16, false>;
   return k < 16 ? (const void*)k_predict<4, false> : (const void*)k_predict<8, false>;
 }
 

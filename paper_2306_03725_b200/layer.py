@@ -21,7 +21,7 @@ FF_FLAG_STORE_GRADS = 2
 FF_FLAG_NO_PIPE = 4
 FF_DH_ATOMIC, FF_DH_CSC = 0, 1
 FF_LOSS_BCE, FF_LOSS_SQH = 0, 1
-FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 32, 128, 8
+FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 64, 128, 8
 _STATUS = {1: "FF_ERR_ARG", 2: "FF_ERR_CONFIG", 3: "FF_ERR_RANGE", 4: "FF_ERR_NONFINITE", 5: "FF_ERR_CUDA",
            6: "FF_ERR_STATE"}
 

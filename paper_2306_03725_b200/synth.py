@@ -40,6 +40,10 @@ SHAPES = {
     "wiki-500k": Shape("wiki-500k", 501070, 32768, 32, 32, 4.77),
     "amazon-670k": Shape("amazon-670k", 670091, 32768, 32, 32, 5.45),
     "amazon-3m": Shape("amazon-3m", 2812281, 32768, 32, 32, 36.04),
+    # sweeps of SURVEY §8(d): the paper's Table-5 architecture (64 nnz/label, 65k intermediate,
+    # P:869-870) and the 16k intermediate of the loss comparison
+    "amazon-670k-k64-m65k": Shape("amazon-670k-k64-m65k", 670091, 65536, 64, 32, 5.45),
+    "amazon-670k-m16k": Shape("amazon-670k-m16k", 670091, 16384, 32, 32, 5.45),
 }
 
 

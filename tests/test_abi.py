@@ -48,7 +48,7 @@ def test_workspace_size_matches_layout_model():
 
 @pytest.mark.parametrize("kw,msg", [
     (dict(L_global=10, m=8, k=9), "k="),            # k > m
-    (dict(L_global=10, m=64, k=33), "k="),          # k > FF_MAX_FANIN
+    (dict(L_global=10, m=128, k=65), "k="),         # k > FF_MAX_FANIN (64)
     (dict(L_global=10, m=64, k=8, row_begin=5, L_local=6), "shard"),
     (dict(L_global=10, m=64, k=8, max_batch=129), "max_batch"),
     (dict(L_global=10, m=64, k=8, max_topk=9), "max_topk"),

@@ -64,6 +64,12 @@ def dh_close(a, b):
     return torch.allclose(a, b, rtol=1e-5, atol=1e-5 * scale + 1e-30)
 
 
+def adam_A(W_old, W_new_ref):
+    """R19 companion of p' = p - lr*mhat/(sqrt(vhat)+eps): |p| + |update| (the subtraction's terms)."""
+    W_old = np.asarray(W_old, dtype=np.float64)
+    return np.abs(W_old) + np.abs(np.asarray(W_new_ref) - W_old)
+
+
 def state_of(lay):
     p = lay.get_params()
     return {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in p.items()}
@@ -74,7 +80,8 @@ ADAM = dict(beta1=F32(0.9), beta2=F32(0.999), eps=F32(1e-8))
 
 # ------------------------------------------------------------------ init (bit-exact)
 @pytest.mark.parametrize("L,m,k,row_begin,Lg", [(1000, 256, 16, 0, 1000), (777, 4096, 32, 123, 5000),
-                                                  (50, 37, 13, 0, 50), (40, 5, 5, 10, 50), (3, 1, 1, 0, 3)])
+                                                  (50, 37, 13, 0, 50), (40, 5, 5, 10, 50), (3, 1, 1, 0, 3),
+                                                  (300, 65536, 64, 7, 400), (90, 70, 47, 0, 90), (20, 64, 64, 0, 20)])
 def test_init_bit_exact(L, m, k, row_begin, Lg):
     lay = make(L, m, k, L_global=Lg, row_begin=row_begin, L_local=L, seed=42)
     s = state_of(lay)
@@ -97,7 +104,7 @@ def test_init_full_amazon_670k_sampled_rows():
 
 # --------------------------------------------------------------- forward / backward
 CASES = [(1000, 256, 16, 32), (1000, 256, 16, 5), (333, 100, 13, 37), (2000, 512, 32, 100), (97, 64, 1, 1),
-         (64, 32, 32, 128)]
+         (64, 32, 32, 128), (1500, 2048, 64, 32), (400, 300, 50, 40), (130, 64, 64, 7)]
 
 
 @pytest.mark.parametrize("L,m,k,B", CASES)
@@ -149,10 +156,10 @@ def test_backward_and_adam_parity(L, m, k, B, dh_mode, loss):
     lr32 = F32(1e-3)
     Wr, mr, vr = oracle.adam(W, dWg, np.zeros_like(dWg), np.zeros_like(dWg), 1, lr32, **ADAM)
     br, mbr, vbr = oracle.adam(bias, dbg, np.zeros(L), np.zeros(L), 1, lr32, **ADAM)
-    assert_close(s["W"], Wr, 0, "W'")
+    assert_close(s["W"], Wr, adam_A(W, Wr), "W'")
     assert_close(s["mW"], mr, 0, "mW'")
     assert_close(s["vW"], vr, 1e-30, "vW'")
-    assert_close(s["bias"], br, 0, "bias'")
+    assert_close(s["bias"], br, adam_A(bias, br), "bias'")
     assert s["t"] == 1
 
 
@@ -191,7 +198,7 @@ def test_fused_step_equals_unfused_path(L, m, k, B, dh_mode):
 
 @LOSS
 @DH
-@pytest.mark.parametrize("k", [16, 32])
+@pytest.mark.parametrize("k", [16, 32, 64])
 def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k):
     L, m, B = 1000, 256, 32
     layer = L_()
@@ -214,7 +221,8 @@ def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k):
         # Adam applied by the oracle to the GPU's gradient: tight elementwise parity
         s1 = state_of(lay)
         Wr, mr, vr = oracle.adam(s0["W"], dW.cpu().numpy(), s0["mW"], s0["vW"], s0["t"] + 1, F32(1e-3), **ADAM)
-        assert_close(s1["W"], Wr, 0, "W'"); assert_close(s1["mW"], mr, 0, "m'"); assert_close(s1["vW"], vr, 1e-30, "v'")
+        assert_close(s1["W"], Wr, adam_A(s0["W"], Wr), "W'")
+        assert_close(s1["mW"], mr, 0, "m'"); assert_close(s1["vW"], vr, 1e-30, "v'")
         assert s1["t"] == step + 1
 
 
@@ -261,7 +269,8 @@ def test_free_running_tiny_run_matches_oracle(dh_mode):
 
 # ------------------------------------------------------------------- redistribution
 @pytest.mark.parametrize("L,m,k,frac,step", [(1000, 256, 16, 0.1, 1000), (3000, 4096, 32, 0.1, 7),
-                                              (500, 40, 32, 0.25, 3), (64, 3, 2, 0.5, 1)])
+                                              (500, 40, 32, 0.25, 3), (64, 3, 2, 0.5, 1), (800, 65536, 64, 0.1, 1000),
+                                              (300, 120, 48, 0.3, 11), (50, 70, 64, 0.05, 2)])
 def test_redistribution_bit_exact(L, m, k, frac, step):
     lay = make(L, m, k, seed=11, prune_frac=frac)
     W, idx, _ = synth.random_params(L, m, k, seed=3)
@@ -293,7 +302,7 @@ def test_redistribution_config_errors():
 
 # ------------------------------------------------------------------------- top-K
 @pytest.mark.parametrize("L,m,k,B,K", [(1000, 256, 16, 32, 5), (5000, 512, 32, 70, 8), (9, 16, 4, 3, 1),
-                                        (8, 16, 4, 3, 8)])
+                                        (8, 16, 4, 3, 8), (3000, 4096, 64, 32, 5), (700, 500, 40, 50, 3)])
 def test_predict_topk_bit_exact(L, m, k, B, K):
     lay = make(L, m, k, B=B, seed=3)
     h = tens(synth.hidden_batch(B, m, step=1))
@@ -382,7 +391,7 @@ def test_empty_batch_and_empty_shard(dh_mode):
     lay.train_step(h, ptr, ids, 1e-3)                     # no samples: zero gradients, Adam still steps
     s1 = state_of(lay)
     Wr, _, _ = oracle.adam(s0["W"], np.zeros((L, k)), s0["mW"], s0["vW"], 1, F32(1e-3), **ADAM)
-    assert_close(s1["W"], Wr, 0, "W' with B=0")
+    assert_close(s1["W"], Wr, adam_A(s0["W"], Wr), "W' with B=0")
     assert s1["t"] == 1
     empty = make(0, m, k, B=8, L_global=10, row_begin=10, L_local=0, dh_mode=dh_mode)
     hb = tens(synth.hidden_batch(3, m))
@@ -464,7 +473,7 @@ def test_full_size_amazon_670k_sampled_parity():
         assert_close(dW[rows], dWr, AdW, "dW rows")
         assert_close(db[rows], dbr, Adb, "db rows")
         Wr, mr, vr = oracle.adam(s0["W"][rows], dW[rows], s0["mW"][rows], s0["vW"][rows], 1, F32(1e-3), **ADAM)
-        assert_close(s1["W"][rows], Wr, 0, "W' rows")
+        assert_close(s1["W"][rows], Wr, adam_A(s0["W"][rows], Wr), "W' rows")
         dhr, Adh = oracle.input_grad(s0["W"], s0["idx"], g, m)
         assert_close(dh.cpu().numpy(), dhr, Adh, f"dh full (mode {dh_mode})")
         del lay
