@@ -447,25 +447,26 @@ def test_csc_dh_is_deterministic_and_matches_atomic():
     assert dh_close(d1, d3)
 
 
-def test_full_size_amazon_670k_sampled_parity():
-    """BASELINE.json's Amazon-670K shape in the bench's launch configuration: one fused
-    step (CSC and atomic dh), checked on sampled label rows (dW, db, W') and on full dh
-    (the oracle's Alg. 2 over all 21.4 M connections), lockstep (R20)."""
+@pytest.mark.parametrize("shape_name,dh_modes", [("wiki10-31k", (0,)), ("wiki-500k", (0,)), ("amazon-670k", (1, 0)),
+                                                  ("amazon-3m", (1, 0)), ("amazon-670k-k64-m65k", (0, 1))])
+def test_full_size_sampled_parity(shape_name, dh_modes):
+    """BASELINE.json's shapes in the bench's launch configuration: one fused step checked on
+    sampled label rows (y, dW, db, W') and on the full dh (the oracle's Alg. 2 over every
+    connection), lockstep (R20)."""
     layer = L_()
-    shape = synth.SHAPES["amazon-670k"]
+    shape = synth.SHAPES[shape_name]
     L, m, k, B = shape.L, shape.m, shape.k, shape.B
     h = synth.hidden_batch(B, m, step=0)
     ptr, ids = synth.label_batch(B, L, shape.avg_pos, step=0)
     rng = np.random.default_rng(5)
     rows = np.sort(rng.choice(L, 256, replace=False))
-    for dh_mode in (1, 0):
+    for dh_mode in dh_modes:
         lay = make(L, m, k, B=B, seed=42, flags=layer.FF_FLAG_STORE_GRADS, dh_mode=dh_mode)
         s0 = state_of(lay)
         y = lay.forward(tens(h)).cpu().numpy().astype(np.float64)
         dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
         dW, db = (x.cpu().numpy() for x in lay.get_grads())
         s1 = state_of(lay)
-        # scores of sampled rows from the GPU state (Alg. 1) vs the GPU forward
         yr, Ay = oracle.forward(s0["W"][rows], s0["idx"][rows], s0["bias"][rows], h)
         assert_close(y[:, rows], yr, Ay, "y rows")
         g, _ = oracle.bce_grad(y, ptr, ids, F32(1.0 / B))
