@@ -41,6 +41,7 @@ struct RowArgs {
   float* wcsc;                // CSC mode: pre-update W in CSC order
   float* gT;                  // CSC mode: g[j - j_begin][nb][32] (per-label gradient lines of the tile)
   int64_t j_begin, j_end;     // label rows processed by this launch (a tile; multiple of 32)
+  int br;                     // rows per warp block (32, 16, 8 or 4): smaller for small L
   int64_t L; int k; int B; int nb; int cstride;   // cstride = 64*nb floats per column
   float grad_scale;
   float* y_out;               // forward: y[B][L]
@@ -240,7 +241,7 @@ __device__ __forceinline__ void row_dw_slots(const float (&dwp)[NG], int lane, f
 // Alg. 3 weight gradient, bias gradient and Alg. 2 input-gradient scatter
 // for MODE backward; all of those plus Adam for MODE train — the
 // fused step, in which y, g and dW live only in registers.
-// Work split: a warp owns blocks of 32 consecutive label rows (persistent, strided over
+// Work split: a warp owns blocks of br consecutive label rows (32, or 16/8/4 when L is small) (persistent, strided over
 // blocks) and walks their rows one at a time, prefetching the next row's state.  Per-label
 // scalars (bias, its moments, the positive mask) are one coalesced vector per block
 // (lane i <-> row i) and the bias Adam update runs once per block, vectorized.
@@ -253,7 +254,8 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
   const int k = FULL ? 4 * NG : a.k, nb = a.nb, B = a.B;
   const uint32_t cfl = (uint32_t)a.cstride;
   float* const hd_lane = a.hd + 4 * bq;            // this lane's segment, column 0, chunk 0
-  const int64_t L = a.L, jb = a.j_begin, nblk = (a.j_end - jb + 31) >> 5;
+  const int br = a.br;
+  const int64_t L = a.L, jb = a.j_begin, nblk = (a.j_end - jb + br - 1) / br;
   bool act[KPL];
 #pragma unroll
   for (int e = 0; e < KPL; ++e) act[e] = lane + 32 * e < k;
@@ -279,11 +281,11 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
     }
   };
   int64_t blk = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
-  if (blk < nblk) prefetch_row(jb + blk * 32);
+  if (blk < nblk) prefetch_row(jb + blk * br);
 
   for (; blk < nblk; blk += nw) {
-    const int64_t j0 = jb + blk * 32;
-    const int nl = (int)min((int64_t)32, a.j_end - j0);
+    const int64_t j0 = jb + blk * br;
+    const int nl = (int)min((int64_t)br, a.j_end - j0);
     const bool lv = lane < nl;                  // lane i <-> row j0 + i for the block vectors
     float bias_v = 0.f, mb_v = 0.f, vb_v = 0.f, db_v = 0.f;
     uint32_t pm_v = 0u;
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 #pragma unroll
       for (int e = 0; e < KPL; ++e) { w[e] = w_n[e]; mw[e] = mw_n[e]; vw[e] = vw_n[e]; c[e] = c_n[e]; pe[e] = p_n[e]; }
       if (i + 1 < nl) prefetch_row(j + 1);
-      else if (blk + nw < nblk) prefetch_row(jb + (blk + nw) * 32);
+      else if (blk + nw < nblk) prefetch_row(jb + (blk + nw) * br);
       const int64_t row = j * k;
       const float bj = __shfl_sync(kFull, bias_v, i);
       uint32_t pm = __shfl_sync(kFull, pm_v, i);
@@ -419,7 +421,7 @@ constexpr int kPipeThreads = FF_PIPE_THREADS;
 constexpr int kPipeMinBlocks = FF_PIPE_MINB;
 
 struct PipeCursor {             // position of one row in this warp's sequence of rows
-  int64_t blk;                  // 32-row block index within [j_begin, j_end)
+  int64_t blk;                  // br-row block index within [j_begin, j_end)
   int i;                        // row within the block
 };
 
@@ -437,7 +439,8 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   const float grad_scale = a.grad_scale;
   const bool want_loss = a.loss != nullptr, check = a.check_finite != 0, sqh = a.sqh != 0;
   const int64_t jb = a.j_begin, je = a.j_end;
-  const int nblk = (int)((je - jb + 31) >> 5);
+  const int br = a.br;
+  const int nblk = (int)((je - jb + br - 1) / br);
   const int b = 4 * bq + gq;                            // this lane's own sample
   const bool bvalid = b < B;
   float loss_acc = 0.0f;
@@ -446,12 +449,12 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
 
   // this warp's rows: blocks w, w + nwarp, ...; cursor = (block, row in block, rows in block)
   struct Cur { int blk, i, nl; };
-  auto nl_of = [&](int blk) { return (int)min((int64_t)32, je - (jb + (int64_t)blk * 32)); };
+  auto nl_of = [&](int blk) { return (int)min((int64_t)br, je - (jb + (int64_t)blk * br)); };
   auto adv = [&](Cur c) {
     if (++c.i >= c.nl) { c.blk += nwarp; c.i = 0; c.nl = c.blk < nblk ? nl_of(c.blk) : 0; }
     return c;
   };
-  auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * 32 + c.i; };
+  auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * br + c.i; };
 
   struct St { float w, mw, vw; int c, pe; };
   auto load_st = [&](const Cur& cu, St& st) {
@@ -468,7 +471,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   auto load_bv = [&](int blk, Bv& v) {
     v.bias = v.mb = v.vb = 0.0f; v.pm = 0u;
     if (blk < nblk && lane < nl_of(blk)) {
-      const int64_t j = jb + (int64_t)blk * 32 + lane;
+      const int64_t j = jb + (int64_t)blk * br + lane;
       v.bias = ld_na(a.bias + j); v.mb = ld_na(a.mb + j); v.vb = ld_na(a.vb + j); v.pm = a.posmask[j];
     }
   };
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     st_na(mW + row, st.mw);
     st_na(vW + row, st.vw);
     if (i == cu.nl - 1) {                                // block done: vectorized bias update
-      const int64_t jl = jb + (int64_t)cu.blk * 32 + lane;
+      const int64_t jl = jb + (int64_t)cu.blk * br + lane;
       __syncwarp();
       if (lane <= i) db_v = db_block_sum(gbuf, lane);
       __syncwarp();

@@ -269,8 +269,18 @@ ff_status launch_dh_csc(ff_layer* l, int B, int tile, cudaStream_t st) {
   return FF_OK;
 }
 
+// Rows per warp block: 32 unless that leaves resident warps idle (small L), then 16, 8 or 4
+// so that every warp gets at least two blocks.
+int block_rows(int64_t rows, int grid, int threads) {
+  const int64_t warps = (int64_t)grid * (threads / 32);
+  int br = 32;
+  while (br > 4 && (rows + br - 1) / br < 2 * warps) br >>= 1;
+  return br;
+}
+
 // One row-kernel launch, bracketed by a profiling event pair while profiling is on.
 ff_status timed_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads) {
+  a.br = block_rows(a.j_end - a.j_begin, grid, threads);
   const bool timed = 2 * (l->prof_used + 1) <= (int)l->prof_ev.size();
   if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used], st));
   ff_status s = launch_rows(fn, grid, a, st, threads);
@@ -504,6 +514,7 @@ ff_status fixedfanin_forward(ff_layer* l, const float* h, int32_t B, float* y, f
   if (l->cfg.L_local == 0) return FF_OK;
   RowArgs a = row_args(l, B);
   a.y_out = y;
+  a.br = block_rows(l->cfg.L_local, l->grid_fwd, kRowThreads);
   return launch_rows(row_kernel<kModeForward, false>(l->cfg.k, false), l->grid_fwd, a, st);
 }
 

@@ -1,0 +1,3 @@
+set -x
+python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -3
+bash tools/gpu_shapes.sh
