@@ -118,6 +118,13 @@ __device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z,
 __device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
 
 // ---------------------------------------------------------------- warp helpers
+// This thread's global warp index, broadcast from lane 0 so that ptxas can prove it (and
+// every loop bound derived from it) warp-uniform: without that it guards each later
+// shuffle with a divergence check (UMOV + BRA.DIV, two extra issues per SHFL).
+__device__ __forceinline__ int64_t global_warp() {
+  return (int64_t)__shfl_sync(kFull, (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), 0);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);

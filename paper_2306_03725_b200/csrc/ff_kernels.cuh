@@ -84,8 +84,10 @@ __device__ __forceinline__ void block_atomic_add(float v, float* dst) {
 // arithmetic, so their scores are bit-identical: the top-K parity relies on it)
 
 // Broadcast each connection's weight and hd column to the lanes that gather it: lane
-// (gq, bq) handles connections s = 4q + gq, q < NG.  Columns stay raw 32-bit indices: the
-// line address base + c * cfloats is then one IMAD.WIDE.U32 at the load.
+// (gq, bq) handles connections s = 4q + gq, q < NG (the 8 lanes of equal gq read one
+// 128-B line together, so register q must name the same connection on all of them).
+// Columns stay raw 32-bit indices: the line address base + c * cfloats is then one
+// IMAD.WIDE.U32 at the load.
 template <int NG>
 __device__ __forceinline__ void row_spread(float w, int c, int gq, float (&ws)[NG], uint32_t (&cs)[NG]) {
 #pragma unroll
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       }
     }
   };
-  int64_t blk = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
+  int64_t blk = global_warp();
   if (blk < nblk) prefetch_row(jb + blk * br);
 
   for (; blk < nblk; blk += nw) {
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
         g4.z = __shfl_sync(kFull, g, (2 << 3) | bq);
         g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
 #pragma unroll
-        for (int q = 0; q < NG; ++q) dwp[q] += dw_partial(g4, hv[q]);
+        for (int q = 0; q < NG; ++q) dwp[q] = q2 == 0 ? dw_partial(g4, hv[q]) : dwp[q] + dw_partial(g4, hv[q]);
         if (CSC) {
           // CSC mode: publish g[., j] (one 128-B line per chunk); dh is pulled later (k_dh_csc)
           st_hint(a.gT + ((j - jb) * nb + q2) * 32 + 4 * bq + gq, g, pol_l);
@@ -420,10 +422,6 @@ constexpr int kPipeThreads = FF_PIPE_THREADS;
 #endif
 constexpr int kPipeMinBlocks = FF_PIPE_MINB;
 
-struct PipeCursor {             // position of one row in this warp's sequence of rows
-  int64_t blk;                  // br-row block index within [j_begin, j_end)
-  int i;                        // row within the block
-};
 
 template <bool STORE_GRADS, bool CSC>
 __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(RowArgs a) {
@@ -440,26 +438,28 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   const bool want_loss = a.loss != nullptr, check = a.check_finite != 0, sqh = a.sqh != 0;
   const int64_t jb = a.j_begin, je = a.j_end;
   const int br = a.br;
-  const int nblk = (int)((je - jb + br - 1) / br);
   const int b = 4 * bq + gq;                            // this lane's own sample
   const bool bvalid = b < B;
   float loss_acc = 0.0f;
   __shared__ DbBuf dbbuf[kPipeThreads / 32];
   DbBuf& gbuf = dbbuf[threadIdx.x >> 5];
 
-  // this warp's rows: blocks w, w + nwarp, ...; cursor = (block, row in block, rows in block)
-  struct Cur { int blk, i, nl; };
-  auto nl_of = [&](int blk) { return (int)min((int64_t)br, je - (jb + (int64_t)blk * br)); };
+  // this warp's rows: blocks w, w + nwarp, ...; cursor = (first row of the block relative
+  // to j_begin, row in block, rows in block).  32-bit row arithmetic: L * k < 2^31.
+  const uint32_t nrows = (uint32_t)(je - jb), jb32 = (uint32_t)jb, bstride = (uint32_t)nwarp * (uint32_t)br;
+  struct Cur { uint32_t j0; int i, nl; };
+  auto nl_of = [&](uint32_t j0) { return (int)min((uint32_t)br, nrows - j0); };
   auto adv = [&](Cur c) {
-    if (++c.i >= c.nl) { c.blk += nwarp; c.i = 0; c.nl = c.blk < nblk ? nl_of(c.blk) : 0; }
+    if (++c.i >= c.nl) { c.j0 += bstride; c.i = 0; c.nl = c.j0 < nrows ? nl_of(c.j0) : 0; }
     return c;
   };
-  auto row_of = [&](const Cur& c) { return jb + (int64_t)c.blk * br + c.i; };
+  auto live = [&](const Cur& c) { return c.j0 < nrows; };
+  auto row_of = [&](const Cur& c) { return jb32 + c.j0 + (uint32_t)c.i; };
 
   struct St { float w, mw, vw; int c, pe; };
   auto load_st = [&](const Cur& cu, St& st) {
-    if (cu.blk < nblk) {
-      const uint32_t row = (uint32_t)row_of(cu) * 32u + lane;   // L*k < 2^31: 32-bit indices
+    if (live(cu)) {
+      const uint32_t row = row_of(cu) * 32u + lane;
       st.w = ld_na(W + row);
       st.c = ld_na_ro(idx + row);
       st.mw = ld_na(mW + row);
@@ -468,24 +468,24 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     }
   };
   struct Bv { float bias, mb, vb; uint32_t pm; };
-  auto load_bv = [&](int blk, Bv& v) {
+  auto load_bv = [&](const Cur& cu, Bv& v) {
     v.bias = v.mb = v.vb = 0.0f; v.pm = 0u;
-    if (blk < nblk && lane < nl_of(blk)) {
-      const int64_t j = jb + (int64_t)blk * br + lane;
+    if (live(cu) && lane < cu.nl) {
+      const uint32_t j = jb32 + cu.j0 + lane;
       v.bias = ld_na(a.bias + j); v.mb = ld_na(a.mb + j); v.vb = ld_na(a.vb + j); v.pm = a.posmask[j];
     }
   };
 
-  Cur X{(int)((((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5), 0, 0};
-  if (X.blk < nblk) {                                   // (no early return: block_atomic_add syncs)
-  X.nl = nl_of(X.blk);
+  Cur X{(uint32_t)global_warp() * (uint32_t)br, 0, 0};
+  if (live(X)) {                                        // (no early return: block_atomic_add syncs)
+  X.nl = nl_of(X.j0);
   Cur Y = adv(X), Z = adv(Y);
   St sX{}, sY{}, sZ{};
   Bv bv{}, bv_next{};
   float db_v = 0.0f;
   load_st(X, sX);
   load_st(Y, sY);
-  load_bv(X.blk, bv);
+  load_bv(X, bv);
 
   float wsA[NG], wsB[NG]; uint32_t csA[NG], csB[NG]; float4 hvA[NG], hvB[NG];
   auto issue = [&](const St& st, float (&ws)[NG], uint32_t (&cs)[NG], float4 (&hv)[NG]) {
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     float ws[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q) ws[q] = (CSC && FF_WS_RECOMPUTE) ? __shfl_sync(kFull, st.w, 4 * q + gq) : ws_in[q];
-    const int64_t j = row_of(cu);
+    const uint32_t j = row_of(cu);
     const int i = cu.i;
     const float bj = __shfl_sync(kFull, bv.bias, i);
     const uint32_t pm = __shfl_sync(kFull, bv.pm, i);
@@ -521,9 +521,9 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
     float dwp[NG];
 #pragma unroll
-    for (int q = 0; q < NG; ++q) dwp[q] = 0.0f + dw_partial(g4, hv[q]);
+    for (int q = 0; q < NG; ++q) dwp[q] = dw_partial(g4, hv[q]);
     if (CSC) {
-      st_hint(a.gT + (size_t)((uint32_t)(j - jb) * 32u + b), g, pol_l);
+      st_hint(a.gT + (size_t)((j - jb32) * 32u + b), g, pol_l);
       a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;        // 0: column pass skips (w*g == 0)
     } else {
       const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
@@ -533,14 +533,14 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     }
     const float gW = row_dw_slot<NG>(dwp, lane);
     gbuf.v[i][b] = g;
-    const uint32_t row = (uint32_t)j * 32u + lane;
+    const uint32_t row = j * 32u + lane;
     if (STORE_GRADS) a.dW[row] = gW;
     adam_update(st.w, st.mw, st.vw, gW, a.adam);
     st_na(W + row, st.w);
     st_na(mW + row, st.mw);
     st_na(vW + row, st.vw);
     if (i == cu.nl - 1) {                                // block done: vectorized bias update
-      const int64_t jl = jb + (int64_t)cu.blk * br + lane;
+      const uint32_t jl = jb32 + cu.j0 + lane;
       __syncwarp();
       if (lane <= i) db_v = db_block_sum(gbuf, lane);
       __syncwarp();
@@ -562,9 +562,9 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   // swap roles without register moves.
   auto step = [&](float (&wsC)[NG], uint32_t (&csC)[NG], float4 (&hvC)[NG],
                   float (&wsN)[NG], uint32_t (&csN)[NG], float4 (&hvN)[NG]) -> bool {
-    if (Y.blk < nblk) {
+    if (live(Y)) {
       issue(sY, wsN, csN, hvN);
-      if (Y.i == 0) load_bv(Y.blk, bv_next);
+      if (Y.i == 0) load_bv(Y, bv_next);
     }
     const Cur Zn = adv(Z);
     St sZn{};
@@ -572,8 +572,8 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     compute(X, sX, wsC, csC, hvC);
     X = Y; Y = Z; Z = Zn;
     sX = sY; sY = sZ; sZ = sZn;
-    if (X.blk < nblk && X.i == 0) bv = bv_next;
-    return X.blk < nblk;
+    if (live(X) && X.i == 0) bv = bv_next;
+    return live(X);
   };
   while (true) {
     if (!step(wsA, csA, hvA, wsB, csB, hvB)) break;
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
   const int* cp = col_ptr + (int64_t)tile * m;
   const int jb = (int)j_begin;
   const uint32_t gstride = 32u * (uint32_t)nb;               // floats per gT row
-  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < m; c += nw) {
+  for (int c = (int)global_warp(); c < m; c += nw) {
     const int p0 = cp[c], p1 = cp[c + 1];
     for (int q2 = 0; q2 < nb; ++q2) {
       const float* gb = gT + q2 * 32 + 4 * bq;                // this lane's slice of chunk q2
@@ -771,7 +771,7 @@ __global__ void k_init(float* __restrict__ W, int* __restrict__ idx, float* __re
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t thr = (uint32_t)(0x100000000ull % (uint64_t)m);
-  for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < L; j += nw) {
+  for (int64_t j = global_warp(); j < L; j += nw) {
     const uint32_t grow = (uint32_t)(row_begin + j);
     int mine[2] = {-1, -1};
     int count = 0;
@@ -821,7 +821,7 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t thr = (uint32_t)(0x100000000ull % (uint64_t)m);
   const int KPL = k > 32 ? 2 : 1;
-  for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < L; j += nw) {
+  for (int64_t j = global_warp(); j < L; j += nw) {
     bool act[2]; int c[2]; uint32_t key[2]; int rank[2] = {0, 0};
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -877,7 +877,7 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
 __global__ void k_validate_idx(const int* __restrict__ idx, int64_t L, int m, int k, int* err) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < L; j += nw) {
+  for (int64_t j = global_warp(); j < L; j += nw) {
     bool act[2]; int c[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
     float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll
     for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
-    int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
+    int64_t j = global_warp();
     float w_n[KPL], bj_n = 0.f; int c_n[KPL];
     auto load = [&](int64_t jj) {
 #pragma unroll
@@ -982,7 +982,7 @@ __global__ void k_merge_topk(const float* __restrict__ in_s, const int* __restri
                              float* __restrict__ out_s, int* __restrict__ out_i) {
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nw) {
+  for (int b = (int)global_warp(); b < B; b += nw) {
     float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll
     for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
