@@ -353,7 +353,7 @@ def run_ours(a, shape, world, rank, local_rank):
                 "path": "fixedfanin_train_step_host (C ABI, pinned host buffers)" if world == 1 else
                         "torch H2D + ShardedLayer.train_step + D2H loss", "clocks_sm_mhz": c2["sm_mhz"]},
         "gpu_launches": gpu_launches,
-        "roofline": {"bound": "hbm", "kernel": "k_train_pipe (fused fwd/BCE/dW/db/dh-or-g/Adam row pass)",
+        "roofline": {"bound": "hbm", "kernel": "k_train_ring (fused fwd/BCE/dW/db/dh-or-g/Adam row pass)",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": kb / launches_per_step, "launches_per_step": launches_per_step,

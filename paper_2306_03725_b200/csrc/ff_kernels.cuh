@@ -214,15 +214,16 @@ __device__ __forceinline__ float row_dw_slot(const float (&dwp)[NG], int lane) {
   return __shfl_sync(kFull, v[0], ((lane & 3) << 3) | ((lane >> 2) & (NG > 4 ? 7 : 3)));
 }
 
-// Bias gradient of a 32-row block without a per-row warp reduction: row i's per-sample
-// gradients are parked in a per-warp shared buffer gb[i][sample]; at the end of the block
-// lane r sums row r over samples 0..31 in ascending order (fixed order, all kernels).
-struct DbBuf { float v[32][33]; };
-__device__ __forceinline__ float db_block_sum(const DbBuf& gb, int r) {
-  float s = 0.0f;
-#pragma unroll
-  for (int b = 0; b < 32; ++b) s += gb.v[r][b];
-  return s;
+// Bias gradient of one row over one 32-sample chunk: this lane's 4 samples
+// (g0 + g1) + (g2 + g3), then a butterfly over the 8 lanes of equal gq (xor 1, 2, 4).
+// IEEE addition is commutative, so every lane ends with the same bits; shared by every
+// kernel so their db are bit-identical.
+__device__ __forceinline__ float row_db_chunk(const float4& g4) {
+  float p = (g4.x + g4.y) + (g4.z + g4.w);
+  p += __shfl_xor_sync(kFull, p, 1);
+  p += __shfl_xor_sync(kFull, p, 2);
+  p += __shfl_xor_sync(kFull, p, 4);
+  return p;
 }
 
 // dW of this lane's slots (lane, lane + 32 for k > 32).
@@ -262,8 +263,6 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 #pragma unroll
   for (int e = 0; e < KPL; ++e) act[e] = lane + 32 * e < k;
   float loss_acc = 0.0f;
-  __shared__ DbBuf dbbuf[kRowThreads / 32];
-  DbBuf& gbuf = dbbuf[threadIdx.x >> 5];
 
   float w_n[KPL], mw_n[KPL], vw_n[KPL];
   int c_n[KPL], p_n[KPL];
@@ -313,7 +312,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       float dwp[NG];
 #pragma unroll
       for (int q = 0; q < NG; ++q) dwp[q] = 0.0f;
-      float dbp = 0.0f;
+      float dbr = 0.0f;                                // this row's bias gradient
       bool gany = false;                               // any nonzero gradient in this row
 
       for (int q2 = 0; q2 < nb; ++q2) {
@@ -343,7 +342,6 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
         if (a.loss != nullptr && b < B) loss_acc += lt;
         gany |= __any_sync(kFull, g != 0.0f);
         if (a.check_finite && __any_sync(kFull, b < B && !isfinite(y)) && lane == 0) atomicOr(a.err, kErrNonFinite);
-        dbp += g;
         float4 g4;
         g4.x = __shfl_sync(kFull, g, (0 << 3) | bq);
         g4.y = __shfl_sync(kFull, g, (1 << 3) | bq);
@@ -351,6 +349,8 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
         g4.w = __shfl_sync(kFull, g, (3 << 3) | bq);
 #pragma unroll
         for (int q = 0; q < NG; ++q) dwp[q] = q2 == 0 ? dw_partial(g4, hv[q]) : dwp[q] + dw_partial(g4, hv[q]);
+        const float dbc = row_db_chunk(g4);
+        dbr = q2 == 0 ? dbc : dbr + dbc;
         if (CSC) {
           // CSC mode: publish g[., j] (one 128-B line per chunk); dh is pulled later (k_dh_csc)
           st_hint(a.gT + ((j - jb) * nb + q2) * 32 + 4 * bq + gq, g, pol_l);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       // column pass skips the gather (its contribution w*g is exactly zero anyway)
       float gW[KPL];
       row_dw_slots<NG>(dwp, lane, gW);
-      gbuf.v[i][4 * bq + gq] = dbp;                   // this lane's sample (over all chunks)
+      if (lane == i) db_v = dbr;                      // lane i <-> row j0 + i
 #pragma unroll
       for (int e = 0; e < KPL; ++e) {
         if (!act[e]) continue;
@@ -387,9 +387,6 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       }
     }
     if (MODE == kModeForward) continue;
-    __syncwarp();
-    if (lv) db_v = db_block_sum(gbuf, lane);
-    __syncwarp();
     if (lv) {
       if (pm_v != 0u) a.posmask[j0 + lane] = 0u;      // self-clearing mask (chunk 0)
       if (MODE == kModeBackward || STORE_GRADS) a.db[j0 + lane] = db_v;
@@ -406,29 +403,46 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 
 // ------------------------------------------------------------------ pipelined train step
 // The fused training step of k_rows<train> for the hot configuration (k = 32 connections,
-// B <= 32 samples), software-pipelined for memory-level parallelism: while row X is being
-// computed, the 32 h-line gathers of row X+1 are already in flight (two register buffers
-// A/B, alternating) and the state of row X+2 is being loaded.  Same arithmetic (the shared
-// row_* helpers, same order) as k_rows, so results are bit-identical to the generic kernel.
-#ifndef FF_PIPE_THREADS
-#define FF_PIPE_THREADS 128
-#endif
-#ifndef FF_PIPE_MINB
-#define FF_PIPE_MINB 3
-#endif
-constexpr int kPipeThreads = FF_PIPE_THREADS;
-#ifndef FF_WS_RECOMPUTE
-#define FF_WS_RECOMPUTE 1   // CSC mode: re-shuffle the row's weights at compute time (saves registers)
-#endif
-constexpr int kPipeMinBlocks = FF_PIPE_MINB;
+// B <= 32 samples), software-pipelined for memory-level parallelism.  The h-line gathers
+// are staged through a per-warp shared-memory ring (cp.async.cg, 16 B per lane per
+// connection, L2 -> smem without registers): while row X is computed, the gathers of the
+// next D - 1 rows are in flight and the state of row X + D is being loaded.  In-flight
+// data does not occupy registers (107-111 regs), so 16-24 warps fit per SM.  Each lane reads
+// back exactly the 16-B slices it copied, so no cross-lane synchronisation is needed.
+// Same arithmetic (the shared row_* helpers, same order) as k_rows: bit-identical results.
+// Measured (Amazon-670K): CSC mode is latency/LSU-bound and prefers D = 2 with
+// 6 CTAs/SM; atomic mode is bound by the L1->XBAR red path and is insensitive (D = 3, 4 CTAs).
+template <bool CSC> struct RingCfg {
+  static constexpr int D = CSC ? 2 : 3;                 // ring stages per warp
+  static constexpr int kMinBlocks = CSC ? 6 : 4;        // CTAs per SM (register budget)
+};
+constexpr int kRingThreads = 128;
+constexpr int kRingStageBytes = 8 * 32 * 16;            // 8 registers x 32 lanes x 16 B = 32 h lines
+template <bool CSC>
+constexpr int ring_smem() { return (kRingThreads / 32) * RingCfg<CSC>::D * kRingStageBytes; }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
 
 template <bool STORE_GRADS, bool CSC>
-__global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(RowArgs a) {
-  constexpr int NG = 8;
+__global__ void __launch_bounds__(kRingThreads, RingCfg<CSC>::kMinBlocks) k_train_ring(RowArgs a) {
+  constexpr int NG = 8, D = RingCfg<CSC>::D;
   constexpr uint32_t kColFloats = 64;                   // hd column stride at nb = 1 (h | dh lines)
+  extern __shared__ __align__(16) unsigned char ring_smem[];
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int nwarp = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  // this lane's slot of stage 0 of this warp's ring; slot of connection 4q + gq = + q * 512
+  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring_smem) +
+                         (uint32_t)(threadIdx.x >> 5) * D * kRingStageBytes + (uint32_t)lane * 16u;
   const uint64_t pol_l = policy_evict_last();
   const int B = a.B;
   float* const hb = a.hd + 4 * bq;
@@ -441,8 +455,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
   const int b = 4 * bq + gq;                            // this lane's own sample
   const bool bvalid = b < B;
   float loss_acc = 0.0f;
-  __shared__ DbBuf dbbuf[kPipeThreads / 32];
-  DbBuf& gbuf = dbbuf[threadIdx.x >> 5];
 
   // this warp's rows: blocks w, w + nwarp, ...; cursor = (first row of the block relative
   // to j_begin, row in block, rows in block).  32-bit row arithmetic: L * k < 2^31.
@@ -475,33 +487,58 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
       v.bias = ld_na(a.bias + j); v.mb = ld_na(a.mb + j); v.vb = ld_na(a.vb + j); v.pm = a.posmask[j];
     }
   };
+  // gathers of one row into ring stage `stg` (always commits a group, possibly empty)
+  auto issue = [&](const Cur& cu, const St& st, uint32_t stg) {
+    if (live(cu)) {
+      const uint32_t dst = ring0 + stg * (uint32_t)kRingStageBytes;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        const uint32_t c = (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq);
+        cp_async16(dst + (uint32_t)q * 512u, col_line(hb, c, kColFloats));
+      }
+    }
+    cp_async_commit();
+  };
 
   Cur X{(uint32_t)global_warp() * (uint32_t)br, 0, 0};
   if (live(X)) {                                        // (no early return: block_atomic_add syncs)
   X.nl = nl_of(X.j0);
-  Cur Y = adv(X), Z = adv(Y);
-  St sX{}, sY{}, sZ{};
+  // rows X .. X+D-2 in flight before the loop; states of rows X .. X+D-1 loaded
+  Cur q_cur[D];
+  St q_st[D];
+  q_cur[0] = X;
+#pragma unroll
+  for (int d = 1; d < D; ++d) q_cur[d] = adv(q_cur[d - 1]);
+#pragma unroll
+  for (int d = 0; d < D; ++d) load_st(q_cur[d], q_st[d]);
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) issue(q_cur[d], q_st[d], (uint32_t)d);
   Bv bv{}, bv_next{};
-  float db_v = 0.0f;
-  load_st(X, sX);
-  load_st(Y, sY);
   load_bv(X, bv);
+  float db_v = 0.0f;
+  uint32_t stg = 0;                                     // ring stage of the row being computed
 
-  float wsA[NG], wsB[NG]; uint32_t csA[NG], csB[NG]; float4 hvA[NG], hvB[NG];
-  auto issue = [&](const St& st, float (&ws)[NG], uint32_t (&cs)[NG], float4 (&hv)[NG]) {
-    row_spread<NG>(st.w, st.c, gq, ws, cs);
-    // atomic mode: keep hd (h and dh lines) evict_last against the state stream, else plain
-    if (CSC) row_gather_plain<NG>(hb, cs, kColFloats, hv);
-    else row_gather<NG, true>(hb, cs, kColFloats, 32, gq, pol_l, hv);
-  };
-  issue(sX, wsA, csA, hvA);
-  load_st(Z, sZ);
+  while (true) {
+    // issue the row D-1 ahead into the stage freed by the previous compute; load the state
+    // of the row after it
+    issue(q_cur[D - 1], q_st[D - 1], stg == 0 ? (uint32_t)(D - 1) : stg - 1);
+    const Cur cu = q_cur[0];
+    St st = q_st[0];
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) { q_cur[d] = q_cur[d + 1]; q_st[d] = q_st[d + 1]; }
+    q_cur[D - 1] = adv(q_cur[D - 2]);
+    load_st(q_cur[D - 1], q_st[D - 1]);
+    if (live(q_cur[0]) && q_cur[0].i == 0) load_bv(q_cur[0], bv_next);
 
-  auto compute = [&](const Cur& cu, St& st, const float (&ws_in)[NG], const uint32_t (&cs)[NG],
-                     const float4 (&hv)[NG]) {
+    cp_async_wait<D - 1>();                             // this row's group is complete
+    float4 hv[NG];
+    const uint32_t src = ring0 + stg * (uint32_t)kRingStageBytes;
+#pragma unroll
+    for (int q = 0; q < NG; ++q) hv[q] = lds4(src + (uint32_t)q * 512u);
     float ws[NG];
 #pragma unroll
-    for (int q = 0; q < NG; ++q) ws[q] = (CSC && FF_WS_RECOMPUTE) ? __shfl_sync(kFull, st.w, 4 * q + gq) : ws_in[q];
+    for (int q = 0; q < NG; ++q) ws[q] = __shfl_sync(kFull, st.w, 4 * q + gq);
+
     const uint32_t j = row_of(cu);
     const int i = cu.i;
     const float bj = __shfl_sync(kFull, bv.bias, i);
@@ -524,15 +561,18 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     for (int q = 0; q < NG; ++q) dwp[q] = dw_partial(g4, hv[q]);
     if (CSC) {
       st_hint(a.gT + (size_t)((j - jb32) * 32u + b), g, pol_l);
-      a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;        // 0: column pass skips (w*g == 0)
+      a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;      // 0: column pass skips (w*g == 0)
     } else {
       const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
-      for (int q = 0; q < NG; ++q)
-        if (gnz) red_add4(col_line(hb, cs[q], kColFloats) + 32, dh_contrib(ws[q], g4), pol_l);
+      for (int q = 0; q < NG; ++q) {
+        const uint32_t c = (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq);
+        if (gnz) red_add4(col_line(hb, c, kColFloats) + 32, dh_contrib(ws[q], g4), pol_l);
+      }
     }
     const float gW = row_dw_slot<NG>(dwp, lane);
-    gbuf.v[i][b] = g;
+    const float dbr = row_db_chunk(g4);
+    if (lane == i) db_v = dbr;
     const uint32_t row = j * 32u + lane;
     if (STORE_GRADS) a.dW[row] = gW;
     adam_update(st.w, st.mw, st.vw, gW, a.adam);
@@ -541,9 +581,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
     st_na(vW + row, st.vw);
     if (i == cu.nl - 1) {                                // block done: vectorized bias update
       const uint32_t jl = jb32 + cu.j0 + lane;
-      __syncwarp();
-      if (lane <= i) db_v = db_block_sum(gbuf, lane);
-      __syncwarp();
       if (lane <= i) {
         if (bv.pm != 0u) a.posmask[jl] = 0u;
         if (STORE_GRADS) a.db[jl] = db_v;
@@ -555,30 +592,11 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeMinBlocks) k_train_pipe(Row
       }
       db_v = 0.0f;
     }
-  };
-
-  // one pipeline step: issue Y's gathers into the free buffer, load the state of Z's
-  // successor, compute X; then X <- Y <- Z <- adv(Z).  Written twice so the A/B buffers
-  // swap roles without register moves.
-  auto step = [&](float (&wsC)[NG], uint32_t (&csC)[NG], float4 (&hvC)[NG],
-                  float (&wsN)[NG], uint32_t (&csN)[NG], float4 (&hvN)[NG]) -> bool {
-    if (live(Y)) {
-      issue(sY, wsN, csN, hvN);
-      if (Y.i == 0) load_bv(Y, bv_next);
-    }
-    const Cur Zn = adv(Z);
-    St sZn{};
-    load_st(Zn, sZn);
-    compute(X, sX, wsC, csC, hvC);
-    X = Y; Y = Z; Z = Zn;
-    sX = sY; sY = sZ; sZ = sZn;
-    if (live(X) && X.i == 0) bv = bv_next;
-    return live(X);
-  };
-  while (true) {
-    if (!step(wsA, csA, hvA, wsB, csB, hvB)) break;
-    if (!step(wsB, csB, hvB, wsA, csA, hvA)) break;
+    stg = stg + 1 == (uint32_t)D ? 0u : stg + 1;
+    if (!live(q_cur[0])) break;
+    if (q_cur[0].i == 0) bv = bv_next;
   }
+  cp_async_wait<0>();
   }
   if (a.loss != nullptr) block_atomic_add(loss_acc * a.grad_scale, a.loss);
 }

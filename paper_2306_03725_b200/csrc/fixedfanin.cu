@@ -156,7 +156,7 @@ struct ff_layer {
   uint32_t* posmask;
   int64_t t;
   bool grads_valid;
-  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_pipe;
+  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring;
   int nsm;
   std::vector<cudaEvent_t> prof_ev;   // pairs (before, after) of the fused row kernel
   int prof_used = 0;
@@ -235,22 +235,22 @@ const void* predict_kernel(int k) {
 }
 
 // Pipelined fused step (k = 32, B <= 32): same arithmetic as k_rows<train>, more gathers in flight.
-const void* pipe_kernel(bool sg, bool csc) {
-  if (sg) return csc ? (const void*)k_train_pipe<true, true> : (const void*)k_train_pipe<true, false>;
-  return csc ? (const void*)k_train_pipe<false, true> : (const void*)k_train_pipe<false, false>;
+const void* ring_kernel(bool sg, bool csc) {
+  if (sg) return csc ? (const void*)k_train_ring<true, true> : (const void*)k_train_ring<true, false>;
+  return csc ? (const void*)k_train_ring<false, true> : (const void*)k_train_ring<false, false>;
 }
-constexpr int kPipeLaunchThreads = kPipeThreads;
+int ring_smem_of(bool csc) { return csc ? ring_smem<true>() : ring_smem<false>(); }
 
-ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads = kRowThreads) {
+ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads = kRowThreads, int smem = 0) {
   void* args[] = {&a};
-  FF_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, st));
+  FF_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, (size_t)smem, st));
   ++g_launches;
   return FF_OK;
 }
 
-int occupancy_grid(const void* fn, int nsm, int threads) {
+int occupancy_grid(const void* fn, int nsm, int threads, int smem = 0) {
   int per = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0) != cudaSuccess || per < 1) per = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, (size_t)smem) != cudaSuccess || per < 1) per = 1;
   return nsm * per;
 }
 
@@ -279,11 +279,11 @@ int block_rows(int64_t rows, int grid, int threads) {
 }
 
 // One row-kernel launch, bracketed by a profiling event pair while profiling is on.
-ff_status timed_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads) {
+ff_status timed_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads, int smem) {
   a.br = block_rows(a.j_end - a.j_begin, grid, threads);
   const bool timed = 2 * (l->prof_used + 1) <= (int)l->prof_ev.size();
   if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used], st));
-  ff_status s = launch_rows(fn, grid, a, st, threads);
+  ff_status s = launch_rows(fn, grid, a, st, threads, smem);
   if (s != FF_OK) return s;
   if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used++ + 1], st));
   return FF_OK;
@@ -291,15 +291,15 @@ ff_status timed_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, cudaStre
 
 // The row pass (+ the CSC column pass per label tile in CSC mode).
 ff_status run_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, int B, cudaStream_t st,
-                   int threads = kRowThreads) {
+                   int threads = kRowThreads, int smem = 0) {
   if (!l->csc) {
     if (l->cfg.L_local == 0) return FF_OK;
-    return timed_rows(l, fn, grid, a, st, threads);
+    return timed_rows(l, fn, grid, a, st, threads, smem);
   }
   for (int t = 0; t < l->ntiles; ++t) {
     a.j_begin = (int64_t)t * l->tile_rows;
     a.j_end = std::min<int64_t>(a.j_begin + l->tile_rows, l->cfg.L_local);
-    ff_status s = timed_rows(l, fn, grid, a, st, threads);
+    ff_status s = timed_rows(l, fn, grid, a, st, threads, smem);
     if (s != FF_OK) return s;
     if (B > 0) {
       s = launch_dh_csc(l, B, t, st);
@@ -356,9 +356,12 @@ ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t*
   a.adam = adam_args(l, lr, l->t);
   const bool sg = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
   const bool pipe = l->cfg.k == 32 && B <= 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE);
-  const void* fn = pipe ? pipe_kernel(sg, l->csc)
-                        : (sg ? row_kernel<kModeTrain, true>(l->cfg.k, l->csc) : row_kernel<kModeTrain, false>(l->cfg.k, l->csc));
-  s = run_rows(l, fn, pipe ? l->grid_pipe : l->grid_train, a, B, st, pipe ? kPipeLaunchThreads : kRowThreads);
+  if (pipe) {
+    s = run_rows(l, ring_kernel(sg, l->csc), l->grid_ring, a, B, st, kRingThreads, ring_smem_of(l->csc));
+  } else {
+    const void* fn = sg ? row_kernel<kModeTrain, true>(l->cfg.k, l->csc) : row_kernel<kModeTrain, false>(l->cfg.k, l->csc);
+    s = run_rows(l, fn, l->grid_train, a, B, st, kRowThreads);
+  }
   if (s != FF_OK) return s;
   l->grads_valid = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
   if (B == 0) return FF_OK;
@@ -421,7 +424,14 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->grid_fwd = occupancy_grid(row_kernel<kModeForward, false>(c.k, false), l->nsm, kRowThreads);
   l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k, l->csc), l->nsm, kRowThreads);
   l->grid_csc = occupancy_grid((const void*)k_dh_csc<true>, l->nsm, 256);
-  l->grid_pipe = occupancy_grid(pipe_kernel(false, l->csc), l->nsm, kPipeLaunchThreads);
+  for (int sg = 0; sg < 2; ++sg)
+    for (int cs = 0; cs < 2; ++cs)
+      if (cudaFuncSetAttribute(ring_kernel(sg, cs), cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem_of(cs)) !=
+          cudaSuccess) {
+        delete l;
+        return fail(FF_ERR_CUDA, "pipelined kernel smem attribute");
+      }
+  l->grid_ring = occupancy_grid(ring_kernel(false, l->csc), l->nsm, kRingThreads, ring_smem_of(l->csc));
   if (l->csc) {
     // tile = a whole number of row-kernel "waves" (warps x 32 labels) within the L2 budget
     const int64_t cap = (int64_t)csc_tile_cap(c), wave = (int64_t)l->grid_train * (kRowThreads / 32) * 32;

@@ -506,8 +506,9 @@ def test_csc_multi_tile_dh_and_grads():
 @DH
 @pytest.mark.parametrize("L,m,B", [(5000, 1024, 32), (1234, 700, 19), (31, 64, 32), (70000, 4096, 32)])
 def test_pipelined_step_equals_generic_step(L, m, B, dh_mode, loss):
-    """k = 32, B <= 32 runs the software-pipelined fused kernel; FF_FLAG_NO_PIPE forces the
-    generic one.  Both implement the same arithmetic: state and gradients bit-identical."""
+    """k = 32, B <= 32 runs the software-pipelined fused kernel (cp.async shared-memory ring);
+    FF_FLAG_NO_PIPE forces the generic one.  Both implement the same arithmetic: state and
+    gradients bit-identical."""
     layer = L_()
     k = 32
     flags = layer.FF_FLAG_STORE_GRADS
