@@ -63,7 +63,7 @@ typedef enum {
 /* Compile-time limits of this build (checked at create). */
 #define FF_MAX_FANIN 64     /* k <= 64 (the paper's largest, 64 nnz/label): a label
                                row is one or two warp-wide 128-B lines per array               */
-#define FF_MAX_BATCH 128    /* B <= 128: processed as ceil(B/32) 32-sample lane groups        */
+#define FF_MAX_BATCH 1024   /* B <= 1024: processed as ceil(B/32) 32-sample lane groups       */
 #define FF_MAX_TOPK 8       /* K <= 8 (the paper reports P@1/3/5)                  */
 
 /* ff_config.flags */
@@ -179,6 +179,20 @@ ff_status fixedfanin_redistribute(ff_layer* layer, uint64_t step, ff_stream_t st
  * ids [B][K] int32 GLOBAL ids.  1 <= K <= min(max_topk, L_local).                      */
 ff_status fixedfanin_predict_topk(ff_layer* layer, const float* h, int32_t B, int32_t K,
                                   float* scores, int32_t* ids, ff_stream_t stream);
+
+/* Shortlist scoring (restricting scoring to a label shortlist is "a trivial
+ * matrix slicing operation"): for every candidate entry p of instance b,
+ * cand_ptr[b] <= p < cand_ptr[b+1] (CSR, int32, device),
+ *   scores[p] = y[b, cand_ids[p]] = bias_j + sum_i W[j][i] * h[b][idx[j][i]]  (Alg. 1)
+ * bit-identical to the score the forward / predict_topk compute for the same (b, j).
+ * h float [B][m] row-major (device).  cand_ids are GLOBAL label ids; entries whose label
+ * is not in this shard's rows are written as +0 (so the shards' outputs sum to the full
+ * result); ids outside [0, L_global) are written as NaN and reported as FF_ERR_RANGE by
+ * fixedfanin_check.  B >= 0 (no max_batch limit: no workspace is used).  cand_ids and
+ * scores may be NULL when the list is empty (cand_ptr[B] == 0).                        */
+ff_status fixedfanin_score_shortlist(ff_layer* layer, const float* h, int32_t B,
+                                     const int32_t* cand_ptr, const int32_t* cand_ids,
+                                     float* scores, ff_stream_t stream);
 
 /* Merge per-shard top-K lists: in_scores/in_ids [P][B][K] (device) -> out [B][K] under
  * the same total order.  Stateless.  1 <= K <= FF_MAX_TOPK, 1 <= P <= 1024.            */

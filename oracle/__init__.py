@@ -50,10 +50,12 @@ def lib():
         L.oracle_init.argtypes = [i64, i64, i32, i32, u64, f32, P, P]
         L.oracle_redistribute.argtypes = [i64, i64, i32, i32, i32, u64, u64, P, P, P, P]
         L.oracle_topk.argtypes = [i64, i64, i32, P, i32, P, P]
+        L.oracle_score_shortlist.argtypes = [i64, i64, i32, i32, i32, P, P, P, P, P, P, P, P]
         L.oracle_precision_at_k.argtypes = [i32, i32, P, P, P]
         L.oracle_precision_at_k.restype = f64
         for f in ("oracle_forward", "oracle_bce_grad", "oracle_sqh_grad", "oracle_weight_grad", "oracle_input_grad",
-                  "oracle_adam", "oracle_philox4x32_10", "oracle_init", "oracle_redistribute", "oracle_topk"):
+                  "oracle_adam", "oracle_philox4x32_10", "oracle_init", "oracle_redistribute", "oracle_topk",
+                  "oracle_score_shortlist"):
             getattr(L, f).restype = None
         _lib = L
     return _lib
@@ -82,6 +84,19 @@ def forward(W, idx, bias, h):
     y = np.empty((B, L)); Ay = np.empty((B, L))
     lib().oracle_forward(L, m, k, B, _p(W), _p(idx), _p(bias), _p(h), _p(y), _p(Ay))
     return y, Ay
+
+
+def score_shortlist(W, idx, bias, h, cand_ptr, cand_ids, row_begin=0):
+    """Alg. 1 restricted to a CSR shortlist of (instance, label) pairs
+    (P:1057-1059); 0 for labels outside this shard (reading R24).  Returns (y[nnz], Ay[nnz])."""
+    W, idx, bias, h = _f64(W), _i32(idx), _f64(bias), _f64(h)
+    L, k = W.shape
+    B, m = h.shape
+    cp, ci = _i32(cand_ptr), _i32(cand_ids if len(cand_ids) else np.zeros(1, np.int32))
+    n = int(cp[-1])
+    y = np.empty(max(n, 1)); Ay = np.empty(max(n, 1))
+    lib().oracle_score_shortlist(L, row_begin, m, k, B, _p(W), _p(idx), _p(bias), _p(h), _p(cp), _p(ci), _p(y), _p(Ay))
+    return y[:n], Ay[:n]
 
 
 def labels_csr(pos_lists):

@@ -57,6 +57,34 @@ void oracle_forward(int64_t L, int32_t m, int32_t k, int32_t B,
     }
 }
 
+/* Shortlist scoring ("a trivial matrix slicing operation"): Alg. 1 restricted
+ * to the (instance, label) pairs of a CSR candidate list: for cand_ptr[b] <= p < cand_ptr[b+1],
+ *   y[p] = bias[j] + sum_i W[j,i] h[b, idx[j,i]],  j = cand_ids[p] - row_begin,
+ * and y[p] = 0 when j is outside this shard's rows [0, L) (reading R24).  Ay as above.  */
+void oracle_score_shortlist(int64_t L, int64_t row_begin, int32_t m, int32_t k, int32_t B,
+                            const double* W, const int32_t* idx, const double* bias, const double* h,
+                            const int32_t* cand_ptr, const int32_t* cand_ids, double* y, double* Ay)
+{
+    for (int32_t instance = 0; instance < B; ++instance) {
+        for (int32_t p = cand_ptr[instance]; p < cand_ptr[instance + 1]; ++p) {
+            int64_t label = (int64_t)cand_ids[p] - row_begin;
+            double value = 0.0, avalue = 0.0;
+            if (label >= 0 && label < L) {
+                value = bias[label];
+                avalue = fabs(bias[label]);
+                for (int32_t weight_idx = 0; weight_idx < k; ++weight_idx) {
+                    int32_t source = idx[label * k + weight_idx];
+                    double feature = h[(int64_t)instance * m + source];
+                    value += feature * W[label * k + weight_idx];
+                    avalue += fabs(feature * W[label * k + weight_idx]);
+                }
+            }
+            y[p] = value;
+            Ay[p] = avalue;
+        }
+    }
+}
+
 /* Is global label `gid` a positive of instance b?  y in {0,1}^L stored sparse
  * (P:92-97): positives of b are lbl_ids[lbl_ptr[b] .. lbl_ptr[b+1]).            */
 static int is_positive(const int32_t* lbl_ptr, const int32_t* lbl_ids, int32_t b, int64_t gid)

@@ -1025,4 +1025,63 @@ __global__ void k_merge_topk(const float* __restrict__ in_s, const int* __restri
   }
 }
 
+// ---------------------------------------------------------------------- shortlist scoring
+// Scores of explicit (sample, label) pairs — the "trivial matrix slicing" of P:1057-1059.
+// One thread per pair.  score_one<NG> evaluates exactly the operation sequence the warp
+// kernels perform for that pair (row_score_own): per connection group g = s mod 4 two fma
+// chains over slots s = 4q + g (q even / odd, slots >= k contribute fma(0, 0, .)), their
+// sum P_g, then ((P_0 + P_2) + (P_1 + P_3)) + bias — so the result is bit-identical to the
+// forward / predict score of the same pair (IEEE addition is commutative).
+template <int NG>
+__device__ __forceinline__ float score_one(const float* __restrict__ Wj, const int* __restrict__ ij,
+                                           const float* __restrict__ hrow, int k, float bj) {
+  float P[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    float ca = 0.0f, cb = 0.0f;
+#pragma unroll
+    for (int q = 0; q < NG; q += 2) {
+      const int s0 = 4 * q + g, s1 = 4 * (q + 1) + g;
+      const float w0 = s0 < k ? Wj[s0] : 0.0f, h0 = s0 < k ? __ldg(hrow + ij[s0]) : 0.0f;
+      ca = __fmaf_rn(w0, h0, ca);
+      if (q + 1 < NG) {
+        const float w1 = s1 < k ? Wj[s1] : 0.0f, h1 = s1 < k ? __ldg(hrow + ij[s1]) : 0.0f;
+        cb = __fmaf_rn(w1, h1, cb);
+      }
+    }
+    P[g] = __fadd_rn(ca, cb);
+  }
+  return __fadd_rn(__fadd_rn(__fadd_rn(P[0], P[2]), __fadd_rn(P[1], P[3])), bj);
+}
+
+// Warp per sample (grid-stride), lanes over its candidate entries.  Entries whose label is
+// not in this shard's rows get +0 (shards' outputs sum to the full result); ids outside
+// [0, L_global) set kErrLabelRange and get NaN.
+template <int NG>
+__global__ void __launch_bounds__(256) k_shortlist(const float* __restrict__ W, const int* __restrict__ idx,
+                                                   const float* __restrict__ bias, const float* __restrict__ h,
+                                                   int64_t m, int k, int64_t L, int64_t row_begin, int64_t L_global,
+                                                   int B, const int* __restrict__ cand_ptr,
+                                                   const int* __restrict__ cand_ids, float* __restrict__ scores,
+                                                   int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  for (int b = (int)global_warp(); b < B; b += nw) {
+    const int p0 = cand_ptr[b], p1 = cand_ptr[b + 1];
+    const float* hrow = h + (int64_t)b * m;
+    for (int p = p0 + lane; p < p1; p += 32) {
+      const int gid = cand_ids[p];
+      const int64_t j = (int64_t)gid - row_begin;
+      float y = 0.0f;
+      if (gid < 0 || gid >= L_global) {
+        atomicOr(err, kErrLabelRange);
+        y = __int_as_float(0x7fc00000);
+      } else if (j >= 0 && j < L) {
+        y = score_one<NG>(W + j * k, idx + j * k, hrow, k, bias[j]);
+      }
+      scores[p] = y;
+    }
+  }
+}
+
 }  // namespace ff

@@ -651,6 +651,33 @@ ff_status fixedfanin_predict_topk(ff_layer* l, const float* h, int32_t B, int32_
   return FF_OK;
 }
 
+ff_status fixedfanin_score_shortlist(ff_layer* l, const float* h, int32_t B, const int32_t* cand_ptr,
+                                     const int32_t* cand_ids, float* scores, ff_stream_t stream) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (B < 0) return fail(FF_ERR_ARG, "B=%d < 0", B);
+  if (B == 0) return FF_OK;
+  // cand_ids / scores are only dereferenced for existing entries (NULL allowed if cand_ptr[B] == 0)
+  if (!h || !cand_ptr) return fail(FF_ERR_ARG, "null h/cand_ptr");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int k = l->cfg.k;
+  // the same NG the warp kernels use for this k (predict_kernel / row_kernel_csc)
+  const void* fn = k == 64 ? (const void*)k_shortlist<16> : k > 32 ? (const void*)k_shortlist<16>
+                 : k == 32 ? (const void*)k_shortlist<8> : k <= 16 ? (const void*)k_shortlist<4>
+                 : (const void*)k_shortlist<8>;
+  {
+    const float* W = l->W; const int* idx = l->idx; const float* bias = l->bias;
+    int64_t m = l->cfg.m, L = l->cfg.L_local, rb = l->cfg.row_begin, Lg = l->cfg.L_global;
+    int kk = k, BB = B;
+    int* err = l->err;
+    void* args[] = {&W, &idx, &bias, &h, &m, &kk, &L, &rb, &Lg, &BB, &cand_ptr, &cand_ids, &scores, &err};
+    const int grid = std::max(1, std::min((B + 7) / 8, 8 * l->nsm));
+    FF_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(256), args, 0, st));
+    ++g_launches;
+  }
+  return FF_OK;
+}
+
 ff_status fixedfanin_merge_topk(const float* in_s, const int32_t* in_i, int32_t P, int32_t B, int32_t K, float* out_s,
                                 int32_t* out_i, ff_stream_t stream) {
   g_launches = 0;

@@ -21,7 +21,7 @@ FF_FLAG_STORE_GRADS = 2
 FF_FLAG_NO_PIPE = 4
 FF_DH_ATOMIC, FF_DH_CSC = 0, 1
 FF_LOSS_BCE, FF_LOSS_SQH = 0, 1
-FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 64, 128, 8
+FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 64, 1024, 8
 _STATUS = {1: "FF_ERR_ARG", 2: "FF_ERR_CONFIG", 3: "FF_ERR_RANGE", 4: "FF_ERR_NONFINITE", 5: "FF_ERR_CUDA",
            6: "FF_ERR_STATE"}
 
@@ -29,7 +29,8 @@ EXPORTS = [
     "fixedfanin_workspace_size", "fixedfanin_create", "fixedfanin_destroy", "fixedfanin_set_params",
     "fixedfanin_get_params", "fixedfanin_forward", "fixedfanin_backward", "fixedfanin_get_grads",
     "fixedfanin_adam_step", "fixedfanin_train_step", "fixedfanin_train_step_host", "fixedfanin_redistribute",
-    "fixedfanin_predict_topk", "fixedfanin_merge_topk", "fixedfanin_check", "fixedfanin_profile_begin",
+    "fixedfanin_predict_topk", "fixedfanin_score_shortlist", "fixedfanin_merge_topk", "fixedfanin_check",
+    "fixedfanin_profile_begin",
     "fixedfanin_profile_end", "fixedfanin_last_launch_count",
     "fixedfanin_last_error",
 ]
@@ -78,6 +79,7 @@ def lib() -> ctypes.CDLL:
             "fixedfanin_redistribute": [P, u64, P],
             "fixedfanin_predict_topk": [P, P, i32, i32, P, P, P],
             "fixedfanin_merge_topk": [P, P, i32, i32, i32, P, P, P],
+            "fixedfanin_score_shortlist": [P, P, i32, P, P, P, P],
             "fixedfanin_check": [P, P],
             "fixedfanin_profile_begin": [P, i32],
             "fixedfanin_profile_end": [P, P, P],
@@ -250,6 +252,16 @@ class FixedFanInLayer:
         ids = torch.empty((B, K), dtype=torch.int32, device=self.device)
         _check(lib().fixedfanin_predict_topk(self._h, _ptr(h), B, K, _ptr(scores), _ptr(ids), _stream(stream)))
         return scores, ids
+
+    def score_shortlist(self, h, cand_ptr, cand_ids, scores=None, stream=None):
+        """Scores y[b, cand_ids[p]] of a CSR shortlist; +0 for labels of other
+        shards.  h [B][m], cand_ptr int32 [B+1], cand_ids int32 [nnz] (device)."""
+        B = h.shape[0]
+        if scores is None:
+            scores = torch.empty(cand_ids.shape[0], dtype=torch.float32, device=self.device)
+        _check(lib().fixedfanin_score_shortlist(self._h, _ptr(h), B, _ptr(cand_ptr), _ptr(cand_ids), _ptr(scores),
+                                                _stream(stream)))
+        return scores
 
     def profile_begin(self, max_launches: int):
         _check(lib().fixedfanin_profile_begin(self._h, int(max_launches)))

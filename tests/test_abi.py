@@ -50,7 +50,7 @@ def test_workspace_size_matches_layout_model():
     (dict(L_global=10, m=8, k=9), "k="),            # k > m
     (dict(L_global=10, m=128, k=65), "k="),         # k > FF_MAX_FANIN (64)
     (dict(L_global=10, m=64, k=8, row_begin=5, L_local=6), "shard"),
-    (dict(L_global=10, m=64, k=8, max_batch=129), "max_batch"),
+    (dict(L_global=10, m=64, k=8, max_batch=1025), "max_batch"),
     (dict(L_global=10, m=64, k=8, max_topk=9), "max_topk"),
     (dict(L_global=2 ** 31, m=64, k=8), "L_global"),
     (dict(L_global=10, m=64, k=8, prune_frac=1.0), "prune_frac"),

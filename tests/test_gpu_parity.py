@@ -104,7 +104,7 @@ def test_init_full_amazon_670k_sampled_rows():
 
 # --------------------------------------------------------------- forward / backward
 CASES = [(1000, 256, 16, 32), (1000, 256, 16, 5), (333, 100, 13, 37), (2000, 512, 32, 100), (97, 64, 1, 1),
-         (64, 32, 32, 128), (1500, 2048, 64, 32), (400, 300, 50, 40), (130, 64, 64, 7)]
+         (64, 32, 32, 128), (1500, 2048, 64, 32), (400, 300, 50, 40), (130, 64, 64, 7), (700, 512, 32, 300)]
 
 
 @pytest.mark.parametrize("L,m,k,B", CASES)
@@ -302,7 +302,8 @@ def test_redistribution_config_errors():
 
 # ------------------------------------------------------------------------- top-K
 @pytest.mark.parametrize("L,m,k,B,K", [(1000, 256, 16, 32, 5), (5000, 512, 32, 70, 8), (9, 16, 4, 3, 1),
-                                        (8, 16, 4, 3, 8), (3000, 4096, 64, 32, 5), (700, 500, 40, 50, 3)])
+                                        (8, 16, 4, 3, 8), (3000, 4096, 64, 32, 5), (700, 500, 40, 50, 3),
+                                        (4000, 1024, 32, 1024, 5)])
 def test_predict_topk_bit_exact(L, m, k, B, K):
     lay = make(L, m, k, B=B, seed=3)
     h = tens(synth.hidden_batch(B, m, step=1))
@@ -563,3 +564,60 @@ def test_sqh_implicit_negative_mining_skips_are_exact(dh_mode, k, B):
     assert_close(db, dbr, Adb, "db")
     assert_close(dh.cpu().numpy(), dhr, Adh, "dh")
     assert abs(loss.item() - lref) <= RTOL * lref
+
+
+# ---------------------------------------------------------- shortlist scoring (NEXT-3)
+def _shortlist(B, L_global, n, seed):
+    """CSR shortlist: n candidates per instance (some repeated), sorted per instance."""
+    r = np.random.default_rng(seed)
+    ptr = np.arange(B + 1, dtype=np.int32) * n
+    ids = np.concatenate([np.sort(r.integers(0, L_global, size=n)) for _ in range(B)]).astype(np.int32) \
+        if B * n else np.zeros(0, np.int32)
+    return ptr, ids
+
+
+@pytest.mark.parametrize("L,m,k,B,n", [(1000, 256, 16, 32, 40), (5000, 1024, 32, 70, 100), (400, 300, 50, 9, 33),
+                                        (3000, 4096, 64, 32, 17), (333, 100, 13, 5, 200), (97, 64, 1, 3, 5)])
+def test_shortlist_scores_parity_and_bit_exact_vs_forward(L, m, k, B, n):
+    """P:1057-1059 (R24): shortlist scores match the oracle within R19 and equal the
+    forward's score of the same (instance, label) bit for bit."""
+    lay = make(L, m, k, B=min(B, 128), seed=5)
+    W, idx, bias = synth.random_params(L, m, k, seed=L + k)
+    lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    h = synth.hidden_batch(B, m, step=2)
+    ptr, ids = _shortlist(B, L, n, seed=L + n)
+    sc = lay.score_shortlist(tens(h), tens(ptr), tens(ids)).cpu().numpy()
+    p = state_of(lay)
+    yr, Ay = oracle.score_shortlist(p["W"], p["idx"], p["bias"], h, ptr, ids)
+    assert_close(sc, yr, Ay, "shortlist")
+    y = lay.forward(tens(h)).cpu().numpy()
+    b_of = np.repeat(np.arange(B), np.diff(ptr))
+    assert np.array_equal(sc.view(np.uint32), y[b_of, ids].view(np.uint32))
+
+
+def test_shortlist_sharded_sum_and_errors():
+    """Labels owned by another shard score +0, so the shards' outputs sum to the unsharded
+    result; an id outside [0, L_global) is NaN and reported by check(); empty lists."""
+    layer = L_()
+    L, m, k, B = 1000, 256, 16, 6
+    full = make(L, m, k, B=B, seed=9)
+    sh = [make(500, m, k, B=B, seed=9, L_global=L, row_begin=r, L_local=500) for r in (0, 500)]
+    p = full.get_params()
+    for r, s in zip((0, 500), sh):
+        s.set_params(**{key: v[r:r + 500] for key, v in p.items() if torch.is_tensor(v) and v.shape[0] == L})
+    h = tens(synth.hidden_batch(B, m, step=4))
+    ptr = np.array([0, 3, 3, 5, 9, 9, 12], np.int32)
+    ids = np.array([0, 499, 500, 7, 999, 1, 2, 3, 4, 998, 500, 501], np.int32)
+    ref = full.score_shortlist(h, tens(ptr), tens(ids))
+    parts = [s.score_shortlist(h, tens(ptr), tens(ids)) for s in sh]
+    assert torch.equal(parts[0] + parts[1], ref)
+    assert (parts[0][torch.from_numpy(ids >= 500).to(dev())] == 0).all()
+    bad = np.array([0, 1, 1, 1, 1, 1, 1], np.int32)
+    out = full.score_shortlist(h, tens(bad), tens(np.array([L], np.int32)))
+    assert torch.isnan(out).all()
+    with pytest.raises(layer.FFError) as e:
+        full.check()
+    assert e.value.status == layer.FF_ERR_RANGE
+    empty = full.score_shortlist(h, tens(np.zeros(B + 1, np.int32)), tens(np.zeros(0, np.int32)))
+    assert empty.numel() == 0
+    full.check()

@@ -94,6 +94,28 @@ def test_dense_mask_equivalence(L, m, k, B):
     np.testing.assert_allclose(db, g.sum(0), atol=1e-12)
 
 
+@pytest.mark.parametrize("row_begin", [0, 11])
+def test_shortlist_is_a_slice_of_the_dense_layer(row_begin):
+    """P:1057-1059 (R24): shortlist scores are the entries (b, j) of h @ D + bias for the
+    listed pairs (dense matmul with the scatter matrix, a route independent of Alg. 1's
+    loop), 0 for labels outside this shard; an empty list scores nothing."""
+    L, m, k, B = 40, 30, 6, 5
+    W, idx, bias = synth.random_params(L, m, k, seed=77)
+    W = W.astype(np.float64); bias = bias.astype(np.float64)
+    h = np.random.default_rng(3).standard_normal((B, m))
+    Yd = h @ dense_equivalent(W, idx, m) + bias
+    ptr = np.array([0, 4, 4, 7, 12, 13], np.int32)
+    ids = np.array([11, 50, 12, 11, 0, 39 + 11, 20, 30, 31, 51, 10, 13, 25], np.int32)
+    y, Ay = oracle.score_shortlist(W, idx, bias, h, ptr, ids, row_begin=row_begin)
+    b_of = np.repeat(np.arange(B), np.diff(ptr))
+    j = ids.astype(np.int64) - row_begin
+    own = (j >= 0) & (j < L)
+    np.testing.assert_allclose(y[own], Yd[b_of[own], j[own]], rtol=0, atol=1e-12 * Ay.max())
+    assert (y[~own] == 0).all() and (~own).any() and own.any()
+    y0, _ = oracle.score_shortlist(W, idx, bias, h, np.zeros(B + 1, np.int32), np.zeros(0, np.int32))
+    assert y0.shape == (0,)
+
+
 def test_full_fan_in_equals_dense_layer():
     """k = m: every label connects to every feature -> a dense layer."""
     L, m, B = 12, 8, 5
