@@ -322,6 +322,35 @@ def run_ours(a, shape, world, rank, local_rank):
     barrier()
     ms_pred = max_over_ranks(e0.elapsed_time(e1))
 
+    # ---- NEXT-3: large-batch inference and shortlist scoring, one GPU
+    big = None
+    if world == 1:
+        from paper_2306_03725_b200.layer import FixedFanInLayer, LayerConfig
+        BI, NCAND = 1024, 100
+        inf = FixedFanInLayer(LayerConfig(L_global=shape.L, m=shape.m, k=shape.k, max_batch=BI,
+                                          seed=synth.PARAM_SEED), device=dev)
+        inf.set_params(**{key: v for key, v in eng.get_params().items() if torch.is_tensor(v)})
+        hb = torch.from_numpy(synth.hidden_batch(BI, shape.m, step=99)).to(dev)
+        rng = np.random.default_rng(7)
+        cptr = torch.arange(BI + 1, dtype=torch.int32, device=dev) * NCAND
+        cids = torch.from_numpy(rng.integers(0, shape.L, size=BI * NCAND).astype(np.int32)).to(dev)
+        scores = torch.empty(BI * NCAND, dtype=torch.float32, device=dev)
+        res = {}
+        for name, fn, reps in (("predict", lambda: inf.predict_topk(hb, K), 5),
+                               ("shortlist", lambda: inf.score_shortlist(hb, cptr, cids, scores), 50)):
+            fn()
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            res[name] = e0.elapsed_time(e1) / reps
+        big = {"B": BI, "K": K, "predict_samples_per_s": BI / (res["predict"] * 1e-3),
+               "predict_ms_per_batch": res["predict"],
+               "shortlist_candidates_per_sample": NCAND, "shortlist_pairs_per_s": BI * NCAND / (res["shortlist"] * 1e-3),
+               "shortlist_ms_per_batch": res["shortlist"]}
+        del inf
+
     if rank != 0:
         return
     peak, peak_src = peaks()
@@ -367,6 +396,7 @@ def run_ours(a, shape, world, rank, local_rank):
                     "ms_per_batch": ms_pred / n_pred,
                     "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,
                     "frac": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9 / peak},
+        "inference_large_batch": big,
     }
     # NEXT-4 memory report: this layer's device bytes vs the dense/COO formats of P:37-45
     Lk = shape.L * shape.k
