@@ -183,6 +183,63 @@ def run_reference(a, shape, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- NEXT-2
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 148 SMs x 128 FP32 lanes x FMA x max SM clock
+
+
+def run_model(eng, shape, dev, stream, e0, e1, d=512, dropout=0.1, steps=100):
+    """the whole proposed architecture (Fig. 2): 512-d Slice-like features
+     -> 10% input dropout -> dense Wd -> ReLU -> the fixed fan-in layer, one
+    fused fixedfanin_model_train_step per batch; plus the two dense kernels timed alone."""
+    import torch
+    from paper_2306_03725_b200 import synth
+    from paper_2306_03725_b200.layer import DenseConfig, DenseLayer, last_launch_count, model_train_step
+    B = shape.B
+    dn = DenseLayer(DenseConfig(d=d, m=shape.m, max_batch=B, seed=synth.PARAM_SEED + 1, dropout=dropout), device=dev)
+    xs = [torch.from_numpy(synth.feature_batch(B, d, step=s)).to(dev) for s in range(N_BATCHES)]
+    lbl = [(torch.from_numpy(p).to(dev), torch.from_numpy(i).to(dev))
+           for p, i in (synth.label_batch(B, shape.L, shape.avg_pos, step=s) for s in range(N_BATCHES))]
+    loss = torch.zeros(1, device=dev)
+    for s in range(3):
+        model_train_step(dn, eng, xs[s % N_BATCHES], s, *lbl[s % N_BATCHES], LR, loss=loss)
+    launches = last_launch_count()
+    e0.record(stream)
+    for s in range(steps):
+        model_train_step(dn, eng, xs[s % N_BATCHES], s, *lbl[s % N_BATCHES], LR, loss=loss)
+    e1.record(stream)
+    e1.synchronize()
+    ms_model = e0.elapsed_time(e1) / steps
+    h = torch.empty((B, shape.m), device=dev)
+    dh = torch.from_numpy(synth.hidden_batch(B, shape.m, step=5) * np.float32(1e-3)).to(dev)
+    res = {}
+    for name, fn in (("fwd", lambda: dn.forward(xs[0], step=1, train=True, h=h)),
+                     ("bwd", lambda: (dn.forward(xs[0], step=1, train=True, h=h), dn.backward_adam(dh, LR)))):
+        fn()
+        e0.record(stream)
+        for _ in range(20):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        res[name] = e0.elapsed_time(e1) / 20
+    res["bwd"] -= res["fwd"]
+    peak, peak_src = peaks()
+    bwd_bytes = 24 * d * shape.m + 8 * d * 32 + 8 * shape.m * 32 + 4 * B * shape.m
+    fwd_flops = 2 * B * d * shape.m
+    del dn
+    return {"workload": f"{shape.name} + dense intermediate d={d}, dropout {dropout}", "d": d, "B": B,
+            "value": B / (ms_model * 1e-3), "unit": "samples/s", "ms_per_step": ms_model,
+            "launches_per_step": launches,
+            "dense_fwd": {"ms": res["fwd"], "bound": "alu", "achieved_tflops": fwd_flops / (res["fwd"] * 1e-3) / 1e12,
+                          "peak_tflops": FP32_PEAK_TFLOPS, "frac": fwd_flops / (res["fwd"] * 1e-3) / 1e12 / FP32_PEAK_TFLOPS,
+                          "note": "dropout + fp32 FFMA2 GEMM 32 x d x m (+ ReLU, h|dh lines); peak = 148 SMs x 128 "
+                                  "FP32 lanes x 2 x 1.965 GHz"},
+            "dense_bwd_adam": {"ms": res["bwd"], "bound": "hbm", "alg_bytes": bwd_bytes,
+                               "achieved_gbs": bwd_bytes / (res["bwd"] * 1e-3) / 1e9, "peak_gbs": peak,
+                               "peak_source": peak_src, "frac": bwd_bytes / (res["bwd"] * 1e-3) / 1e9 / peak,
+                               "note": "dh transpose-in + dWd = xt^T dz fused with Adam over Wd/mWd/vWd "
+                                       "(24 B per weight)"}}
+
+
 # ----------------------------------------------------------------------------- ours
 def run_ours(a, shape, world, rank, local_rank):
     import torch
@@ -323,7 +380,7 @@ def run_ours(a, shape, world, rank, local_rank):
     ms_pred = max_over_ranks(e0.elapsed_time(e1))
 
     # ---- NEXT-3: large-batch inference and shortlist scoring, one GPU
-    big = None
+    big = model = None
     if world == 1:
         from paper_2306_03725_b200.layer import FixedFanInLayer, LayerConfig
         BI, NCAND = 1024, 100
@@ -350,6 +407,7 @@ def run_ours(a, shape, world, rank, local_rank):
                "shortlist_candidates_per_sample": NCAND, "shortlist_pairs_per_s": BI * NCAND / (res["shortlist"] * 1e-3),
                "shortlist_ms_per_batch": res["shortlist"]}
         del inf
+        model = run_model(eng, shape, dev, stream, e0, e1)
 
     if rank != 0:
         return
@@ -397,6 +455,7 @@ def run_ours(a, shape, world, rank, local_rank):
                     "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,
                     "frac": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9 / peak},
         "inference_large_batch": big,
+        "model": model if world == 1 else None,
     }
     # NEXT-4 memory report: this layer's device bytes vs the dense/COO formats of P:37-45
     Lk = shape.L * shape.k

@@ -200,6 +200,82 @@ ff_status fixedfanin_merge_topk(const float* in_scores, const int32_t* in_ids, i
                                 int32_t B, int32_t K, float* out_scores, int32_t* out_ids,
                                 ff_stream_t stream);
 
+/* ======================================================================================
+ * NEXT-2: the intermediate layer of the proposed architecture (Fig. 2,
+ * P:1013-1022): fixed features x -> input dropout -> dense W_d
+ * -> ReLU (R18) -> the fixed fan-in layer.  Readings R25-R28.
+ * Layouts: x float [B][d] (d = feature dimension: 512 Slice / 768 Cascade),
+ *          Wd float [d][m] (input-feature major), bd float [m], h and dh float [B][m].
+ * One ff_dense handle = one replica of the dense layer (it is not label-sharded: under
+ * label sharding every rank holds the same replica and feeds it the all-reduced dh).
+ * Same conventions as above: caller-owned workspace, async on `stream`, status codes.
+ * ====================================================================================== */
+typedef struct ff_dense ff_dense;
+
+typedef struct {
+    int32_t d;           /* input feature dimension, >= 1                                       */
+    int32_t m;           /* output width = the fixed fan-in layer's m, >= 1                     */
+    int32_t max_batch;   /* largest B, 1..FF_MAX_BATCH                                          */
+    int32_t reserved;    /* 0                                                                   */
+    uint64_t seed;       /* Philox key: Wd init (domain 4, R27) and dropout masks (domain 3, R25) */
+    float init_scale;    /* Wd ~ U(-a, a); 0 -> a = fp32(sqrt(6 / (d + m))) (Glorot uniform, R27) */
+    float dropout;       /* input dropout rate p in [0, 1) (0.1 Amazon-670K)         */
+    float beta1, beta2, eps;   /* Adam; 0 -> 0.9 / 0.999 / 1e-8 (R6)                            */
+    uint32_t flags;      /* FF_FLAG_STORE_GRADS: keep dWd/dbd for fixedfanin_dense_get_grads    */
+} ff_dense_config;
+
+/* Bytes of device workspace for `cfg` (host-only).  FF_ERR_CONFIG on a bad config.       */
+ff_status fixedfanin_dense_workspace_size(const ff_dense_config* cfg, size_t* bytes_host);
+
+/* Carve `workspace` (>= workspace_size bytes, 256-B aligned) and initialize on `stream`:
+ * Wd[f][c] = a * (2 * ((u >> 8) * 2^-24) - 1) in fp32, u = word c of the Philox stream
+ * (ctr = (c/4, f, 0, 4), key = seed) (R27); bd = moments = 0; t = 0.                     */
+ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, size_t bytes,
+                                  ff_stream_t stream, ff_dense** out_host);
+ff_status fixedfanin_dense_destroy(ff_dense* dense);
+
+/* Overwrite / read the state (any pointer NULL = keep / skip); both synchronize `stream`.
+ * Wd, mWd, vWd [d][m]; bd, mbd, vbd [m]; t_host = the dense layer's Adam step count.     */
+ff_status fixedfanin_dense_set_params(ff_dense* dense, const float* Wd, const float* bd,
+                                      const float* mWd, const float* vWd, const float* mbd,
+                                      const float* vbd, const int64_t* t_host, ff_stream_t stream);
+ff_status fixedfanin_dense_get_params(ff_dense* dense, float* Wd, float* bd, float* mWd,
+                                      float* vWd, float* mbd, float* vbd, int64_t* t_host,
+                                      ff_stream_t stream);
+
+/* Forward: xt = dropout(x) if train (R25: sample b, feature f is kept iff
+ * (u >> 8) * 2^-24 >= p for u = word f of the Philox stream (ctr = (f/4, b, step, 3),
+ * key = seed), kept values scaled by fp32(1/(1-p))), else xt = x;
+ * z[b][c] = bd[c] + sum_f xt[b][f] Wd[f][c] (f ascending); h = max(z, 0).  Writes h
+ * [B][m] if h != NULL and keeps xt and h for the backward.  0 <= B <= max_batch.         */
+ff_status fixedfanin_dense_forward(ff_dense* dense, const float* x, int32_t B, uint64_t step,
+                                   int32_t train, float* h, ff_stream_t stream);
+
+/* Backward + Adam of the last training forward (same B): dz = dh * [z > 0] (R26),
+ * dWd[f][c] = sum_b xt[b][f] dz[b][c], dbd[c] = sum_b dz[b][c], then t += 1 and Adam
+ * (R6, R28: the dense layer's own t) over Wd and bd.  dh float [B][m] — under
+ * label sharding, the all-reduced sum of the shards' dh.  FF_ERR_STATE without a
+ * preceding training forward.                                                            */
+ff_status fixedfanin_dense_backward_adam(ff_dense* dense, const float* dh, int32_t B, float lr,
+                                         ff_stream_t stream);
+
+/* dWd [d][m], dbd [m] of the last backward (needs FF_FLAG_STORE_GRADS, else FF_ERR_STATE). */
+ff_status fixedfanin_dense_get_grads(ff_dense* dense, float* dWd, float* dbd, ff_stream_t stream);
+
+/* One training step of the whole architecture on one GPU (unsharded `layer`, same m):
+ * dense forward with dropout (step keys the masks) -> the fixed fan-in layer's fused
+ * train_step -> dense backward + Adam.  h and dh never leave the layer's internal
+ * h|dh column lines (no [B][m] round trip).  loss as in fixedfanin_train_step.           */
+ff_status fixedfanin_model_train_step(ff_dense* dense, ff_layer* layer, const float* x, int32_t B,
+                                      uint64_t step, const int32_t* lbl_ptr,
+                                      const int32_t* lbl_ids, float grad_scale, float lr,
+                                      float* loss, ff_stream_t stream);
+
+/* Inference of the architecture: dense forward without dropout, then predict_topk.       */
+ff_status fixedfanin_model_predict_topk(ff_dense* dense, ff_layer* layer, const float* x,
+                                        int32_t B, int32_t K, float* scores, int32_t* ids,
+                                        ff_stream_t stream);
+
 /* Synchronize `stream` and report asynchronous errors raised by earlier calls
  * (FF_ERR_RANGE for bad label ids, FF_ERR_NONFINITE, FF_ERR_CUDA); clears them.       */
 ff_status fixedfanin_check(ff_layer* layer, ff_stream_t stream);

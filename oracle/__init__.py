@@ -53,6 +53,12 @@ def lib():
         L.oracle_score_shortlist.argtypes = [i64, i64, i32, i32, i32, P, P, P, P, P, P, P, P]
         L.oracle_precision_at_k.argtypes = [i32, i32, P, P, P]
         L.oracle_precision_at_k.restype = f64
+        L.oracle_dropout.argtypes = [i32, i32, f64, f64, u64, ctypes.c_uint32, P, P, P]
+        L.oracle_dense_forward.argtypes = [i32, i32, i32, P, P, P, P, P, P]
+        L.oracle_dense_backward.argtypes = [i32, i32, i32, P, P, P, P, P, P, P]
+        L.oracle_dense_init.argtypes = [i32, i32, u64, f32, P]
+        for f in ("oracle_dropout", "oracle_dense_forward", "oracle_dense_backward", "oracle_dense_init"):
+            getattr(L, f).restype = None
         for f in ("oracle_forward", "oracle_bce_grad", "oracle_sqh_grad", "oracle_weight_grad", "oracle_input_grad",
                   "oracle_adam", "oracle_philox4x32_10", "oracle_init", "oracle_redistribute", "oracle_topk",
                   "oracle_score_shortlist"):
@@ -262,3 +268,97 @@ def train_step(st: State, h, lbl_ptr, lbl_ids, grad_scale, lr, row_begin=0,
     st.W, st.mW, st.vW = adam(st.W, dW, st.mW, st.vW, st.t, lr, beta1, beta2, eps)
     st.bias, st.mb, st.vb = adam(st.bias, db, st.mb, st.vb, st.t, lr, beta1, beta2, eps)
     return StepResult(y, Ay, g, loss, dW, AdW, db, Adb, dh, Adh)
+
+
+# --------------------------------------------------------------------------- NEXT-2
+# The intermediate layer of the proposed architecture (Fig. 2)
+# and input dropout.  Readings R25-R28.
+def dropout(x, p, seed, step):
+    """Inverted input dropout (reading R25).  Returns (xt[B][d], keep uint8[B][d], s)
+    with s = fp32(1/(1-p)) the keep scale."""
+    x = _f64(x)
+    B, d = x.shape
+    s = float(np.float32(1.0) / (np.float32(1.0) - np.float32(p)))
+    xt = np.empty_like(x); keep = np.empty((B, d), dtype=np.uint8)
+    lib().oracle_dropout(B, d, float(np.float32(p)), s, seed, step & 0xFFFFFFFF, _p(x), _p(xt), _p(keep))
+    return xt, keep, s
+
+
+def dense_forward(Wd, bd, xt):
+    """z = xt Wd + bd, h = ReLU(z) (R18).  Returns (z, Az, h)."""
+    Wd, bd, xt = _f64(Wd), _f64(bd), _f64(xt)
+    d, m = Wd.shape
+    B = xt.shape[0]
+    z = np.empty((B, m)); Az = np.empty((B, m)); h = np.empty((B, m))
+    lib().oracle_dense_forward(B, d, m, _p(Wd), _p(bd), _p(xt), _p(z), _p(Az), _p(h))
+    return z, Az, h
+
+
+def dense_backward(xt, z, dh):
+    """dz = dh [z > 0]; dWd = xt^T dz; dbd = sum_b dz (R26).  Returns (dWd, AdWd, dbd, Adbd)."""
+    xt, z, dh = _f64(xt), _f64(z), _f64(dh)
+    B, d = xt.shape
+    m = z.shape[1]
+    dWd = np.empty((d, m)); AdWd = np.empty((d, m)); dbd = np.empty(m); Adbd = np.empty(m)
+    lib().oracle_dense_backward(B, d, m, _p(xt), _p(z), _p(dh), _p(dWd), _p(AdWd), _p(dbd), _p(Adbd))
+    return dWd, AdWd, dbd, Adbd
+
+
+def dense_init(d, m, seed, init_scale=0.0):
+    """Glorot-uniform Wd (reading R27) from the Philox domain-4 stream.  Returns float32 [d][m]."""
+    a = np.float32(np.sqrt(6.0 / (d + m))) if init_scale == 0 else np.float32(init_scale)
+    Wd = np.empty((d, m), dtype=np.float32)
+    lib().oracle_dense_init(d, m, seed, float(a), _p(Wd))
+    return Wd
+
+
+@dataclass
+class DenseState:
+    """fp64 state of the dense intermediate layer (Wd, bd, Adam moments, its own t)."""
+    Wd: np.ndarray
+    bd: np.ndarray
+    mWd: np.ndarray
+    vWd: np.ndarray
+    mbd: np.ndarray
+    vbd: np.ndarray
+    t: int = 0
+
+    @staticmethod
+    def create(d, m, seed, init_scale=0.0):
+        Wd = dense_init(d, m, seed, init_scale).astype(np.float64)
+        z = np.zeros((d, m)); zm = np.zeros(m)
+        return DenseState(Wd, zm.copy(), z.copy(), z.copy(), zm.copy(), zm.copy(), 0)
+
+    def copy(self):
+        return DenseState(self.Wd.copy(), self.bd.copy(), self.mWd.copy(), self.vWd.copy(), self.mbd.copy(),
+                          self.vbd.copy(), self.t)
+
+
+@dataclass
+class ModelStepResult:
+    xt: np.ndarray
+    keep: np.ndarray
+    z: np.ndarray
+    Az: np.ndarray
+    h: np.ndarray
+    sparse: StepResult
+    dWd: np.ndarray
+    AdWd: np.ndarray
+    dbd: np.ndarray
+    Adbd: np.ndarray
+
+
+def model_train_step(ds: DenseState, st: State, x, step, dropout_p, seed, lbl_ptr, lbl_ids, grad_scale, lr,
+                     beta1=0.9, beta2=0.999, eps=1e-8, loss="bce"):
+    """One step of the proposed architecture (Fig. 2): input dropout, dense
+    intermediate layer + ReLU, the sparse layer's step (train_step above; its dh
+    uses the pre-update sparse weights), then the dense layer's backward and Adam (its own
+    global t, reading R28).  Mutates ``ds`` and ``st``."""
+    xt, keep, _ = dropout(x, dropout_p, seed, step)
+    z, Az, h = dense_forward(ds.Wd, ds.bd, xt)
+    r = train_step(st, h, lbl_ptr, lbl_ids, grad_scale, lr, beta1=beta1, beta2=beta2, eps=eps, loss=loss)
+    dWd, AdWd, dbd, Adbd = dense_backward(xt, z, r.dh)
+    ds.t += 1
+    ds.Wd, ds.mWd, ds.vWd = adam(ds.Wd, dWd, ds.mWd, ds.vWd, ds.t, lr, beta1, beta2, eps)
+    ds.bd, ds.mbd, ds.vbd = adam(ds.bd, dbd, ds.mbd, ds.vbd, ds.t, lr, beta1, beta2, eps)
+    return ModelStepResult(xt, keep, z, Az, h, r, dWd, AdWd, dbd, Adbd)

@@ -399,3 +399,99 @@ double oracle_precision_at_k(int32_t B, int32_t K, const int64_t* ids,
     }
     return total / (double)B;
 }
+
+/* ========================================================================= */
+/* NEXT-2: the intermediate layer of the proposed architecture,
+ * features -> input dropout -> dense W_d -> uniform-sparse W (Fig. 2, P:1013-1022;
+ * "adding an intermediate layer between the embedding layer and the final
+ * classification layer"; "we apply dropout to the input features",
+ * P:686-689).  Layouts: x, xt [B][d] (d = feature dimension), Wd [d][m] (input
+ * feature major), bd [m], z, h, dh [B][m].  Readings R25-R28.       */
+
+/* Input dropout (inverted dropout as TF's tf.nn.dropout, reading R25):
+ *   u = word f of the stream keyed (seed) with counter (f/4, b, step, domain 3);
+ *   kept iff (u >> 8) * 2^-24 >= p;  xt[b][f] = x[b][f] * s if kept, else 0,
+ * with s = fp32(1 / (1 - p)) supplied by the caller.  keep[b][f] = 0/1.         */
+void oracle_dropout(int32_t B, int32_t d, double p, double s, uint64_t seed, uint32_t step,
+                    const double* x, double* xt, uint8_t* keep)
+{
+    for (int32_t b = 0; b < B; ++b) {
+        for (int32_t f = 0; f < d; ++f) {
+            uint32_t u = stream_word(seed, (uint32_t)b, step, 3, (uint64_t)f);
+            double unit = (double)(u >> 8) / 16777216.0;
+            int kept = unit >= p;
+            keep[(int64_t)b * d + f] = (uint8_t)kept;
+            xt[(int64_t)b * d + f] = kept ? x[(int64_t)b * d + f] * s : 0.0;
+        }
+    }
+}
+
+/* Dense intermediate layer, forward: z[b][c] = bd[c] + sum_f xt[b][f] Wd[f][c]
+ * (f ascending), h = max(z, 0) (ReLU; the activation is unnamed in the paper, reading
+ * R18).  Az = |bd[c]| + sum_f |xt[b][f] Wd[f][c]| (R19 companion).               */
+void oracle_dense_forward(int32_t B, int32_t d, int32_t m, const double* Wd, const double* bd,
+                          const double* xt, double* z, double* Az, double* h)
+{
+    for (int32_t b = 0; b < B; ++b) {
+        for (int32_t c = 0; c < m; ++c) {
+            double value = bd[c], avalue = fabs(bd[c]);
+            for (int32_t f = 0; f < d; ++f) {
+                double term = xt[(int64_t)b * d + f] * Wd[(int64_t)f * m + c];
+                value += term;
+                avalue += fabs(term);
+            }
+            z[(int64_t)b * m + c] = value;
+            Az[(int64_t)b * m + c] = avalue;
+            h[(int64_t)b * m + c] = value > 0.0 ? value : 0.0;
+        }
+    }
+}
+
+/* Dense intermediate layer, backward: dz = dh * [z > 0] (ReLU'(0) = 0, reading R26);
+ *   dWd[f][c] = sum_b xt[b][f] dz[b][c] (b ascending),  dbd[c] = sum_b dz[b][c],
+ * with the |term| companions AdWd, Adbd.  The input gradient (w.r.t. the fixed
+ * features) is not needed: the embeddings are not trained.           */
+void oracle_dense_backward(int32_t B, int32_t d, int32_t m, const double* xt, const double* z,
+                           const double* dh, double* dWd, double* AdWd, double* dbd, double* Adbd)
+{
+    for (int32_t f = 0; f < d; ++f) {
+        for (int32_t c = 0; c < m; ++c) {
+            double value = 0.0, avalue = 0.0;
+            for (int32_t b = 0; b < B; ++b) {
+                double dz = z[(int64_t)b * m + c] > 0.0 ? dh[(int64_t)b * m + c] : 0.0;
+                double term = xt[(int64_t)b * d + f] * dz;
+                value += term;
+                avalue += fabs(term);
+            }
+            dWd[(int64_t)f * m + c] = value;
+            AdWd[(int64_t)f * m + c] = avalue;
+        }
+    }
+    for (int32_t c = 0; c < m; ++c) {
+        double value = 0.0, avalue = 0.0;
+        for (int32_t b = 0; b < B; ++b) {
+            double dz = z[(int64_t)b * m + c] > 0.0 ? dh[(int64_t)b * m + c] : 0.0;
+            value += dz;
+            avalue += fabs(dz);
+        }
+        dbd[c] = value;
+        Adbd[c] = avalue;
+    }
+}
+
+/* Dense init (reading R27; TF's Dense default is Glorot-uniform): Wd[f][c] =
+ * a * (2 * ((u >> 8) * 2^-24) - 1) in fp32 with u = word c of the stream keyed (seed)
+ * with counter (c/4, f, 0, domain 4) (the R17 word map on a new domain);
+ * a = fp32(init_scale), default sqrt(6 / (d + m)); bd = 0.                       */
+void oracle_dense_init(int32_t d, int32_t m, uint64_t seed, float a, float* Wd)
+{
+    for (int32_t f = 0; f < d; ++f) {
+        for (int32_t c = 0; c < m; ++c) {
+            uint32_t u = stream_word(seed, (uint32_t)f, 0, 4, (uint64_t)c);
+            float unit = (float)(u >> 8) * (1.0f / 16777216.0f);
+            float centered = 2.0f * unit - 1.0f;
+            volatile float value = a * centered;
+            Wd[(int64_t)f * m + c] = value;
+        }
+    }
+}

@@ -1,0 +1,293 @@
+// ff_dense.cuh — sm_100a kernels of the intermediate layer of the proposed architecture
+// (SURVEY §8(f) NEXT-2): features -> input dropout -> dense W_d (P:594-603,
+// Fig. 2) -> ReLU (reading R18) -> the fixed fan-in layer.
+//
+// Layouts:
+//   Wd, mWd, vWd, dWd  f32 [d][ldw], ldw = m rounded up to 4 (16-B aligned rows; the pad
+//                      columns stay 0), input-feature major: one Wd row is contiguous in c;
+//   bd, mbd, vbd, dbd  f32 [ldw];
+//   xT  f32 [d][ldx], ldx = 32*nb: the dropped-out, scaled features, transposed so that
+//       the 32 samples of one feature are one 128-B line (broadcast operand);
+//   hd  the fixed fan-in layer's h|dh column lines [m][nb][64] (ff_kernels.cuh): the
+//       forward writes h = ReLU(z) into the h half (and zeroes the dh half), the backward
+//       reads the ReLU mask from the h half and dh from the dh half.  No tensor cores: at
+//       the paper's B = 32 the layer is a 32-row GEMM whose backward + Adam is bound by
+//       streaming Wd and its moments (24 B per weight), not by FMAs.
+#pragma once
+#include "ff_device.cuh"
+#include "ff_kernels.cuh"   // cp.async helpers
+
+namespace ff {
+
+constexpr uint32_t kDomDropout = 3;
+
+// Input dropout (reading R25): xT[f][b] = x[b][f] * scale if word f of the
+// Philox stream (ctr = (f/4, b, step, 3), key = seed) has (u >> 8) * 2^-24 >= p, else 0.
+// train = 0: xT = x (inference, no dropout).  Samples B..ldx-1 are 0.  Thread per (b, f/4).
+__global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, float p, float scale, int train,
+                            uint32_t step, uint32_t key0, uint32_t key1, float* __restrict__ xT) {
+  const int nq = (d + 3) / 4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)ldx * nq;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / nq), q = (int)(e % nq);
+    U4 v{0u, 0u, 0u, 0u};
+    if (train && b < B) v = philox((uint32_t)q, (uint32_t)b, step, kDomDropout, key0, key1);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int f = 4 * q + w;
+      if (f >= d) break;
+      float val = 0.0f;
+      if (b < B) {
+        const float xv = x[(int64_t)b * d + f];
+        if (!train) {
+          val = xv;
+        } else {
+          const float unit = __fmul_rn((float)(word_of(v, w) >> 8), 1.0f / 16777216.0f);   // exact
+          val = unit >= p ? __fmul_rn(xv, scale) : 0.0f;
+        }
+      }
+      xT[(int64_t)f * ldx + b] = val;
+    }
+  }
+}
+
+// Forward: z[b][c] = bd[c] + sum_f xT[f][b] Wd[f][c] (f ascending, fp32 FMA chain, the
+// oracle's order), h = max(z, 0).  CTA = 128 threads -> 128 columns x 32 samples (chunk
+// blockIdx.y); lane -> 4 columns, warp w -> samples 8w..8w+7 (8 x 4 accumulators).  The Wd
+// tile (64 features x 128 columns, 32 KB) and the xT tile (64 x 32) of the next feature
+// chunk are copied into a second shared-memory stage (cp.async, 16 B per thread-copy)
+// while the current chunk is computed, so the HBM latency of Wd is hidden behind the FMAs.
+constexpr int kDenseFwdThreads = 128, kDenseFch = 64;
+constexpr int kDenseFwdSmem = 2 * kDenseFch * (128 + 32) * 4;
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const float* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __restrict__ Wd,
+                                                                const float* __restrict__ bd,
+                                                                const float* __restrict__ xT, int d, int m, int ldw,
+                                                                int ldx, int B, float* __restrict__ hd, int cstride,
+                                                                int zero_dh, float* __restrict__ h_out) {
+  extern __shared__ __align__(16) float dsm[];
+  float* const wbuf = dsm;                                   // [2][64][128]
+  float* const xbuf = dsm + 2 * kDenseFch * 128;             // [2][64][32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q2 = blockIdx.y;
+  const int ct = blockIdx.x * 128, c0 = ct + 4 * lane;
+  const bool cok = c0 < ldw;
+  const int nchunk = (d + kDenseFch - 1) / kDenseFch;
+  auto issue = [&](int ch) {
+    const int f0 = ch * kDenseFch, stg = ch & 1;
+    const uint32_t wdst = (uint32_t)__cvta_generic_to_shared(wbuf + stg * kDenseFch * 128);
+    const uint32_t xdst = (uint32_t)__cvta_generic_to_shared(xbuf + stg * kDenseFch * 32);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {                          // 64 rows x 32 float4
+      const int e = u * kDenseFwdThreads + threadIdx.x, r = e >> 5, cq = (e & 31) * 4;
+      const bool ok = f0 + r < d && ct + cq < ldw;
+      cp_async16_zfill(wdst + (uint32_t)(r * 128 + cq) * 4u, ok ? Wd + (int64_t)(f0 + r) * ldw + ct + cq : Wd, ok);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {                           // 64 rows x 8 float4
+      const int e = u * kDenseFwdThreads + threadIdx.x, r = e >> 3, s4 = (e & 7) * 4;
+      const bool ok = f0 + r < d;
+      cp_async16_zfill(xdst + (uint32_t)(r * 32 + s4) * 4u, ok ? xT + (int64_t)(f0 + r) * ldx + q2 * 32 + s4 : xT, ok);
+    }
+    cp_async_commit();
+  };
+  float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (cok) bias4 = *reinterpret_cast<const float4*>(bd + c0);
+  float2 acc[8][2];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) { acc[s][0] = make_float2(bias4.x, bias4.y); acc[s][1] = make_float2(bias4.z, bias4.w); }
+  issue(0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    if (ch + 1 < nchunk) { issue(ch + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
+    __syncthreads();
+    const int nf = min(kDenseFch, d - ch * kDenseFch);
+    const float* wt = wbuf + (ch & 1) * kDenseFch * 128 + 4 * lane;
+    const float* xt = xbuf + (ch & 1) * kDenseFch * 32 + 8 * w;
+    for (int r = 0; r < nf; ++r) {
+      const float4 w4 = *reinterpret_cast<const float4*>(wt + r * 128);
+      const float4 xa = *reinterpret_cast<const float4*>(xt + r * 32);
+      const float4 xb = *reinterpret_cast<const float4*>(xt + r * 32 + 4);
+      const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        acc[s][0] = ffma2(bc2(xv[s]), make_float2(w4.x, w4.y), acc[s][0]);
+        acc[s][1] = ffma2(bc2(xv[s]), make_float2(w4.z, w4.w), acc[s][1]);
+      }
+    }
+    __syncthreads();                                         // stage ch & 1 is refilled next
+  }
+  if (!cok) return;
+  float hv[8][4];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int b = q2 * 32 + 8 * w + s;
+    const bool valid = b < B;
+    hv[s][0] = valid ? fmaxf(acc[s][0].x, 0.0f) : 0.0f;
+    hv[s][1] = valid ? fmaxf(acc[s][0].y, 0.0f) : 0.0f;
+    hv[s][2] = valid ? fmaxf(acc[s][1].x, 0.0f) : 0.0f;
+    hv[s][3] = valid ? fmaxf(acc[s][1].y, 0.0f) : 0.0f;
+    if (h_out != nullptr && valid) {
+      float* hp = h_out + (int64_t)b * m + c0;
+      if ((m & 3) == 0 && c0 + 3 < m) {                // 16-B aligned rows only
+        *reinterpret_cast<float4*>(hp) = make_float4(hv[s][0], hv[s][1], hv[s][2], hv[s][3]);
+      } else {
+        for (int u = 0; u < 4 && c0 + u < m; ++u) hp[u] = hv[s][u];
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + u;
+    if (c >= m) break;
+    float* line = hd + (int64_t)c * cstride + q2 * 64 + 8 * w;
+    *reinterpret_cast<float4*>(line) = make_float4(hv[0][u], hv[1][u], hv[2][u], hv[3][u]);
+    *reinterpret_cast<float4*>(line + 4) = make_float4(hv[4][u], hv[5][u], hv[6][u], hv[7][u]);
+    if (zero_dh) {
+      *reinterpret_cast<float4*>(line + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(line + 36) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+// Backward + Adam: dz[b][c] = dh[b][c] * [h[b][c] > 0] (ReLU'(0) = 0, R26);
+// dWd[f][c] = sum_b xT[f][b] dz[b][c] (b ascending), dbd[c] = sum_b dz[b][c]; then Adam
+// (R6) over Wd and bd with those gradients.  CTA = 128 threads -> 128 columns x
+// 64 features: lane -> 4 columns, warp w -> features f0 + 16w .. + 15 (four groups of 4
+// rows, 64 accumulators).  Per 32-sample chunk the CTA stages dz [32][128] (from the h|dh
+// lines of hd) and xT [64][32] in shared memory.  CTAs with blockIdx.y == 0 also do the
+// bias (warp 0).  Gradients are stored to dWd/dbd when those are non-null.
+constexpr int kDenseBwdThreads = 128, kDenseBwdRows = 64;
+__global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
+    float* __restrict__ Wd, float* __restrict__ mWd, float* __restrict__ vWd, float* __restrict__ bd,
+    float* __restrict__ mbd, float* __restrict__ vbd, const float* __restrict__ xT, int d, int m, int ldw, int ldx,
+    int nb, const float* __restrict__ hd, int cstride, AdamArgs adam, float* __restrict__ dWd,
+    float* __restrict__ dbd) {
+  __shared__ __align__(16) float dzs[32][128];
+  __shared__ __align__(16) float xs[kDenseBwdRows][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ct = blockIdx.x * 128, c0 = ct + 4 * lane;
+  const int fb = blockIdx.y * kDenseBwdRows, fw = fb + 16 * w;
+  const bool cok = c0 < ldw;
+  const bool do_bias = blockIdx.y == 0 && w == 0;
+  float2 acc[16][2];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
+  float db[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int q2 = 0; q2 < nb; ++q2) {
+    __syncthreads();
+    {   // dz tile: thread t <-> column ct + t (32 h + 32 dh floats of its 256-B line)
+      const int c = ct + threadIdx.x;
+      const float* line = hd + (int64_t)c * cstride + q2 * 64;
+#pragma unroll
+      for (int s4 = 0; s4 < 32; s4 += 4) {
+        float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), gv = hv;
+        if (c < m) { hv = *reinterpret_cast<const float4*>(line + s4); gv = *reinterpret_cast<const float4*>(line + 32 + s4); }
+        dzs[s4 + 0][threadIdx.x] = hv.x > 0.0f ? gv.x : 0.0f;
+        dzs[s4 + 1][threadIdx.x] = hv.y > 0.0f ? gv.y : 0.0f;
+        dzs[s4 + 2][threadIdx.x] = hv.z > 0.0f ? gv.z : 0.0f;
+        dzs[s4 + 3][threadIdx.x] = hv.w > 0.0f ? gv.w : 0.0f;
+      }
+    }
+    for (int e = threadIdx.x; e < kDenseBwdRows * 8; e += kDenseBwdThreads) {
+      const int r = e >> 3, s4 = (e & 7) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (fb + r < d) v = *reinterpret_cast<const float4*>(xT + (int64_t)(fb + r) * ldx + q2 * 32 + s4);
+      *reinterpret_cast<float4*>(&xs[r][s4]) = v;
+    }
+    __syncthreads();
+    if (!cok) continue;
+    for (int b4 = 0; b4 < 32; b4 += 4) {
+      float4 dz4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dz4[u] = *reinterpret_cast<const float4*>(&dzs[b4 + u][4 * lane]);
+      if (do_bias) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {   // b ascending
+          db[0] = __fadd_rn(db[0], dz4[u].x); db[1] = __fadd_rn(db[1], dz4[u].y);
+          db[2] = __fadd_rn(db[2], dz4[u].z); db[3] = __fadd_rn(db[3], dz4[u].w);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const float4 x4 = *reinterpret_cast<const float4*>(&xs[16 * w + r][b4]);
+        const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {   // b = b4 + u ascending
+          acc[r][0] = ffma2(bc2(xv[u]), make_float2(dz4[u].x, dz4[u].y), acc[r][0]);
+          acc[r][1] = ffma2(bc2(xv[u]), make_float2(dz4[u].z, dz4[u].w), acc[r][1]);
+        }
+      }
+    }
+  }
+  if (!cok) return;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int f = fw + r;
+    if (f >= d) continue;
+    const int64_t o = (int64_t)f * ldw + c0;
+    float4 p = *reinterpret_cast<const float4*>(Wd + o);
+    float4 mo = *reinterpret_cast<const float4*>(mWd + o);
+    float4 ve = *reinterpret_cast<const float4*>(vWd + o);
+    const float4 g = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
+    if (dWd != nullptr) *reinterpret_cast<float4*>(dWd + o) = g;
+    adam_update(p.x, mo.x, ve.x, g.x, adam);
+    adam_update(p.y, mo.y, ve.y, g.y, adam);
+    adam_update(p.z, mo.z, ve.z, g.z, adam);
+    adam_update(p.w, mo.w, ve.w, g.w, adam);
+    *reinterpret_cast<float4*>(Wd + o) = p;
+    *reinterpret_cast<float4*>(mWd + o) = mo;
+    *reinterpret_cast<float4*>(vWd + o) = ve;
+  }
+  if (do_bias) {
+    float4 p = *reinterpret_cast<const float4*>(bd + c0);
+    float4 mo = *reinterpret_cast<const float4*>(mbd + c0);
+    float4 ve = *reinterpret_cast<const float4*>(vbd + c0);
+    if (dbd != nullptr) *reinterpret_cast<float4*>(dbd + c0) = make_float4(db[0], db[1], db[2], db[3]);
+    adam_update(p.x, mo.x, ve.x, db[0], adam);
+    adam_update(p.y, mo.y, ve.y, db[1], adam);
+    adam_update(p.z, mo.z, ve.z, db[2], adam);
+    adam_update(p.w, mo.w, ve.w, db[3], adam);
+    *reinterpret_cast<float4*>(bd + c0) = p;
+    *reinterpret_cast<float4*>(mbd + c0) = mo;
+    *reinterpret_cast<float4*>(vbd + c0) = ve;
+  }
+}
+
+// dh [B][m] (user layout) -> the dh half of hd (standalone dense backward).  Grid
+// ceil(m/32) x nb, 32x8 threads; samples >= B get 0.
+__global__ void k_dh_in(const float* __restrict__ dh, int B, int m, int nb, float* __restrict__ hd) {
+  __shared__ float t[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int c0 = blockIdx.x * 32, q2 = blockIdx.y;
+  for (int r = ty; r < 32; r += 8) {
+    const int b = q2 * 32 + r, c = c0 + tx;
+    t[r][tx] = (b < B && c < m) ? dh[(int64_t)b * m + c] : 0.0f;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int c = c0 + r;
+    if (c < m) hd[(int64_t)c * 64 * nb + q2 * 64 + 32 + tx] = t[tx][r];
+  }
+}
+
+// Dense init (reading R27): Wd[f][c] = a * (2 * ((u >> 8) * 2^-24) - 1) in fp32, u = word c
+// of the stream (ctr = (c/4, f, 0, 4), key = seed); pad columns and bd, moments = 0.
+__global__ void k_dense_init(float* __restrict__ Wd, int d, int m, int ldw, uint32_t key0, uint32_t key1, float a) {
+  const int nq = ldw / 4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)d * nq;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)(e / nq), q = (int)(e % nq);
+    const U4 v = philox((uint32_t)q, (uint32_t)f, 0u, 4u, key0, key1);
+    float out[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float unit = __fmul_rn((float)(word_of(v, u) >> 8), 1.0f / 16777216.0f);
+      const float centered = __fsub_rn(__fmul_rn(2.0f, unit), 1.0f);
+      out[u] = 4 * q + u < m ? __fmul_rn(a, centered) : 0.0f;
+    }
+    *reinterpret_cast<float4*>(Wd + (int64_t)f * ldw + 4 * q) = make_float4(out[0], out[1], out[2], out[3]);
+  }
+}
+
+}  // namespace ff

@@ -929,6 +929,12 @@ __device__ __forceinline__ void topk_insert(float (&ts)[kTopkMax], int (&ti)[kTo
   }
 }
 
+// Insert only when the candidate beats the current K-th entry: after the first rows almost
+// every row is rejected by this one comparison (the insertion network is ~70 instructions).
+__device__ __forceinline__ void topk_consider(float (&ts)[kTopkMax], int (&ti)[kTopkMax], float s, int i) {
+  if (better(s, i, ts[kTopkMax - 1], ti[kTopkMax - 1])) topk_insert(ts, ti, s, i);
+}
+
 // Fused forward + per-lane running top-K (y is never written).  For each 32-sample chunk
 // q2 every lane owns sample q2*32 + 4*bq + gq; a block merges its warps' lists and writes
 // candidates cand[blk][ldh][kTopkMax].
@@ -976,7 +982,7 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
       row_spread_k<NG, KPL>(w, c, gq, ws, cs);
       row_gather<NG, FULL>(hb, cs, cfl, k, gq, pol_l, hv);
       const float y = row_score_own<NG>(ws, hv, gq, bj);
-      if (b < B) topk_insert(ts, ti, y, (int)(row_begin + j));
+      if (b < B) topk_consider(ts, ti, y, (int)(row_begin + j));
     }
 #pragma unroll
     for (int q = 0; q < kTopkMax; ++q) { ss[wid][lane][q] = ts[q]; si[wid][lane][q] = ti[q]; }
@@ -990,6 +996,147 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
       for (int q = 0; q < kTopkMax; ++q) { cand_s[base + q] = ts[q]; cand_i[base + q] = ti[q]; }
     }
     __syncthreads();
+  }
+}
+
+// Fused forward + running top-K for the hot configuration (k = 32, B <= 32), pipelined like
+// k_train_ring: the h-line gathers of the next D - 1 rows are in flight (cp.async into a
+// per-warp shared-memory ring) and the state (W, idx, bias) of row X + D is being loaded
+// while row X is scored.  Same score arithmetic as k_predict / k_rows (row_score_own on the
+// same operands): bit-identical y.  Warp w scores rows w, w + nwarp, ...; the block merges
+// its warps' lists into cand[blk][32][kTopkMax] like k_predict.
+constexpr int kPredRingD = 3;
+constexpr int kPredRingThreads = 128;
+constexpr int kPredRingSmem = (kPredRingThreads / 32) * kPredRingD * 8 * 32 * 16;
+__global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* __restrict__ W,
+                                                                   const int* __restrict__ idx,
+                                                                   const float* __restrict__ bias,
+                                                                   const float* __restrict__ hd, int64_t L, int B,
+                                                                   int64_t row_begin, float* __restrict__ cand_s,
+                                                                   int* __restrict__ cand_i) {
+  constexpr int NG = 8, D = kPredRingD;
+  constexpr uint32_t kColFloats = 64, kStage = 8 * 32 * 16;
+  extern __shared__ __align__(16) unsigned char ring_smem[];
+  __shared__ float ss[kPredRingThreads / 32][32][kTopkMax];
+  __shared__ int si[kPredRingThreads / 32][32][kTopkMax];
+  const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7, wid = threadIdx.x >> 5;
+  const uint32_t nwarp = (uint32_t)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring_smem) + (uint32_t)wid * D * kStage + (uint32_t)lane * 16u;
+  const float* const hb = hd + 4 * bq;
+  const int b = 4 * bq + gq;
+  const uint32_t nrows = (uint32_t)L;
+  float ts[kTopkMax]; int ti[kTopkMax];
+#pragma unroll
+  for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
+
+  struct St { float w, bj; int c; };
+  auto load_st = [&](uint32_t j, St& st) {
+    if (j < nrows) {
+      st.w = ld_na(W + j * 32u + lane);
+      st.c = ld_na_ro(idx + j * 32u + lane);
+      st.bj = ld_na(bias + j);
+    }
+  };
+  auto issue = [&](uint32_t j, const St& st, uint32_t stg) {
+    if (j < nrows) {
+      const uint32_t dst = ring0 + stg * kStage;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        const uint32_t c = (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq);
+        cp_async16(dst + (uint32_t)q * 512u, col_line(hb, c, kColFloats));
+      }
+    }
+    cp_async_commit();
+  };
+  const uint32_t j0 = (uint32_t)global_warp();
+  uint32_t qj[D];
+  St qs[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) { qj[d] = j0 + (uint32_t)d * nwarp; qs[d] = St{0.f, 0.f, 0}; load_st(qj[d], qs[d]); }
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) issue(qj[d], qs[d], (uint32_t)d);
+  uint32_t stg = 0;
+  while (qj[0] < nrows) {
+    issue(qj[D - 1], qs[D - 1], stg == 0 ? (uint32_t)(D - 1) : stg - 1);
+    const uint32_t j = qj[0];
+    const St st = qs[0];
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) { qj[d] = qj[d + 1]; qs[d] = qs[d + 1]; }
+    qj[D - 1] = qj[D - 2] + nwarp;
+    load_st(qj[D - 1], qs[D - 1]);
+    cp_async_wait<D - 1>();
+    float4 hv[NG];
+    const uint32_t src = ring0 + stg * kStage;
+#pragma unroll
+    for (int q = 0; q < NG; ++q) hv[q] = lds4(src + (uint32_t)q * 512u);
+    float ws[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) ws[q] = __shfl_sync(kFull, st.w, 4 * q + gq);
+    const float y = row_score_own<NG>(ws, hv, gq, st.bj);
+    if (b < B) topk_consider(ts, ti, y, (int)(row_begin + j));
+    stg = stg + 1 == (uint32_t)D ? 0u : stg + 1;
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int q = 0; q < kTopkMax; ++q) { ss[wid][lane][q] = ts[q]; si[wid][lane][q] = ti[q]; }
+  __syncthreads();
+  if (wid == 0) {
+    for (int w2 = 1; w2 < kPredRingThreads / 32; ++w2)
+#pragma unroll
+      for (int q = 0; q < kTopkMax; ++q) topk_insert(ts, ti, ss[w2][lane][q], si[w2][lane][q]);
+    const int64_t base = ((int64_t)blockIdx.x * 32 + b) * kTopkMax;
+#pragma unroll
+    for (int q = 0; q < kTopkMax; ++q) { cand_s[base + q] = ts[q]; cand_i[base + q] = ti[q]; }
+  }
+}
+
+// Block per sample: merge `nlist` sorted candidate lists (first Kin entries used) into the
+// top K.  Each thread keeps a running top-kTopkMax over lists tid, tid + blockDim, ...; each
+// warp reduces its lanes by K rounds of arg-best + pop; warp 0 merges the warps' lists the
+// same way.  Exact under the total order (score desc, id asc).
+__device__ __forceinline__ void warp_topk_pop(float (&ts)[kTopkMax], int (&ti)[kTopkMax], int K, float* os, int* oi) {
+  const int lane = threadIdx.x & 31;
+  for (int r = 0; r < K; ++r) {
+    float bs = ts[0]; int bi = ti[0];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const float s2 = __shfl_xor_sync(kFull, bs, o); const int i2 = __shfl_xor_sync(kFull, bi, o);
+      if (better(s2, i2, bs, bi)) { bs = s2; bi = i2; }
+    }
+    if (lane == 0) { os[r] = bs; oi[r] = bi; }
+    if (ti[0] == bi && ts[0] == bs && bi != INT_MAX) {
+#pragma unroll
+      for (int q = 0; q < kTopkMax - 1; ++q) { ts[q] = ts[q + 1]; ti[q] = ti[q + 1]; }
+      ts[kTopkMax - 1] = -INFINITY; ti[kTopkMax - 1] = INT_MAX;
+    }
+  }
+}
+__global__ void __launch_bounds__(256) k_merge_topk_block(const float* __restrict__ in_s, const int* __restrict__ in_i,
+                                                          int nlist, int64_t list_stride, int64_t sample_stride,
+                                                          int Kin, int K, float* __restrict__ out_s,
+                                                          int* __restrict__ out_i) {
+  __shared__ float ws_s[8][kTopkMax];
+  __shared__ int ws_i[8][kTopkMax];
+  const int b = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  float ts[kTopkMax]; int ti[kTopkMax];
+#pragma unroll
+  for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
+  for (int l = threadIdx.x; l < nlist; l += blockDim.x) {
+    const int64_t base = (int64_t)l * list_stride + (int64_t)b * sample_stride;
+    for (int q = 0; q < Kin; ++q) {
+      const float s = in_s[base + q]; const int i = in_i[base + q];
+      if (!better(s, i, ts[kTopkMax - 1], ti[kTopkMax - 1])) break;   // lists are sorted
+      topk_insert(ts, ti, s, i);
+    }
+  }
+  warp_topk_pop(ts, ti, K, ws_s[wid], ws_i[wid]);
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
+    if (lane < nwp)
+      for (int q = 0; q < K; ++q) topk_insert(ts, ti, ws_s[lane][q], ws_i[lane][q]);
+    warp_topk_pop(ts, ti, K, out_s + (int64_t)b * K, out_i + (int64_t)b * K);
   }
 }
 

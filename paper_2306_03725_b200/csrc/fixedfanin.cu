@@ -3,6 +3,7 @@
 // (the caller owns the workspace) and no call synchronizes except set/get_params/check.
 #include "fixedfanin.h"
 #include "ff_kernels.cuh"
+#include "ff_dense.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -156,7 +157,7 @@ struct ff_layer {
   uint32_t* posmask;
   int64_t t;
   bool grads_valid;
-  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring;
+  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring, grid_pred_ring;
   int nsm;
   std::vector<cudaEvent_t> prof_ev;   // pairs (before, after) of the fused row kernel
   int prof_used = 0;
@@ -343,11 +344,14 @@ ff_status csc_rebuild(ff_layer* l, cudaStream_t st) {
   return FF_OK;
 }
 
+// hd_ready: h is already in the h half of hd and (atomic mode) the dh half is zero (the
+// model step's dense forward wrote them); dh then stays in hd (dh may be NULL).
 ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t* lbl_ptr, const int32_t* lbl_ids,
-                          float grad_scale, float lr, float* dh, float* loss, cudaStream_t st) {
+                          float grad_scale, float lr, float* dh, float* loss, cudaStream_t st, bool hd_ready = false) {
   if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
-  if (!ptr_ok(h, B) || !ptr_ok(dh, B) || lbl_ptr == nullptr) return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
-  ff_status s = launch_prep(l, h, B, !l->csc, lbl_ptr, lbl_ids, loss, st);
+  if ((!hd_ready && (!ptr_ok(h, B) || !ptr_ok(dh, B))) || lbl_ptr == nullptr)
+    return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
+  ff_status s = launch_prep(l, hd_ready ? nullptr : h, B, !l->csc && !hd_ready, lbl_ptr, lbl_ids, loss, st);
   if (s != FF_OK) return s;
   l->t += 1;
   RowArgs a = row_args(l, B);
@@ -364,8 +368,143 @@ ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t*
   }
   if (s != FF_OK) return s;
   l->grads_valid = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
-  if (B == 0) return FF_OK;
+  if (B == 0 || dh == nullptr) return FF_OK;
   return launch_dh_out(l, B, dh, st);
+}
+
+// Top-K of the scores of h; hd_ready: h is already in the h half of hd (model predict).
+ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float* scores, int32_t* ids,
+                       cudaStream_t st, bool hd_ready) {
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
+  if (K < 1 || K > l->cfg.max_topk || K > l->cfg.L_local)
+    return fail(FF_ERR_ARG, "K=%d outside [1, min(max_topk=%d, L_local=%lld)]", K, l->cfg.max_topk,
+                (long long)l->cfg.L_local);
+  if (B == 0) return FF_OK;
+  if ((!h && !hd_ready) || !scores || !ids) return fail(FF_ERR_ARG, "null h/scores/ids");
+  if (!hd_ready) {
+    ff_status s = launch_prep(l, h, B, false, nullptr, nullptr, nullptr, st);
+    if (s != FF_OK) return s;
+  }
+  const int nb = nb_of(B), ldh = 32 * nb;
+  const float* W = l->W; const int* idx = l->idx; const float* bias = l->bias; const float* hd = l->hd;
+  int64_t L = l->cfg.L_local, rb = l->cfg.row_begin; int k = l->cfg.k, BB = B, nbb = nb;
+  float* cs = l->cand_s; int* ci = l->cand_i;
+  int nlist = l->grid_pred;
+  if (k == 32 && nb == 1) {            // hot configuration: pipelined kernel (bit-identical scores)
+    nlist = l->grid_pred_ring;
+    void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &rb, &cs, &ci};
+    FF_CUDA(cudaLaunchKernel((const void*)k_predict_ring, dim3(nlist), dim3(kPredRingThreads), args, kPredRingSmem, st));
+  } else {
+    void* args[] = {&W, &idx, &bias, &hd, &L, &k, &BB, &nbb, &rb, &cs, &ci};
+    FF_CUDA(cudaLaunchKernel(predict_kernel(l->cfg.k), dim3(l->grid_pred), dim3(kRowThreads), args, 0, st));
+  }
+  ++g_launches;
+  k_merge_topk_block<<<B, 256, 0, st>>>(l->cand_s, l->cand_i, nlist, (int64_t)ldh * kTopkMax, kTopkMax, kTopkMax, K,
+                                        scores, ids);
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
+
+// ============================================================ NEXT-2: the intermediate layer
+struct DenseLayout {
+  size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, hd, x_stage, total;
+};
+int ldw_of(int m) { return (m + 3) / 4 * 4; }
+DenseLayout dense_layout_of(const ff_dense_config& c) {
+  DenseLayout o{};
+  const size_t dw = (size_t)c.d * (size_t)ldw_of(c.m), w = (size_t)ldw_of(c.m);
+  const size_t nbm = (size_t)nb_of(c.max_batch), ldx = 32 * nbm;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t r = off; off += up(bytes); return r; };
+  o.Wd = take(4 * dw); o.mWd = take(4 * dw); o.vWd = take(4 * dw);
+  o.dWd = (c.flags & FF_FLAG_STORE_GRADS) ? take(4 * dw) : 0;
+  o.bd = take(4 * w); o.mbd = take(4 * w); o.vbd = take(4 * w); o.dbd = take(4 * w);
+  o.xT = take(4 * (size_t)c.d * ldx);
+  o.hd = take(8 * (size_t)c.m * ldx);     // own h|dh lines for the standalone forward/backward
+  o.x_stage = take(4 * (size_t)c.max_batch * (size_t)c.d);
+  o.total = off;
+  return o;
+}
+ff_status dense_validate(const ff_dense_config* c) {
+  if (!c) return fail(FF_ERR_ARG, "cfg is NULL");
+  if (c->d < 1 || c->m < 1) return fail(FF_ERR_CONFIG, "d=%d, m=%d must be >= 1", c->d, c->m);
+  if ((int64_t)c->d * ldw_of(c->m) >= (int64_t(1) << 40)) return fail(FF_ERR_CONFIG, "d*m too large");
+  if (c->max_batch < 1 || c->max_batch > FF_MAX_BATCH)
+    return fail(FF_ERR_CONFIG, "max_batch=%d outside [1, %d]", c->max_batch, FF_MAX_BATCH);
+  if (!(c->dropout >= 0.0f && c->dropout < 1.0f)) return fail(FF_ERR_CONFIG, "dropout outside [0, 1)");
+  if (c->beta1 < 0.0f || c->beta1 >= 1.0f || c->beta2 < 0.0f || c->beta2 >= 1.0f || c->eps < 0.0f)
+    return fail(FF_ERR_CONFIG, "Adam hyper-parameters out of range");
+  return FF_OK;
+}
+ff_dense_config dense_defaults(const ff_dense_config& in) {
+  ff_dense_config c = in;
+  if (c.beta1 == 0.0f) c.beta1 = 0.9f;
+  if (c.beta2 == 0.0f) c.beta2 = 0.999f;
+  if (c.eps == 0.0f) c.eps = 1e-8f;
+  if (c.init_scale == 0.0f) c.init_scale = (float)std::sqrt(6.0 / ((double)c.d + (double)c.m));
+  return c;
+}
+AdamArgs adam_args_of(float beta1, float beta2, float eps, float lr, int64_t t) {
+  AdamArgs a;
+  a.lr = lr; a.beta1 = beta1; a.beta2 = beta2; a.one_minus_b1 = 1.0f - beta1; a.one_minus_b2 = 1.0f - beta2;
+  a.rbc1 = (float)(1.0 / (1.0 - std::pow((double)beta1, (double)t)));
+  a.rbc2 = (float)(1.0 / (1.0 - std::pow((double)beta2, (double)t)));
+  a.eps = eps;
+  return a;
+}
+
+}  // namespace
+
+struct ff_dense {
+  ff_dense_config cfg;
+  DenseLayout lay;
+  char* ws;
+  float *Wd, *mWd, *vWd, *dWd, *bd, *mbd, *vbd, *dbd, *xT, *hd, *x_stage;
+  int ldw;
+  int64_t t;
+  int fwd_B;            // batch of the last training forward (-1: none since the last backward)
+  bool grads_valid;
+};
+
+namespace {
+
+// dropout + forward into `hd` (the dense layer's own lines or a fixed fan-in layer's)
+ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, bool train, float* hd,
+                             float* h_out, cudaStream_t st) {
+  const int nb = nb_of(B), ldx = 32 * nb;
+  const float p = n->cfg.dropout;
+  const float scale = (float)(1.0f / (1.0f - p));
+  {
+    const int64_t work = (int64_t)ldx * ((n->cfg.d + 3) / 4);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 4096));
+    k_dropout_T<<<grid, 256, 0, st>>>(x, B, n->cfg.d, ldx, p, scale, (train && p > 0.0f) ? 1 : 0, (uint32_t)step,
+                                      (uint32_t)n->cfg.seed, (uint32_t)(n->cfg.seed >> 32), n->xT);
+    FF_LAUNCHED();
+  }
+  dim3 grid((n->ldw + 127) / 128, nb);
+  k_dense_fwd<<<grid, kDenseFwdThreads, kDenseFwdSmem, st>>>(n->Wd, n->bd, n->xT, n->cfg.d, n->cfg.m, n->ldw, ldx, B, hd,
+                                                64 * nb, 1, h_out);
+  FF_LAUNCHED();
+  if (train) n->fwd_B = B;
+  return FF_OK;
+}
+
+// backward + Adam from the h|dh lines of `hd` (t += 1)
+ff_status dense_backward_impl(ff_dense* n, int B, float lr, const float* hd, cudaStream_t st) {
+  const int nb = nb_of(B), ldx = 32 * nb;
+  n->t += 1;
+  const AdamArgs a = adam_args_of(n->cfg.beta1, n->cfg.beta2, n->cfg.eps, lr, n->t);
+  const bool sg = (n->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
+  dim3 grid((n->ldw + 127) / 128, (n->cfg.d + kDenseBwdRows - 1) / kDenseBwdRows);
+  k_dense_bwd_adam<<<grid, kDenseBwdThreads, 0, st>>>(n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d,
+                                                      n->cfg.m, n->ldw, ldx, nb, hd, 64 * nb, a,
+                                                      sg ? n->dWd : nullptr, sg ? n->dbd : nullptr);
+  FF_LAUNCHED();
+  n->grads_valid = sg;
+  n->fwd_B = -1;
+  return FF_OK;
 }
 
 }  // namespace
@@ -439,6 +578,13 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
     l->ntiles = (int)std::max<int64_t>(1, (c.L_local + l->tile_rows - 1) / l->tile_rows);
   }
   l->grid_pred = std::min(kMaxCandBlocks, occupancy_grid(predict_kernel(c.k), l->nsm, kRowThreads));
+  if (cudaFuncSetAttribute((const void*)k_predict_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, kPredRingSmem) !=
+      cudaSuccess) {
+    delete l;
+    return fail(FF_ERR_CUDA, "pipelined predict smem attribute");
+  }
+  l->grid_pred_ring =
+      std::min(kMaxCandBlocks, occupancy_grid((const void*)k_predict_ring, l->nsm, kPredRingThreads, kPredRingSmem));
   l->grid_rows = l->nsm * 8;
   // zero everything that must start at zero (moments, masks, dW/db, dhT, scalars)
   e = cudaMemsetAsync(ws, 0, lay.total, st);
@@ -626,29 +772,7 @@ ff_status fixedfanin_redistribute(ff_layer* l, uint64_t step, ff_stream_t stream
 ff_status fixedfanin_predict_topk(ff_layer* l, const float* h, int32_t B, int32_t K, float* scores, int32_t* ids,
                                   ff_stream_t stream) {
   g_launches = 0;
-  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
-  if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
-  if (K < 1 || K > l->cfg.max_topk || K > l->cfg.L_local)
-    return fail(FF_ERR_ARG, "K=%d outside [1, min(max_topk=%d, L_local=%lld)]", K, l->cfg.max_topk,
-                (long long)l->cfg.L_local);
-  if (B == 0) return FF_OK;
-  if (!h || !scores || !ids) return fail(FF_ERR_ARG, "null h/scores/ids");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  ff_status s = launch_prep(l, h, B, false, nullptr, nullptr, nullptr, st);
-  if (s != FF_OK) return s;
-  const int nb = nb_of(B), ldh = 32 * nb;
-  {
-    const float* W = l->W; const int* idx = l->idx; const float* bias = l->bias; const float* hd = l->hd;
-    int64_t L = l->cfg.L_local, rb = l->cfg.row_begin; int k = l->cfg.k, BB = B, nbb = nb;
-    float* cs = l->cand_s; int* ci = l->cand_i;
-    void* args[] = {&W, &idx, &bias, &hd, &L, &k, &BB, &nbb, &rb, &cs, &ci};
-    FF_CUDA(cudaLaunchKernel(predict_kernel(l->cfg.k), dim3(l->grid_pred), dim3(kRowThreads), args, 0, st));
-    ++g_launches;
-  }
-  k_merge_topk<<<(B + 7) / 8, 256, 0, st>>>(l->cand_s, l->cand_i, l->grid_pred, (int64_t)ldh * kTopkMax, kTopkMax, K,
-                                           B, K, scores, ids);
-  FF_LAUNCHED();
-  return FF_OK;
+  return predict_impl(l, h, B, K, scores, ids, reinterpret_cast<cudaStream_t>(stream), false);
 }
 
 ff_status fixedfanin_score_shortlist(ff_layer* l, const float* h, int32_t B, const int32_t* cand_ptr,
@@ -730,6 +854,184 @@ ff_status fixedfanin_check(ff_layer* l, ff_stream_t stream) {
   if (herr & kErrLabelRange) return fail(FF_ERR_RANGE, "a label id was outside [0, L_global=%lld)", (long long)l->cfg.L_global);
   if (herr & kErrNonFinite) return fail(FF_ERR_NONFINITE, "non-finite score seen (FF_FLAG_CHECK_FINITE)");
   return FF_OK;
+}
+
+
+// ============================================================ NEXT-2: the intermediate layer
+ff_status fixedfanin_dense_workspace_size(const ff_dense_config* cfg, size_t* bytes) {
+  g_launches = 0;
+  ff_status s = dense_validate(cfg);
+  if (s != FF_OK) return s;
+  if (!bytes) return fail(FF_ERR_ARG, "bytes is NULL");
+  *bytes = dense_layout_of(dense_defaults(*cfg)).total;
+  return FF_OK;
+}
+
+ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, size_t bytes, ff_stream_t stream,
+                                  ff_dense** out) {
+  g_launches = 0;
+  ff_status s = dense_validate(cfg);
+  if (s != FF_OK) return s;
+  if (!out || !workspace) return fail(FF_ERR_ARG, "out/workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(FF_ERR_ARG, "workspace not 256-B aligned");
+  const ff_dense_config c = dense_defaults(*cfg);
+  const DenseLayout lay = dense_layout_of(c);
+  if (bytes < lay.total) return fail(FF_ERR_ARG, "workspace %zu B < required %zu B", bytes, lay.total);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  FF_CUDA(cudaGetLastError());
+  ff_dense* n = new (std::nothrow) ff_dense();
+  if (!n) return fail(FF_ERR_ARG, "host allocation failed");
+  n->cfg = c; n->lay = lay;
+  char* ws = static_cast<char*>(workspace);
+  n->ws = ws;
+  n->Wd = at<float>(ws, lay.Wd); n->mWd = at<float>(ws, lay.mWd); n->vWd = at<float>(ws, lay.vWd);
+  n->dWd = (c.flags & FF_FLAG_STORE_GRADS) ? at<float>(ws, lay.dWd) : nullptr;
+  n->bd = at<float>(ws, lay.bd); n->mbd = at<float>(ws, lay.mbd); n->vbd = at<float>(ws, lay.vbd);
+  n->dbd = at<float>(ws, lay.dbd);
+  n->xT = at<float>(ws, lay.xT); n->hd = at<float>(ws, lay.hd); n->x_stage = at<float>(ws, lay.x_stage);
+  n->ldw = ldw_of(c.m);
+  n->t = 0; n->fwd_B = -1; n->grads_valid = false;
+  if (cudaFuncSetAttribute((const void*)k_dense_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseFwdSmem) !=
+      cudaSuccess) {
+    delete n;
+    return fail(FF_ERR_CUDA, "dense forward smem attribute");
+  }
+  cudaError_t e = cudaMemsetAsync(ws, 0, lay.total, st);
+  if (e != cudaSuccess) { delete n; return fail(FF_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); }
+  const int64_t work = (int64_t)c.d * (n->ldw / 4);
+  k_dense_init<<<(int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8192)), 256, 0, st>>>(
+      n->Wd, c.d, c.m, n->ldw, (uint32_t)c.seed, (uint32_t)(c.seed >> 32), c.init_scale);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { delete n; return fail(FF_ERR_CUDA, "init launch: %s", cudaGetErrorString(e)); }
+  ++g_launches;
+  *out = n;
+  return FF_OK;
+}
+
+ff_status fixedfanin_dense_destroy(ff_dense* n) {
+  delete n;
+  return FF_OK;
+}
+
+ff_status fixedfanin_dense_set_params(ff_dense* n, const float* Wd, const float* bd, const float* mWd,
+                                      const float* vWd, const float* mbd, const float* vbd, const int64_t* t,
+                                      ff_stream_t stream) {
+  g_launches = 0;
+  if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t m4 = 4 * (size_t)n->cfg.m, lw4 = 4 * (size_t)n->ldw;
+  auto cp2 = [&](float* dst, const float* src) -> cudaError_t {   // [d][m] -> [d][ldw]
+    return src ? cudaMemcpy2DAsync(dst, lw4, src, m4, m4, n->cfg.d, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  };
+  auto cp1 = [&](float* dst, const float* src) -> cudaError_t {
+    return src ? cudaMemcpyAsync(dst, src, m4, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  };
+  FF_CUDA(cp2(n->Wd, Wd)); FF_CUDA(cp2(n->mWd, mWd)); FF_CUDA(cp2(n->vWd, vWd));
+  FF_CUDA(cp1(n->bd, bd)); FF_CUDA(cp1(n->mbd, mbd)); FF_CUDA(cp1(n->vbd, vbd));
+  if (t) n->t = *t;
+  n->grads_valid = false;
+  FF_CUDA(cudaStreamSynchronize(st));
+  return FF_OK;
+}
+
+ff_status fixedfanin_dense_get_params(ff_dense* n, float* Wd, float* bd, float* mWd, float* vWd, float* mbd,
+                                      float* vbd, int64_t* t, ff_stream_t stream) {
+  g_launches = 0;
+  if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t m4 = 4 * (size_t)n->cfg.m, lw4 = 4 * (size_t)n->ldw;
+  auto cp2 = [&](float* dst, const float* src) -> cudaError_t {
+    return dst ? cudaMemcpy2DAsync(dst, m4, src, lw4, m4, n->cfg.d, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  };
+  auto cp1 = [&](float* dst, const float* src) -> cudaError_t {
+    return dst ? cudaMemcpyAsync(dst, src, m4, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  };
+  FF_CUDA(cp2(Wd, n->Wd)); FF_CUDA(cp2(mWd, n->mWd)); FF_CUDA(cp2(vWd, n->vWd));
+  FF_CUDA(cp1(bd, n->bd)); FF_CUDA(cp1(mbd, n->mbd)); FF_CUDA(cp1(vbd, n->vbd));
+  if (t) *t = n->t;
+  FF_CUDA(cudaStreamSynchronize(st));
+  return FF_OK;
+}
+
+ff_status fixedfanin_dense_forward(ff_dense* n, const float* x, int32_t B, uint64_t step, int32_t train, float* h,
+                                   ff_stream_t stream) {
+  g_launches = 0;
+  if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
+  if (B < 0 || B > n->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, n->cfg.max_batch);
+  if (B == 0) return FF_OK;
+  if (!x) return fail(FF_ERR_ARG, "null x");
+  return dense_forward_impl(n, x, B, step, train != 0, n->hd, h, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ff_status fixedfanin_dense_backward_adam(ff_dense* n, const float* dh, int32_t B, float lr, ff_stream_t stream) {
+  g_launches = 0;
+  if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
+  if (n->fwd_B < 0) return fail(FF_ERR_STATE, "dense backward without a preceding training forward");
+  if (B != n->fwd_B) return fail(FF_ERR_ARG, "B=%d differs from the forward's B=%d", B, n->fwd_B);
+  if (B > 0 && !dh) return fail(FF_ERR_ARG, "null dh");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = nb_of(B);
+  if (B > 0) {
+    dim3 grid((n->cfg.m + 31) / 32, nb), block(32, 8);
+    k_dh_in<<<grid, block, 0, st>>>(dh, B, n->cfg.m, nb, n->hd);
+    FF_LAUNCHED();
+  }
+  const int32_t pre = g_launches;
+  ff_status s = dense_backward_impl(n, std::max(B, 1), lr, n->hd, st);
+  g_launches += pre;
+  return s;
+}
+
+ff_status fixedfanin_dense_get_grads(ff_dense* n, float* dWd, float* dbd, ff_stream_t stream) {
+  g_launches = 0;
+  if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
+  if (!n->grads_valid) return fail(FF_ERR_STATE, "no gradients: create with FF_FLAG_STORE_GRADS and run a backward");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t m4 = 4 * (size_t)n->cfg.m, lw4 = 4 * (size_t)n->ldw;
+  if (dWd) FF_CUDA(cudaMemcpy2DAsync(dWd, m4, n->dWd, lw4, m4, n->cfg.d, cudaMemcpyDeviceToDevice, st));
+  if (dbd) FF_CUDA(cudaMemcpyAsync(dbd, n->dbd, m4, cudaMemcpyDeviceToDevice, st));
+  return FF_OK;
+}
+
+ff_status fixedfanin_model_train_step(ff_dense* n, ff_layer* l, const float* x, int32_t B, uint64_t step,
+                                      const int32_t* lbl_ptr, const int32_t* lbl_ids, float grad_scale, float lr,
+                                      float* loss, ff_stream_t stream) {
+  g_launches = 0;
+  if (!n || !l) return fail(FF_ERR_ARG, "dense layer / layer is NULL");
+  if (n->cfg.m != l->cfg.m) return fail(FF_ERR_CONFIG, "dense m=%d != layer m=%d", n->cfg.m, l->cfg.m);
+  if (l->cfg.L_local != l->cfg.L_global)
+    return fail(FF_ERR_CONFIG, "model step needs an unsharded layer (sharded: dense_forward, train_step, "
+                               "all-reduce dh, dense_backward_adam)");
+  if (B < 0 || B > n->cfg.max_batch || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside max_batch", B);
+  if (B == 0) return FF_OK;
+  if (!x || !lbl_ptr) return fail(FF_ERR_ARG, "null x/lbl_ptr");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ff_status s = dense_forward_impl(n, x, B, step, true, l->hd, nullptr, st);
+  if (s != FF_OK) return s;
+  int32_t nl = g_launches;
+  s = train_step_impl(l, nullptr, B, lbl_ptr, lbl_ids, grad_scale, lr, nullptr, loss, st, true);
+  if (s != FF_OK) return s;
+  nl += g_launches;
+  s = dense_backward_impl(n, B, lr, l->hd, st);
+  g_launches += nl;
+  return s;
+}
+
+ff_status fixedfanin_model_predict_topk(ff_dense* n, ff_layer* l, const float* x, int32_t B, int32_t K,
+                                        float* scores, int32_t* ids, ff_stream_t stream) {
+  g_launches = 0;
+  if (!n || !l) return fail(FF_ERR_ARG, "dense layer / layer is NULL");
+  if (n->cfg.m != l->cfg.m) return fail(FF_ERR_CONFIG, "dense m=%d != layer m=%d", n->cfg.m, l->cfg.m);
+  if (B < 0 || B > n->cfg.max_batch || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside max_batch", B);
+  if (B == 0) return FF_OK;
+  if (!x) return fail(FF_ERR_ARG, "null x");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ff_status s = dense_forward_impl(n, x, B, 0, false, l->hd, nullptr, st);
+  if (s != FF_OK) return s;
+  const int32_t nl = g_launches;
+  s = predict_impl(l, nullptr, B, K, scores, ids, st, true);
+  g_launches += nl;
+  return s;
 }
 
 }  // extern "C"

@@ -33,6 +33,11 @@ EXPORTS = [
     "fixedfanin_profile_begin",
     "fixedfanin_profile_end", "fixedfanin_last_launch_count",
     "fixedfanin_last_error",
+    # NEXT-2: the intermediate layer and the whole architecture
+    "fixedfanin_dense_workspace_size", "fixedfanin_dense_create", "fixedfanin_dense_destroy",
+    "fixedfanin_dense_set_params", "fixedfanin_dense_get_params", "fixedfanin_dense_forward",
+    "fixedfanin_dense_backward_adam", "fixedfanin_dense_get_grads", "fixedfanin_model_train_step",
+    "fixedfanin_model_predict_topk",
 ]
 
 
@@ -50,6 +55,14 @@ class ff_config(ctypes.Structure):
         ("seed", ctypes.c_uint64), ("init_scale", ctypes.c_float), ("beta1", ctypes.c_float),
         ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("prune_frac", ctypes.c_float),
         ("flags", ctypes.c_uint32), ("loss", ctypes.c_int32),
+    ]
+
+
+class ff_dense_config(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int32), ("m", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("seed", ctypes.c_uint64), ("init_scale", ctypes.c_float), ("dropout", ctypes.c_float),
+        ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("flags", ctypes.c_uint32),
     ]
 
 
@@ -83,6 +96,16 @@ def lib() -> ctypes.CDLL:
             "fixedfanin_check": [P, P],
             "fixedfanin_profile_begin": [P, i32],
             "fixedfanin_profile_end": [P, P, P],
+            "fixedfanin_dense_workspace_size": [P, P],
+            "fixedfanin_dense_create": [P, P, ctypes.c_size_t, P, P],
+            "fixedfanin_dense_destroy": [P],
+            "fixedfanin_dense_set_params": [P, P, P, P, P, P, P, P, P],
+            "fixedfanin_dense_get_params": [P, P, P, P, P, P, P, P, P],
+            "fixedfanin_dense_forward": [P, P, i32, u64, i32, P, P],
+            "fixedfanin_dense_backward_adam": [P, P, i32, f32, P],
+            "fixedfanin_dense_get_grads": [P, P, P, P],
+            "fixedfanin_model_train_step": [P, P, P, i32, u64, P, P, f32, f32, P, P],
+            "fixedfanin_model_predict_topk": [P, P, P, i32, i32, P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -284,3 +307,100 @@ def merge_topk(scores, ids, stream=None):
     _check(lib().fixedfanin_merge_topk(_ptr(scores.contiguous()), _ptr(ids.contiguous()), P, B, K, _ptr(out_s),
                                        _ptr(out_i), _stream(stream)))
     return out_s, out_i
+
+
+# ------------------------------------------------------------------ NEXT-2
+@dataclass
+class DenseConfig:
+    """The intermediate layer of the proposed architecture (Fig. 2)."""
+    d: int
+    m: int
+    max_batch: int = 32
+    seed: int = 7
+    init_scale: float = 0.0
+    dropout: float = 0.0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    flags: int = 0
+
+    def c(self) -> ff_dense_config:
+        return ff_dense_config(self.d, self.m, self.max_batch, 0, self.seed, self.init_scale, self.dropout,
+                               self.beta1, self.beta2, self.eps, self.flags)
+
+
+class DenseLayer:
+    """Input dropout -> dense Wd -> ReLU on one GPU (a replica under label sharding)."""
+
+    def __init__(self, cfg: DenseConfig, device=None, stream=None):
+        self.cfg = cfg
+        self._c = cfg.c()
+        self.device = torch.device(device if device is not None else "cuda")
+        n = ctypes.c_size_t(0)
+        _check(lib().fixedfanin_dense_workspace_size(ctypes.byref(self._c), ctypes.byref(n)))
+        self.workspace = torch.empty(int(n.value), dtype=torch.uint8, device=self.device)
+        self._h = ctypes.c_void_p()
+        _check(lib().fixedfanin_dense_create(ctypes.byref(self._c), _ptr(self.workspace), int(n.value),
+                                             _stream(stream), ctypes.byref(self._h)))
+        self.d, self.m = cfg.d, cfg.m
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().fixedfanin_dense_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def get_params(self, stream=None):
+        d, m, dev = self.d, self.m, self.device
+        Wd, mWd, vWd = (torch.empty((d, m), dtype=torch.float32, device=dev) for _ in range(3))
+        bd, mbd, vbd = (torch.empty(m, dtype=torch.float32, device=dev) for _ in range(3))
+        t = ctypes.c_int64(0)
+        _check(lib().fixedfanin_dense_get_params(self._h, _ptr(Wd), _ptr(bd), _ptr(mWd), _ptr(vWd), _ptr(mbd),
+                                                 _ptr(vbd), ctypes.byref(t), _stream(stream)))
+        return dict(Wd=Wd, bd=bd, mWd=mWd, vWd=vWd, mbd=mbd, vbd=vbd, t=int(t.value))
+
+    def set_params(self, Wd=None, bd=None, mWd=None, vWd=None, mbd=None, vbd=None, t=None, stream=None):
+        tt = ctypes.c_int64(int(t)) if t is not None else None
+        _check(lib().fixedfanin_dense_set_params(self._h, _ptr(Wd), _ptr(bd), _ptr(mWd), _ptr(vWd), _ptr(mbd),
+                                                 _ptr(vbd), ctypes.byref(tt) if tt is not None else None,
+                                                 _stream(stream)))
+
+    def forward(self, x, step=0, train=True, h=None, stream=None):
+        B = x.shape[0]
+        if h is None:
+            h = torch.empty((B, self.m), dtype=torch.float32, device=self.device)
+        _check(lib().fixedfanin_dense_forward(self._h, _ptr(x), B, int(step), 1 if train else 0, _ptr(h),
+                                              _stream(stream)))
+        return h
+
+    def backward_adam(self, dh, lr, stream=None):
+        _check(lib().fixedfanin_dense_backward_adam(self._h, _ptr(dh), dh.shape[0], lr, _stream(stream)))
+
+    def get_grads(self, stream=None):
+        dWd = torch.empty((self.d, self.m), dtype=torch.float32, device=self.device)
+        dbd = torch.empty(self.m, dtype=torch.float32, device=self.device)
+        _check(lib().fixedfanin_dense_get_grads(self._h, _ptr(dWd), _ptr(dbd), _stream(stream)))
+        return dWd, dbd
+
+
+def model_train_step(dense: DenseLayer, layer: FixedFanInLayer, x, step, lbl_ptr, lbl_ids, lr, grad_scale=None,
+                     loss=None, stream=None):
+    """One step of the whole architecture (dropout -> dense -> ReLU -> fixed fan-in -> loss ->
+    backward through both layers -> Adam on both) through fixedfanin_model_train_step."""
+    B = x.shape[0]
+    gs = 1.0 / max(B, 1) if grad_scale is None else grad_scale
+    _check(lib().fixedfanin_model_train_step(dense._h, layer._h, _ptr(x), B, int(step), _ptr(lbl_ptr), _ptr(lbl_ids),
+                                             gs, lr, _ptr(loss), _stream(stream)))
+    return loss
+
+
+def model_predict_topk(dense: DenseLayer, layer: FixedFanInLayer, x, K, stream=None):
+    B = x.shape[0]
+    scores = torch.empty((B, K), dtype=torch.float32, device=layer.device)
+    ids = torch.empty((B, K), dtype=torch.int32, device=layer.device)
+    _check(lib().fixedfanin_model_predict_topk(dense._h, layer._h, _ptr(x), B, K, _ptr(scores), _ptr(ids),
+                                               _stream(stream)))
+    return scores, ids

@@ -47,6 +47,13 @@ SHAPES = {
 }
 
 
+# The proposed architecture's fixed input features: 512-d fastText-based (Slice)
+# or 768-d CascadeXML embeddings; input dropout 10% for Amazon-670K / Wiki-500K Slice, 20% for
+# Wiki10 / Wiki-500K Cascade.  NEXT-2 of SURVEY §8(f).
+FEATURE_DIMS = {"slice": 512, "cascade": 768}
+DROPOUT = {"amazon-670k": 0.1, "wiki-500k": 0.1, "wiki10-31k": 0.2}
+
+
 def _rng(seed: int, step: int, stream: int) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, step, stream])))
 
@@ -55,6 +62,11 @@ def hidden_batch(B: int, m: int, step: int = 0, seed: int = DATA_SEED) -> np.nda
     """h[B][m] float32 = ReLU(N(0,1)), a fresh batch per step."""
     z = _rng(seed, step, 1).standard_normal((B, m), dtype=np.float32)
     return np.maximum(z, np.float32(0.0))
+
+
+def feature_batch(B: int, d: int, step: int = 0, seed: int = DATA_SEED) -> np.ndarray:
+    """x[B][d] float32 ~ N(0,1): stand-in for the fixed dense embeddings (no dataset)."""
+    return _rng(seed, step, 3).standard_normal((B, d), dtype=np.float32)
 
 
 @lru_cache(maxsize=8)

@@ -1,0 +1,226 @@
+"""GPU parity of NEXT-2: the intermediate layer of the proposed architecture
+(input dropout P:686-689 -> dense Wd P:594-603 -> ReLU) and the whole-architecture step,
+through the C ABI, against the fp64 oracle.
+
+Tolerances as in test_gpu_parity.py (R19): err = |x - x_ref| / max(|x_ref|, A_ref) <= 1e-4.
+Bit-exact: the Philox init of Wd, the dropout keep mask.  Where a float decides an integer
+(the ReLU mask of the backward) the oracle takes the GPU's decision (lockstep, R20).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2306_03725_b200 import synth
+from test_gpu_parity import ADAM, F32, adam_A, assert_close, dev, make, state_of, tens
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__ as g
+    g.build_lib()
+
+
+def L_():
+    from paper_2306_03725_b200 import layer
+    return layer
+
+
+def make_dense(d, m, B=32, **kw):
+    layer = L_()
+    return layer.DenseLayer(layer.DenseConfig(d=d, m=m, max_batch=B, **kw), device=dev())
+
+
+def dstate(dn):
+    return {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in dn.get_params().items()}
+
+
+SHAPES = [(32, 512, 1000), (7, 37, 203), (70, 64, 300), (1, 5, 3), (32, 130, 4096)]
+
+
+@pytest.mark.parametrize("d,m,seed", [(512, 1000, 7), (37, 203, 3), (5, 3, 1), (768, 4096, 42)])
+def test_dense_init_bit_exact(d, m, seed):
+    dn = make_dense(d, m, seed=seed)
+    s = dstate(dn)
+    ref = oracle.dense_init(d, m, seed)
+    assert (s["Wd"].view(np.uint32) == ref.view(np.uint32)).all()
+    assert (s["bd"] == 0).all() and (s["mWd"] == 0).all() and (s["vWd"] == 0).all() and s["t"] == 0
+
+
+@pytest.mark.parametrize("B,d,p,step", [(32, 64, 0.1, 5), (7, 37, 0.2, 0), (70, 16, 0.5, 123456)])
+def test_dropout_mask_bit_exact(B, d, p, step):
+    """Wd = I, bd = 0, x > 0: h = xt, so h exposes the keep mask (bit-exact) and the scaled
+    values (fp32 x*s vs the oracle's exact product)."""
+    dn = make_dense(d, d, B=B, seed=99, dropout=p)
+    dn.set_params(Wd=tens(np.eye(d, dtype=np.float32)))
+    x = np.abs(synth.feature_batch(B, d, step=3)) + np.float32(0.1)
+    h = dn.forward(tens(x), step=step, train=True).cpu().numpy()
+    xt, keep, s = oracle.dropout(x, p, seed=99, step=step)
+    assert ((h != 0) == (keep == 1)).all()
+    assert_close(h, xt, 0, "dropped-out features")
+    assert (h[keep == 1].astype(np.float32) == (x[keep == 1] * np.float32(s)).astype(np.float32)).all()
+    h0 = dn.forward(tens(x), step=step, train=False).cpu().numpy()      # inference: no dropout
+    assert (h0 == x).all()
+
+
+@pytest.mark.parametrize("B,d,m", SHAPES)
+@pytest.mark.parametrize("train", [False, True])
+def test_dense_forward_matches_oracle(B, d, m, train):
+    dn = make_dense(d, m, B=B, seed=5, dropout=0.1)
+    bd = (np.random.default_rng(2).random(m, dtype=np.float32) - np.float32(0.5)) * np.float32(0.2)
+    dn.set_params(bd=tens(bd))
+    s = dstate(dn)
+    x = synth.feature_batch(B, d, step=1)
+    h = dn.forward(tens(x), step=11, train=train).cpu().numpy()
+    xt = oracle.dropout(x, 0.1, seed=5, step=11)[0] if train else x.astype(np.float64)
+    z, Az, href = oracle.dense_forward(s["Wd"], s["bd"], xt)
+    assert_close(h, href, Az, "h = ReLU(z)")
+
+
+@pytest.mark.parametrize("B,d,m", SHAPES)
+def test_dense_backward_adam_lockstep(B, d, m):
+    layer = L_()
+    dn = make_dense(d, m, B=B, seed=8, dropout=0.1, flags=layer.FF_FLAG_STORE_GRADS)
+    rng = np.random.default_rng(4)
+    mWd = (rng.random((d, m), dtype=np.float32) * np.float32(1e-3))
+    vWd = (rng.random((d, m), dtype=np.float32) * np.float32(1e-6))
+    dn.set_params(mWd=tens(mWd), vWd=tens(vWd), t=3)
+    s0 = dstate(dn)
+    x = synth.feature_batch(B, d, step=2)
+    h = dn.forward(tens(x), step=4, train=True).cpu().numpy()
+    dh = synth.feature_batch(B, m, step=9) * np.float32(0.01)
+    lr = F32(1e-3)
+    dn.backward_adam(tens(dh), lr)
+    dWd, dbd = (t.cpu().numpy() for t in dn.get_grads())
+    s1 = dstate(dn)
+    xt = oracle.dropout(x, 0.1, seed=8, step=4)[0]
+    # the ReLU mask is the GPU's decision (h > 0 <=> z > 0): feed h as z (R20)
+    rW, AW, rb, Ab = oracle.dense_backward(xt, h.astype(np.float64), dh)
+    assert_close(dWd, rW, AW, "dWd")
+    assert_close(dbd, rb, Ab, "dbd")
+    assert s1["t"] == 4
+    Wr, mr, vr = oracle.adam(s0["Wd"], dWd, s0["mWd"], s0["vWd"], 4, lr, **ADAM)
+    assert_close(s1["Wd"], Wr, adam_A(s0["Wd"], Wr), "Wd'")
+    # m' = b1 m + (1 - b1) q: R19 companion = the two terms' magnitudes (they can cancel)
+    Am = np.abs(ADAM["beta1"] * s0["mWd"].astype(np.float64)) + np.abs((1 - ADAM["beta1"]) * dWd.astype(np.float64))
+    assert_close(s1["mWd"], mr, Am, "mWd'"); assert_close(s1["vWd"], vr, 1e-30, "vWd'")
+    br, mbr, vbr = oracle.adam(s0["bd"], dbd, s0["mbd"], s0["vbd"], 4, lr, **ADAM)
+    assert_close(s1["bd"], br, adam_A(s0["bd"], br), "bd'")
+
+
+def test_dense_backward_requires_forward_and_same_batch():
+    layer = L_()
+    dn = make_dense(8, 16, B=4)
+    with pytest.raises(layer.FFError) as e:
+        dn.backward_adam(tens(np.zeros((4, 16), np.float32)), 1e-3)
+    assert e.value.status == layer.FF_ERR_STATE
+    dn.forward(tens(synth.feature_batch(4, 8)), train=True)
+    with pytest.raises(layer.FFError):
+        dn.backward_adam(tens(np.zeros((3, 16), np.float32)), 1e-3)
+
+
+def _model(L, m, k, d, B, dh_mode, p, flags=0):
+    layer = L_()
+    lay = make(L, m, k, B=B, seed=42, dh_mode=dh_mode, flags=flags)
+    dn = make_dense(d, m, B=B, seed=17, dropout=p, flags=flags)
+    return lay, dn
+
+
+@pytest.mark.parametrize("dh_mode", [0, 1])
+def test_model_step_equals_composed_calls(dh_mode):
+    """fixedfanin_model_train_step (h, dh stay in the layer's column lines) == dense_forward ->
+    train_step -> dense_backward_adam through [B][m] buffers.  CSC dh is deterministic, so
+    the two paths are bit-identical there; atomic dh within rounding of its sum order."""
+    layer = L_()
+    L, m, k, d, B = 3000, 1024, 32, 96, 32
+    lay1, dn1 = _model(L, m, k, d, B, dh_mode, 0.1)
+    lay2, dn2 = _model(L, m, k, d, B, dh_mode, 0.1)
+    loss1 = torch.zeros(1, device=dev()); loss2 = torch.zeros(1, device=dev())
+    for step in range(3):
+        x = tens(synth.feature_batch(B, d, step=step))
+        ptr, ids = (tens(a) for a in synth.label_batch(B, L, 5.0, step=step))
+        layer.model_train_step(dn1, lay1, x, step, ptr, ids, F32(1e-3), loss=loss1)
+        h = dn2.forward(x, step=step, train=True)
+        dh, _ = lay2.train_step(h, ptr, ids, F32(1e-3), loss=loss2)
+        dn2.backward_adam(dh, F32(1e-3))
+    s1, s2, d1, d2 = state_of(lay1), state_of(lay2), dstate(dn1), dstate(dn2)
+    if dh_mode == 1:
+        for kk in ("W", "idx", "bias", "mW", "vW"):
+            assert (s1[kk] == s2[kk]).all(), kk
+        for kk in ("Wd", "bd", "mWd", "vWd"):
+            assert (d1[kk] == d2[kk]).all(), kk
+        # the loss is summed across CTAs with atomics: equal up to that order
+        assert abs(loss1.item() - loss2.item()) <= 1e-6 * abs(loss2.item())
+    else:
+        assert (s1["idx"] == s2["idx"]).all()
+        assert np.allclose(s1["W"], s2["W"], rtol=1e-5, atol=1e-6)
+        assert np.allclose(d1["Wd"], d2["Wd"], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("dh_mode", [0, 1])
+def test_model_step_lockstep_vs_oracle(dh_mode):
+    """One whole-architecture step vs oracle.model_train_step from the GPU's state: loss, the
+    sparse layer's and the dense layer's gradients (R19), then Adam on those gradients."""
+    layer = L_()
+    L, m, k, d, B = 2000, 512, 16, 64, 32
+    lay, dn = _model(L, m, k, d, B, dh_mode, 0.1, flags=layer.FF_FLAG_STORE_GRADS)
+    s0, d0 = state_of(lay), dstate(dn)
+    x = synth.feature_batch(B, d, step=5)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=5)
+    loss = torch.zeros(1, device=dev())
+    lr = F32(1e-3)
+    layer.model_train_step(dn, lay, tens(x), 5, tens(ptr), tens(ids), lr, loss=loss)
+    dW, db = (t.cpu().numpy() for t in lay.get_grads())
+    dWd, dbd = (t.cpu().numpy() for t in dn.get_grads())
+    s1, d1 = state_of(lay), dstate(dn)
+    st = oracle.State(s0["W"].astype(np.float64), s0["idx"], s0["bias"].astype(np.float64),
+                      s0["mW"].astype(np.float64), s0["vW"].astype(np.float64), s0["mb"].astype(np.float64),
+                      s0["vb"].astype(np.float64), s0["t"])
+    ds = oracle.DenseState(d0["Wd"].astype(np.float64), d0["bd"].astype(np.float64), d0["mWd"].astype(np.float64),
+                           d0["vWd"].astype(np.float64), d0["mbd"].astype(np.float64), d0["vbd"].astype(np.float64),
+                           d0["t"])
+    r = oracle.model_train_step(ds, st, x, 5, 0.1, 17, ptr, ids, F32(1.0 / B), lr, **ADAM)
+    assert abs(loss.item() - r.sparse.loss) <= 1e-4 * abs(r.sparse.loss)
+    assert_close(dW, r.sparse.dW, r.sparse.AdW, "sparse dW")
+    assert_close(db, r.sparse.db, r.sparse.Adb, "sparse db")
+    # dense gradients: ReLU mask of the oracle's z may differ at |z| ~ rounding; compare where
+    # every sample's z is clear of 0 by the forward tolerance
+    clear = (np.abs(r.z) > 1e-4 * r.Az).all(axis=0)
+    assert clear.mean() > 0.99
+    assert_close(dWd[:, clear], r.dWd[:, clear], r.AdWd[:, clear], "dense dWd")
+    assert_close(dbd[clear], r.dbd[clear], r.Adbd[clear], "dense dbd")
+    assert s1["t"] == 1 and d1["t"] == 1
+    Wr, _, _ = oracle.adam(d0["Wd"], dWd, d0["mWd"], d0["vWd"], 1, lr, **ADAM)
+    assert_close(d1["Wd"], Wr, adam_A(d0["Wd"], Wr), "Wd'")
+
+
+@pytest.mark.parametrize("dh_mode", [0, 1])
+def test_model_free_running_tiny_matches_oracle(dh_mode):
+    """tiny config + the intermediate layer (d = 32): 5 whole-architecture steps, then one
+    redistribution and a model prediction, the oracle evolving its own fp64 state."""
+    layer = L_()
+    L, m, k, d, B = 1000, 256, 16, 32, 32
+    lay, dn = _model(L, m, k, d, B, dh_mode, 0.1)
+    st = oracle.State.create(L, m, k, seed=42)
+    ds = oracle.DenseState.create(d, m, seed=17)
+    lr = F32(1e-3)
+    for step in range(5):
+        x = synth.feature_batch(B, d, step=step)
+        ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        layer.model_train_step(dn, lay, tens(x), step, tens(ptr), tens(ids), lr)
+        oracle.model_train_step(ds, st, x, step, 0.1, 17, ptr, ids, F32(1.0 / B), lr, **ADAM)
+    s, dd = state_of(lay), dstate(dn)
+    assert_close(s["W"], st.W, np.abs(st.W) + 5 * lr, "W after 5 model steps")
+    assert_close(dd["Wd"], ds.Wd, np.abs(ds.Wd) + 5 * lr, "Wd after 5 model steps")
+    assert_close(s["bias"], st.bias, np.abs(st.bias) + 5 * lr, "bias after 5 model steps")
+    lay.redistribute(5)
+    x = synth.feature_batch(B, d, step=50)
+    sc, ids_ = layer.model_predict_topk(dn, lay, tens(x), 5)
+    h = dn.forward(tens(x), train=False)
+    y = lay.forward(h).cpu().numpy().astype(np.float64)
+    rs, rid = oracle.topk(y, 5)
+    assert (ids_.cpu().numpy() == rid).all() and (sc.cpu().numpy() == rs).all()

@@ -303,7 +303,10 @@ def test_redistribution_config_errors():
 # ------------------------------------------------------------------------- top-K
 @pytest.mark.parametrize("L,m,k,B,K", [(1000, 256, 16, 32, 5), (5000, 512, 32, 70, 8), (9, 16, 4, 3, 1),
                                         (8, 16, 4, 3, 8), (3000, 4096, 64, 32, 5), (700, 500, 40, 50, 3),
-                                        (4000, 1024, 32, 1024, 5)])
+                                        (4000, 1024, 32, 1024, 5),
+                                        # k = 32, B <= 32: the pipelined predict kernel
+                                        (5000, 512, 32, 32, 5), (3001, 300, 32, 7, 8), (40, 64, 32, 32, 8),
+                                        (200003, 4096, 32, 32, 5)])
 def test_predict_topk_bit_exact(L, m, k, B, K):
     lay = make(L, m, k, B=B, seed=3)
     h = tens(synth.hidden_batch(B, m, step=1))
@@ -322,6 +325,16 @@ def test_predict_topk_ties_resolved_by_lower_id():
     lay.set_params(W=tens(W), bias=tens(bias))
     sc, ids = lay.predict_topk(tens(synth.hidden_batch(B, m)), 6)
     assert (ids.cpu().numpy() == np.array([5, 17, 100, 250, 0, 1])).all()
+
+
+def test_predict_topk_ties_resolved_by_lower_id_pipelined():
+    L, m, k, B = 5000, 64, 32, 32          # k = 32, B <= 32: k_predict_ring + block merge
+    lay = make(L, m, k, B=B)
+    W = np.zeros((L, k), np.float32)
+    bias = np.zeros(L, np.float32); bias[[4999, 17, 5, 2500, 100]] = 1.0
+    lay.set_params(W=tens(W), bias=tens(bias))
+    sc, ids = lay.predict_topk(tens(synth.hidden_batch(B, m)), 8)
+    assert (ids.cpu().numpy() == np.array([5, 17, 100, 2500, 4999, 0, 1, 2])).all()
 
 
 @DH

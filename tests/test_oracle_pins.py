@@ -437,3 +437,125 @@ def test_sqh_zero_count_equals_margin_count_and_fd():
         ym = y.copy(); ym[pos] -= e
         num = (oracle.sqh_grad(yp, ptr, ids, 0.5)[1] - oracle.sqh_grad(ym, ptr, ids, 0.5)[1]) / (2 * e)
         assert num == pytest.approx(g[pos], rel=1e-6, abs=1e-9)
+
+
+# ------------------------------------------- NEXT-2: intermediate layer + input dropout
+def test_dropout_p0_is_identity_and_kept_values_are_scaled_exactly():
+    x = synth.feature_batch(6, 40, step=2).astype(np.float64)
+    xt, keep, s = oracle.dropout(x, 0.0, seed=9, step=5)
+    assert s == 1.0 and keep.all() and (xt == x).all()
+    xt, keep, s = oracle.dropout(x, 0.25, seed=9, step=5)
+    assert s == np.float32(1.0) / np.float32(0.75)
+    assert (xt[keep == 1] == x[keep == 1] * s).all() and (xt[keep == 0] == 0.0).all()
+
+
+def test_dropout_decision_uses_the_pinned_philox_stream():
+    """The keep decision of (b, f) is word f % 4 of Philox(ctr = (f/4, b, step, 3), key = seed)
+    (reading R25), with Philox itself pinned by the Random123 vectors above."""
+    B, d, seed, step, p = 3, 9, 0x1234_5678_9ABC, 17, 0.3
+    _, keep, _ = oracle.dropout(np.ones((B, d)), p, seed, step)
+    for b in range(B):
+        for f in range(d):
+            u = oracle.philox4x32_10([f // 4, b, step, 3], [seed & 0xFFFFFFFF, seed >> 32])[f % 4]
+            assert keep[b, f] == ((u >> 8) / 2.0 ** 24 >= np.float32(p))
+
+
+def test_dropout_rate_and_keying():
+    B, d, p = 32, 2048, 0.1                 # P:686-689: 10% for Amazon-670K features
+    _, k1, _ = oracle.dropout(np.ones((B, d)), p, seed=42, step=7)
+    n = B * d
+    drop = n - int(k1.sum())
+    assert abs(drop - p * n) < 5 * math.sqrt(n * p * (1 - p))
+    _, k2, _ = oracle.dropout(np.ones((B, d)), p, seed=42, step=8)
+    _, k3, _ = oracle.dropout(np.ones((B, d)), p, seed=43, step=7)
+    _, k4, _ = oracle.dropout(np.ones((B, d)), p, seed=42, step=7)
+    assert (k1 != k2).any() and (k1 != k3).any() and (k1 == k4).all()
+    assert (k1[0] != k1[1]).any()           # samples get independent masks
+
+
+def test_dense_forward_is_a_matmul_plus_bias_then_relu():
+    B, d, m = 5, 24, 40
+    x = synth.feature_batch(B, d).astype(np.float64)
+    Wd = oracle.dense_init(d, m, seed=3).astype(np.float64)
+    bd = np.linspace(-0.2, 0.2, m)
+    z, Az, h = oracle.dense_forward(Wd, bd, x)
+    ref = x @ Wd + bd                       # library matmul (the operation's definition)
+    assert np.allclose(z, ref, rtol=0, atol=1e-13)
+    assert (h == np.maximum(z, 0.0)).all()
+    assert (Az >= np.abs(z) - 1e-15).all()
+    assert 0.2 < (h == 0).mean() < 0.8
+
+
+def test_dense_backward_matches_matmul_and_relu_prime_at_zero_is_zero():
+    B, d, m = 7, 10, 12
+    xt = synth.feature_batch(B, d, step=1).astype(np.float64)
+    z = synth.feature_batch(B, m, step=2).astype(np.float64)
+    z[0, :3] = 0.0                           # exactly at the kink: ReLU'(0) = 0 (R26)
+    dh = synth.feature_batch(B, m, step=3).astype(np.float64)
+    dWd, AdWd, dbd, Adbd = oracle.dense_backward(xt, z, dh)
+    dz = dh * (z > 0)
+    assert np.allclose(dWd, xt.T @ dz, rtol=0, atol=1e-13)
+    assert np.allclose(dbd, dz.sum(0), rtol=0, atol=1e-13)
+    dWd0, _, dbd0, _ = oracle.dense_backward(xt[:1], z[:1], dh[:1])
+    assert (dWd0[:, :3] == 0).all() and (dbd0[:3] == 0).all()
+
+
+def test_dense_init_range_uniformity_and_keying():
+    d, m = 64, 512
+    Wd = oracle.dense_init(d, m, seed=11)
+    a = np.float32(np.sqrt(6.0 / (d + m)))
+    assert Wd.dtype == np.float32 and np.abs(Wd).max() <= a
+    hist, _ = np.histogram(Wd, bins=16, range=(-a, a))
+    exp = Wd.size / 16
+    assert ((hist - exp) ** 2 / exp).sum() < 50.0          # chi^2, 15 dof
+    assert (oracle.dense_init(d, m, seed=11) == Wd).all() and (oracle.dense_init(d, m, seed=12) != Wd).any()
+
+
+def _model_loss(Wd, bd, xt, st, ptr, ids, s):
+    _, _, h = oracle.dense_forward(Wd, bd, xt)
+    y, _ = oracle.forward(st.W, st.idx, st.bias, h)
+    return oracle.bce_grad(y, ptr, ids, s)[1]
+
+
+def test_model_gradients_match_central_finite_differences():
+    """dWd / dbd of the whole architecture (dropout -> dense -> ReLU -> sparse -> BCE) against
+    central finite differences of the loss: pins the dense backward, the ReLU mask and the
+    sparse layer's dh feeding it (Fig. 2)."""
+    B, d, m, L, k = 4, 6, 16, 30, 4
+    x = synth.feature_batch(B, d, step=4).astype(np.float64)
+    ds = oracle.DenseState.create(d, m, seed=5)
+    ds.bd = np.linspace(-0.05, 0.1, m)
+    st = oracle.State.create(L, m, k, seed=6)
+    st.bias = np.linspace(-1, 1, L)
+    ptr, ids = synth.label_batch(B, L, 3.0, step=1)
+    s = 1.0 / B
+    r = oracle.model_train_step(ds.copy(), st.copy(), x, step=3, dropout_p=0.2, seed=77, lbl_ptr=ptr,
+                                lbl_ids=ids, grad_scale=s, lr=0.0)
+    eps = 1e-6
+    assert (np.abs(r.z) > 1e-4).all()        # no kink within the FD step
+    rng = np.random.default_rng(0)
+    for (f, c) in [tuple(rng.integers(0, (d, m))) for _ in range(12)]:
+        Wp, Wm = ds.Wd.copy(), ds.Wd.copy()
+        Wp[f, c] += eps; Wm[f, c] -= eps
+        fd = (_model_loss(Wp, ds.bd, r.xt, st, ptr, ids, s) - _model_loss(Wm, ds.bd, r.xt, st, ptr, ids, s)) / (2 * eps)
+        assert abs(fd - r.dWd[f, c]) <= 1e-6 * max(1.0, abs(fd)) + 1e-9, (f, c, fd, r.dWd[f, c])
+    for c in range(0, m, 3):
+        bp, bm = ds.bd.copy(), ds.bd.copy()
+        bp[c] += eps; bm[c] -= eps
+        fd = (_model_loss(ds.Wd, bp, r.xt, st, ptr, ids, s) - _model_loss(ds.Wd, bm, r.xt, st, ptr, ids, s)) / (2 * eps)
+        assert abs(fd - r.dbd[c]) <= 1e-6 * max(1.0, abs(fd)) + 1e-9
+
+
+def test_model_step_updates_both_layers_with_their_own_t():
+    B, d, m, L, k = 3, 5, 12, 20, 4
+    x = synth.feature_batch(B, d).astype(np.float64)
+    ds, st = oracle.DenseState.create(d, m, seed=1), oracle.State.create(L, m, k, seed=2)
+    ptr, ids = synth.label_batch(B, L, 2.0)
+    W0, Wd0 = st.W.copy(), ds.Wd.copy()
+    r = oracle.model_train_step(ds, st, x, 0, 0.1, 9, ptr, ids, 1.0 / B, 1e-3)
+    assert ds.t == 1 and st.t == 1
+    # Adam's first step moves every parameter with a nonzero gradient by ~lr (sign step, S:385)
+    moved = np.abs(ds.Wd - Wd0)
+    nz = np.abs(r.dWd) > 1e-6
+    assert np.allclose(moved[nz], 1e-3, rtol=1e-2) and (moved[r.dWd == 0] == 0).all()
+    assert (np.abs(st.W - W0) > 0).any()
