@@ -121,3 +121,37 @@ class OverlappedTrainer:
             if self.bcast[i] is not None:
                 self.bcast[i].wait()
                 self.bcast[i] = None
+
+
+class ShardedModel:
+    """The whole proposed architecture (Fig. 2) under label sharding (NEXT-2):
+    every rank holds a replica of the dense intermediate layer (``dense``: the CUDA
+    ``DenseLayer`` by default) and one label shard of the fixed fan-in layer.
+
+    Per step: the features x (replicated; broadcast from rank 0) go through the replica's
+    dropout + dense forward — identical on every rank, because the dropout mask is keyed on
+    (seed, step, sample) (reading R25) — the shard's fused step yields its partial dh, the
+    dh all-reduce sums the shards, and every replica applies the same dense backward + Adam
+    to the same summed dh, so the replicas stay identical without another collective."""
+
+    def __init__(self, layer: ShardedLayer, dense=None, d: int | None = None, device=None, **dense_cfg):
+        self.layer = layer
+        if dense is None:
+            from .layer import DenseConfig, DenseLayer
+            dense = DenseLayer(DenseConfig(d=d, m=layer.m, **dense_cfg), device=device)
+        self.dense = dense
+
+    def broadcast_x(self, x: torch.Tensor, src: int = 0) -> torch.Tensor:
+        if self.layer.world > 1:
+            dist.broadcast(x, src=src, group=self.layer.group)
+        return x
+
+    def train_step(self, x, step, lbl_ptr, lbl_ids, lr, grad_scale=None, dh=None, loss=None, reduce_loss=False):
+        h = self.dense.forward(x, step=step, train=True)
+        dh, loss = self.layer.train_step(h, lbl_ptr, lbl_ids, lr, grad_scale=grad_scale, dh=dh, loss=loss,
+                                         reduce_loss=reduce_loss)
+        self.dense.backward_adam(dh, lr)
+        return dh, loss
+
+    def predict_topk(self, x, K: int):
+        return self.layer.predict_topk(self.dense.forward(x, train=False), K)

@@ -187,3 +187,84 @@ def test_overlapped_trainer_two_ranks():
     for rank in range(world):
         np.testing.assert_allclose(results[rank][0], ref[1], rtol=1e-12, atol=1e-14)
         np.testing.assert_allclose(results[rank][1], ref[2], rtol=1e-12, atol=1e-14)
+
+
+# ------------------------------------------------ NEXT-2: the whole architecture, sharded
+D_FEAT, P_DROP, DSEED = 12, 0.2, 5
+
+
+class OracleDense:
+    """CPU stand-in for DenseLayer (same method signatures) backed by the oracle."""
+
+    def __init__(self):
+        self.ds = oracle.DenseState.create(D_FEAT, M, DSEED)
+        self.xt = self.z = None
+
+    def forward(self, x, step=0, train=True):
+        xt = oracle.dropout(x.numpy(), P_DROP, DSEED, step)[0] if train else x.numpy()
+        z, _, h = oracle.dense_forward(self.ds.Wd, self.ds.bd, xt)
+        self.xt, self.z = xt, z
+        return torch.from_numpy(h)
+
+    def backward_adam(self, dh, lr):
+        dWd, _, dbd, _ = oracle.dense_backward(self.xt, self.z, dh.numpy())
+        ds = self.ds
+        ds.t += 1
+        ds.Wd, ds.mWd, ds.vWd = oracle.adam(ds.Wd, dWd, ds.mWd, ds.vWd, ds.t, lr)
+        ds.bd, ds.mbd, ds.vbd = oracle.adam(ds.bd, dbd, ds.mbd, ds.vbd, ds.t, lr)
+
+
+def _worker_model(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2306_03725_b200.sharded import ShardedModel
+        rb, re_ = shard_rows(L, rank, world)
+        eng = OracleEngine(L, M, K_FAN, rb, re_, SEED)
+        model = ShardedModel(ShardedLayer(L, M, K_FAN, rank=rank, world=world, engine=eng, merge_fn=cpu_merge),
+                             dense=OracleDense())
+        out = {}
+        for step in range(3):
+            x = torch.from_numpy(synth.feature_batch(B, D_FEAT, step=step).astype(np.float64))
+            if rank != 0:
+                x = torch.zeros_like(x)                 # only the producer rank has the features
+            model.broadcast_x(x)
+            ptr, ids = synth.label_batch(B, L, 3.0, step=step)
+            _, loss = model.train_step(x, step, torch.from_numpy(ptr), torch.from_numpy(ids), 1e-2,
+                                       loss=torch.zeros(1, dtype=torch.float64), reduce_loss=True)
+            out[f"loss{step}"] = float(loss.item())
+        x = torch.from_numpy(synth.feature_batch(B, D_FEAT, step=9).astype(np.float64))
+        s, i = model.predict_topk(x, 5)
+        out["top_i"] = i.numpy()
+        out["Wd"] = model.dense.ds.Wd
+        out["W"] = eng.st.W
+        results[rank] = out
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_model_matches_unsharded_oracle():
+    """ShardedModel over 2 gloo ranks (dense replica per rank + label shards + dh all-reduce)
+    == the unsharded oracle.model_train_step: identical dense replicas, shard rows, losses
+    and merged top-K."""
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker_model, args=(world, _free_port(), results), nprocs=world, join=True)
+    st = oracle.State.create(L, M, K_FAN, SEED)
+    ds = oracle.DenseState.create(D_FEAT, M, DSEED)
+    for step in range(3):
+        x = synth.feature_batch(B, D_FEAT, step=step).astype(np.float64)
+        ptr, ids = synth.label_batch(B, L, 3.0, step=step)
+        r = oracle.model_train_step(ds, st, x, step, P_DROP, DSEED, ptr, ids, 1.0 / B, 1e-2)
+        for rank in range(world):
+            assert results[rank][f"loss{step}"] == pytest.approx(r.sparse.loss, rel=1e-12)
+    for rank in range(world):
+        np.testing.assert_allclose(results[rank]["Wd"], ds.Wd, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.concatenate([results[r]["W"] for r in range(world)]), st.W, rtol=0, atol=1e-12)
+    _, _, h = oracle.dense_forward(ds.Wd, ds.bd, synth.feature_batch(B, D_FEAT, step=9).astype(np.float64))
+    y, _ = oracle.forward(st.W, st.idx, st.bias, h)
+    _, i_ref = oracle.topk(y, 5)
+    for rank in range(world):
+        assert (results[rank]["top_i"] == i_ref).all()
