@@ -52,7 +52,9 @@ def args_():
     p.add_argument("--margin-bias", type=float, default=0.0,
                    help="sqh: start every label bias at -X so that a controlled fraction of negatives meets the "
                         "margin (engineered-margin analog of a trained model, SURVEY §8(f) NEXT-1)")
-    p.add_argument("--dh-mode", default="atomic", choices=["atomic", "csc"],
+    p.add_argument("--hybrid-frac", type=float, default=0.0,
+                   help="--dh-mode hybrid: fraction of the columns reduced by red (0 -> library default 0.5)")
+    p.add_argument("--dh-mode", default="atomic", choices=["atomic", "csc", "hybrid"],
                    help="dh scatter: red.global atomics (default: measured faster, DESIGN.md §6) or the "
                         "deterministic CSC pull")
     return p.parse_args()
@@ -255,10 +257,11 @@ def run_ours(a, shape, world, rank, local_rank):
             for s in range(N_BATCHES)]
     max_nnz = max(int(d[1][-1]) for d in data)
     from paper_2306_03725_b200.layer import FF_DH_ATOMIC, FF_DH_CSC, FF_LOSS_BCE, FF_LOSS_SQH
-    dh_mode = FF_DH_CSC if a.dh_mode == "csc" else FF_DH_ATOMIC
+    from paper_2306_03725_b200.layer import FF_DH_HYBRID
+    dh_mode = {"csc": FF_DH_CSC, "hybrid": FF_DH_HYBRID}.get(a.dh_mode, FF_DH_ATOMIC)
     layer = ShardedLayer(shape.L, shape.m, shape.k, rank=rank, world=world, device=dev, max_batch=B,
                          seed=synth.PARAM_SEED, max_nnz=max_nnz, dh_mode=dh_mode, flags=a.flags,
-                         loss=FF_LOSS_SQH if a.loss == "sqh" else FF_LOSS_BCE)
+                         loss=FF_LOSS_SQH if a.loss == "sqh" else FF_LOSS_BCE, hybrid_frac=a.hybrid_frac)
     eng = layer.engine
     L_local = layer.row_end - layer.row_begin
     stream = torch.cuda.current_stream()
@@ -428,6 +431,7 @@ def run_ours(a, shape, world, rank, local_rank):
         "data": "synthetic: h = ReLU(N(0,1)), Zipf(1.0) sparse labels, Philox-initialized W/idx (no dataset)",
         "config": {"workload": shape.name, "L": shape.L, "m": shape.m, "k": shape.k, "B": B, "global_batch": B,
                    "avg_pos": shape.avg_pos, "parallelism": f"label-shard x{world}", "dh_mode": a.dh_mode,
+                   "hybrid_frac": (a.hybrid_frac or 0.5) if a.dh_mode == "hybrid" else None,
                    "loss": a.loss, "margin_bias": a.margin_bias, "grad_skip_fraction": skip_fraction,
                    "redistribution": f"every {REDIST_EVERY} steps inside the timed region (global step counter)",
                    "l2": "no flush: per-step state stream 617 MB >> 126 MB L2 (inputs larger than L2)"},

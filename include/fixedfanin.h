@@ -80,6 +80,8 @@ typedef enum {
 /* ff_config.dh_mode */
 #define FF_DH_ATOMIC 0           /* dh by coalesced red.global.add (Alg. 2 with atomics) */
 #define FF_DH_CSC 1              /* dh by a transposed (CSC) index gather, rebuilt after redistribution */
+#define FF_DH_HYBRID 2           /* columns c < hybrid_frac*m by red (the L1->L2 write path), the rest by
+                                    the CSC gather (the read path): both paths busy at once */
 
 typedef struct {
     int64_t L_global;    /* total labels, 1 <= L_global < 2^31 (32-bit label ids)   */
@@ -90,13 +92,14 @@ typedef struct {
     int32_t max_batch;   /* largest B that will be passed, 1..FF_MAX_BATCH                      */
     int32_t max_topk;    /* largest K that will be passed to predict_topk, 1..FF_MAX_TOPK       */
     int32_t max_nnz;     /* largest lbl_ptr[B] for the *_host entry points (0 -> 64*max_batch)  */
-    int32_t dh_mode;     /* FF_DH_ATOMIC or FF_DH_CSC                                           */
+    int32_t dh_mode;     /* FF_DH_ATOMIC, FF_DH_CSC or FF_DH_HYBRID                             */
     uint64_t seed;       /* Philox key for init and redistribution (R13)                        */
     float init_scale;    /* W init U(-a, a); 0 -> a = fp32(1/sqrt(k)) (R17)                     */
     float beta1, beta2, eps;   /* Adam; 0 -> 0.9 / 0.999 / 1e-8 (R6)                            */
     float prune_frac;    /* SET fraction alpha, p = floor(alpha*k) per row; 0 -> 0.1    */
     uint32_t flags;      /* FF_FLAG_*                                                           */
     int32_t loss;        /* FF_LOSS_BCE (default) or FF_LOSS_SQH                                */
+    float hybrid_frac;   /* FF_DH_HYBRID: fraction of the columns reduced by red; 0 -> 0.5        */
 } ff_config;
 
 /* Bytes of device workspace the layer needs for `cfg` (host-only, no CUDA calls). */

@@ -21,6 +21,18 @@ namespace ff {
 
 constexpr uint32_t kDomDropout = 3;
 
+// streamed 16-B accesses of the dense layer's Adam state (no L1 allocation)
+__device__ __forceinline__ float4 ld_na4(const float* a) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a));
+  return v;
+}
+__device__ __forceinline__ void st_na4(float* a, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
 // Input dropout (reading R25): xT[f][b] = x[b][f] * scale if word f of the
 // Philox stream (ctr = (f/4, b, step, 3), key = seed) has (u >> 8) * 2^-24 >= p, else 0.
 // train = 0: xT = x (inference, no dropout).  Samples B..ldx-1 are 0.  Thread per (b, f/4).
@@ -52,12 +64,12 @@ __global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, 
 }
 
 // Forward: z[b][c] = bd[c] + sum_f xT[f][b] Wd[f][c] (f ascending, fp32 FMA chain, the
-// oracle's order), h = max(z, 0).  CTA = 128 threads -> 128 columns x 32 samples (chunk
-// blockIdx.y); lane -> 4 columns, warp w -> samples 8w..8w+7 (8 x 4 accumulators).  The Wd
+// oracle's order), h = max(z, 0).  CTA = 256 threads -> 128 columns x 32 samples (chunk
+// blockIdx.y); lane -> 4 columns, warp w -> samples 4w..4w+3 (4 x 4 accumulators).  The Wd
 // tile (64 features x 128 columns, 32 KB) and the xT tile (64 x 32) of the next feature
 // chunk are copied into a second shared-memory stage (cp.async, 16 B per thread-copy)
 // while the current chunk is computed, so the HBM latency of Wd is hidden behind the FMAs.
-constexpr int kDenseFwdThreads = 128, kDenseFch = 64;
+constexpr int kDenseFwdThreads = 256, kDenseFch = 64;
 constexpr int kDenseFwdSmem = 2 * kDenseFch * (128 + 32) * 4;
 __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const float* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
@@ -79,13 +91,13 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
     const uint32_t wdst = (uint32_t)__cvta_generic_to_shared(wbuf + stg * kDenseFch * 128);
     const uint32_t xdst = (uint32_t)__cvta_generic_to_shared(xbuf + stg * kDenseFch * 32);
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {                          // 64 rows x 32 float4
+    for (int u = 0; u < 8; ++u) {                           // 64 rows x 32 float4
       const int e = u * kDenseFwdThreads + threadIdx.x, r = e >> 5, cq = (e & 31) * 4;
       const bool ok = f0 + r < d && ct + cq < ldw;
       cp_async16_zfill(wdst + (uint32_t)(r * 128 + cq) * 4u, ok ? Wd + (int64_t)(f0 + r) * ldw + ct + cq : Wd, ok);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {                           // 64 rows x 8 float4
+    for (int u = 0; u < 2; ++u) {                           // 64 rows x 8 float4
       const int e = u * kDenseFwdThreads + threadIdx.x, r = e >> 3, s4 = (e & 7) * 4;
       const bool ok = f0 + r < d;
       cp_async16_zfill(xdst + (uint32_t)(r * 32 + s4) * 4u, ok ? xT + (int64_t)(f0 + r) * ldx + q2 * 32 + s4 : xT, ok);
@@ -94,23 +106,23 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
   };
   float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
   if (cok) bias4 = *reinterpret_cast<const float4*>(bd + c0);
-  float2 acc[8][2];
+  float2 acc[4][2];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) { acc[s][0] = make_float2(bias4.x, bias4.y); acc[s][1] = make_float2(bias4.z, bias4.w); }
+  for (int s = 0; s < 4; ++s) { acc[s][0] = make_float2(bias4.x, bias4.y); acc[s][1] = make_float2(bias4.z, bias4.w); }
   issue(0);
   for (int ch = 0; ch < nchunk; ++ch) {
     if (ch + 1 < nchunk) { issue(ch + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
     __syncthreads();
     const int nf = min(kDenseFch, d - ch * kDenseFch);
     const float* wt = wbuf + (ch & 1) * kDenseFch * 128 + 4 * lane;
-    const float* xt = xbuf + (ch & 1) * kDenseFch * 32 + 8 * w;
+    const float* xt = xbuf + (ch & 1) * kDenseFch * 32 + 4 * w;
+#pragma unroll 4
     for (int r = 0; r < nf; ++r) {
       const float4 w4 = *reinterpret_cast<const float4*>(wt + r * 128);
-      const float4 xa = *reinterpret_cast<const float4*>(xt + r * 32);
-      const float4 xb = *reinterpret_cast<const float4*>(xt + r * 32 + 4);
-      const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+      const float4 x4 = *reinterpret_cast<const float4*>(xt + r * 32);
+      const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
+      for (int s = 0; s < 4; ++s) {
         acc[s][0] = ffma2(bc2(xv[s]), make_float2(w4.x, w4.y), acc[s][0]);
         acc[s][1] = ffma2(bc2(xv[s]), make_float2(w4.z, w4.w), acc[s][1]);
       }
@@ -118,10 +130,10 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
     __syncthreads();                                         // stage ch & 1 is refilled next
   }
   if (!cok) return;
-  float hv[8][4];
+  float hv[4][4];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int b = q2 * 32 + 8 * w + s;
+  for (int s = 0; s < 4; ++s) {
+    const int b = q2 * 32 + 4 * w + s;
     const bool valid = b < B;
     hv[s][0] = valid ? fmaxf(acc[s][0].x, 0.0f) : 0.0f;
     hv[s][1] = valid ? fmaxf(acc[s][0].y, 0.0f) : 0.0f;
@@ -140,24 +152,22 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
   for (int u = 0; u < 4; ++u) {
     const int c = c0 + u;
     if (c >= m) break;
-    float* line = hd + (int64_t)c * cstride + q2 * 64 + 8 * w;
+    float* line = hd + (int64_t)c * cstride + q2 * 64 + 4 * w;
     *reinterpret_cast<float4*>(line) = make_float4(hv[0][u], hv[1][u], hv[2][u], hv[3][u]);
-    *reinterpret_cast<float4*>(line + 4) = make_float4(hv[4][u], hv[5][u], hv[6][u], hv[7][u]);
-    if (zero_dh) {
-      *reinterpret_cast<float4*>(line + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(line + 36) = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    if (zero_dh) *reinterpret_cast<float4*>(line + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
 // Backward + Adam: dz[b][c] = dh[b][c] * [h[b][c] > 0] (ReLU'(0) = 0, R26);
 // dWd[f][c] = sum_b xT[f][b] dz[b][c] (b ascending), dbd[c] = sum_b dz[b][c]; then Adam
-// (R6) over Wd and bd with those gradients.  CTA = 128 threads -> 128 columns x
-// 64 features: lane -> 4 columns, warp w -> features f0 + 16w .. + 15 (four groups of 4
-// rows, 64 accumulators).  Per 32-sample chunk the CTA stages dz [32][128] (from the h|dh
-// lines of hd) and xT [64][32] in shared memory.  CTAs with blockIdx.y == 0 also do the
-// bias (warp 0).  Gradients are stored to dWd/dbd when those are non-null.
-constexpr int kDenseBwdThreads = 128, kDenseBwdRows = 64;
+// (R6) over Wd and bd with those gradients.  CTA = 256 threads -> 128 columns x
+// 32 features: lane -> 4 columns, warp w -> features fb + 4w .. + 3 (16 accumulators).
+// The thread's 4 x 3 float4 of Wd / mWd / vWd are loaded at kernel entry, so their HBM
+// latency overlaps the staging and the FMAs (this kernel streams 24 B per weight and is
+// HBM-bound).  Per 32-sample chunk the CTA stages dz [32][128] (from the h|dh lines of hd)
+// and xT [32][32] in shared memory.  CTAs with blockIdx.y == 0 also do the bias (warp 0).
+// Gradients are stored to dWd/dbd when those are non-null.
+constexpr int kDenseBwdThreads = 256, kDenseBwdRows = 32;
 __global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
     float* __restrict__ Wd, float* __restrict__ mWd, float* __restrict__ vWd, float* __restrict__ bd,
     float* __restrict__ mbd, float* __restrict__ vbd, const float* __restrict__ xT, int d, int m, int ldw, int ldx,
@@ -167,16 +177,25 @@ __global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
   __shared__ __align__(16) float xs[kDenseBwdRows][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int ct = blockIdx.x * 128, c0 = ct + 4 * lane;
-  const int fb = blockIdx.y * kDenseBwdRows, fw = fb + 16 * w;
+  const int fb = blockIdx.y * kDenseBwdRows, fw = fb + 4 * w;
   const bool cok = c0 < ldw;
   const bool do_bias = blockIdx.y == 0 && w == 0;
-  float2 acc[16][2];
+  float4 P[4], Mo[4], Ve[4];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
+  for (int r = 0; r < 4; ++r) {                       // prefetch this thread's Adam operands
+    P[r] = Mo[r] = Ve[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cok && fw + r < d) {
+      const int64_t o = (int64_t)(fw + r) * ldw + c0;
+      P[r] = ld_na4(Wd + o); Mo[r] = ld_na4(mWd + o); Ve[r] = ld_na4(vWd + o);
+    }
+  }
+  float2 acc[4][2];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
   float db[4] = {0.f, 0.f, 0.f, 0.f};
   for (int q2 = 0; q2 < nb; ++q2) {
     __syncthreads();
-    {   // dz tile: thread t <-> column ct + t (32 h + 32 dh floats of its 256-B line)
+    if (threadIdx.x < 128) {   // dz tile: thread t <-> column ct + t (32 h + 32 dh floats of its 256-B line)
       const int c = ct + threadIdx.x;
       const float* line = hd + (int64_t)c * cstride + q2 * 64;
 #pragma unroll
@@ -188,15 +207,19 @@ __global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
         dzs[s4 + 2][threadIdx.x] = hv.z > 0.0f ? gv.z : 0.0f;
         dzs[s4 + 3][threadIdx.x] = hv.w > 0.0f ? gv.w : 0.0f;
       }
-    }
-    for (int e = threadIdx.x; e < kDenseBwdRows * 8; e += kDenseBwdThreads) {
-      const int r = e >> 3, s4 = (e & 7) * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (fb + r < d) v = *reinterpret_cast<const float4*>(xT + (int64_t)(fb + r) * ldx + q2 * 32 + s4);
-      *reinterpret_cast<float4*>(&xs[r][s4]) = v;
+    } else {
+      const int e = threadIdx.x - 128;                  // 32 rows x 8 float4 = 256 float4, 2 per thread
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int ee = e + 128 * u, r = ee >> 3, s4 = (ee & 7) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (fb + r < d) v = *reinterpret_cast<const float4*>(xT + (int64_t)(fb + r) * ldx + q2 * 32 + s4);
+        *reinterpret_cast<float4*>(&xs[r][s4]) = v;
+      }
     }
     __syncthreads();
     if (!cok) continue;
+#pragma unroll 2
     for (int b4 = 0; b4 < 32; b4 += 4) {
       float4 dz4[4];
 #pragma unroll
@@ -209,8 +232,8 @@ __global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
         }
       }
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const float4 x4 = *reinterpret_cast<const float4*>(&xs[16 * w + r][b4]);
+      for (int r = 0; r < 4; ++r) {
+        const float4 x4 = *reinterpret_cast<const float4*>(&xs[4 * w + r][b4]);
         const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {   // b = b4 + u ascending
@@ -222,22 +245,19 @@ __global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
   }
   if (!cok) return;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) {
+  for (int r = 0; r < 4; ++r) {
     const int f = fw + r;
     if (f >= d) continue;
     const int64_t o = (int64_t)f * ldw + c0;
-    float4 p = *reinterpret_cast<const float4*>(Wd + o);
-    float4 mo = *reinterpret_cast<const float4*>(mWd + o);
-    float4 ve = *reinterpret_cast<const float4*>(vWd + o);
     const float4 g = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
     if (dWd != nullptr) *reinterpret_cast<float4*>(dWd + o) = g;
-    adam_update(p.x, mo.x, ve.x, g.x, adam);
-    adam_update(p.y, mo.y, ve.y, g.y, adam);
-    adam_update(p.z, mo.z, ve.z, g.z, adam);
-    adam_update(p.w, mo.w, ve.w, g.w, adam);
-    *reinterpret_cast<float4*>(Wd + o) = p;
-    *reinterpret_cast<float4*>(mWd + o) = mo;
-    *reinterpret_cast<float4*>(vWd + o) = ve;
+    adam_update(P[r].x, Mo[r].x, Ve[r].x, g.x, adam);
+    adam_update(P[r].y, Mo[r].y, Ve[r].y, g.y, adam);
+    adam_update(P[r].z, Mo[r].z, Ve[r].z, g.z, adam);
+    adam_update(P[r].w, Mo[r].w, Ve[r].w, g.w, adam);
+    st_na4(Wd + o, P[r]);
+    st_na4(mWd + o, Mo[r]);
+    st_na4(vWd + o, Ve[r]);
   }
   if (do_bias) {
     float4 p = *reinterpret_cast<const float4*>(bd + c0);

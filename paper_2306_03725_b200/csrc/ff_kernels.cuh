@@ -51,6 +51,7 @@ struct RowArgs {
   AdamArgs adam;
   uint32_t check_finite;
   int sqh;                    // loss: 0 = BCE, 1 = squared hinge (exact zeros skipped)
+  uint32_t split;             // CSC modes: columns c < split get their dh by red (hybrid), the rest by the pull
 };
 
 // Loss gradient of one score and its loss term (BCE or squared hinge).
@@ -354,6 +355,14 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
         if (CSC) {
           // CSC mode: publish g[., j] (one 128-B line per chunk); dh is pulled later (k_dh_csc)
           st_hint(a.gT + ((j - jb) * nb + q2) * 32 + 4 * bq + gq, g, pol_l);
+          if (a.split != 0u) {                        // hybrid: columns < split by red
+            const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
+#pragma unroll
+            for (int q = 0; q < NG; ++q) {
+              if ((FULL || 4 * q + gq < k) && gnz && cs[q] < a.split)
+                red_add4(col_line(hb, cs[q], cfl) + 32, dh_contrib(ws[q], g4), pol_l);
+            }
+          }
         } else {
           // Alg. 2 with the pre-update weights: dh[b][idx[j][i]] += W[j][i] g[b][j], skipping
           // this lane's reductions when its 4 gradients are exactly zero
@@ -376,7 +385,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       for (int e = 0; e < KPL; ++e) {
         if (!act[e]) continue;
         const int64_t r = row + lane + 32 * e;
-        if (CSC) a.wcsc[pe[e]] = gany ? w[e] : 0.0f;
+        if (CSC && (uint32_t)c[e] >= a.split) a.wcsc[pe[e]] = gany ? w[e] : 0.0f;
         if (MODE == kModeBackward || STORE_GRADS) a.dW[r] = gW[e];
         if (MODE == kModeTrain) {
           adam_update(w[e], mw[e], vw[e], gW[e], a.adam);
@@ -412,14 +421,15 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 // Same arithmetic (the shared row_* helpers, same order) as k_rows: bit-identical results.
 // Measured (Amazon-670K): CSC mode is latency/LSU-bound and prefers D = 2 with
 // 6 CTAs/SM; atomic mode is bound by the L1->XBAR red path and is insensitive (D = 3, 4 CTAs).
-template <bool CSC> struct RingCfg {
-  static constexpr int D = CSC ? 2 : 3;                 // ring stages per warp
-  static constexpr int kMinBlocks = CSC ? 6 : 4;        // CTAs per SM (register budget)
+// MODE: 0 = atomic dh, 1 = CSC pull, 2 = hybrid (columns < split by red, the rest pulled)
+template <int MODE> struct RingCfg {
+  static constexpr int D = MODE == 1 ? 2 : 3;           // ring stages per warp
+  static constexpr int kMinBlocks = MODE == 1 ? 6 : 4;  // CTAs per SM (register budget)
 };
 constexpr int kRingThreads = 128;
 constexpr int kRingStageBytes = 8 * 32 * 16;            // 8 registers x 32 lanes x 16 B = 32 h lines
-template <bool CSC>
-constexpr int ring_smem() { return (kRingThreads / 32) * RingCfg<CSC>::D * kRingStageBytes; }
+template <int MODE>
+constexpr int ring_smem() { return (kRingThreads / 32) * RingCfg<MODE>::D * kRingStageBytes; }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
@@ -433,9 +443,10 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
   return v;
 }
 
-template <bool STORE_GRADS, bool CSC>
-__global__ void __launch_bounds__(kRingThreads, RingCfg<CSC>::kMinBlocks) k_train_ring(RowArgs a) {
-  constexpr int NG = 8, D = RingCfg<CSC>::D;
+template <bool STORE_GRADS, int MODE>
+__global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_train_ring(RowArgs a) {
+  constexpr int NG = 8, D = RingCfg<MODE>::D;
+  constexpr bool CSC = MODE != 0, HYB = MODE == 2;
   constexpr uint32_t kColFloats = 64;                   // hd column stride at nb = 1 (h | dh lines)
   extern __shared__ __align__(16) unsigned char ring_smem[];
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
@@ -450,6 +461,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<CSC>::kMinBlocks) k_trai
   const int* const idx = a.idx; const int* const pos = a.pos;
   const float grad_scale = a.grad_scale;
   const bool want_loss = a.loss != nullptr, check = a.check_finite != 0, sqh = a.sqh != 0;
+  const uint32_t split = a.split;
   const int64_t jb = a.j_begin, je = a.j_end;
   const int br = a.br;
   const int b = 4 * bq + gq;                            // this lane's own sample
@@ -561,7 +573,15 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<CSC>::kMinBlocks) k_trai
     for (int q = 0; q < NG; ++q) dwp[q] = dw_partial(g4, hv[q]);
     if (CSC) {
       st_hint(a.gT + (size_t)((j - jb32) * 32u + b), g, pol_l);
-      a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;      // 0: column pass skips (w*g == 0)
+      if (!HYB || (uint32_t)st.c >= split) a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;   // 0: column pass skips
+      if (HYB) {                                         // hybrid: columns < split by red
+        const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          const uint32_t c = (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq);
+          if (gnz && c < split) red_add4(col_line(hb, c, kColFloats) + 32, dh_contrib(ws[q], g4), pol_l);
+        }
+      }
     } else {
       const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
@@ -613,7 +633,8 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<CSC>::kMinBlocks) k_trai
 template <bool NB1>
 __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr, const int* __restrict__ ent_row,
                                                 const float* __restrict__ wcsc, const float* __restrict__ gT,
-                                                int m, int nb_rt, int tile, int64_t j_begin, float* __restrict__ hd) {
+                                                int m, int nb_rt, int tile, int64_t j_begin, float* __restrict__ hd,
+                                                int c_begin) {
   const int nb = NB1 ? 1 : nb_rt;
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -621,7 +642,7 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
   const int* cp = col_ptr + (int64_t)tile * m;
   const int jb = (int)j_begin;
   const uint32_t gstride = 32u * (uint32_t)nb;               // floats per gT row
-  for (int c = (int)global_warp(); c < m; c += nw) {
+  for (int c = c_begin + (int)global_warp(); c < m; c += nw) {
     const int p0 = cp[c], p1 = cp[c + 1];
     for (int q2 = 0; q2 < nb; ++q2) {
       const float* gb = gT + q2 * 32 + 4 * bq;                // this lane's slice of chunk q2

@@ -87,7 +87,7 @@ Layout layout_of(const ff_config& c) {
   o.lbl_stage = take(4 * ((size_t)c.max_batch + 1 + nnz));
   o.dh_stage = take(4 * (size_t)c.max_batch * m);
   o.scalars = take(kAlign);       // [0] int err, [1] float loss
-  if (c.dh_mode == FF_DH_CSC) {
+  if (c.dh_mode != FF_DH_ATOMIC) {          // CSC and hybrid
     o.ent_row = take(4 * Lk); o.pos = take(4 * Lk); o.wcsc = take(4 * Lk); o.sort_keys = take(4 * Lk);
     // tiles are >= cap/2 rows (create rounds the cap down to whole row-kernel waves, or keeps it)
     const size_t lt = csc_tile_cap(c), ntile = (2 * L + lt - 1) / lt + 1;
@@ -115,9 +115,10 @@ ff_status validate(const ff_config* c) {
   if (c->max_topk < 1 || c->max_topk > FF_MAX_TOPK)
     return fail(FF_ERR_CONFIG, "max_topk=%d outside [1, %d]", c->max_topk, FF_MAX_TOPK);
   if (c->max_nnz < 0) return fail(FF_ERR_CONFIG, "max_nnz < 0");
-  if (c->dh_mode != FF_DH_ATOMIC && c->dh_mode != FF_DH_CSC)
-    return fail(FF_ERR_CONFIG, "dh_mode=%d is neither FF_DH_ATOMIC nor FF_DH_CSC", c->dh_mode);
-  if (c->dh_mode == FF_DH_CSC && c->L_local * (int64_t)c->k >= (int64_t(1) << 31))
+  if (c->dh_mode != FF_DH_ATOMIC && c->dh_mode != FF_DH_CSC && c->dh_mode != FF_DH_HYBRID)
+    return fail(FF_ERR_CONFIG, "dh_mode=%d is not FF_DH_ATOMIC, FF_DH_CSC or FF_DH_HYBRID", c->dh_mode);
+  if (!(c->hybrid_frac >= 0.0f && c->hybrid_frac <= 1.0f)) return fail(FF_ERR_CONFIG, "hybrid_frac outside [0, 1]");
+  if (c->dh_mode != FF_DH_ATOMIC && c->L_local * (int64_t)c->k >= (int64_t(1) << 31))
     return fail(FF_ERR_CONFIG, "CSC mode needs L_local*k < 2^31");
   if (c->prune_frac < 0.0f || c->prune_frac >= 1.0f) return fail(FF_ERR_CONFIG, "prune_frac outside [0, 1)");
   if (c->loss != FF_LOSS_BCE && c->loss != FF_LOSS_SQH) return fail(FF_ERR_CONFIG, "loss=%d unknown", c->loss);
@@ -134,6 +135,7 @@ ff_config with_defaults(const ff_config& in) {
   if (c.prune_frac == 0.0f) c.prune_frac = 0.1f;
   if (c.init_scale == 0.0f) c.init_scale = (float)(1.0 / std::sqrt((double)c.k));
   if (c.max_nnz == 0) c.max_nnz = 64 * c.max_batch;
+  if (c.hybrid_frac == 0.0f) c.hybrid_frac = 0.5f;
   return c;
 }
 
@@ -149,7 +151,8 @@ struct ff_layer {
   float *wcsc, *gT;
   int* sort_keys;
   void* sort_tmp;
-  bool csc;
+  bool csc;                         // CSC or hybrid dh
+  uint32_t split;                   // hybrid: columns [0, split) by red, [split, m) by the CSC pull; else 0
   int grid_csc;
   int64_t tile_rows;                // CSC mode: labels per tile (multiple of 32)
   int ntiles;
@@ -164,6 +167,8 @@ struct ff_layer {
 };
 
 namespace {
+
+int ring_mode(const ff_layer* l) { return !l->csc ? 0 : l->split > 0 ? 2 : 1; }
 
 template <typename T>
 T* at(char* base, size_t off) { return reinterpret_cast<T*>(base + off); }
@@ -209,6 +214,7 @@ RowArgs row_args(ff_layer* l, int B) {
   a.j_begin = 0; a.j_end = l->cfg.L_local;
   a.check_finite = (l->cfg.flags & FF_FLAG_CHECK_FINITE) ? 1u : 0u;
   a.sqh = l->cfg.loss == FF_LOSS_SQH ? 1 : 0;
+  a.split = l->split;
   return a;
 }
 
@@ -236,11 +242,15 @@ const void* predict_kernel(int k) {
 }
 
 // Pipelined fused step (k = 32, B <= 32): same arithmetic as k_rows<train>, more gathers in flight.
-const void* ring_kernel(bool sg, bool csc) {
-  if (sg) return csc ? (const void*)k_train_ring<true, true> : (const void*)k_train_ring<true, false>;
-  return csc ? (const void*)k_train_ring<false, true> : (const void*)k_train_ring<false, false>;
+// ring kernel MODE: 0 atomic, 1 CSC, 2 hybrid
+int ring_mode(const ff_layer* l);
+const void* ring_kernel(bool sg, int mode) {
+  if (sg) return mode == 2 ? (const void*)k_train_ring<true, 2> : mode == 1 ? (const void*)k_train_ring<true, 1>
+                                                                           : (const void*)k_train_ring<true, 0>;
+  return mode == 2 ? (const void*)k_train_ring<false, 2> : mode == 1 ? (const void*)k_train_ring<false, 1>
+                                                                     : (const void*)k_train_ring<false, 0>;
 }
-int ring_smem_of(bool csc) { return csc ? ring_smem<true>() : ring_smem<false>(); }
+int ring_smem_of(int mode) { return mode == 2 ? ring_smem<2>() : mode == 1 ? ring_smem<1>() : ring_smem<0>(); }
 
 ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads = kRowThreads, int smem = 0) {
   void* args[] = {&a};
@@ -262,10 +272,10 @@ bool ptr_ok(const void* p, int64_t n) { return n == 0 || p != nullptr; }
 ff_status launch_dh_csc(ff_layer* l, int B, int tile, cudaStream_t st) {
   if (B <= 32)
     k_dh_csc<true><<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent_row, l->wcsc, l->gT, l->cfg.m, 1, tile,
-                                                 (int64_t)tile * l->tile_rows, l->hd);
+                                                 (int64_t)tile * l->tile_rows, l->hd, (int)l->split);
   else
     k_dh_csc<false><<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent_row, l->wcsc, l->gT, l->cfg.m, nb_of(B), tile,
-                                                  (int64_t)tile * l->tile_rows, l->hd);
+                                                  (int64_t)tile * l->tile_rows, l->hd, (int)l->split);
   FF_LAUNCHED();
   return FF_OK;
 }
@@ -351,7 +361,8 @@ ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t*
   if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
   if ((!hd_ready && (!ptr_ok(h, B) || !ptr_ok(dh, B))) || lbl_ptr == nullptr)
     return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
-  ff_status s = launch_prep(l, hd_ready ? nullptr : h, B, !l->csc && !hd_ready, lbl_ptr, lbl_ids, loss, st);
+  ff_status s = launch_prep(l, hd_ready ? nullptr : h, B, (!l->csc || l->split > 0) && !hd_ready, lbl_ptr, lbl_ids,
+                            loss, st);
   if (s != FF_OK) return s;
   l->t += 1;
   RowArgs a = row_args(l, B);
@@ -361,7 +372,8 @@ ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t*
   const bool sg = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
   const bool pipe = l->cfg.k == 32 && B <= 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE);
   if (pipe) {
-    s = run_rows(l, ring_kernel(sg, l->csc), l->grid_ring, a, B, st, kRingThreads, ring_smem_of(l->csc));
+    const int rm = ring_mode(l);
+    s = run_rows(l, ring_kernel(sg, rm), l->grid_ring, a, B, st, kRingThreads, ring_smem_of(rm));
   } else {
     const void* fn = sg ? row_kernel<kModeTrain, true>(l->cfg.k, l->csc) : row_kernel<kModeTrain, false>(l->cfg.k, l->csc);
     s = run_rows(l, fn, l->grid_train, a, B, st, kRowThreads);
@@ -548,7 +560,9 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->h_stage = at<float>(ws, lay.h_stage); l->lbl_stage = at<int>(ws, lay.lbl_stage);
   l->dh_stage = at<float>(ws, lay.dh_stage);
   l->err = at<int>(ws, lay.scalars); l->loss_scratch = at<float>(ws, lay.scalars + 4);
-  l->csc = c.dh_mode == FF_DH_CSC;
+  l->csc = c.dh_mode != FF_DH_ATOMIC;
+  l->split = c.dh_mode == FF_DH_HYBRID
+                 ? (uint32_t)std::min<double>(c.m, std::floor((double)c.hybrid_frac * (double)c.m + 0.5)) : 0u;
   if (l->csc) {
     l->ent_row = at<int>(ws, lay.ent_row); l->pos = at<int>(ws, lay.pos); l->wcsc = at<float>(ws, lay.wcsc);
     l->gT = at<float>(ws, lay.gT); l->col_ptr = at<int>(ws, lay.col_ptr); l->sort_tmp = ws + lay.sort_tmp;
@@ -564,13 +578,13 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k, l->csc), l->nsm, kRowThreads);
   l->grid_csc = occupancy_grid((const void*)k_dh_csc<true>, l->nsm, 256);
   for (int sg = 0; sg < 2; ++sg)
-    for (int cs = 0; cs < 2; ++cs)
+    for (int cs = 0; cs < 3; ++cs)
       if (cudaFuncSetAttribute(ring_kernel(sg, cs), cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem_of(cs)) !=
           cudaSuccess) {
         delete l;
         return fail(FF_ERR_CUDA, "pipelined kernel smem attribute");
       }
-  l->grid_ring = occupancy_grid(ring_kernel(false, l->csc), l->nsm, kRingThreads, ring_smem_of(l->csc));
+  l->grid_ring = occupancy_grid(ring_kernel(false, ring_mode(l)), l->nsm, kRingThreads, ring_smem_of(ring_mode(l)));
   if (l->csc) {
     // tile = a whole number of row-kernel "waves" (warps x 32 labels) within the L2 budget
     const int64_t cap = (int64_t)csc_tile_cap(c), wave = (int64_t)l->grid_train * (kRowThreads / 32) * 32;
@@ -682,7 +696,7 @@ ff_status fixedfanin_backward(ff_layer* l, const float* h, const float* y, int32
   if (!ptr_ok(h, B) || !ptr_ok(dh, B) || lbl_ptr == nullptr || (B > 0 && l->cfg.L_local > 0 && !y))
     return fail(FF_ERR_ARG, "null h/y/dh/lbl_ptr");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  ff_status s = launch_prep(l, h, B, !l->csc, lbl_ptr, lbl_ids, loss, st);
+  ff_status s = launch_prep(l, h, B, !l->csc || l->split > 0, lbl_ptr, lbl_ids, loss, st);
   if (s != FF_OK) return s;
   RowArgs a = row_args(l, B);
   a.y_in = y; a.grad_scale = grad_scale; a.loss = loss;

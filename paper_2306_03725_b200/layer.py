@@ -19,7 +19,7 @@ FF_OK, FF_ERR_ARG, FF_ERR_CONFIG, FF_ERR_RANGE, FF_ERR_NONFINITE, FF_ERR_CUDA, F
 FF_FLAG_CHECK_FINITE = 1
 FF_FLAG_STORE_GRADS = 2
 FF_FLAG_NO_PIPE = 4
-FF_DH_ATOMIC, FF_DH_CSC = 0, 1
+FF_DH_ATOMIC, FF_DH_CSC, FF_DH_HYBRID = 0, 1, 2
 FF_LOSS_BCE, FF_LOSS_SQH = 0, 1
 FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 64, 1024, 8
 _STATUS = {1: "FF_ERR_ARG", 2: "FF_ERR_CONFIG", 3: "FF_ERR_RANGE", 4: "FF_ERR_NONFINITE", 5: "FF_ERR_CUDA",
@@ -54,7 +54,7 @@ class ff_config(ctypes.Structure):
         ("max_topk", ctypes.c_int32), ("max_nnz", ctypes.c_int32), ("dh_mode", ctypes.c_int32),
         ("seed", ctypes.c_uint64), ("init_scale", ctypes.c_float), ("beta1", ctypes.c_float),
         ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("prune_frac", ctypes.c_float),
-        ("flags", ctypes.c_uint32), ("loss", ctypes.c_int32),
+        ("flags", ctypes.c_uint32), ("loss", ctypes.c_int32), ("hybrid_frac", ctypes.c_float),
     ]
 
 
@@ -166,12 +166,13 @@ class LayerConfig:
     prune_frac: float = 0.1
     flags: int = 0
     loss: int = FF_LOSS_BCE
+    hybrid_frac: float = 0.0
 
     def c(self) -> ff_config:
         L_local = self.L_global - self.row_begin if self.L_local is None else self.L_local
         return ff_config(self.L_global, self.row_begin, L_local, self.m, self.k, self.max_batch, self.max_topk,
                          self.max_nnz, self.dh_mode, self.seed, self.init_scale, self.beta1, self.beta2, self.eps,
-                         self.prune_frac, self.flags, self.loss)
+                         self.prune_frac, self.flags, self.loss, self.hybrid_frac)
 
 
 def workspace_size(cfg: LayerConfig) -> int:

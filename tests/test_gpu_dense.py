@@ -161,7 +161,7 @@ def test_model_step_equals_composed_calls(dh_mode):
         assert np.allclose(d1["Wd"], d2["Wd"], rtol=1e-5, atol=1e-6)
 
 
-@pytest.mark.parametrize("dh_mode", [0, 1])
+@pytest.mark.parametrize("dh_mode", [0, 1, 2])
 def test_model_step_lockstep_vs_oracle(dh_mode):
     """One whole-architecture step vs oracle.model_train_step from the GPU's state: loss, the
     sparse layer's and the dense layer's gradients (R19), then Adam on those gradients."""

@@ -118,7 +118,7 @@ def test_forward_parity(L, m, k, B):
     assert_close(y, yr, Ay, "y")
 
 
-DH = pytest.mark.parametrize("dh_mode", [0, 1], ids=["atomic", "csc"])
+DH = pytest.mark.parametrize("dh_mode", [0, 1, 2], ids=["atomic", "csc", "hybrid"])
 
 
 LOSS = pytest.mark.parametrize("loss", ["bce", "sqh"])
@@ -461,7 +461,7 @@ def test_csc_dh_is_deterministic_and_matches_atomic():
     assert dh_close(d1, d3)
 
 
-@pytest.mark.parametrize("shape_name,dh_modes", [("wiki10-31k", (0,)), ("wiki-500k", (0,)), ("amazon-670k", (1, 0)),
+@pytest.mark.parametrize("shape_name,dh_modes", [("wiki10-31k", (0,)), ("wiki-500k", (0,)), ("amazon-670k", (1, 0, 2)),
                                                   ("amazon-3m", (1, 0)), ("amazon-670k-k64-m65k", (0, 1))])
 def test_full_size_sampled_parity(shape_name, dh_modes):
     """BASELINE.json's shapes in the bench's launch configuration: one fused step checked on
