@@ -162,9 +162,12 @@ ff_status fixedfanin_train_step(ff_layer* layer, const float* h, int32_t B,
                                 ff_stream_t stream);
 
 /* Same as train_step with HOST inputs/outputs (end-to-end path): copies h_host [B][m]
- * and the label CSR (host) into workspace staging, runs the fused step, then copies the
- * loss (and dh if dh_host != NULL) back.  Use pinned host memory for asynchrony; the
- * host outputs are valid after `stream` is synchronized.  lbl_ptr_host[B] <= max_nnz. */
+ * and the label CSR (host) into one of two workspace staging slots on a library-owned copy
+ * stream (so that, with pinned memory, the next call's copy overlaps this call's kernels;
+ * `stream` waits for the copy with an event), runs the fused step on `stream`, then copies
+ * the loss (and dh if dh_host != NULL) back on `stream`.  The host inputs must stay
+ * unmodified, and the host outputs are valid, once `stream` is synchronized.
+ * lbl_ptr_host[B] <= max_nnz (read on the host for the copy size).                      */
 ff_status fixedfanin_train_step_host(ff_layer* layer, const float* h_host, int32_t B,
                                      const int32_t* lbl_ptr_host, const int32_t* lbl_ids_host,
                                      float grad_scale, float lr, float* dh_host,

@@ -3,8 +3,10 @@
 // Fig. 2) -> ReLU (reading R18) -> the fixed fan-in layer.
 //
 // Layouts:
-//   Wd, mWd, vWd, dWd  f32 [d][ldw], ldw = m rounded up to 4 (16-B aligned rows; the pad
-//                      columns stay 0), input-feature major: one Wd row is contiguous in c;
+//   Wd, mWd, vWd, dWd  f32 tiled [ldw/128][d][128], ldw = m rounded up to 128 (the pad
+//                      columns stay 0): element (f, c) at ((c/128)*d + f)*128 + c%128, so a
+//                      CTA's 128-column tile over all features is one contiguous range of
+//                      HBM;
 //   bd, mbd, vbd, dbd  f32 [ldw];
 //   xT  f32 [d][ldx], ldx = 32*nb: the dropped-out, scaled features, transposed so that
 //       the 32 samples of one feature are one 128-B line (broadcast operand);
@@ -63,12 +65,15 @@ __global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, 
   }
 }
 
-// Forward: z[b][c] = bd[c] + sum_f xT[f][b] Wd[f][c] (f ascending, fp32 FMA chain, the
-// oracle's order), h = max(z, 0).  CTA = 256 threads -> 128 columns x 32 samples (chunk
-// blockIdx.y); lane -> 4 columns, warp w -> samples 4w..4w+3 (4 x 4 accumulators).  The Wd
-// tile (64 features x 128 columns, 32 KB) and the xT tile (64 x 32) of the next feature
-// chunk are copied into a second shared-memory stage (cp.async, 16 B per thread-copy)
-// while the current chunk is computed, so the HBM latency of Wd is hidden behind the FMAs.
+// Forward: z[b][c] = bd[c] + sum_f xT[f][b] Wd[f][c], h = max(z, 0).  CTA = 256 threads ->
+// 128 columns x 32 samples (chunk blockIdx.y).  The Wd tile (64 features x 128 columns,
+// 32 KB) and the xT tile (64 x 32) of the next feature chunk are copied into a second
+// shared-memory stage (cp.async) while the current chunk is computed, so the HBM latency of
+// Wd hides behind the FMAs.  Warp w: lane -> 4 columns, samples 8(w&3)..+7, and the first
+// (w < 4) or second (w >= 4) half of every chunk's 64 features: a thread's 32 accumulators
+// amortise each 16-B shared load of Wd over 8 samples (the kernel is bound by shared-memory
+// wavefronts, not FMAs).  The two halves are added at the end: z = (bd + sum over first
+// halves, f ascending) + (sum over second halves, f ascending) — a fixed order.
 constexpr int kDenseFwdThreads = 256, kDenseFch = 64;
 constexpr int kDenseFwdSmem = 2 * kDenseFch * (128 + 32) * 4;
 __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const float* src, bool ok) {
@@ -83,6 +88,7 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
   float* const wbuf = dsm;                                   // [2][64][128]
   float* const xbuf = dsm + 2 * kDenseFch * 128;             // [2][64][32]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q2 = blockIdx.y;
+  const int sg = w & 3, half = w >> 2;                       // samples 8sg..8sg+7; feature half
   const int ct = blockIdx.x * 128, c0 = ct + 4 * lane;
   const bool cok = c0 < ldw;
   const int nchunk = (d + kDenseFch - 1) / kDenseFch;
@@ -94,7 +100,8 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
     for (int u = 0; u < 8; ++u) {                           // 64 rows x 32 float4
       const int e = u * kDenseFwdThreads + threadIdx.x, r = e >> 5, cq = (e & 31) * 4;
       const bool ok = f0 + r < d && ct + cq < ldw;
-      cp_async16_zfill(wdst + (uint32_t)(r * 128 + cq) * 4u, ok ? Wd + (int64_t)(f0 + r) * ldw + ct + cq : Wd, ok);
+      cp_async16_zfill(wdst + (uint32_t)(r * 128 + cq) * 4u,
+                       ok ? Wd + ((int64_t)blockIdx.x * d + f0 + r) * 128 + cq : Wd, ok);
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {                           // 64 rows x 8 float4
@@ -105,40 +112,56 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
     cp_async_commit();
   };
   float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (cok) bias4 = *reinterpret_cast<const float4*>(bd + c0);
-  float2 acc[4][2];
+  if (cok && half == 0) bias4 = *reinterpret_cast<const float4*>(bd + c0);
+  float2 acc[8][2];
 #pragma unroll
-  for (int s = 0; s < 4; ++s) { acc[s][0] = make_float2(bias4.x, bias4.y); acc[s][1] = make_float2(bias4.z, bias4.w); }
+  for (int s = 0; s < 8; ++s) { acc[s][0] = make_float2(bias4.x, bias4.y); acc[s][1] = make_float2(bias4.z, bias4.w); }
   issue(0);
   for (int ch = 0; ch < nchunk; ++ch) {
     if (ch + 1 < nchunk) { issue(ch + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
     __syncthreads();
     const int nf = min(kDenseFch, d - ch * kDenseFch);
+    const int r0 = half * (kDenseFch / 2), r1 = min(nf, r0 + kDenseFch / 2);
     const float* wt = wbuf + (ch & 1) * kDenseFch * 128 + 4 * lane;
-    const float* xt = xbuf + (ch & 1) * kDenseFch * 32 + 4 * w;
+    const float* xt = xbuf + (ch & 1) * kDenseFch * 32 + 8 * sg;
 #pragma unroll 4
-    for (int r = 0; r < nf; ++r) {
+    for (int r = r0; r < r1; ++r) {
       const float4 w4 = *reinterpret_cast<const float4*>(wt + r * 128);
-      const float4 x4 = *reinterpret_cast<const float4*>(xt + r * 32);
-      const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+      const float4 xa = *reinterpret_cast<const float4*>(xt + r * 32);
+      const float4 xb = *reinterpret_cast<const float4*>(xt + r * 32 + 4);
+      const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
+      for (int s = 0; s < 8; ++s) {
         acc[s][0] = ffma2(bc2(xv[s]), make_float2(w4.x, w4.y), acc[s][0]);
         acc[s][1] = ffma2(bc2(xv[s]), make_float2(w4.z, w4.w), acc[s][1]);
       }
     }
     __syncthreads();                                         // stage ch & 1 is refilled next
   }
-  if (!cok) return;
-  float hv[4][4];
+  // second-half warps hand their partial sums to the first-half warps (stage buffers reused)
+  float* const part = dsm + (size_t)(w & 3) * 32 * 33;       // [lane][33] per sample group
+  if (half == 1) {
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int b = q2 * 32 + 4 * w + s;
+    for (int s = 0; s < 8; ++s) {
+      part[lane * 33 + 4 * s + 0] = acc[s][0].x; part[lane * 33 + 4 * s + 1] = acc[s][0].y;
+      part[lane * 33 + 4 * s + 2] = acc[s][1].x; part[lane * 33 + 4 * s + 3] = acc[s][1].y;
+    }
+  }
+  __syncthreads();
+  if (half == 1 || !cok) return;
+  float hv[8][4];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int b = q2 * 32 + 8 * sg + s;
     const bool valid = b < B;
-    hv[s][0] = valid ? fmaxf(acc[s][0].x, 0.0f) : 0.0f;
-    hv[s][1] = valid ? fmaxf(acc[s][0].y, 0.0f) : 0.0f;
-    hv[s][2] = valid ? fmaxf(acc[s][1].x, 0.0f) : 0.0f;
-    hv[s][3] = valid ? fmaxf(acc[s][1].y, 0.0f) : 0.0f;
+    const float z0 = __fadd_rn(acc[s][0].x, part[lane * 33 + 4 * s + 0]);
+    const float z1 = __fadd_rn(acc[s][0].y, part[lane * 33 + 4 * s + 1]);
+    const float z2 = __fadd_rn(acc[s][1].x, part[lane * 33 + 4 * s + 2]);
+    const float z3 = __fadd_rn(acc[s][1].y, part[lane * 33 + 4 * s + 3]);
+    hv[s][0] = valid ? fmaxf(z0, 0.0f) : 0.0f;
+    hv[s][1] = valid ? fmaxf(z1, 0.0f) : 0.0f;
+    hv[s][2] = valid ? fmaxf(z2, 0.0f) : 0.0f;
+    hv[s][3] = valid ? fmaxf(z3, 0.0f) : 0.0f;
     if (h_out != nullptr && valid) {
       float* hp = h_out + (int64_t)b * m + c0;
       if ((m & 3) == 0 && c0 + 3 < m) {                // 16-B aligned rows only
@@ -152,50 +175,42 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
   for (int u = 0; u < 4; ++u) {
     const int c = c0 + u;
     if (c >= m) break;
-    float* line = hd + (int64_t)c * cstride + q2 * 64 + 4 * w;
+    float* line = hd + (int64_t)c * cstride + q2 * 64 + 8 * sg;
     *reinterpret_cast<float4*>(line) = make_float4(hv[0][u], hv[1][u], hv[2][u], hv[3][u]);
-    if (zero_dh) *reinterpret_cast<float4*>(line + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(line + 4) = make_float4(hv[4][u], hv[5][u], hv[6][u], hv[7][u]);
+    if (zero_dh) {
+      *reinterpret_cast<float4*>(line + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(line + 36) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
 }
 
 // Backward + Adam: dz[b][c] = dh[b][c] * [h[b][c] > 0] (ReLU'(0) = 0, R26);
 // dWd[f][c] = sum_b xT[f][b] dz[b][c] (b ascending), dbd[c] = sum_b dz[b][c]; then Adam
-// (R6) over Wd and bd with those gradients.  CTA = 256 threads -> 128 columns x
-// 32 features: lane -> 4 columns, warp w -> features fb + 4w .. + 3 (16 accumulators).
-// The thread's 4 x 3 float4 of Wd / mWd / vWd are loaded at kernel entry, so their HBM
-// latency overlaps the staging and the FMAs (this kernel streams 24 B per weight and is
-// HBM-bound).  Per 32-sample chunk the CTA stages dz [32][128] (from the h|dh lines of hd)
-// and xT [32][32] in shared memory.  CTAs with blockIdx.y == 0 also do the bias (warp 0).
-// Gradients are stored to dWd/dbd when those are non-null.
-constexpr int kDenseBwdThreads = 256, kDenseBwdRows = 32;
-__global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
+// (R6) over Wd and bd with those gradients.  This kernel streams 24 B per weight
+// (read + write Wd, mWd, vWd) and is HBM-bound, so it is organised around keeping loads in
+// flight: CTA = 256 threads -> 128 columns x a range of features, walked in blocks of 16
+// features (lane -> 4 columns, warp w -> features 2w, 2w+1 of the block); the Adam operands
+// of block i+1 are loaded into registers while block i is reduced and updated.  dz [32][128]
+// (from the h|dh lines of hd) is staged in shared memory once per CTA (B <= 32; per block
+// and 32-sample chunk otherwise), xT per block.  CTAs with blockIdx.y == 0 also do the
+// bias (warp 0).  Gradients are stored to dWd/dbd when those are non-null.
+constexpr int kDenseBwdThreads = 256, kDenseBwdBlk = 16;
+__global__ void __launch_bounds__(kDenseBwdThreads, 2) k_dense_bwd_adam(
     float* __restrict__ Wd, float* __restrict__ mWd, float* __restrict__ vWd, float* __restrict__ bd,
     float* __restrict__ mbd, float* __restrict__ vbd, const float* __restrict__ xT, int d, int m, int ldw, int ldx,
     int nb, const float* __restrict__ hd, int cstride, AdamArgs adam, float* __restrict__ dWd,
-    float* __restrict__ dbd) {
+    float* __restrict__ dbd, int rows_per_cta) {
   __shared__ __align__(16) float dzs[32][128];
-  __shared__ __align__(16) float xs[kDenseBwdRows][32];
+  __shared__ __align__(16) float xs[kDenseBwdBlk][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int ct = blockIdx.x * 128, c0 = ct + 4 * lane;
-  const int fb = blockIdx.y * kDenseBwdRows, fw = fb + 4 * w;
+  const int f_lo = blockIdx.y * rows_per_cta, f_hi = min(d, f_lo + rows_per_cta);
+  const int nblk = f_hi > f_lo ? (f_hi - f_lo + kDenseBwdBlk - 1) / kDenseBwdBlk : 0;
   const bool cok = c0 < ldw;
-  const bool do_bias = blockIdx.y == 0 && w == 0;
-  float4 P[4], Mo[4], Ve[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {                       // prefetch this thread's Adam operands
-    P[r] = Mo[r] = Ve[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (cok && fw + r < d) {
-      const int64_t o = (int64_t)(fw + r) * ldw + c0;
-      P[r] = ld_na4(Wd + o); Mo[r] = ld_na4(mWd + o); Ve[r] = ld_na4(vWd + o);
-    }
-  }
-  float2 acc[4][2];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
-  float db[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int q2 = 0; q2 < nb; ++q2) {
-    __syncthreads();
-    if (threadIdx.x < 128) {   // dz tile: thread t <-> column ct + t (32 h + 32 dh floats of its 256-B line)
+  const bool bias_cta = blockIdx.y == 0;
+  auto stage_dz = [&](int q2) {
+    if (threadIdx.x < 128) {   // thread t <-> column ct + t (32 h + 32 dh floats of its 256-B line)
       const int c = ct + threadIdx.x;
       const float* line = hd + (int64_t)c * cstride + q2 * 64;
 #pragma unroll
@@ -207,59 +222,89 @@ __global__ void __launch_bounds__(kDenseBwdThreads) k_dense_bwd_adam(
         dzs[s4 + 2][threadIdx.x] = hv.z > 0.0f ? gv.z : 0.0f;
         dzs[s4 + 3][threadIdx.x] = hv.w > 0.0f ? gv.w : 0.0f;
       }
-    } else {
-      const int e = threadIdx.x - 128;                  // 32 rows x 8 float4 = 256 float4, 2 per thread
+    }
+  };
+  auto stage_x = [&](int fblk, int q2) {   // 16 rows x 8 float4, threads 128..255
+    if (threadIdx.x >= 128) {
+      const int e = threadIdx.x - 128, r = e >> 3, s4 = (e & 7) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (fblk + r < f_hi) v = *reinterpret_cast<const float4*>(xT + (int64_t)(fblk + r) * ldx + q2 * 32 + s4);
+      *reinterpret_cast<float4*>(&xs[r][s4]) = v;
+    }
+  };
+  float4 P[2], Mo[2], Ve[2], Pn[2], Mn[2], Vn[2];
+  auto load_ops = [&](int fblk, float4 (&p)[2], float4 (&mo)[2], float4 (&ve)[2]) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int ee = e + 128 * u, r = ee >> 3, s4 = (ee & 7) * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (fb + r < d) v = *reinterpret_cast<const float4*>(xT + (int64_t)(fb + r) * ldx + q2 * 32 + s4);
-        *reinterpret_cast<float4*>(&xs[r][s4]) = v;
+    for (int r = 0; r < 2; ++r) {
+      const int f = fblk + 2 * w + r;
+      p[r] = mo[r] = ve[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (cok && f < f_hi) {
+        const int64_t o = ((int64_t)blockIdx.x * d + f) * 128 + 4 * lane;   // tiled layout
+        p[r] = ld_na4(Wd + o); mo[r] = ld_na4(mWd + o); ve[r] = ld_na4(vWd + o);
       }
     }
-    __syncthreads();
-    if (!cok) continue;
-#pragma unroll 2
-    for (int b4 = 0; b4 < 32; b4 += 4) {
-      float4 dz4[4];
+  };
+  if (nblk > 0) load_ops(f_lo, P, Mo, Ve);
+  if (nb == 1) stage_dz(0);
+  float db[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int bi = 0; bi < nblk; ++bi) {
+    const int fblk = f_lo + bi * kDenseBwdBlk;
+    if (bi + 1 < nblk) load_ops(fblk + kDenseBwdBlk, Pn, Mn, Vn);
+    const bool do_bias = bias_cta && bi == 0 && w == 0;
+    float2 acc[2][2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dz4[u] = *reinterpret_cast<const float4*>(&dzs[b4 + u][4 * lane]);
-      if (do_bias) {
+    for (int r = 0; r < 2; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
+    for (int q2 = 0; q2 < nb; ++q2) {
+      __syncthreads();                                   // previous block's readers are done
+      if (nb > 1) stage_dz(q2);
+      stage_x(fblk, q2);
+      __syncthreads();
+      if (!cok) continue;
+#pragma unroll 4
+      for (int b4 = 0; b4 < 32; b4 += 4) {
+        float4 dz4[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {   // b ascending
-          db[0] = __fadd_rn(db[0], dz4[u].x); db[1] = __fadd_rn(db[1], dz4[u].y);
-          db[2] = __fadd_rn(db[2], dz4[u].z); db[3] = __fadd_rn(db[3], dz4[u].w);
+        for (int u = 0; u < 4; ++u) dz4[u] = *reinterpret_cast<const float4*>(&dzs[b4 + u][4 * lane]);
+        if (do_bias) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {   // b ascending
+            db[0] = __fadd_rn(db[0], dz4[u].x); db[1] = __fadd_rn(db[1], dz4[u].y);
+            db[2] = __fadd_rn(db[2], dz4[u].z); db[3] = __fadd_rn(db[3], dz4[u].w);
+          }
         }
-      }
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float4 x4 = *reinterpret_cast<const float4*>(&xs[4 * w + r][b4]);
-        const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+        for (int r = 0; r < 2; ++r) {
+          const float4 x4 = *reinterpret_cast<const float4*>(&xs[2 * w + r][b4]);
+          const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {   // b = b4 + u ascending
-          acc[r][0] = ffma2(bc2(xv[u]), make_float2(dz4[u].x, dz4[u].y), acc[r][0]);
-          acc[r][1] = ffma2(bc2(xv[u]), make_float2(dz4[u].z, dz4[u].w), acc[r][1]);
+          for (int u = 0; u < 4; ++u) {   // b = b4 + u ascending
+            acc[r][0] = ffma2(bc2(xv[u]), make_float2(dz4[u].x, dz4[u].y), acc[r][0]);
+            acc[r][1] = ffma2(bc2(xv[u]), make_float2(dz4[u].z, dz4[u].w), acc[r][1]);
+          }
         }
       }
     }
-  }
-  if (!cok) return;
+    if (cok) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int f = fw + r;
-    if (f >= d) continue;
-    const int64_t o = (int64_t)f * ldw + c0;
-    const float4 g = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
-    if (dWd != nullptr) *reinterpret_cast<float4*>(dWd + o) = g;
-    adam_update(P[r].x, Mo[r].x, Ve[r].x, g.x, adam);
-    adam_update(P[r].y, Mo[r].y, Ve[r].y, g.y, adam);
-    adam_update(P[r].z, Mo[r].z, Ve[r].z, g.z, adam);
-    adam_update(P[r].w, Mo[r].w, Ve[r].w, g.w, adam);
-    st_na4(Wd + o, P[r]);
-    st_na4(mWd + o, Mo[r]);
-    st_na4(vWd + o, Ve[r]);
+      for (int r = 0; r < 2; ++r) {
+        const int f = fblk + 2 * w + r;
+        if (f >= f_hi) continue;
+        const int64_t o = ((int64_t)blockIdx.x * d + f) * 128 + 4 * lane;   // tiled layout
+        const float4 g = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
+        if (dWd != nullptr) *reinterpret_cast<float4*>(dWd + o) = g;
+        adam_update(P[r].x, Mo[r].x, Ve[r].x, g.x, adam);
+        adam_update(P[r].y, Mo[r].y, Ve[r].y, g.y, adam);
+        adam_update(P[r].z, Mo[r].z, Ve[r].z, g.z, adam);
+        adam_update(P[r].w, Mo[r].w, Ve[r].w, g.w, adam);
+        st_na4(Wd + o, P[r]);
+        st_na4(mWd + o, Mo[r]);
+        st_na4(vWd + o, Ve[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) { P[r] = Pn[r]; Mo[r] = Mn[r]; Ve[r] = Vn[r]; }
   }
-  if (do_bias) {
+  if (bias_cta && w == 0 && cok && nblk > 0) {
     float4 p = *reinterpret_cast<const float4*>(bd + c0);
     float4 mo = *reinterpret_cast<const float4*>(mbd + c0);
     float4 ve = *reinterpret_cast<const float4*>(vbd + c0);
@@ -293,20 +338,32 @@ __global__ void k_dh_in(const float* __restrict__ dh, int B, int m, int nb, floa
 
 // Dense init (reading R27): Wd[f][c] = a * (2 * ((u >> 8) * 2^-24) - 1) in fp32, u = word c
 // of the stream (ctr = (c/4, f, 0, 4), key = seed); pad columns and bd, moments = 0.
+// Thread per (tile, feature, 4 columns), tiled layout.
 __global__ void k_dense_init(float* __restrict__ Wd, int d, int m, int ldw, uint32_t key0, uint32_t key1, float a) {
-  const int nq = ldw / 4;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)d * nq;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(e / nq), q = (int)(e % nq);
-    const U4 v = philox((uint32_t)q, (uint32_t)f, 0u, 4u, key0, key1);
+  const int64_t n4 = (int64_t)d * (ldw / 4);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / ((int64_t)d * 32);
+    const int f = (int)((e / 32) % d), cq = (int)(e % 32);
+    const int c = (int)t * 128 + 4 * cq;
+    const U4 v = philox((uint32_t)(c / 4), (uint32_t)f, 0u, 4u, key0, key1);
     float out[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const float unit = __fmul_rn((float)(word_of(v, u) >> 8), 1.0f / 16777216.0f);
       const float centered = __fsub_rn(__fmul_rn(2.0f, unit), 1.0f);
-      out[u] = 4 * q + u < m ? __fmul_rn(a, centered) : 0.0f;
+      out[u] = c + u < m ? __fmul_rn(a, centered) : 0.0f;
     }
-    *reinterpret_cast<float4*>(Wd + (int64_t)f * ldw + 4 * q) = make_float4(out[0], out[1], out[2], out[3]);
+    *reinterpret_cast<float4*>(Wd + e * 4) = make_float4(out[0], out[1], out[2], out[3]);
+  }
+}
+
+// user [d][m] <-> tiled [ldw/128][d][128] (set/get_params, get_grads); pad columns untouched
+__global__ void k_dense_retile(const float* __restrict__ src, float* __restrict__ dst, int d, int m, int to_tiled) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)d * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)(e / m), c = (int)(e % m);
+    const int64_t t = ((int64_t)(c >> 7) * d + f) * 128 + (c & 127);
+    if (to_tiled) dst[t] = src[e]; else dst[e] = src[t];
   }
 }
 

@@ -1038,9 +1038,13 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   constexpr int NG = 8, D = kPredRingD;
   constexpr uint32_t kColFloats = 64, kStage = 8 * 32 * 16;
   extern __shared__ __align__(16) unsigned char ring_smem[];
+  // per-warp candidate buffer [slot][lane] while scoring (conflict-free), reused as the
+  // block-merge lists [lane][q] at the end (same per-warp 1-KB regions)
   __shared__ float ss[kPredRingThreads / 32][32][kTopkMax];
   __shared__ int si[kPredRingThreads / 32][32][kTopkMax];
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7, wid = threadIdx.x >> 5;
+  float* const cbs = &ss[wid][0][0];
+  int* const cbi = &si[wid][0][0];
   const uint32_t nwarp = (uint32_t)(((int64_t)gridDim.x * blockDim.x) >> 5);
   const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring_smem) + (uint32_t)wid * D * kStage + (uint32_t)lane * 16u;
   const float* const hb = hd + 4 * bq;
@@ -1049,6 +1053,13 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll
   for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
+  float thr_s = -INFINITY; int thr_i = INT_MAX;        // the lane's current K-th best
+  int ncand = 0;
+  auto flush = [&]() {
+    for (int q = 0; q < ncand; ++q) topk_consider(ts, ti, cbs[q * 32 + lane], cbi[q * 32 + lane]);
+    ncand = 0;
+    thr_s = ts[kTopkMax - 1]; thr_i = ti[kTopkMax - 1];
+  };
 
   struct St { float w, bj; int c; };
   auto load_st = [&](uint32_t j, St& st) {
@@ -1094,10 +1105,16 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
 #pragma unroll
     for (int q = 0; q < NG; ++q) ws[q] = __shfl_sync(kFull, st.w, 4 * q + gq);
     const float y = row_score_own<NG>(ws, hv, gq, st.bj);
-    if (b < B) topk_consider(ts, ti, y, (int)(row_begin + j));
+    // candidates better than the lane's current K-th best are appended to its buffer (no
+    // divergent insertion per row); a full buffer in any lane flushes the warp's buffers
+    const int jid = (int)(row_begin + j);
+    if (b < B && better(y, jid, thr_s, thr_i)) { cbs[ncand * 32 + lane] = y; cbi[ncand * 32 + lane] = jid; ++ncand; }
+    if (__any_sync(kFull, ncand == kTopkMax)) flush();
     stg = stg + 1 == (uint32_t)D ? 0u : stg + 1;
   }
   cp_async_wait<0>();
+  flush();
+  __syncwarp();
 #pragma unroll
   for (int q = 0; q < kTopkMax; ++q) { ss[wid][lane][q] = ts[q]; si[wid][lane][q] = ti[q]; }
   __syncthreads();

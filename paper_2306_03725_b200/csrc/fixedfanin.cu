@@ -83,8 +83,8 @@ Layout layout_of(const ff_config& c) {
   o.hd = take(8 * m * ldh);         // [m][nb][h 32 | dh 32]
   o.cand_s = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
   o.cand_i = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
-  o.h_stage = take(4 * (size_t)c.max_batch * m);
-  o.lbl_stage = take(4 * ((size_t)c.max_batch + 1 + nnz));
+  o.h_stage = take(2 * 4 * (size_t)c.max_batch * m);                 // double-buffered (host entry point)
+  o.lbl_stage = take(2 * 4 * ((size_t)c.max_batch + 1 + nnz));
   o.dh_stage = take(4 * (size_t)c.max_batch * m);
   o.scalars = take(kAlign);       // [0] int err, [1] float loss
   if (c.dh_mode != FF_DH_ATOMIC) {          // CSC and hybrid
@@ -163,6 +163,11 @@ struct ff_layer {
   int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring, grid_pred_ring;
   int nsm;
   std::vector<cudaEvent_t> prof_ev;   // pairs (before, after) of the fused row kernel
+  // host entry point: H2D copies on a library stream into one of two staging slots, so the
+  // next step's copy overlaps this step's kernels
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  int stage_slot = 0;
   int prof_used = 0;
 };
 
@@ -423,7 +428,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
 struct DenseLayout {
   size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, hd, x_stage, total;
 };
-int ldw_of(int m) { return (m + 3) / 4 * 4; }
+int ldw_of(int m) { return (m + 127) / 128 * 128; }   // Wd is stored in 128-column tiles
 DenseLayout dense_layout_of(const ff_dense_config& c) {
   DenseLayout o{};
   const size_t dw = (size_t)c.d * (size_t)ldw_of(c.m), w = (size_t)ldw_of(c.m);
@@ -475,6 +480,7 @@ struct ff_dense {
   char* ws;
   float *Wd, *mWd, *vWd, *dWd, *bd, *mbd, *vbd, *dbd, *xT, *hd, *x_stage;
   int ldw;
+  int nsm;
   int64_t t;
   int fwd_B;            // batch of the last training forward (-1: none since the last backward)
   bool grads_valid;
@@ -509,10 +515,14 @@ ff_status dense_backward_impl(ff_dense* n, int B, float lr, const float* hd, cud
   n->t += 1;
   const AdamArgs a = adam_args_of(n->cfg.beta1, n->cfg.beta2, n->cfg.eps, lr, n->t);
   const bool sg = (n->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
-  dim3 grid((n->ldw + 127) / 128, (n->cfg.d + kDenseBwdRows - 1) / kDenseBwdRows);
+  // feature ranges per column tile: about 4 CTAs per SM in total, whole 16-feature blocks
+  const int gx = (n->ldw + 127) / 128;
+  const int fq = std::max(1, std::min((n->cfg.d + kDenseBwdBlk - 1) / kDenseBwdBlk, (4 * n->nsm + gx - 1) / gx));
+  const int rows = ((n->cfg.d + fq - 1) / fq + kDenseBwdBlk - 1) / kDenseBwdBlk * kDenseBwdBlk;
+  dim3 grid(gx, (n->cfg.d + rows - 1) / rows);
   k_dense_bwd_adam<<<grid, kDenseBwdThreads, 0, st>>>(n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d,
                                                       n->cfg.m, n->ldw, ldx, nb, hd, 64 * nb, a,
-                                                      sg ? n->dWd : nullptr, sg ? n->dbd : nullptr);
+                                                      sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows);
   FF_LAUNCHED();
   n->grads_valid = sg;
   n->fwd_B = -1;
@@ -620,6 +630,13 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
 
 ff_status fixedfanin_destroy(ff_layer* l) {
   if (l) for (cudaEvent_t e : l->prof_ev) cudaEventDestroy(e);
+  if (l) {
+    for (int i = 0; i < 2; ++i) {
+      if (l->ev_ready[i]) cudaEventDestroy(l->ev_ready[i]);
+      if (l->ev_free[i]) cudaEventDestroy(l->ev_free[i]);
+    }
+    if (l->copy_st) cudaStreamDestroy(l->copy_st);
+  }
   delete l;
   return FF_OK;
 }
@@ -753,14 +770,30 @@ ff_status fixedfanin_train_step_host(ff_layer* l, const float* h_host, int32_t B
   if (nnz < 0 || nnz > l->cfg.max_nnz) return fail(FF_ERR_ARG, "lbl_ptr[B]=%d outside [0, max_nnz=%d]", nnz, l->cfg.max_nnz);
   if (nnz > 0 && !lbl_ids_host) return fail(FF_ERR_ARG, "null lbl_ids_host");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!l->copy_st) {
+    FF_CUDA(cudaStreamCreateWithFlags(&l->copy_st, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      FF_CUDA(cudaEventCreateWithFlags(&l->ev_ready[i], cudaEventDisableTiming));
+      FF_CUDA(cudaEventCreateWithFlags(&l->ev_free[i], cudaEventDisableTiming));
+    }
+  }
+  // staging slot of this call: its previous user (two calls ago) must have finished reading it
+  const int slot = l->stage_slot;
+  l->stage_slot ^= 1;
+  float* h_stage = l->h_stage + (size_t)slot * l->cfg.max_batch * l->cfg.m;
+  int* lbl_stage = l->lbl_stage + (size_t)slot * ((size_t)l->cfg.max_batch + 1 + (size_t)l->cfg.max_nnz);
   const size_t hb = (size_t)B * l->cfg.m * 4;
-  if (hb) FF_CUDA(cudaMemcpyAsync(l->h_stage, h_host, hb, cudaMemcpyHostToDevice, st));
-  FF_CUDA(cudaMemcpyAsync(l->lbl_stage, lbl_ptr_host, 4 * (size_t)(B + 1), cudaMemcpyHostToDevice, st));
-  if (nnz) FF_CUDA(cudaMemcpyAsync(l->lbl_stage + B + 1, lbl_ids_host, 4 * (size_t)nnz, cudaMemcpyHostToDevice, st));
-  ff_status s = train_step_impl(l, l->h_stage, B, l->lbl_stage, l->lbl_stage + B + 1, grad_scale, lr, l->dh_stage,
+  FF_CUDA(cudaStreamWaitEvent(l->copy_st, l->ev_free[slot], 0));
+  if (hb) FF_CUDA(cudaMemcpyAsync(h_stage, h_host, hb, cudaMemcpyHostToDevice, l->copy_st));
+  FF_CUDA(cudaMemcpyAsync(lbl_stage, lbl_ptr_host, 4 * (size_t)(B + 1), cudaMemcpyHostToDevice, l->copy_st));
+  if (nnz) FF_CUDA(cudaMemcpyAsync(lbl_stage + B + 1, lbl_ids_host, 4 * (size_t)nnz, cudaMemcpyHostToDevice, l->copy_st));
+  FF_CUDA(cudaEventRecord(l->ev_ready[slot], l->copy_st));
+  FF_CUDA(cudaStreamWaitEvent(st, l->ev_ready[slot], 0));
+  ff_status s = train_step_impl(l, h_stage, B, lbl_stage, lbl_stage + B + 1, grad_scale, lr, l->dh_stage,
                                 l->loss_scratch, st);
   const int32_t launches = g_launches;
   if (s != FF_OK) return s;
+  FF_CUDA(cudaEventRecord(l->ev_free[slot], st));
   if (loss_host) FF_CUDA(cudaMemcpyAsync(loss_host, l->loss_scratch, 4, cudaMemcpyDeviceToHost, st));
   if (dh_host && hb) FF_CUDA(cudaMemcpyAsync(dh_host, l->dh_stage, hb, cudaMemcpyDeviceToHost, st));
   g_launches = launches;
@@ -905,6 +938,12 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
   n->xT = at<float>(ws, lay.xT); n->hd = at<float>(ws, lay.hd); n->x_stage = at<float>(ws, lay.x_stage);
   n->ldw = ldw_of(c.m);
   n->t = 0; n->fwd_B = -1; n->grads_valid = false;
+  {
+    int dev = 0;
+    cudaError_t e2 = cudaGetDevice(&dev);
+    if (e2 == cudaSuccess) e2 = cudaDeviceGetAttribute(&n->nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (e2 != cudaSuccess) { delete n; return fail(FF_ERR_CUDA, "device query: %s", cudaGetErrorString(e2)); }
+  }
   if (cudaFuncSetAttribute((const void*)k_dense_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseFwdSmem) !=
       cudaSuccess) {
     delete n;
@@ -933,9 +972,13 @@ ff_status fixedfanin_dense_set_params(ff_dense* n, const float* Wd, const float*
   g_launches = 0;
   if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const size_t m4 = 4 * (size_t)n->cfg.m, lw4 = 4 * (size_t)n->ldw;
-  auto cp2 = [&](float* dst, const float* src) -> cudaError_t {   // [d][m] -> [d][ldw]
-    return src ? cudaMemcpy2DAsync(dst, lw4, src, m4, m4, n->cfg.d, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  const size_t m4 = 4 * (size_t)n->cfg.m;
+  const int64_t dm = (int64_t)n->cfg.d * n->cfg.m;
+  const int rg = (int)std::max<int64_t>(1, std::min<int64_t>((dm + 255) / 256, 8192));
+  auto cp2 = [&](float* dst, const float* src) -> cudaError_t {   // [d][m] -> tiled
+    if (!src) return cudaSuccess;
+    k_dense_retile<<<rg, 256, 0, st>>>(src, dst, n->cfg.d, n->cfg.m, 1);
+    return cudaGetLastError();
   };
   auto cp1 = [&](float* dst, const float* src) -> cudaError_t {
     return src ? cudaMemcpyAsync(dst, src, m4, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
@@ -953,9 +996,13 @@ ff_status fixedfanin_dense_get_params(ff_dense* n, float* Wd, float* bd, float* 
   g_launches = 0;
   if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const size_t m4 = 4 * (size_t)n->cfg.m, lw4 = 4 * (size_t)n->ldw;
-  auto cp2 = [&](float* dst, const float* src) -> cudaError_t {
-    return dst ? cudaMemcpy2DAsync(dst, m4, src, lw4, m4, n->cfg.d, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+  const size_t m4 = 4 * (size_t)n->cfg.m;
+  const int64_t dm = (int64_t)n->cfg.d * n->cfg.m;
+  const int rg = (int)std::max<int64_t>(1, std::min<int64_t>((dm + 255) / 256, 8192));
+  auto cp2 = [&](float* dst, const float* src) -> cudaError_t {   // tiled -> [d][m]
+    if (!dst) return cudaSuccess;
+    k_dense_retile<<<rg, 256, 0, st>>>(src, dst, n->cfg.d, n->cfg.m, 0);
+    return cudaGetLastError();
   };
   auto cp1 = [&](float* dst, const float* src) -> cudaError_t {
     return dst ? cudaMemcpyAsync(dst, src, m4, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
@@ -1001,8 +1048,13 @@ ff_status fixedfanin_dense_get_grads(ff_dense* n, float* dWd, float* dbd, ff_str
   if (!n) return fail(FF_ERR_ARG, "dense layer is NULL");
   if (!n->grads_valid) return fail(FF_ERR_STATE, "no gradients: create with FF_FLAG_STORE_GRADS and run a backward");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const size_t m4 = 4 * (size_t)n->cfg.m, lw4 = 4 * (size_t)n->ldw;
-  if (dWd) FF_CUDA(cudaMemcpy2DAsync(dWd, m4, n->dWd, lw4, m4, n->cfg.d, cudaMemcpyDeviceToDevice, st));
+  const size_t m4 = 4 * (size_t)n->cfg.m;
+  const int64_t dm = (int64_t)n->cfg.d * n->cfg.m;
+  if (dWd) {
+    k_dense_retile<<<(int)std::max<int64_t>(1, std::min<int64_t>((dm + 255) / 256, 8192)), 256, 0, st>>>(
+        n->dWd, dWd, n->cfg.d, n->cfg.m, 0);
+    FF_CUDA(cudaGetLastError());
+  }
   if (dbd) FF_CUDA(cudaMemcpyAsync(dbd, n->dbd, m4, cudaMemcpyDeviceToDevice, st));
   return FF_OK;
 }
