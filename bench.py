@@ -128,6 +128,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# measured ceilings of the step's on-chip pattern (tools/microbench/l2bench.cu, profiles/r01_l2bench.txt and
+# r01b_l2bench_bulkred.txt): 21.4 M random 128-B line gathers + 21.4 M 128-B red.v4 lines = 11.2 TB/s combined
+# (atomic dh); two gathers per connection (CSC pull) ~19.9 TB/s
+ONCHIP_CEILING_GBS = {"atomic": 11200.0, "csc": 19900.0}
+
+
 # ----------------------------------------------------------------------------- byte models
 def alg_bytes_train_kernel(L, k):
     """Algorithmic HBM bytes of one fused-step kernel launch:
@@ -451,6 +457,10 @@ def run_ours(a, shape, world, rank, local_rank):
                      "avg_launch_ms": k_step_ms / launches_per_step,
                      "kernel_share_of_step": k_step_ms / (ms / a.steps)},
         "onchip": {"l2_bytes_per_step": onchip, "l2_gbs": onchip / (ms / a.steps * 1e-3) / 1e9,
+                   "kernel_gbs": onchip / (k_step_ms * 1e-3) / 1e9,
+                   "ceiling_gbs": ONCHIP_CEILING_GBS.get(a.dh_mode),
+                   "kernel_frac_of_ceiling": (onchip / (k_step_ms * 1e-3) / 1e9 / ONCHIP_CEILING_GBS[a.dh_mode]
+                                              if a.dh_mode in ONCHIP_CEILING_GBS else None),
                    "note": ("h 128-B line gather + dh 128-B red.v4 per connection" if a.dh_mode == "atomic" else
                             "h 128-B line gather (row pass) + g 128-B line gather (CSC column pass) per connection")
                            + "; measured ceilings (profiles/r01_l2bench.txt): gather ~19.9 TB/s, red ~6.3-6.6 TB/s"},

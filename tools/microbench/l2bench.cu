@@ -136,6 +136,41 @@ __global__ void k_bulkred(const int* __restrict__ idx, float* dhT, long nconn) {
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+// gather (ld.v4 into registers) + bulk reduce: the contributions of a row go to a per-warp
+// smem buffer (two buffers, alternating) and each lane issues one 128-B cp.reduce.async.bulk
+// for its connection: the reductions leave through the TMA path, not the LSU -> L1 -> XBAR path
+__global__ void k_gbulk(const int* __restrict__ idx, const float* __restrict__ hT, float* dhT, long nconn, float* out) {
+  extern __shared__ float sm[];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  long nw = (gridDim.x * (long)blockDim.x) >> 5;
+  float acc = 0.f;
+  int it = 0;
+  for (long r = warp; r * 32 < nconn; r += nw, ++it) {
+    float* buf = sm + (wib * 2 + (it & 1)) * 1024;
+    int c = __ldg(idx + r * 32 + lane);
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { int ci = __shfl_sync(~0u, c, i * 4 + (lane >> 3));
+      v[i] = __ldg(reinterpret_cast<const float4*>(hT + (long)ci * 32 + 4 * (lane & 7))); }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += v[i].x + v[i].y + v[i].z + v[i].w;
+    float s = __shfl_xor_sync(~0u, acc, 1) * 1e-30f;
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // buffer it&1 free again
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      *reinterpret_cast<float4*>(buf + (i * 4 + (lane >> 3)) * 32 + 4 * (lane & 7)) = make_float4(s, s, s, s);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + lane * 32);
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 128;"
+                 :: "l"(dhT + (long)c * 32), "r"(sa) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (acc == 12345.f) out[0] = acc;
+}
 __global__ void k_stream(const float4* __restrict__ a, long n4, float* out) {
   float acc = 0.f;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += gridDim.x * (long)blockDim.x) {
@@ -185,6 +220,9 @@ int main(int argc, char** argv) {
     snprintf(nm, 64, "bulk red g=%d", grid);
     CK(cudaFuncSetAttribute(k_bulkred, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096));
     timeit(nm, gbytes, [&] { k_bulkred<<<grid, tpb, 8 * 4096>>>(idx, dhT, nconn); });
+    snprintf(nm, 64, "gather v4+bulk red g=%d", grid);
+    CK(cudaFuncSetAttribute(k_gbulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    timeit(nm, 2 * gbytes, [&] { k_gbulk<<<grid, tpb, 16 * 4096>>>(idx, hT, dhT, nconn, out); });
   }
   timeit("hbm read 1GiB", (double)nbig, [&] { k_stream<<<nsm * 8, 512>>>(big, nbig / 16, out); });
   timeit("hbm copy 1GiB", 2.0 * nbig, [&] { k_copy<<<nsm * 8, 512>>>(big, big2, nbig / 16); });
