@@ -1,0 +1,12 @@
+# Round measurement: parity tests, smoke, default bench, reference arm, ncu launch list, ncu --set full of the fused kernel.
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/pytest_gpu.txt; cat gpurun_out/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -1 gpurun_out/bench_default.json | cut -c1-400
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>&1; tail -1 gpurun_out/bench_ref.json | cut -c1-200
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/launches.log 2>&1; tail -1 gpurun_out/launches.log | cut -c1-100
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_train" -s 6 -c 1 \
+  -o gpurun_out/prof_full python bench.py --steps 3 --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_dense|k_predict_ring|k_merge_topk_block" -s 0 -c 3 \
+  -o gpurun_out/prof_aux python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_aux.log 2>&1; tail -1 gpurun_out/ncu_aux.log
