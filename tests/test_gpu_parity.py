@@ -445,6 +445,26 @@ def test_host_entry_point_equals_device_entry_point(dh_mode):
     assert (sa["W"] == sb["W"]).all() and (sa["bias"] == sb["bias"]).all()
 
 
+@DH
+def test_host_entry_point_double_buffering_over_many_steps(dh_mode):
+    """train_step_host stages into two alternating slots on its own copy stream: a run of
+    host-entry steps with different batches (no synchronisation in between) leaves exactly
+    the state of the same run through the device entry point."""
+    L, m, k, B = 3000, 512, 32, 32
+    a, b = make(L, m, k, B=B, seed=6, dh_mode=dh_mode), make(L, m, k, B=B, seed=6, dh_mode=dh_mode)
+    hs = [torch.from_numpy(synth.hidden_batch(B, m, step=s)).pin_memory() for s in range(5)]
+    lb = [synth.label_batch(B, L, 5.0, step=s) for s in range(5)]
+    loss_host = torch.empty(1).pin_memory()
+    for s in range(5):
+        a.train_step_host(hs[s], torch.from_numpy(lb[s][0]), torch.from_numpy(lb[s][1]), 1e-3, loss_host=loss_host)
+    for s in range(5):
+        b.train_step(hs[s].to(dev()), tens(lb[s][0]), tens(lb[s][1]), 1e-3)
+    torch.cuda.synchronize()
+    sa, sb = state_of(a), state_of(b)
+    for key in ("W", "bias", "mW", "vW", "idx"):
+        assert (sa[key] == sb[key]).all(), key
+
+
 def test_csc_dh_is_deterministic_and_matches_atomic():
     L, m, k, B = 3000, 1024, 32, 32
     a, b = make(L, m, k, B=B, seed=2, dh_mode=1), make(L, m, k, B=B, seed=2, dh_mode=0)
