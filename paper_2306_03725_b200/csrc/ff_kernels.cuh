@@ -1026,8 +1026,14 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
 // while row X is scored.  Same score arithmetic as k_predict / k_rows (row_score_own on the
 // same operands): bit-identical y.  Warp w scores rows w, w + nwarp, ...; the block merges
 // its warps' lists into cand[blk][32][kTopkMax] like k_predict.
-constexpr int kPredRingD = 3;
-constexpr int kPredRingThreads = 128;
+#ifndef FF_PRED_RING_D
+#define FF_PRED_RING_D 2
+#endif
+#ifndef FF_PRED_RING_THREADS
+#define FF_PRED_RING_THREADS 128
+#endif
+constexpr int kPredRingD = FF_PRED_RING_D;
+constexpr int kPredRingThreads = FF_PRED_RING_THREADS;
 constexpr int kPredRingSmem = (kPredRingThreads / 32) * kPredRingD * 8 * 32 * 16;
 __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* __restrict__ W,
                                                                    const int* __restrict__ idx,
