@@ -422,9 +422,15 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 // Measured (Amazon-670K): CSC mode is latency/LSU-bound and prefers D = 2 with
 // 6 CTAs/SM; atomic mode is bound by the L1->XBAR red path and is insensitive (D = 3, 4 CTAs).
 // MODE: 0 = atomic dh, 1 = CSC pull, 2 = hybrid (columns < split by red, the rest pulled)
+#ifndef FF_CSC_RING_D
+#define FF_CSC_RING_D 2
+#endif
+#ifndef FF_CSC_RING_MINB
+#define FF_CSC_RING_MINB 6
+#endif
 template <int MODE> struct RingCfg {
-  static constexpr int D = MODE == 1 ? 2 : 3;           // ring stages per warp
-  static constexpr int kMinBlocks = MODE == 1 ? 6 : 4;  // CTAs per SM (register budget)
+  static constexpr int D = MODE == 1 ? FF_CSC_RING_D : 3;                 // ring stages per warp
+  static constexpr int kMinBlocks = MODE == 1 ? FF_CSC_RING_MINB : 4;     // CTAs per SM (register budget)
 };
 constexpr int kRingThreads = 128;
 constexpr int kRingStageBytes = 8 * 32 * 16;            // 8 registers x 32 lanes x 16 B = 32 h lines
