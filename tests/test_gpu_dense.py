@@ -227,3 +227,47 @@ def test_model_free_running_tiny_matches_oracle(dh_mode):
     y = lay.forward(h).cpu().numpy().astype(np.float64)
     rs, rid = oracle.topk(y, 5)
     assert (ids_.cpu().numpy() == rid).all() and (sc.cpu().numpy() == rs).all()
+
+
+@pytest.mark.parametrize("dh_mode", [0, 1])
+def test_model_full_size_amazon_670k_sampled(dh_mode):
+    """The bench's `model` configuration (Amazon-670K, 512-d features, 10% dropout, B = 32):
+    the dense forward h against the oracle over the full [B][m]; one whole-architecture step
+    checked on sampled label rows (sparse dW, db, W') and sampled dense columns (dWd, Wd'),
+    lockstep (R20: the oracle takes the GPU's h, its ReLU mask and the GPU's dh)."""
+    layer = L_()
+    shape = synth.SHAPES["amazon-670k"]
+    L, m, k, B, d = shape.L, shape.m, shape.k, shape.B, 512
+    lay = make(L, m, k, B=B, seed=42, flags=layer.FF_FLAG_STORE_GRADS, dh_mode=dh_mode)
+    dn = make_dense(d, m, B=B, seed=43, dropout=0.1, flags=layer.FF_FLAG_STORE_GRADS)
+    s0, d0 = state_of(lay), dstate(dn)
+    x = synth.feature_batch(B, d, step=3)
+    ptr, ids = synth.label_batch(B, L, shape.avg_pos, step=3)
+    h_gpu = dn.forward(tens(x), step=3, train=True)
+    y = lay.forward(h_gpu).cpu().numpy().astype(np.float64)
+    h_gpu = h_gpu.cpu().numpy().astype(np.float64)
+    xt = oracle.dropout(x, 0.1, seed=43, step=3)[0]
+    z, Az, href = oracle.dense_forward(d0["Wd"], d0["bd"], xt)
+    assert_close(h_gpu, href, Az, "h (full)")
+    loss = torch.zeros(1, device=dev())
+    layer.model_train_step(dn, lay, tens(x), 3, tens(ptr), tens(ids), F32(1e-3), loss=loss)
+    dW, db = (t.cpu().numpy() for t in lay.get_grads())
+    dWd, dbd = (t.cpu().numpy() for t in dn.get_grads())
+    s1, d1 = state_of(lay), dstate(dn)
+    rng = np.random.default_rng(9)
+    rows = np.sort(rng.choice(L, 256, replace=False))
+    g, lref = oracle.bce_grad(y, ptr, ids, F32(1.0 / B))
+    assert abs(loss.item() - lref) <= 1e-4 * abs(lref)
+    dWr, AdW, dbr, Adb = oracle.weight_grad(s0["idx"][rows], h_gpu, g[:, rows])
+    assert_close(dW[rows], dWr, AdW, "sparse dW rows")
+    assert_close(db[rows], dbr, Adb, "sparse db rows")
+    Wr, _, _ = oracle.adam(s0["W"][rows], dW[rows], s0["mW"][rows], s0["vW"][rows], 1, F32(1e-3), **ADAM)
+    assert_close(s1["W"][rows], Wr, adam_A(s0["W"][rows], Wr), "W' rows")
+    # dense gradients on sampled columns, from the oracle's Alg. 2 dh over every connection
+    dhr, _ = oracle.input_grad(s0["W"], s0["idx"], g, m)
+    cols = np.sort(rng.choice(m, 512, replace=False))
+    rWd, AWd, rbd, Abd = oracle.dense_backward(xt, h_gpu[:, cols], dhr[:, cols])
+    assert_close(dWd[:, cols], rWd, AWd, "dense dWd cols")
+    assert_close(dbd[cols], rbd, Abd, "dense dbd cols")
+    Wdr, _, _ = oracle.adam(d0["Wd"][:, cols], dWd[:, cols], d0["mWd"][:, cols], d0["vWd"][:, cols], 1, F32(1e-3), **ADAM)
+    assert_close(d1["Wd"][:, cols], Wdr, adam_A(d0["Wd"][:, cols], Wdr), "Wd' cols")
