@@ -520,9 +520,14 @@ ff_status dense_backward_impl(ff_dense* n, int B, float lr, const float* hd, cud
   const int fq = std::max(1, std::min((n->cfg.d + kDenseBwdBlk - 1) / kDenseBwdBlk, (4 * n->nsm + gx - 1) / gx));
   const int rows = ((n->cfg.d + fq - 1) / fq + kDenseBwdBlk - 1) / kDenseBwdBlk * kDenseBwdBlk;
   dim3 grid(gx, (n->cfg.d + rows - 1) / rows);
-  k_dense_bwd_adam<<<grid, kDenseBwdThreads, 0, st>>>(n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d,
-                                                      n->cfg.m, n->ldw, ldx, nb, hd, 64 * nb, a,
-                                                      sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows);
+  if (nb == 1)
+    k_dense_bwd_adam_b32<<<grid, kDenseBwdThreads, kDenseBwd1Smem, st>>>(
+        n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d, n->cfg.m, ldx, hd, 64 * nb, a,
+        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows);
+  else
+    k_dense_bwd_adam<<<grid, kDenseBwdThreads, 0, st>>>(n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d,
+                                                        n->cfg.m, n->ldw, ldx, nb, hd, 64 * nb, a,
+                                                        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows);
   FF_LAUNCHED();
   n->grads_valid = sg;
   n->fwd_B = -1;
@@ -945,7 +950,9 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
     if (e2 != cudaSuccess) { delete n; return fail(FF_ERR_CUDA, "device query: %s", cudaGetErrorString(e2)); }
   }
   if (cudaFuncSetAttribute((const void*)k_dense_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseFwdSmem) !=
-      cudaSuccess) {
+          cudaSuccess ||
+      cudaFuncSetAttribute((const void*)k_dense_bwd_adam_b32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kDenseBwd1Smem) != cudaSuccess) {
     delete n;
     return fail(FF_ERR_CUDA, "dense forward smem attribute");
   }
