@@ -66,15 +66,22 @@ __global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, 
 }
 
 // Forward: z[b][c] = bd[c] + sum_f xT[f][b] Wd[f][c], h = max(z, 0).  CTA = 256 threads ->
-// 128 columns x 32 samples (chunk blockIdx.y).  The Wd tile (64 features x 128 columns,
-// 32 KB) and the xT tile (64 x 32) of the next feature chunk are copied into a second
+// 128 columns x 32 samples (chunk blockIdx.y).  The Wd tile (32 features x 128 columns,
+// 16 KB) and the xT tile (32 x 32) of the next feature chunk are copied into a second
 // shared-memory stage (cp.async) while the current chunk is computed, so the HBM latency of
 // Wd hides behind the FMAs.  Warp w: lane -> 4 columns, samples 8(w&3)..+7, and the first
-// (w < 4) or second (w >= 4) half of every chunk's 64 features: a thread's 32 accumulators
+// (w < 4) or second (w >= 4) half of every chunk's features: a thread's 32 accumulators
 // amortise each 16-B shared load of Wd over 8 samples (the kernel is bound by shared-memory
-// wavefronts, not FMAs).  The two halves are added at the end: z = (bd + sum over first
-// halves, f ascending) + (sum over second halves, f ascending) — a fixed order.
-constexpr int kDenseFwdThreads = 256, kDenseFch = 64;
+// wavefronts, not FMAs).  For B <= 32 the chunks are also split over two CTAs (gridDim.z =
+// 2, for occupancy: one 32-sample chunk gives only m/128 CTAs).  Summation order, fixed:
+// per CTA (bd + first halves) + second halves, f ascending within each; then CTA 0 + CTA 1.
+#ifndef FF_DENSE_FCH
+#define FF_DENSE_FCH 64
+#endif
+#ifndef FF_DENSE_SPLIT
+#define FF_DENSE_SPLIT 1
+#endif
+constexpr int kDenseFwdThreads = 256, kDenseFch = FF_DENSE_FCH, kDenseFwdSplit = FF_DENSE_SPLIT;
 constexpr int kDenseFwdSmem = 2 * kDenseFch * (128 + 32) * 4;
 __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const float* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
@@ -83,28 +90,33 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
                                                                 const float* __restrict__ bd,
                                                                 const float* __restrict__ xT, int d, int m, int ldw,
                                                                 int ldx, int B, float* __restrict__ hd, int cstride,
-                                                                int zero_dh, float* __restrict__ h_out) {
+                                                                int zero_dh, float* __restrict__ h_out,
+                                                                float* __restrict__ zpart, unsigned* __restrict__ cnt) {
   extern __shared__ __align__(16) float dsm[];
-  float* const wbuf = dsm;                                   // [2][64][128]
-  float* const xbuf = dsm + 2 * kDenseFch * 128;             // [2][64][32]
+  float* const wbuf = dsm;                                   // [2][kDenseFch][128]
+  float* const xbuf = dsm + 2 * kDenseFch * 128;             // [2][kDenseFch][32]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q2 = blockIdx.y;
   const int sg = w & 3, half = w >> 2;                       // samples 8sg..8sg+7; feature half
   const int ct = blockIdx.x * 128, c0 = ct + 4 * lane;
   const bool cok = c0 < ldw;
-  const int nchunk = (d + kDenseFch - 1) / kDenseFch;
+  // split over CTAs (gridDim.z = 2, B <= 32): CTA kz takes chunks [ch_lo, ch_hi); the two
+  // partial sums meet in zpart and the second CTA to finish adds them (part 0 + part 1)
+  const int nch_all = (d + kDenseFch - 1) / kDenseFch, kz = blockIdx.z;
+  const int ch_lo = kz == 0 ? 0 : (nch_all + 1) / 2, ch_hi = gridDim.z == 1 || kz == 1 ? nch_all : (nch_all + 1) / 2;
   auto issue = [&](int ch) {
     const int f0 = ch * kDenseFch, stg = ch & 1;
     const uint32_t wdst = (uint32_t)__cvta_generic_to_shared(wbuf + stg * kDenseFch * 128);
     const uint32_t xdst = (uint32_t)__cvta_generic_to_shared(xbuf + stg * kDenseFch * 32);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {                           // 64 rows x 32 float4
+    for (int u = 0; u < kDenseFch * 32 / kDenseFwdThreads; ++u) {   // kDenseFch rows x 32 float4
       const int e = u * kDenseFwdThreads + threadIdx.x, r = e >> 5, cq = (e & 31) * 4;
       const bool ok = f0 + r < d && ct + cq < ldw;
       cp_async16_zfill(wdst + (uint32_t)(r * 128 + cq) * 4u,
                        ok ? Wd + ((int64_t)blockIdx.x * d + f0 + r) * 128 + cq : Wd, ok);
     }
+    static_assert(kDenseFch * 8 % kDenseFwdThreads == 0, "xT tile copy");
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {                           // 64 rows x 8 float4
+    for (int u = 0; u < kDenseFch * 8 / kDenseFwdThreads; ++u) {    // kDenseFch rows x 8 float4
       const int e = u * kDenseFwdThreads + threadIdx.x, r = e >> 3, s4 = (e & 7) * 4;
       const bool ok = f0 + r < d;
       cp_async16_zfill(xdst + (uint32_t)(r * 32 + s4) * 4u, ok ? xT + (int64_t)(f0 + r) * ldx + q2 * 32 + s4 : xT, ok);
@@ -112,13 +124,13 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
     cp_async_commit();
   };
   float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (cok && half == 0) bias4 = *reinterpret_cast<const float4*>(bd + c0);
+  if (cok && half == 0 && kz == 0) bias4 = *reinterpret_cast<const float4*>(bd + c0);
   float2 acc[8][2];
 #pragma unroll
   for (int s = 0; s < 8; ++s) { acc[s][0] = make_float2(bias4.x, bias4.y); acc[s][1] = make_float2(bias4.z, bias4.w); }
-  issue(0);
-  for (int ch = 0; ch < nchunk; ++ch) {
-    if (ch + 1 < nchunk) { issue(ch + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
+  if (ch_lo < ch_hi) issue(ch_lo);
+  for (int ch = ch_lo; ch < ch_hi; ++ch) {
+    if (ch + 1 < ch_hi) { issue(ch + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
     __syncthreads();
     const int nf = min(kDenseFch, d - ch * kDenseFch);
     const int r0 = half * (kDenseFch / 2), r1 = min(nf, r0 + kDenseFch / 2);
@@ -148,16 +160,57 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
     }
   }
   __syncthreads();
+  float zz[8][4];
+  if (half == 0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      zz[s][0] = __fadd_rn(acc[s][0].x, part[lane * 33 + 4 * s + 0]);
+      zz[s][1] = __fadd_rn(acc[s][0].y, part[lane * 33 + 4 * s + 1]);
+      zz[s][2] = __fadd_rn(acc[s][1].x, part[lane * 33 + 4 * s + 2]);
+      zz[s][3] = __fadd_rn(acc[s][1].y, part[lane * 33 + 4 * s + 3]);
+    }
+  }
+  if (gridDim.z > 1) {
+    // zpart[kz][c][32 samples] (B <= 32 here); the last of the two CTAs of this tile combines
+    __shared__ unsigned s_last;
+    if (half == 0 && cok) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float* zp = zpart + ((int64_t)kz * ldw + c0 + u) * 32 + 8 * sg;
+        __stcg(reinterpret_cast<float4*>(zp), make_float4(zz[0][u], zz[1][u], zz[2][u], zz[3][u]));
+        __stcg(reinterpret_cast<float4*>(zp + 4), make_float4(zz[4][u], zz[5][u], zz[6][u], zz[7][u]));
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_last = atomicAdd(cnt + blockIdx.x, 1u) == 1u;
+      if (s_last) cnt[blockIdx.x] = 0u;                      // ready for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (half == 0 && cok) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float* z0p = zpart + ((int64_t)0 * ldw + c0 + u) * 32 + 8 * sg;
+        const float* z1p = zpart + ((int64_t)1 * ldw + c0 + u) * 32 + 8 * sg;
+        const float4 a0 = __ldcg(reinterpret_cast<const float4*>(z0p)), a1 = __ldcg(reinterpret_cast<const float4*>(z0p + 4));
+        const float4 b0 = __ldcg(reinterpret_cast<const float4*>(z1p)), b1 = __ldcg(reinterpret_cast<const float4*>(z1p + 4));
+        zz[0][u] = __fadd_rn(a0.x, b0.x); zz[1][u] = __fadd_rn(a0.y, b0.y);
+        zz[2][u] = __fadd_rn(a0.z, b0.z); zz[3][u] = __fadd_rn(a0.w, b0.w);
+        zz[4][u] = __fadd_rn(a1.x, b1.x); zz[5][u] = __fadd_rn(a1.y, b1.y);
+        zz[6][u] = __fadd_rn(a1.z, b1.z); zz[7][u] = __fadd_rn(a1.w, b1.w);
+      }
+    }
+  }
   if (half == 1 || !cok) return;
   float hv[8][4];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const int b = q2 * 32 + 8 * sg + s;
     const bool valid = b < B;
-    const float z0 = __fadd_rn(acc[s][0].x, part[lane * 33 + 4 * s + 0]);
-    const float z1 = __fadd_rn(acc[s][0].y, part[lane * 33 + 4 * s + 1]);
-    const float z2 = __fadd_rn(acc[s][1].x, part[lane * 33 + 4 * s + 2]);
-    const float z3 = __fadd_rn(acc[s][1].y, part[lane * 33 + 4 * s + 3]);
+    const float z0 = zz[s][0], z1 = zz[s][1], z2 = zz[s][2], z3 = zz[s][3];
     hv[s][0] = valid ? fmaxf(z0, 0.0f) : 0.0f;
     hv[s][1] = valid ? fmaxf(z1, 0.0f) : 0.0f;
     hv[s][2] = valid ? fmaxf(z2, 0.0f) : 0.0f;

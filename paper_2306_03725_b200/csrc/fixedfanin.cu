@@ -426,7 +426,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
 
 // ============================================================ NEXT-2: the intermediate layer
 struct DenseLayout {
-  size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, hd, x_stage, total;
+  size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, zpart, cnt, hd, x_stage, total;
 };
 int ldw_of(int m) { return (m + 127) / 128 * 128; }   // Wd is stored in 128-column tiles
 DenseLayout dense_layout_of(const ff_dense_config& c) {
@@ -439,6 +439,8 @@ DenseLayout dense_layout_of(const ff_dense_config& c) {
   o.dWd = (c.flags & FF_FLAG_STORE_GRADS) ? take(4 * dw) : 0;
   o.bd = take(4 * w); o.mbd = take(4 * w); o.vbd = take(4 * w); o.dbd = take(4 * w);
   o.xT = take(4 * (size_t)c.d * ldx);
+  o.zpart = take(2 * 4 * (size_t)ldw_of(c.m) * 32);        // split-feature forward partials (B <= 32)
+  o.cnt = take(4 * (size_t)(ldw_of(c.m) / 128));
   o.hd = take(8 * (size_t)c.m * ldx);     // own h|dh lines for the standalone forward/backward
   o.x_stage = take(4 * (size_t)c.max_batch * (size_t)c.d);
   o.total = off;
@@ -478,7 +480,8 @@ struct ff_dense {
   ff_dense_config cfg;
   DenseLayout lay;
   char* ws;
-  float *Wd, *mWd, *vWd, *dWd, *bd, *mbd, *vbd, *dbd, *xT, *hd, *x_stage;
+  float *Wd, *mWd, *vWd, *dWd, *bd, *mbd, *vbd, *dbd, *xT, *hd, *x_stage, *zpart;
+  unsigned* cnt;
   int ldw;
   int nsm;
   int64_t t;
@@ -501,9 +504,11 @@ ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, 
                                       (uint32_t)n->cfg.seed, (uint32_t)(n->cfg.seed >> 32), n->xT);
     FF_LAUNCHED();
   }
-  dim3 grid((n->ldw + 127) / 128, nb);
+  // B <= 32 and at least two feature chunks: split the features over two CTAs per column tile
+  const int split = (nb == 1 && n->cfg.d >= 2 * kDenseFch) ? kDenseFwdSplit : 1;
+  dim3 grid((n->ldw + 127) / 128, nb, split);
   k_dense_fwd<<<grid, kDenseFwdThreads, kDenseFwdSmem, st>>>(n->Wd, n->bd, n->xT, n->cfg.d, n->cfg.m, n->ldw, ldx, B, hd,
-                                                64 * nb, 1, h_out);
+                                                             64 * nb, 1, h_out, n->zpart, n->cnt);
   FF_LAUNCHED();
   if (train) n->fwd_B = B;
   return FF_OK;
@@ -941,6 +946,7 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
   n->bd = at<float>(ws, lay.bd); n->mbd = at<float>(ws, lay.mbd); n->vbd = at<float>(ws, lay.vbd);
   n->dbd = at<float>(ws, lay.dbd);
   n->xT = at<float>(ws, lay.xT); n->hd = at<float>(ws, lay.hd); n->x_stage = at<float>(ws, lay.x_stage);
+  n->zpart = at<float>(ws, lay.zpart); n->cnt = at<unsigned>(ws, lay.cnt);
   n->ldw = ldw_of(c.m);
   n->t = 0; n->fwd_B = -1; n->grads_valid = false;
   {
