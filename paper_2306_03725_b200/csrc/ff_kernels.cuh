@@ -428,9 +428,15 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 #ifndef FF_CSC_RING_MINB
 #define FF_CSC_RING_MINB 6
 #endif
+#ifndef FF_ATOM_RING_D
+#define FF_ATOM_RING_D 3
+#endif
+#ifndef FF_ATOM_RING_MINB
+#define FF_ATOM_RING_MINB 4
+#endif
 template <int MODE> struct RingCfg {
-  static constexpr int D = MODE == 1 ? FF_CSC_RING_D : 3;                 // ring stages per warp
-  static constexpr int kMinBlocks = MODE == 1 ? FF_CSC_RING_MINB : 4;     // CTAs per SM (register budget)
+  static constexpr int D = MODE == 1 ? FF_CSC_RING_D : FF_ATOM_RING_D;                 // ring stages per warp
+  static constexpr int kMinBlocks = MODE == 1 ? FF_CSC_RING_MINB : FF_ATOM_RING_MINB;  // CTAs per SM (registers)
 };
 constexpr int kRingThreads = 128;
 constexpr int kRingStageBytes = 8 * 32 * 16;            // 8 registers x 32 lanes x 16 B = 32 h lines
