@@ -200,6 +200,16 @@ ff_status fixedfanin_score_shortlist(ff_layer* layer, const float* h, int32_t B,
                                      const int32_t* cand_ptr, const int32_t* cand_ids,
                                      float* scores, ff_stream_t stream);
 
+/* Precision at K, Eq. (1): for each instance b the number of its predicted
+ * labels ids[b][0..K) (e.g. from predict_topk / merge_topk; GLOBAL ids) that are positives
+ * in the label CSR (lbl_ptr [B+1], lbl_ids, device), hits [B] int32 (or NULL), and
+ * mean = (1/B) sum_b hits[b] / K (float[1], or NULL), dividing by K even when an instance
+ * has fewer than K positives (R16).  The mean is summed in a fixed order (deterministic).
+ * Stateless; 1 <= K <= 32, B >= 0 (B = 0 gives mean 0).                                   */
+ff_status fixedfanin_precision_at_k(const int32_t* ids, int32_t B, int32_t K, const int32_t* lbl_ptr,
+                                    const int32_t* lbl_ids, int32_t* hits, float* mean,
+                                    ff_stream_t stream);
+
 /* Merge per-shard top-K lists: in_scores/in_ids [P][B][K] (device) -> out [B][K] under
  * the same total order.  Stateless.  1 <= K <= FF_MAX_TOPK, 1 <= P <= 1024.            */
 ff_status fixedfanin_merge_topk(const float* in_scores, const int32_t* in_ids, int32_t P,

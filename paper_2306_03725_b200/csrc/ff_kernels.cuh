@@ -1228,6 +1228,41 @@ __global__ void k_merge_topk(const float* __restrict__ in_s, const int* __restri
   }
 }
 
+// ---------------------------------------------------------------------- precision at K
+// Eq. (1): hits[b] = |{q < K : ids[b][q] is a positive of b}|, and
+// mean = (1/B) sum_b hits[b] / K (divided by K even with fewer than K positives, R16).
+// One CTA; warp w takes samples w, w + 8, ...; lane q < K holds predicted id q and the
+// warp walks the sample's positives (CSR) 32 at a time.  The mean is summed in a fixed
+// order (per warp over its samples, then over warps), so it is deterministic.
+__global__ void __launch_bounds__(256) k_precision_at_k(const int* __restrict__ ids, int B, int K,
+                                                        const int* __restrict__ lbl_ptr, const int* __restrict__ lbl_ids,
+                                                        int* __restrict__ hits, float* __restrict__ mean) {
+  __shared__ float wsum[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float acc = 0.0f;
+  for (int b = w; b < B; b += 8) {
+    const int id = lane < K ? ids[(int64_t)b * K + lane] : -1;
+    bool hit = false;
+    for (int p = lbl_ptr[b]; p < lbl_ptr[b + 1]; p += 32) {
+      const int n = min(32, lbl_ptr[b + 1] - p);
+      const int pv = lane < n ? lbl_ids[p + lane] : -2;
+      for (int t = 0; t < n; ++t) hit |= (__shfl_sync(kFull, pv, t) == id);
+    }
+    const int nh = __popc(__ballot_sync(kFull, hit && lane < K));
+    if (lane == 0) {
+      if (hits != nullptr) hits[b] = nh;
+      acc = __fadd_rn(acc, __fdiv_rn((float)nh, (float)K));
+    }
+  }
+  if (lane == 0) wsum[w] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0 && mean != nullptr) {
+    float t = 0.0f;
+    for (int i = 0; i < 8; ++i) t = __fadd_rn(t, wsum[i]);
+    *mean = B > 0 ? __fdiv_rn(t, (float)B) : 0.0f;
+  }
+}
+
 // ---------------------------------------------------------------------- shortlist scoring
 // Scores of explicit (sample, label) pairs — the "trivial matrix slicing" of P:1057-1059.
 // One thread per pair.  score_one<NG> evaluates exactly the operation sequence the warp

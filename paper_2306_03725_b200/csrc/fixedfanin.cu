@@ -859,6 +859,17 @@ ff_status fixedfanin_score_shortlist(ff_layer* l, const float* h, int32_t B, con
   return FF_OK;
 }
 
+ff_status fixedfanin_precision_at_k(const int32_t* ids, int32_t B, int32_t K, const int32_t* lbl_ptr,
+                                    const int32_t* lbl_ids, int32_t* hits, float* mean, ff_stream_t stream) {
+  g_launches = 0;
+  if (B < 0 || K < 1 || K > 32) return fail(FF_ERR_ARG, "B=%d / K=%d outside B >= 0, 1 <= K <= 32", B, K);
+  if (!lbl_ptr || (B > 0 && !ids) || (!hits && !mean)) return fail(FF_ERR_ARG, "null ids/lbl_ptr, or no output");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_precision_at_k<<<1, 256, 0, st>>>(ids, B, K, lbl_ptr, lbl_ids, hits, mean);
+  FF_LAUNCHED();
+  return FF_OK;
+}
+
 ff_status fixedfanin_merge_topk(const float* in_s, const int32_t* in_i, int32_t P, int32_t B, int32_t K, float* out_s,
                                 int32_t* out_i, ff_stream_t stream) {
   g_launches = 0;

@@ -30,6 +30,7 @@ EXPORTS = [
     "fixedfanin_get_params", "fixedfanin_forward", "fixedfanin_backward", "fixedfanin_get_grads",
     "fixedfanin_adam_step", "fixedfanin_train_step", "fixedfanin_train_step_host", "fixedfanin_redistribute",
     "fixedfanin_predict_topk", "fixedfanin_score_shortlist", "fixedfanin_merge_topk", "fixedfanin_check",
+    "fixedfanin_precision_at_k",
     "fixedfanin_profile_begin",
     "fixedfanin_profile_end", "fixedfanin_last_launch_count",
     "fixedfanin_last_error",
@@ -92,6 +93,7 @@ def lib() -> ctypes.CDLL:
             "fixedfanin_redistribute": [P, u64, P],
             "fixedfanin_predict_topk": [P, P, i32, i32, P, P, P],
             "fixedfanin_merge_topk": [P, P, i32, i32, i32, P, P, P],
+            "fixedfanin_precision_at_k": [P, i32, i32, P, P, P, P, P],
             "fixedfanin_score_shortlist": [P, P, i32, P, P, P, P],
             "fixedfanin_check": [P, P],
             "fixedfanin_profile_begin": [P, i32],
@@ -308,6 +310,17 @@ def merge_topk(scores, ids, stream=None):
     _check(lib().fixedfanin_merge_topk(_ptr(scores.contiguous()), _ptr(ids.contiguous()), P, B, K, _ptr(out_s),
                                        _ptr(out_i), _stream(stream)))
     return out_s, out_i
+
+
+def precision_at_k(ids, lbl_ptr, lbl_ids, stream=None):
+    """Eq. (1) on the GPU: (hits int32 [B], mean P@K float32 [1]) of predicted
+    GLOBAL ids [B][K] against the positives' CSR (device tensors)."""
+    B, K = ids.shape
+    hits = torch.empty(B, dtype=torch.int32, device=ids.device)
+    mean = torch.empty(1, dtype=torch.float32, device=ids.device)
+    _check(lib().fixedfanin_precision_at_k(_ptr(ids.contiguous()), B, K, _ptr(lbl_ptr), _ptr(lbl_ids), _ptr(hits),
+                                           _ptr(mean), _stream(stream)))
+    return hits, mean
 
 
 # ------------------------------------------------------------------ NEXT-2

@@ -654,3 +654,31 @@ def test_shortlist_sharded_sum_and_errors():
     empty = full.score_shortlist(h, tens(np.zeros(B + 1, np.int32)), tens(np.zeros(0, np.int32)))
     assert empty.numel() == 0
     full.check()
+
+
+@pytest.mark.parametrize("B,K,npos", [(32, 5, 5.0), (7, 1, 1.0), (100, 8, 40.0), (0, 3, 2.0)])
+def test_precision_at_k_matches_oracle(B, K, npos):
+    """Eq. (1) on the GPU: per-instance hits bit-exact, the mean within fp32
+    rounding, for top-K lists that mix positives and negatives (and > 32 positives)."""
+    layer = L_()
+    L, m, k = 3000, 256, 16
+    if B == 0:
+        hits, mean = layer.precision_at_k(torch.empty((0, K), dtype=torch.int32, device=dev()),
+                                          torch.zeros(1, dtype=torch.int32, device=dev()),
+                                          torch.zeros(1, dtype=torch.int32, device=dev()))
+        assert mean.item() == 0.0
+        return
+    lay = make(L, m, k, B=min(B, 1024), seed=5)
+    ptr, ids = synth.label_batch(B, L, npos, step=2)
+    h = synth.hidden_batch(B, m, step=2)
+    _, top = lay.predict_topk(tens(h), K)
+    top = top.cpu().numpy()
+    # plant some positives into the predictions so that hits are not all zero
+    for b in range(0, B, 2):
+        pos = ids[ptr[b]:ptr[b + 1]]
+        top[b, : min(len(pos), K) // 2 + 1] = pos[: min(len(pos), K) // 2 + 1]
+    hits, mean = layer.precision_at_k(tens(top.astype(np.int32)), tens(ptr), tens(ids))
+    ref_h = np.array([sum(int(t in set(ids[ptr[b]:ptr[b + 1]].tolist())) for t in top[b]) for b in range(B)])
+    assert (hits.cpu().numpy() == ref_h).all()
+    ref = oracle.precision_at_k(top.astype(np.int64), ptr, ids)
+    assert abs(mean.item() - ref) <= 1e-6 * max(ref, 1e-30)
