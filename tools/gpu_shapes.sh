@@ -1,5 +1,7 @@
-python -m pytest tests/test_gpu_parity.py -q -m gpu -k full_size 2>&1 | tail -2
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
 for sh in tiny wiki10-31k wiki-500k amazon-670k amazon-670k-m16k amazon-670k-k64-m65k amazon-3m; do
-  timeout 600 python bench.py --shape $sh --steps 500 --warmup 10 --e2e-steps 50 --no-cpu-baseline > gpurun_out/sh.json 2>gpurun_out/sh.err
-  python -c "import json; d=json.load(open('gpurun_out/sh.json')); r=d['roofline']; print('$sh', round(d['value']), 'samples/s', round(d['ms_per_step'],4), 'ms/step', 'row_frac', round(r['frac'],3), 'step_frac', round(d['hbm_step']['frac'],3), 'pred', round(d['predict']['value']), 'mem_MB', round(d['memory']['workspace_bytes_per_gpu']/1e6))" || tail -3 gpurun_out/sh.err
+  timeout 600 python bench.py --shape $sh --steps 500 --warmup 10 --e2e-steps 100 --no-cpu-baseline > gpurun_out/sh_$sh.json 2>gpurun_out/sh.err
+  python -c "
+import json; d=json.load(open('gpurun_out/sh_$sh.json')); r=d['roofline']; m=d.get('model') or {}
+print('%-22s %9d %8.4f %6.3f %6.3f %9d %9d %9d %6d' % ('$sh', d['value'], d['ms_per_step'], r['frac'], d['hbm_step']['frac'], d['e2e']['value'], d['predict']['value'], m.get('value', 0), d['memory']['workspace_bytes_per_gpu']/1e6))" || tail -3 gpurun_out/sh.err
 done
