@@ -79,3 +79,34 @@ def test_merge_topk_argument_validation():
     st = L.lib().fixedfanin_merge_topk(None, None, 0, 1, 1, None, None, None)
     assert st == L.FF_ERR_ARG
     assert b"P" in L.lib().fixedfanin_last_error()
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(d=0, m=64), "d="),
+    (dict(d=16, m=0), "m="),
+    (dict(d=16, m=64, max_batch=0), "max_batch"),
+    (dict(d=16, m=64, max_batch=1025), "max_batch"),
+    (dict(d=16, m=64, dropout=1.0), "dropout"),
+    (dict(d=16, m=64, dropout=-0.1), "dropout"),
+    (dict(d=16, m=64, beta1=1.0), "Adam"),
+])
+def test_bad_dense_configs_rejected(kw, msg):
+    c = L.DenseConfig(**kw).c()
+    n = ctypes.c_size_t(0)
+    st = L.lib().fixedfanin_dense_workspace_size(ctypes.byref(c), ctypes.byref(n))
+    assert st == L.FF_ERR_CONFIG and msg in L.lib().fixedfanin_last_error().decode()
+
+
+def test_dense_workspace_size_matches_layout_model():
+    """Wd, mWd, vWd in 128-column tiles (+ dWd with FF_FLAG_STORE_GRADS), bias vectors, xT,
+    the split-forward scratch, the h|dh lines and the x staging."""
+    d, m, B = 512, 32768, 32
+    sizes = []
+    for flags in (0, L.FF_FLAG_STORE_GRADS):
+        c = L.DenseConfig(d=d, m=m, max_batch=B, flags=flags).c()
+        n = ctypes.c_size_t(0)
+        assert L.lib().fixedfanin_dense_workspace_size(ctypes.byref(c), ctypes.byref(n)) == L.FF_OK
+        sizes.append(n.value)
+    assert sizes[1] - sizes[0] == 4 * d * m                     # dWd
+    core = 3 * 4 * d * m + 4 * 4 * m + 4 * d * 32 + 8 * m * 32 + 4 * B * d
+    assert core <= sizes[0] <= core + 2 * 4 * m * 32 + 4 * (m // 128) + 16 * 256

@@ -104,7 +104,8 @@ def test_init_full_amazon_670k_sampled_rows():
 
 # --------------------------------------------------------------- forward / backward
 CASES = [(1000, 256, 16, 32), (1000, 256, 16, 5), (333, 100, 13, 37), (2000, 512, 32, 100), (97, 64, 1, 1),
-         (64, 32, 32, 128), (1500, 2048, 64, 32), (400, 300, 50, 40), (130, 64, 64, 7), (700, 512, 32, 300)]
+         (64, 32, 32, 128), (1500, 2048, 64, 32), (400, 300, 50, 40), (130, 64, 64, 7), (700, 512, 32, 300),
+         (300, 256, 32, 1024)]                       # FF_MAX_BATCH: 32 sample chunks
 
 
 @pytest.mark.parametrize("L,m,k,B", CASES)
