@@ -192,7 +192,6 @@ def run_reference(a, shape, world, rank):
 
 
 # ----------------------------------------------------------------------------- NEXT-2
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 148 SMs x 128 FP32 lanes x FMA x max SM clock
 
 
 def run_model(eng, shape, dev, stream, e0, e1, d=512, dropout=0.1, steps=100):
@@ -233,14 +232,17 @@ def run_model(eng, shape, dev, stream, e0, e1, d=512, dropout=0.1, steps=100):
     peak, peak_src = peaks()
     bwd_bytes = 24 * d * shape.m + 8 * d * 32 + 8 * shape.m * 32 + 4 * B * shape.m
     fwd_flops = 2 * B * d * shape.m
+    fwd_bytes = 4 * d * shape.m + 8 * 32 * shape.m
     del dn
     return {"workload": f"{shape.name} + dense intermediate d={d}, dropout {dropout}", "d": d, "B": B,
             "value": B / (ms_model * 1e-3), "unit": "samples/s", "ms_per_step": ms_model,
             "launches_per_step": launches,
-            "dense_fwd": {"ms": res["fwd"], "bound": "alu", "achieved_tflops": fwd_flops / (res["fwd"] * 1e-3) / 1e12,
-                          "peak_tflops": FP32_PEAK_TFLOPS, "frac": fwd_flops / (res["fwd"] * 1e-3) / 1e12 / FP32_PEAK_TFLOPS,
-                          "note": "dropout + fp32 FFMA2 GEMM 32 x d x m (+ ReLU, h|dh lines); peak = 148 SMs x 128 "
-                                  "FP32 lanes x 2 x 1.965 GHz"},
+            "dense_fwd": {"ms": res["fwd"], "bound": "hbm", "alg_bytes": fwd_bytes,
+                          "achieved_gbs": fwd_bytes / (res["fwd"] * 1e-3) / 1e9, "peak_gbs": peak,
+                          "frac": fwd_bytes / (res["fwd"] * 1e-3) / 1e9 / peak,
+                          "tflops_3xtf32": 3 * fwd_flops / (res["fwd"] * 1e-3) / 1e12,
+                          "note": "dropout kernel + tcgen05 kind::tf32 3xTF32 GEMM (M = 128 columns, N = 32 samples) + "
+                                  "bias/ReLU epilogue from TMEM; bytes = read Wd + write the h|dh lines"},
             "dense_bwd_adam": {"ms": res["bwd"], "bound": "hbm", "alg_bytes": bwd_bytes,
                                "achieved_gbs": bwd_bytes / (res["bwd"] * 1e-3) / 1e9, "peak_gbs": peak,
                                "peak_source": peak_src, "frac": bwd_bytes / (res["bwd"] * 1e-3) / 1e9 / peak,

@@ -71,6 +71,8 @@ typedef enum {
 #define FF_FLAG_STORE_GRADS 2u   /* fused train_step also stores dW/db (for get_grads/tests)  */
 #define FF_FLAG_NO_PIPE 4u       /* use the generic fused kernel even where the pipelined one
                                     applies (k = 32, B <= 32); same results, for A/B tests     */
+#define FF_FLAG_DENSE_SIMT 8u    /* ff_dense_config.flags: FP32 FMA forward instead of the
+                                    tcgen05 3xTF32 tensor-core forward (B <= 32), for A/B tests */
 
 /* ff_config.loss: the one-vs-all binary loss whose gradient the backward pass consumes */
 #define FF_LOSS_BCE 0            /* binary cross-entropy with logits (the north star's) */

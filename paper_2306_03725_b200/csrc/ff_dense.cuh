@@ -238,6 +238,192 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
   }
 }
 
+// ------------------------------------------------------------------ tensor-core forward
+// The same forward on the 5th-generation tensor cores (tcgen05, kind::tf32) for B <= 32:
+// per CTA D[128 columns][32 samples] (fp32, in TMEM) += A[128][8] . B[8][32] per 8-feature
+// block, A = Wd^T (the 128-column tile) and B = xT, both K-major in shared memory (no
+// swizzle: 8-row x 16-B core matrices; tools/microbench/tcprobe.cu checks the layout) —
+// fp32 accuracy from 3xTF32: a = a_hi + a_lo with a_hi = tf32(a), and
+// a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (the dropped a_lo.b_lo and the tf32 truncation of
+// the lo parts are ~2^-22 relative).  Each thread converts its share of a 32-feature stage
+// (loaded into registers one stage ahead; 2 CTAs per SM) into the hi/lo tiles of one of two
+// shared-memory buffers; thread 0 issues the 3 x 4 MMAs of the stage and commits them to the
+// buffer's mbarrier, which frees it for the stage after next.  Epilogue: warps 0-3 read their
+// 32 TMEM lanes (= columns) x 32 columns (= samples) with tcgen05.ld, add the bias, apply
+// ReLU and write the h|dh lines.  Summation order differs from the SIMT kernel (tensor-core
+// internal), within the R19 tolerance.
+#ifndef FF_TC_FCH
+#define FF_TC_FCH 32
+#endif
+constexpr int kTcThreads = 256, kTcFch = FF_TC_FCH;                // features per stage
+constexpr int kTcAbytes = kTcFch * 128 * 4, kTcBbytes = kTcFch * 32 * 4;          // 32 KB, 8 KB
+constexpr int kTcBuf = 2 * kTcAbytes + 2 * kTcBbytes;                              // hi/lo A, hi/lo B: 80 KB
+constexpr int kTcSmem = 2 * kTcBuf + 1024 + 64;                                    // 2 buffers + align + barriers
+constexpr int kTcAu = kTcFch / 8, kTcBu = kTcFch / 32;       // 16-B chunks per thread per stage (A, B)
+static_assert(kTcFch % 32 == 0 && kTcFch <= 64, "tcgen05 forward stage size");
+
+// shared-memory matrix descriptor, K-major, no swizzle: LBO = byte distance between the two
+// 4-element K halves of an 8-K MMA step, SBO = byte distance between 8-row groups
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;                                         // version (sm_100); layout 0 = no swizzle
+  return d;
+}
+// kind::tf32, D f32, A/B tf32 K-major, M = 128, N = 32
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+               :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r; asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x)); return r;
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t mbar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+               : "=r"(ok) : "r"(mbar), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) { while (!mbar_try_wait(mbar, parity)) {} }
+
+__global__ void __launch_bounds__(kTcThreads, 2) k_dense_fwd_tc(const float* __restrict__ Wd, const float* __restrict__ bd,
+                                                                 const float* __restrict__ xT, int d, int m, int ldx,
+                                                                 int B, float* __restrict__ hd, int cstride, int zero_dh,
+                                                                 float* __restrict__ h_out) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(tsm) + 1023u) & ~1023u;   // 1024-B aligned atoms
+  const uint32_t mbar0 = sbase + 2 * kTcBuf, tptr_s = mbar0 + 16;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int ct = blockIdx.x * 128;
+  const int nst = (d + kTcFch - 1) / kTcFch;
+  if (w == 0) {                                                   // TMEM: 32 columns (N = 32 fp32)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" :: "r"(tptr_s) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  uint32_t tmem_d;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(tmem_d) : "r"(tptr_s) : "memory");
+
+  // this thread's share of a stage: 8 (column, 4 features) quads of Wd^T and 2 (sample,
+  // 4 features) quads of xT — K-major 16-B chunks, read as 4 coalesced scalar loads each
+  float4 wr[kTcAu], xr[kTcBu];
+  auto load_stage = [&](int st) {
+    const int f0 = st * kTcFch;
+#pragma unroll
+    for (int u = 0; u < kTcAu; ++u) {
+      const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
+      float t[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int f = f0 + 4 * kq + i;
+        t[i] = f < d ? Wd[((int64_t)blockIdx.x * d + f) * 128 + c] : 0.0f;
+      }
+      wr[u] = make_float4(t[0], t[1], t[2], t[3]);
+    }
+#pragma unroll
+    for (int u = 0; u < kTcBu; ++u) {
+      const int e = u * kTcThreads + tid, b = e & 31, kq = e >> 5;
+      float t[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int f = f0 + 4 * kq + i;
+        t[i] = f < d ? xT[(int64_t)f * ldx + b] : 0.0f;
+      }
+      xr[u] = make_float4(t[0], t[1], t[2], t[3]);
+    }
+  };
+  auto split_store = [&](uint32_t hi_addr, uint32_t lo_addr, float4 v) {
+    const uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
+    const float l0 = v.x - __uint_as_float(h0), l1 = v.y - __uint_as_float(h1);
+    const float l2 = v.z - __uint_as_float(h2), l3 = v.w - __uint_as_float(h3);
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(hi_addr), "r"(h0), "r"(h1), "r"(h2), "r"(h3) : "memory");
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(lo_addr), "f"(l0), "f"(l1), "f"(l2), "f"(l3) : "memory");
+  };
+  load_stage(0);
+  for (int st = 0; st < nst; ++st) {
+    const int b = st & 1;
+    const uint32_t buf = sbase + (uint32_t)b * kTcBuf;
+    const uint32_t A_hi = buf, A_lo = buf + kTcAbytes, B_hi = buf + 2 * kTcAbytes, B_lo = B_hi + kTcBbytes;
+    if (st >= 2) mbar_wait(mbar0 + 8u * b, (uint32_t)(((st - 2) >> 1) & 1));   // MMAs of stage st-2 done
+    // K-major core matrices: A chunk (column c, K quad kq) at kq*2048 + c*16 (SBO 128 B per
+    // 8 columns, LBO 2048 B per K quad); B chunk (sample b, kq) at kq*512 + b*16
+#pragma unroll
+    for (int u = 0; u < kTcAu; ++u) {
+      const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
+      const uint32_t off = (uint32_t)(kq * 2048 + c * 16);
+      split_store(A_hi + off, A_lo + off, wr[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kTcBu; ++u) {
+      const int e = u * kTcThreads + tid, b = e & 31, kq = e >> 5;
+      const uint32_t off = (uint32_t)(kq * 512 + b * 16);
+      split_store(B_hi + off, B_lo + off, xr[u]);
+    }
+    if (st + 1 < nst) load_stage(st + 1);                          // next stage's loads in flight
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int nkb = min(kTcFch / 8, (d - st * kTcFch + 7) / 8);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint64_t ah = umma_desc_kmajor(A_hi + kb * 4096, 2048, 128), al = umma_desc_kmajor(A_lo + kb * 4096, 2048, 128);
+        const uint64_t bh = umma_desc_kmajor(B_hi + kb * 1024, 512, 128), bl = umma_desc_kmajor(B_lo + kb * 1024, 512, 128);
+        tc_mma_tf32(tmem_d, ah, bh, (st > 0 || kb > 0) ? 1u : 0u);
+        tc_mma_tf32(tmem_d, ah, bl, 1u);
+        tc_mma_tf32(tmem_d, al, bh, 1u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   :: "r"(mbar0 + 8u * b) : "memory");
+    }
+  }
+  mbar_wait(mbar0 + 8u * ((nst - 1) & 1), (uint32_t)(((nst - 1) >> 1) & 1));      // all MMAs done
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (w < 4) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem_d + ((uint32_t)(32 * w) << 16);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                   "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                   "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int c = ct + 32 * w + lane;                              // TMEM lane = column
+    if (c < m) {
+      const float bj = bd[c];
+      float h[32];
+#pragma unroll
+      for (int s2 = 0; s2 < 32; ++s2) h[s2] = s2 < B ? fmaxf(__uint_as_float(v[s2]) + bj, 0.0f) : 0.0f;
+      float* line = hd + (int64_t)c * cstride;
+#pragma unroll
+      for (int s4 = 0; s4 < 32; s4 += 4) {
+        *reinterpret_cast<float4*>(line + s4) = make_float4(h[s4], h[s4 + 1], h[s4 + 2], h[s4 + 3]);
+        if (zero_dh) *reinterpret_cast<float4*>(line + 32 + s4) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (h_out != nullptr) {
+#pragma unroll
+        for (int s2 = 0; s2 < 32; ++s2)
+          if (s2 < B) h_out[(int64_t)s2 * m + c] = h[s2];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" :: "r"(tmem_d) : "memory");
+}
+
 // Backward + Adam: dz[b][c] = dh[b][c] * [h[b][c] > 0] (ReLU'(0) = 0, R26);
 // dWd[f][c] = sum_b xT[f][b] dz[b][c] (b ascending), dbd[c] = sum_b dz[b][c]; then Adam
 // (R6) over Wd and bd with those gradients.  This kernel streams 24 B per weight

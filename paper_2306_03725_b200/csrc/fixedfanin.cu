@@ -504,6 +504,13 @@ ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, 
                                       (uint32_t)n->cfg.seed, (uint32_t)(n->cfg.seed >> 32), n->xT);
     FF_LAUNCHED();
   }
+  if (nb == 1 && !(n->cfg.flags & FF_FLAG_DENSE_SIMT)) {          // tensor cores (tcgen05, 3xTF32)
+    k_dense_fwd_tc<<<(n->ldw + 127) / 128, kTcThreads, kTcSmem, st>>>(n->Wd, n->bd, n->xT, n->cfg.d, n->cfg.m, ldx, B,
+                                                                      hd, 64 * nb, 1, h_out);
+    FF_LAUNCHED();
+    if (train) n->fwd_B = B;
+    return FF_OK;
+  }
   // B <= 32 and at least two feature chunks: split the features over two CTAs per column tile
   const int split = (nb == 1 && n->cfg.d >= 2 * kDenseFch) ? kDenseFwdSplit : 1;
   dim3 grid((n->ldw + 127) / 128, nb, split);
@@ -969,7 +976,9 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
   if (cudaFuncSetAttribute((const void*)k_dense_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseFwdSmem) !=
           cudaSuccess ||
       cudaFuncSetAttribute((const void*)k_dense_bwd_adam_b32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kDenseBwd1Smem) != cudaSuccess) {
+                           kDenseBwd1Smem) != cudaSuccess ||
+      cudaFuncSetAttribute((const void*)k_dense_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem) !=
+          cudaSuccess) {
     delete n;
     return fail(FF_ERR_CUDA, "dense forward smem attribute");
   }
