@@ -245,10 +245,11 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
 // swizzle: 8-row x 16-B core matrices; tools/microbench/tcprobe.cu checks the layout) —
 // fp32 accuracy from 3xTF32: a = a_hi + a_lo with a_hi = tf32(a), and
 // a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (the dropped a_lo.b_lo and the tf32 truncation of
-// the lo parts are ~2^-22 relative).  Each thread converts its share of a 32-feature stage
-// (loaded into registers one stage ahead; 2 CTAs per SM) into the hi/lo tiles of one of two
-// shared-memory buffers; thread 0 issues the 3 x 4 MMAs of the stage and commits them to the
-// buffer's mbarrier, which frees it for the stage after next.  Epilogue: warps 0-3 read their
+// the lo parts are ~2^-22 relative).  Warp-specialised: each of the 256 producer threads
+// converts its share of a 32-feature stage (loaded into registers one stage ahead; 2 CTAs per
+// SM) into the hi/lo tiles of one of two shared-memory buffers and arrives on the buffer's
+// "full" mbarrier; lane 0 of warp 8 waits on it, issues the 3 x 4 MMAs of the stage and
+// commits them to the buffer's "empty" mbarrier, which lets the producers refill it.  Epilogue: warps 0-3 read their
 // 32 TMEM lanes (= columns) x 32 columns (= samples) with tcgen05.ld, add the bias, apply
 // ReLU and write the h|dh lines.  Summation order differs from the SIMT kernel (tensor-core
 // internal), within the R19 tolerance.
@@ -290,13 +291,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t mbar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) { while (!mbar_try_wait(mbar, parity)) {} }
 
-__global__ void __launch_bounds__(kTcThreads, 2) k_dense_fwd_tc(const float* __restrict__ Wd, const float* __restrict__ bd,
+__global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float* __restrict__ Wd, const float* __restrict__ bd,
                                                                  const float* __restrict__ xT, int d, int m, int ldx,
                                                                  int B, float* __restrict__ hd, int cstride, int zero_dh,
                                                                  float* __restrict__ h_out) {
+  // warp-specialised: warps 0-7 produce the operand tiles, warp 8 issues the MMAs; per buffer
+  // a "full" mbarrier (256 producer arrivals) and an "empty" one (the MMAs' tcgen05.commit),
+  // so no CTA-wide barrier sits in the stage loop
   extern __shared__ __align__(1024) unsigned char tsm[];
-  const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(tsm) + 1023u) & ~1023u;   // 1024-B aligned atoms
-  const uint32_t mbar0 = sbase + 2 * kTcBuf, tptr_s = mbar0 + 16;
+  const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(tsm) + 1023u) & ~1023u;
+  const uint32_t mbar0 = sbase + 2 * kTcBuf;                      // empty[0], empty[1]
+  const uint32_t full0 = mbar0 + 16, tptr_s = mbar0 + 32;         // full[0], full[1]; TMEM address
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int ct = blockIdx.x * 128;
   const int nst = (d + kTcFch - 1) / kTcFch;
@@ -307,6 +312,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_dense_fwd_tc(const float* __r
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar0) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar0 + 8) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(full0), "r"(kTcThreads) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(full0 + 8), "r"(kTcThreads) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -315,76 +322,85 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_dense_fwd_tc(const float* __r
   uint32_t tmem_d;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(tmem_d) : "r"(tptr_s) : "memory");
 
-  // this thread's share of a stage: 8 (column, 4 features) quads of Wd^T and 2 (sample,
-  // 4 features) quads of xT — K-major 16-B chunks, read as 4 coalesced scalar loads each
-  float4 wr[kTcAu], xr[kTcBu];
-  auto load_stage = [&](int st) {
-    const int f0 = st * kTcFch;
-#pragma unroll
-    for (int u = 0; u < kTcAu; ++u) {
-      const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
-      float t[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int f = f0 + 4 * kq + i;
-        t[i] = f < d ? Wd[((int64_t)blockIdx.x * d + f) * 128 + c] : 0.0f;
+  if (w == kTcThreads / 32) {                                     // ===== MMA issuer
+    if (lane == 0) {
+      for (int st = 0; st < nst; ++st) {
+        const int b = st & 1;
+        const uint32_t buf = sbase + (uint32_t)b * kTcBuf;
+        const uint32_t A_hi = buf, A_lo = buf + kTcAbytes, B_hi = buf + 2 * kTcAbytes, B_lo = B_hi + kTcBbytes;
+        mbar_wait(full0 + 8u * b, (uint32_t)((st >> 1) & 1));     // the producers filled buffer b
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int nkb = min(kTcFch / 8, (d - st * kTcFch + 7) / 8);
+        for (int kb = 0; kb < nkb; ++kb) {
+          const uint64_t ah = umma_desc_kmajor(A_hi + kb * 4096, 2048, 128), al = umma_desc_kmajor(A_lo + kb * 4096, 2048, 128);
+          const uint64_t bh = umma_desc_kmajor(B_hi + kb * 1024, 512, 128), bl = umma_desc_kmajor(B_lo + kb * 1024, 512, 128);
+          tc_mma_tf32(tmem_d, ah, bh, (st > 0 || kb > 0) ? 1u : 0u);
+          tc_mma_tf32(tmem_d, ah, bl, 1u);
+          tc_mma_tf32(tmem_d, al, bh, 1u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     :: "r"(mbar0 + 8u * b) : "memory");
       }
-      wr[u] = make_float4(t[0], t[1], t[2], t[3]);
     }
+  } else {                                                        // ===== producers
+    // this thread's share of a stage: (column, 4 features) quads of Wd^T and (sample,
+    // 4 features) quads of xT — K-major 16-B chunks, read as 4 coalesced scalar loads each
+    float4 wr[kTcAu], xr[kTcBu];
+    auto load_stage = [&](int st) {
+      const int f0 = st * kTcFch;
 #pragma unroll
-    for (int u = 0; u < kTcBu; ++u) {
-      const int e = u * kTcThreads + tid, b = e & 31, kq = e >> 5;
-      float t[4];
+      for (int u = 0; u < kTcAu; ++u) {
+        const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
+        float t[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int f = f0 + 4 * kq + i;
-        t[i] = f < d ? xT[(int64_t)f * ldx + b] : 0.0f;
+        for (int i = 0; i < 4; ++i) {
+          const int f = f0 + 4 * kq + i;
+          t[i] = f < d ? Wd[((int64_t)blockIdx.x * d + f) * 128 + c] : 0.0f;
+        }
+        wr[u] = make_float4(t[0], t[1], t[2], t[3]);
       }
-      xr[u] = make_float4(t[0], t[1], t[2], t[3]);
-    }
-  };
-  auto split_store = [&](uint32_t hi_addr, uint32_t lo_addr, float4 v) {
-    const uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
-    const float l0 = v.x - __uint_as_float(h0), l1 = v.y - __uint_as_float(h1);
-    const float l2 = v.z - __uint_as_float(h2), l3 = v.w - __uint_as_float(h3);
-    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(hi_addr), "r"(h0), "r"(h1), "r"(h2), "r"(h3) : "memory");
-    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(lo_addr), "f"(l0), "f"(l1), "f"(l2), "f"(l3) : "memory");
-  };
-  load_stage(0);
-  for (int st = 0; st < nst; ++st) {
-    const int b = st & 1;
-    const uint32_t buf = sbase + (uint32_t)b * kTcBuf;
-    const uint32_t A_hi = buf, A_lo = buf + kTcAbytes, B_hi = buf + 2 * kTcAbytes, B_lo = B_hi + kTcBbytes;
-    if (st >= 2) mbar_wait(mbar0 + 8u * b, (uint32_t)(((st - 2) >> 1) & 1));   // MMAs of stage st-2 done
-    // K-major core matrices: A chunk (column c, K quad kq) at kq*2048 + c*16 (SBO 128 B per
-    // 8 columns, LBO 2048 B per K quad); B chunk (sample b, kq) at kq*512 + b*16
 #pragma unroll
-    for (int u = 0; u < kTcAu; ++u) {
-      const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
-      const uint32_t off = (uint32_t)(kq * 2048 + c * 16);
-      split_store(A_hi + off, A_lo + off, wr[u]);
-    }
+      for (int u = 0; u < kTcBu; ++u) {
+        const int e = u * kTcThreads + tid, b = e & 31, kq = e >> 5;
+        float t[4];
 #pragma unroll
-    for (int u = 0; u < kTcBu; ++u) {
-      const int e = u * kTcThreads + tid, b = e & 31, kq = e >> 5;
-      const uint32_t off = (uint32_t)(kq * 512 + b * 16);
-      split_store(B_hi + off, B_lo + off, xr[u]);
-    }
-    if (st + 1 < nst) load_stage(st + 1);                          // next stage's loads in flight
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int nkb = min(kTcFch / 8, (d - st * kTcFch + 7) / 8);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const uint64_t ah = umma_desc_kmajor(A_hi + kb * 4096, 2048, 128), al = umma_desc_kmajor(A_lo + kb * 4096, 2048, 128);
-        const uint64_t bh = umma_desc_kmajor(B_hi + kb * 1024, 512, 128), bl = umma_desc_kmajor(B_lo + kb * 1024, 512, 128);
-        tc_mma_tf32(tmem_d, ah, bh, (st > 0 || kb > 0) ? 1u : 0u);
-        tc_mma_tf32(tmem_d, ah, bl, 1u);
-        tc_mma_tf32(tmem_d, al, bh, 1u);
+        for (int i = 0; i < 4; ++i) {
+          const int f = f0 + 4 * kq + i;
+          t[i] = f < d ? xT[(int64_t)f * ldx + b] : 0.0f;
+        }
+        xr[u] = make_float4(t[0], t[1], t[2], t[3]);
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                   :: "r"(mbar0 + 8u * b) : "memory");
+    };
+    auto split_store = [&](uint32_t hi_addr, uint32_t lo_addr, float4 v) {
+      const uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
+      const float l0 = v.x - __uint_as_float(h0), l1 = v.y - __uint_as_float(h1);
+      const float l2 = v.z - __uint_as_float(h2), l3 = v.w - __uint_as_float(h3);
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(hi_addr), "r"(h0), "r"(h1), "r"(h2), "r"(h3) : "memory");
+      asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(lo_addr), "f"(l0), "f"(l1), "f"(l2), "f"(l3) : "memory");
+    };
+    load_stage(0);
+    for (int st = 0; st < nst; ++st) {
+      const int b = st & 1;
+      const uint32_t buf = sbase + (uint32_t)b * kTcBuf;
+      const uint32_t A_hi = buf, A_lo = buf + kTcAbytes, B_hi = buf + 2 * kTcAbytes, B_lo = B_hi + kTcBbytes;
+      if (st >= 2) mbar_wait(mbar0 + 8u * b, (uint32_t)(((st - 2) >> 1) & 1));   // MMAs of stage st-2 done
+      // K-major core matrices: A chunk (column c, K quad kq) at kq*2048 + c*16 (SBO 128 B per
+      // 8 columns, LBO 2048 B per K quad); B chunk (sample b, kq) at kq*512 + b*16
+#pragma unroll
+      for (int u = 0; u < kTcAu; ++u) {
+        const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
+        const uint32_t off = (uint32_t)(kq * 2048 + c * 16);
+        split_store(A_hi + off, A_lo + off, wr[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kTcBu; ++u) {
+        const int e = u * kTcThreads + tid, bb = e & 31, kq = e >> 5;
+        const uint32_t off = (uint32_t)(kq * 512 + bb * 16);
+        split_store(B_hi + off, B_lo + off, xr[u]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy stores -> tensor core
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(full0 + 8u * b) : "memory");
+      if (st + 1 < nst) load_stage(st + 1);                          // next stage's loads in flight
     }
   }
   mbar_wait(mbar0 + 8u * ((nst - 1) & 1), (uint32_t)(((nst - 1) >> 1) & 1));      // all MMAs done

@@ -505,7 +505,7 @@ ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, 
     FF_LAUNCHED();
   }
   if (nb == 1 && !(n->cfg.flags & FF_FLAG_DENSE_SIMT)) {          // tensor cores (tcgen05, 3xTF32)
-    k_dense_fwd_tc<<<(n->ldw + 127) / 128, kTcThreads, kTcSmem, st>>>(n->Wd, n->bd, n->xT, n->cfg.d, n->cfg.m, ldx, B,
+    k_dense_fwd_tc<<<(n->ldw + 127) / 128, kTcThreads + 32, kTcSmem, st>>>(n->Wd, n->bd, n->xT, n->cfg.d, n->cfg.m, ldx, B,
                                                                       hd, 64 * nb, 1, h_out);
     FF_LAUNCHED();
     if (train) n->fwd_B = B;
