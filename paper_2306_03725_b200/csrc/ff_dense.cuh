@@ -345,30 +345,44 @@ __global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float
   } else {                                                        // ===== producers
     // this thread's share of a stage: (column, 4 features) quads of Wd^T and (sample,
     // 4 features) quads of xT — K-major 16-B chunks, read as 4 coalesced scalar loads each
-    float4 wr[kTcAu], xr[kTcBu];
-    auto load_stage = [&](int st) {
+    // two register sets: while stage st is converted from one, the loads of stage st + 1 are
+    // landing in the other; the set just converted is refilled with stage st + 2
+    float4 wr0[kTcAu], xr0[kTcBu], wr1[kTcAu], xr1[kTcBu];
+    // thread tid owns column c = tid % 128 of A (K quads kq = 2u + tid / 128) and sample
+    // tid % 32 of B (K quads 8u + tid / 32): per stage, loads at fixed strides from two bases
+    static_assert(kTcThreads % 128 == 0, "column ownership");
+    const float* const wcol = Wd + (int64_t)blockIdx.x * d * 128 + (tid & 127) + (int64_t)(4 * (tid >> 7)) * 128;
+    const float* const xcol = xT + (tid & 31) + (int64_t)(4 * (tid >> 5)) * ldx;
+    auto load_stage = [&](int st, float4 (&wr)[kTcAu], float4 (&xr)[kTcBu]) {
       const int f0 = st * kTcFch;
+      const float* wp = wcol + (int64_t)f0 * 128;
+      const float* xp = xcol + (int64_t)f0 * ldx;
+      if (f0 + kTcFch <= d) {                                     // full stage: unguarded
 #pragma unroll
-      for (int u = 0; u < kTcAu; ++u) {
-        const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
-        float t[4];
+        for (int u = 0; u < kTcAu; ++u)
+          wr[u] = make_float4(wp[(8 * u + 0) * 128], wp[(8 * u + 1) * 128], wp[(8 * u + 2) * 128], wp[(8 * u + 3) * 128]);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int f = f0 + 4 * kq + i;
-          t[i] = f < d ? Wd[((int64_t)blockIdx.x * d + f) * 128 + c] : 0.0f;
+        for (int u = 0; u < kTcBu; ++u) {
+          const float* q = xp + (int64_t)(32 * u) * ldx;
+          xr[u] = make_float4(q[0], q[ldx], q[2 * ldx], q[3 * ldx]);
         }
-        wr[u] = make_float4(t[0], t[1], t[2], t[3]);
-      }
+      } else {
 #pragma unroll
-      for (int u = 0; u < kTcBu; ++u) {
-        const int e = u * kTcThreads + tid, b = e & 31, kq = e >> 5;
-        float t[4];
+        for (int u = 0; u < kTcAu; ++u) {
+          const int fb = f0 + 8 * u + 4 * (tid >> 7);
+          float t[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int f = f0 + 4 * kq + i;
-          t[i] = f < d ? xT[(int64_t)f * ldx + b] : 0.0f;
+          for (int i2 = 0; i2 < 4; ++i2) t[i2] = fb + i2 < d ? wp[(8 * u + i2) * 128] : 0.0f;
+          wr[u] = make_float4(t[0], t[1], t[2], t[3]);
         }
-        xr[u] = make_float4(t[0], t[1], t[2], t[3]);
+#pragma unroll
+        for (int u = 0; u < kTcBu; ++u) {
+          const int fb = f0 + 32 * u + 4 * (tid >> 5);
+          float t[4];
+#pragma unroll
+          for (int i2 = 0; i2 < 4; ++i2) t[i2] = fb + i2 < d ? xp[(int64_t)(32 * u + i2) * ldx] : 0.0f;
+          xr[u] = make_float4(t[0], t[1], t[2], t[3]);
+        }
       }
     };
     auto split_store = [&](uint32_t hi_addr, uint32_t lo_addr, float4 v) {
@@ -378,8 +392,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float
       asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(hi_addr), "r"(h0), "r"(h1), "r"(h2), "r"(h3) : "memory");
       asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(lo_addr), "f"(l0), "f"(l1), "f"(l2), "f"(l3) : "memory");
     };
-    load_stage(0);
-    for (int st = 0; st < nst; ++st) {
+    auto produce = [&](int st, float4 (&wr)[kTcAu], float4 (&xr)[kTcBu]) {
       const int b = st & 1;
       const uint32_t buf = sbase + (uint32_t)b * kTcBuf;
       const uint32_t A_hi = buf, A_lo = buf + kTcAbytes, B_hi = buf + 2 * kTcAbytes, B_lo = B_hi + kTcBbytes;
@@ -400,7 +413,13 @@ __global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy stores -> tensor core
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(full0 + 8u * b) : "memory");
-      if (st + 1 < nst) load_stage(st + 1);                          // next stage's loads in flight
+      if (st + 2 < nst) load_stage(st + 2, wr, xr);                  // refill this set: two stages in flight
+    };
+    load_stage(0, wr0, xr0);
+    if (nst > 1) load_stage(1, wr1, xr1);
+    for (int st = 0; st < nst; st += 2) {
+      produce(st, wr0, xr0);
+      if (st + 1 < nst) produce(st + 1, wr1, xr1);
     }
   }
   mbar_wait(mbar0 + 8u * ((nst - 1) & 1), (uint32_t)(((nst - 1) >> 1) & 1));      // all MMAs done
