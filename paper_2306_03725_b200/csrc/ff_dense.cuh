@@ -243,9 +243,9 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
 // per CTA D[128 columns][32 samples] (fp32, in TMEM) += A[128][8] . B[8][32] per 8-feature
 // block, A = Wd^T (the 128-column tile) and B = xT, both K-major in shared memory (no
 // swizzle: 8-row x 16-B core matrices; tools/microbench/tcprobe.cu checks the layout) —
-// fp32 accuracy from 3xTF32: a = a_hi + a_lo with a_hi = tf32(a), and
+// fp32 accuracy from 3xTF32: a = a_hi + a_lo exactly with a_hi = a truncated to tf32, and
 // a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (the dropped a_lo.b_lo and the tf32 truncation of
-// the lo parts are ~2^-22 relative).  Warp-specialised: each of the 256 producer threads
+// the lo parts are <= ~2^-20 relative).  Warp-specialised: each of the 256 producer threads
 // converts its share of a 32-feature stage (loaded into registers one stage ahead; 2 CTAs per
 // SM) into the hi/lo tiles of one of two shared-memory buffers and arrives on the buffer's
 // "full" mbarrier; lane 0 of warp 8 waits on it, issues the 3 x 4 MMAs of the stage and
@@ -279,9 +279,6 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uin
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
                :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
-}
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r; asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x)); return r;
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t mbar, uint32_t parity) {
   uint32_t ok;
@@ -386,7 +383,10 @@ __global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float
       }
     };
     auto split_store = [&](uint32_t hi_addr, uint32_t lo_addr, float4 v) {
-      const uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
+      // hi = a with the 13 low mantissa bits cleared (exactly a tf32 value; one LOP3), lo = a - hi
+      // exactly; the tensor core truncates lo to tf32 (<= 2^-21 |a|), a_lo.b_lo is dropped (<= 2^-20)
+      const uint32_t h0 = __float_as_uint(v.x) & 0xFFFFE000u, h1 = __float_as_uint(v.y) & 0xFFFFE000u;
+      const uint32_t h2 = __float_as_uint(v.z) & 0xFFFFE000u, h3 = __float_as_uint(v.w) & 0xFFFFE000u;
       const float l0 = v.x - __uint_as_float(h0), l1 = v.y - __uint_as_float(h1);
       const float l2 = v.z - __uint_as_float(h2), l3 = v.w - __uint_as_float(h3);
       asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(hi_addr), "r"(h0), "r"(h1), "r"(h2), "r"(h3) : "memory");
