@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float
   // warp-specialised: warps 0-7 produce the operand tiles, warp 8 issues the MMAs; per buffer
   // a "full" mbarrier (256 producer arrivals) and an "empty" one (the MMAs' tcgen05.commit),
   // so no CTA-wide barrier sits in the stage loop
-  extern __shared__ __align__(1024) unsigned char tsm[];
+  extern __shared__ __align__(16) unsigned char tsm[];      // aligned up to 1024 B below (kTcSmem has the slack)
   const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(tsm) + 1023u) & ~1023u;
   const uint32_t mbar0 = sbase + 2 * kTcBuf;                      // empty[0], empty[1]
   const uint32_t full0 = mbar0 + 16, tptr_s = mbar0 + 32;         // full[0], full[1]; TMEM address

@@ -455,20 +455,28 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
   return v;
 }
 
+// Opaque copy of a thread-constant value: ptxas cannot rematerialise an asm output, so the
+// value stays in a register instead of being recomputed from %tid in every loop iteration
+// (ncu source attribution: ~50 instructions per label row went to that in the ring kernel).
+__device__ __forceinline__ int pin(int v) { asm volatile("" : "+r"(v)); return v; }
+__device__ __forceinline__ uint32_t pin(uint32_t v) { asm volatile("" : "+r"(v)); return v; }
+template <class T>
+__device__ __forceinline__ T* pin(T* p) { asm volatile("" : "+l"(p)); return p; }
+
 template <bool STORE_GRADS, int MODE>
 __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_train_ring(RowArgs a) {
   constexpr int NG = 8, D = RingCfg<MODE>::D;
   constexpr bool CSC = MODE != 0, HYB = MODE == 2;
   constexpr uint32_t kColFloats = 64;                   // hd column stride at nb = 1 (h | dh lines)
   extern __shared__ __align__(16) unsigned char ring_smem[];
-  const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
+  const int lane = pin((int)(threadIdx.x & 31)), gq = pin(lane >> 3), bq = pin(lane & 7);
   const int nwarp = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   // this lane's slot of stage 0 of this warp's ring; slot of connection 4q + gq = + q * 512
-  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring_smem) +
-                         (uint32_t)(threadIdx.x >> 5) * D * kRingStageBytes + (uint32_t)lane * 16u;
+  const uint32_t ring0 = pin((uint32_t)__cvta_generic_to_shared(ring_smem) +
+                             (uint32_t)(threadIdx.x >> 5) * D * kRingStageBytes + (uint32_t)lane * 16u);
   const uint64_t pol_l = policy_evict_last();
   const int B = a.B;
-  float* const hb = a.hd + 4 * bq;
+  float* const hb = pin(a.hd + 4 * bq);
   float* const W = a.W; float* const mW = a.mW; float* const vW = a.vW;
   const int* const idx = a.idx; const int* const pos = a.pos;
   const float grad_scale = a.grad_scale;
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
   const uint32_t split = a.split;
   const int64_t jb = a.j_begin, je = a.j_end;
   const int br = a.br;
-  const int b = 4 * bq + gq;                            // this lane's own sample
+  const int b = pin(4 * bq + gq);                       // this lane's own sample
   const bool bvalid = b < B;
   float loss_acc = 0.0f;
 
