@@ -483,25 +483,26 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
   const bool want_loss = a.loss != nullptr, check = a.check_finite != 0, sqh = a.sqh != 0;
   const uint32_t split = a.split;
   const int64_t jb = a.j_begin, je = a.j_end;
-  const int br = a.br;
   const int b = pin(4 * bq + gq);                       // this lane's own sample
   const bool bvalid = b < B;
   float loss_acc = 0.0f;
 
-  // this warp's rows: blocks w, w + nwarp, ...; cursor = (first row of the block relative
-  // to j_begin, row in block, rows in block).  32-bit row arithmetic: L * k < 2^31.
-  const uint32_t nrows = (uint32_t)(je - jb), jb32 = (uint32_t)jb, bstride = (uint32_t)nwarp * (uint32_t)br;
-  struct Cur { uint32_t j0; int i, nl; };
-  auto nl_of = [&](uint32_t j0) { return (int)min((uint32_t)br, nrows - j0); };
-  auto adv = [&](Cur c) {
-    if (++c.i >= c.nl) { c.j0 += bstride; c.i = 0; c.nl = c.j0 < nrows ? nl_of(c.j0) : 0; }
-    return c;
-  };
-  auto live = [&](const Cur& c) { return c.j0 < nrows; };
-  auto row_of = [&](const Cur& c) { return jb32 + c.j0 + (uint32_t)c.i; };
+  // this warp's rows: the contiguous range [r_lo, r_hi) of the launch's rows (relative to
+  // j_begin), walked one row at a time; the per-label vectors (bias, moments, positive mask)
+  // are handled in blocks of 32 rows from r_lo (lane i <-> row block + i).  The cursor is the
+  // row index alone (32-bit: L * k < 2^31).
+  const uint32_t nrows = (uint32_t)(je - jb), jb32 = (uint32_t)jb;
+  const uint32_t wq = (uint32_t)global_warp();
+  const uint32_t r_lo = (uint32_t)(((uint64_t)nrows * wq) / (uint32_t)nwarp);
+  const uint32_t r_hi = (uint32_t)(((uint64_t)nrows * (wq + 1)) / (uint32_t)nwarp);
+  using Cur = uint32_t;
+  auto adv = [&](Cur c) { return c + 1u; };
+  auto live = [&](Cur c) { return c < r_hi; };
+  auto row_of = [&](Cur c) { return jb32 + c; };
+  auto i_of = [&](Cur c) { return (int)((c - r_lo) & 31u); };
 
   struct St { float w, mw, vw; int c, pe; };
-  auto load_st = [&](const Cur& cu, St& st) {
+  auto load_st = [&](Cur cu, St& st) {
     if (live(cu)) {
       const uint32_t row = row_of(cu) * 32u + lane;
       st.w = ld_na(W + row);
@@ -512,15 +513,15 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     }
   };
   struct Bv { float bias, mb, vb; uint32_t pm; };
-  auto load_bv = [&](const Cur& cu, Bv& v) {
+  auto load_bv = [&](Cur cu, Bv& v) {                   // cu = the first row of a block
     v.bias = v.mb = v.vb = 0.0f; v.pm = 0u;
-    if (live(cu) && lane < cu.nl) {
-      const uint32_t j = jb32 + cu.j0 + lane;
+    if (live(cu) && (uint32_t)lane < r_hi - cu) {
+      const uint32_t j = jb32 + cu + lane;
       v.bias = ld_na(a.bias + j); v.mb = ld_na(a.mb + j); v.vb = ld_na(a.vb + j); v.pm = a.posmask[j];
     }
   };
   // gathers of one row into ring stage `stg` (always commits a group, possibly empty)
-  auto issue = [&](const Cur& cu, const St& st, uint32_t stg) {
+  auto issue = [&](Cur cu, const St& st, uint32_t stg) {
     if (live(cu)) {
       const uint32_t dst = ring0 + stg * (uint32_t)kRingStageBytes;
 #pragma unroll
@@ -532,9 +533,8 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     cp_async_commit();
   };
 
-  Cur X{(uint32_t)global_warp() * (uint32_t)br, 0, 0};
+  Cur X = r_lo;
   if (live(X)) {                                        // (no early return: block_atomic_add syncs)
-  X.nl = nl_of(X.j0);
   // rows X .. X+D-2 in flight before the loop; states of rows X .. X+D-1 loaded
   Cur q_cur[D];
   St q_st[D];
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     for (int d = 0; d < D - 1; ++d) { q_cur[d] = q_cur[d + 1]; q_st[d] = q_st[d + 1]; }
     q_cur[D - 1] = adv(q_cur[D - 2]);
     load_st(q_cur[D - 1], q_st[D - 1]);
-    if (live(q_cur[0]) && q_cur[0].i == 0) load_bv(q_cur[0], bv_next);
+    if (live(q_cur[0]) && i_of(q_cur[0]) == 0) load_bv(q_cur[0], bv_next);
 
     cp_async_wait<D - 1>();                             // this row's group is complete
     float4 hv[NG];
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     for (int q = 0; q < NG; ++q) ws[q] = __shfl_sync(kFull, st.w, 4 * q + gq);
 
     const uint32_t j = row_of(cu);
-    const int i = cu.i;
+    const int i = i_of(cu);
     const float bj = __shfl_sync(kFull, bv.bias, i);
     const uint32_t pm = __shfl_sync(kFull, bv.pm, i);
     const float y = row_score_own<NG>(ws, hv, gq, bj);
@@ -619,8 +619,8 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     st_na(W + row, st.w);
     st_na(mW + row, st.mw);
     st_na(vW + row, st.vw);
-    if (i == cu.nl - 1) {                                // block done: vectorized bias update
-      const uint32_t jl = jb32 + cu.j0 + lane;
+    if (i == 31 || cu + 1u == r_hi) {                   // block done: vectorized bias update
+      const uint32_t jl = jb32 + (cu - (uint32_t)i) + lane;
       if (lane <= i) {
         if (bv.pm != 0u) a.posmask[jl] = 0u;
         if (STORE_GRADS) a.db[jl] = db_v;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     }
     stg = stg + 1 == (uint32_t)D ? 0u : stg + 1;
     if (!live(q_cur[0])) break;
-    if (q_cur[0].i == 0) bv = bv_next;
+    if (i_of(q_cur[0]) == 0) bv = bv_next;
   }
   cp_async_wait<0>();
   }
