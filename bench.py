@@ -44,6 +44,8 @@ def args_():
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--shape", default="amazon-670k")
+    p.add_argument("--batch", type=int, default=0,
+                   help="override the shape's mini-batch B (default: the paper's 32, P:685); for batch sweeps")
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--flags", type=int, default=0, help="extra ff_config.flags (A/B experiments)")
@@ -500,6 +502,9 @@ def main():
     a = args_()
     from paper_2306_03725_b200 import synth
     shape = synth.SHAPES[a.shape]
+    if a.batch:
+        import dataclasses
+        shape = dataclasses.replace(shape, B=a.batch)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
