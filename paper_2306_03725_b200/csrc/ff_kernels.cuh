@@ -662,6 +662,64 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
   const int* cp = col_ptr + (int64_t)tile * m;
   const int jb = (int)j_begin;
   const uint32_t gstride = 32u * (uint32_t)nb;               // floats per gT row
+  if (NB1) {
+    // B <= 32: the entries (row, weight) of the next batch — in this column, or the first
+    // batch of the warp's next column — are loaded while the current batch's gathers run, so
+    // the entry stream's DRAM latency is not exposed once per batch.  Same per-lane order of
+    // the FMAs and the same final reduction as below: bit-identical dh.
+    const float* gb = gT + 4 * bq;
+    auto load_ent = [&](int p, int pend, int& jr, float& wv) {
+      const bool ok = p + lane < pend;
+      jr = ok ? ld_na_ro(ent_row + p + lane) : jb;
+      wv = ok ? ld_na(wcsc + p + lane) : 0.0f;
+    };
+    int c = c_begin + (int)global_warp();
+    int p0 = 0, p1 = 0, jr_n = jb; float wv_n = 0.0f;
+    if (c < m) { p0 = cp[c]; p1 = cp[c + 1]; load_ent(p0, p1, jr_n, wv_n); }
+    for (; c < m; c += nw) {
+      const int cn = c + nw;
+      int q0 = 0, q1 = 0;
+      if (cn < m) { q0 = cp[cn]; q1 = cp[cn + 1]; }
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = p0; p < p1; p += 32) {
+        const int jr = jr_n; const float wv = wv_n;
+        if (p + 32 < p1) load_ent(p + 32, p1, jr_n, wv_n);        // next batch, same column
+        else if (cn < m) load_ent(q0, q1, jr_n, wv_n);            // first batch of the next column
+        const bool tail = p + 32 > p1;
+        float4 gv[8]; float ww[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t grow = (uint32_t)(__shfl_sync(kFull, jr, 4 * u + gq) - jb);
+          ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
+          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if ((!tail || p + 4 * u + gq < p1) && ww[u] != 0.0f) gv[u] = ld_line4(col_line(gb, grow, gstride), pol_l);
+        }
+        float2 a01 = lo2(acc), a23 = hi2(acc);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a01 = ffma2(bc2(ww[u]), lo2(gv[u]), a01);
+          a23 = ffma2(bc2(ww[u]), hi2(gv[u]), a23);
+        }
+        acc = make_float4(a01.x, a01.y, a23.x, a23.y);
+      }
+      if (p0 == p1 && cn < m) load_ent(q0, q1, jr_n, wv_n);        // empty column: prefetch here
+#pragma unroll
+      for (int o = 8; o <= 16; o <<= 1) {
+        acc.x += __shfl_xor_sync(kFull, acc.x, o); acc.y += __shfl_xor_sync(kFull, acc.y, o);
+        acc.z += __shfl_xor_sync(kFull, acc.z, o); acc.w += __shfl_xor_sync(kFull, acc.w, o);
+      }
+      if (gq == 0) {
+        float4* dst = reinterpret_cast<float4*>(hd + (int64_t)c * 64 + 32 + 4 * bq);
+        if (tile > 0) {
+          const float4 o = *dst;
+          acc = make_float4(o.x + acc.x, o.y + acc.y, o.z + acc.z, o.w + acc.w);
+        }
+        *dst = acc;
+      }
+      p0 = q0; p1 = q1;
+    }
+    return;
+  }
   for (int c = c_begin + (int)global_warp(); c < m; c += nw) {
     const int p0 = cp[c], p1 = cp[c + 1];
     for (int q2 = 0; q2 < nb; ++q2) {
