@@ -1245,6 +1245,15 @@ __global__ void __launch_bounds__(256) k_merge_topk_block(const float* __restric
   for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
   for (int l = threadIdx.x; l < nlist; l += blockDim.x) {
     const int64_t base = (int64_t)l * list_stride + (int64_t)b * sample_stride;
+    if (Kin == kTopkMax && (base & 3) == 0) {                // whole 8-entry lists: 16-B loads
+      const float4 s0 = *reinterpret_cast<const float4*>(in_s + base), s1 = *reinterpret_cast<const float4*>(in_s + base + 4);
+      const int4 i0 = *reinterpret_cast<const int4*>(in_i + base), i1 = *reinterpret_cast<const int4*>(in_i + base + 4);
+      const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const int iv[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) topk_consider(ts, ti, sv[q], iv[q]);
+      continue;
+    }
     for (int q = 0; q < Kin; ++q) {
       const float s = in_s[base + q]; const int i = in_i[base + q];
       if (!better(s, i, ts[kTopkMax - 1], ti[kTopkMax - 1])) break;   // lists are sorted
