@@ -465,6 +465,12 @@ def run_ours(a, shape, world, rank, local_rank):
                    "ceiling_gbs": ONCHIP_CEILING_GBS.get(a.dh_mode),
                    "kernel_frac_of_ceiling": (onchip / (k_step_ms * 1e-3) / 1e9 / ONCHIP_CEILING_GBS[a.dh_mode]
                                               if a.dh_mode in ONCHIP_CEILING_GBS else None),
+                   # The state stream (W, idx, moments, bias) also passes through the L2 slices: the kernel's
+                   # total L2 rate is the gather/red bytes plus its algorithmic HBM bytes over its duration.
+                   "kernel_l2_total_gbs": (onchip + kb) / (k_step_ms * 1e-3) / 1e9,
+                   "kernel_l2_total_frac_of_ceiling": ((onchip + kb) / (k_step_ms * 1e-3) / 1e9
+                                                       / ONCHIP_CEILING_GBS[a.dh_mode]
+                                                       if a.dh_mode in ONCHIP_CEILING_GBS else None),
                    "note": ("h 128-B line gather + dh 128-B red.v4 per connection" if a.dh_mode == "atomic" else
                             "h 128-B line gather (row pass) + g 128-B line gather (CSC column pass) per connection")
                            + "; measured ceilings (profiles/r01_l2bench.txt): gather ~19.9 TB/s, red ~6.3-6.6 TB/s"},
