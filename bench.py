@@ -392,6 +392,28 @@ def run_ours(a, shape, world, rank, local_rank):
     barrier()
     ms_pred = max_over_ranks(e0.elapsed_time(e1))
 
+    # ---- row a7 on its own: one redistribution (prune + Philox regrow + moment reset, and the
+    # CSC rebuild in csc/hybrid mode), which the timed train loop amortises over 1000 steps.
+    # Algorithmic bytes: read W and idx (8 B per connection) + write idx, W, mW, vW of the
+    # p = floor(0.1 k) regrown slots per row (16 B each).
+    n_red = 5
+    layer.redistribute(10 ** 6)
+    barrier()
+    e0.record(stream)
+    for r in range(n_red):
+        layer.redistribute(10 ** 6 + 1000 * (r + 1))
+    e1.record(stream)
+    barrier()
+    ms_red = max_over_ranks(e0.elapsed_time(e1)) / n_red
+    p_slots = (shape.k * 10) // 100
+    red_bytes = 8.0 * L_local * shape.k + 16.0 * L_local * p_slots
+    redist = {"ms_per_call": ms_red, "amortised_ms_per_step": ms_red / REDIST_EVERY,
+              "share_of_step": ms_red / REDIST_EVERY / (ms / a.steps),
+              "alg_bytes": red_bytes, "achieved_gbs": red_bytes / (ms_red * 1e-3) / 1e9,
+              "frac": red_bytes / (ms_red * 1e-3) / 1e9 / peaks()[0],
+              "note": "prune p = floor(0.1 k) smallest |W| per row, regrow by Philox (seed, step, row)"
+                      + ("; includes the CSC rebuild" if a.dh_mode != "atomic" else "")}
+
     # ---- NEXT-3: large-batch inference and shortlist scoring, one GPU
     big = model = None
     if world == 1:
@@ -478,6 +500,7 @@ def run_ours(a, shape, world, rank, local_rank):
                     "ms_per_batch": ms_pred / n_pred,
                     "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,
                     "frac": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9 / peak},
+        "redistribution": redist,
         "inference_large_batch": big,
         "model": model if world == 1 else None,
     }

@@ -934,34 +934,47 @@ __global__ void k_init(float* __restrict__ W, int* __restrict__ idx, float* __re
 __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, float* __restrict__ mW,
                                float* __restrict__ vW, int64_t L, int64_t row_begin, int m, int k,
                                int p, uint32_t step, uint32_t key0, uint32_t key1) {
+  // The p pruned slots are the p smallest (|W| bits, slot) keys of the row (R9), found by p
+  // rounds of a warp min (redux.sync) + lowest-lane ballot: the same set as ranking every slot
+  // against every other.  The next row's W and idx are loaded while this row is processed.
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t thr = (uint32_t)(0x100000000ull % (uint64_t)m);
-  const int KPL = k > 32 ? 2 : 1;
-  for (int64_t j = global_warp(); j < L; j += nw) {
-    bool act[2]; int c[2]; uint32_t key[2]; int rank[2] = {0, 0};
+  bool act[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) act[e] = lane + 32 * e < k;
+  float w_n[2] = {0.0f, 0.0f}; int c_n[2] = {-1, -1};
+  auto load = [&](int64_t jj) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (act[e]) { w_n[e] = ld_na(W + jj * k + lane + 32 * e); c_n[e] = idx[jj * k + lane + 32 * e]; }   // idx is written here: no .nc
+  };
+  int64_t j = global_warp();
+  if (j < L) load(j);
+  for (; j < L; j += nw) {
+    int c[2]; uint32_t key[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int slot = lane + 32 * e;
-      act[e] = slot < k;
-      const float w = act[e] ? W[j * k + slot] : 0.0f;
-      c[e] = act[e] ? idx[j * k + slot] : -1;
-      key[e] = act[e] ? (__float_as_uint(w) & 0x7fffffffu) : 0xffffffffu;
+      c[e] = c_n[e];
+      key[e] = act[e] ? (__float_as_uint(w_n[e]) & 0x7fffffffu) : 0xffffffffu;
     }
-    for (int e2 = 0; e2 < KPL; ++e2) {                 // compare with every slot q of the row
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const uint32_t kq = __shfl_sync(kFull, key[e2], q);
-        const int sq = q + 32 * e2;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int se = lane + 32 * e;
-          rank[e] += (kq < key[e] || (kq == key[e] && sq < se)) ? 1 : 0;
-        }
+    if (j + nw < L) load(j + nw);
+    uint32_t pm0 = 0u, pm1 = 0u;                       // pruned slots (bit = lane), halves e = 0, 1
+    for (int r = 0; r < p; ++r) {
+      const uint32_t kmin = __reduce_min_sync(kFull, min(key[0], key[1]));
+      const uint32_t b0 = __ballot_sync(kFull, act[0] && key[0] == kmin);
+      const uint32_t b1 = __ballot_sync(kFull, act[1] && key[1] == kmin);
+      if (b0 != 0u) {                                   // lowest slot first (R9)
+        const uint32_t bit = b0 & (0u - b0);
+        pm0 |= bit;
+        if (lane == __ffs(b0) - 1) key[0] = 0xffffffffu;
+      } else {
+        const uint32_t bit = b1 & (0u - b1);
+        pm1 |= bit;
+        if (lane == __ffs(b1) - 1) key[1] = 0xffffffffu;
       }
     }
-    const bool pruned0 = act[0] && rank[0] < p, pruned1 = act[1] && rank[1] < p;
-    const uint32_t pm0 = __ballot_sync(kFull, pruned0), pm1 = __ballot_sync(kFull, pruned1);
+    const bool pruned0 = (pm0 >> lane) & 1u, pruned1 = (pm1 >> lane) & 1u;
     const uint32_t grow = (uint32_t)(row_begin + j);
     int acc = -1, na = 0;                              // accepted draws: lane q holds draw q (p <= 32)
     for (uint32_t n = 0; na < p; ++n) {
@@ -1129,11 +1142,19 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7, wid = threadIdx.x >> 5;
   float* const cbs = &ss[wid][0][0];
   int* const cbi = &si[wid][0][0];
-  const uint32_t nwarp = (uint32_t)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring_smem) + (uint32_t)wid * D * kStage + (uint32_t)lane * 16u;
-  const float* const hb = hd + 4 * bq;
+  // thread constants pinned in registers (see pin()): the source lanes 4q + gq of the
+  // per-connection shuffles, the ring slot, the h-line base and the state pointers
+  const uint32_t nwarp = pin((uint32_t)(((int64_t)gridDim.x * blockDim.x) >> 5));
+  const uint32_t ring0 = pin((uint32_t)__cvta_generic_to_shared(ring_smem) + (uint32_t)wid * D * kStage + (uint32_t)lane * 16u);
+  const float* const hb = pin(hd + 4 * bq);
+  const float* const Wp = pin(W);
+  const int* const idxp = pin(idx);
+  const float* const biasp = pin(bias);
+  int sl[NG];
+#pragma unroll
+  for (int q = 0; q < NG; ++q) sl[q] = pin(4 * q + gq);
   const int b = 4 * bq + gq;
-  const uint32_t nrows = (uint32_t)L;
+  const uint32_t nrows = pin((uint32_t)L);
   float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll
   for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
@@ -1148,9 +1169,9 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   struct St { float w, bj; int c; };
   auto load_st = [&](uint32_t j, St& st) {
     if (j < nrows) {
-      st.w = ld_na(W + j * 32u + lane);
-      st.c = ld_na_ro(idx + j * 32u + lane);
-      st.bj = ld_na(bias + j);
+      st.w = ld_na(Wp + j * 32u + lane);
+      st.c = ld_na_ro(idxp + j * 32u + lane);
+      st.bj = ld_na(biasp + j);
     }
   };
   auto issue = [&](uint32_t j, const St& st, uint32_t stg) {
@@ -1158,7 +1179,7 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
       const uint32_t dst = ring0 + stg * kStage;
 #pragma unroll
       for (int q = 0; q < NG; ++q) {
-        const uint32_t c = (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq);
+        const uint32_t c = (uint32_t)__shfl_sync(kFull, st.c, sl[q]);
         cp_async16(dst + (uint32_t)q * 512u, col_line(hb, c, kColFloats));
       }
     }
@@ -1187,7 +1208,7 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
     for (int q = 0; q < NG; ++q) hv[q] = lds4(src + (uint32_t)q * 512u);
     float ws[NG];
 #pragma unroll
-    for (int q = 0; q < NG; ++q) ws[q] = __shfl_sync(kFull, st.w, 4 * q + gq);
+    for (int q = 0; q < NG; ++q) ws[q] = __shfl_sync(kFull, st.w, sl[q]);
     const float y = row_score_own<NG>(ws, hv, gq, st.bj);
     // candidates better than the lane's current K-th best are appended to its buffer (no
     // divergent insertion per row); a full buffer in any lane flushes the warp's buffers

@@ -290,6 +290,26 @@ def test_redistribution_bit_exact(L, m, k, frac, step):
     assert all(len(set(r)) == k for r in s["idx"])
 
 
+@pytest.mark.parametrize("k", [16, 32, 48])
+def test_redistribution_all_ties(k):
+    """Rows whose |W| are all equal (incl. +-0): the p lowest slots are pruned (R9)."""
+    L, m = 600, 1024
+    lay = make(L, m, k, seed=5, prune_frac=0.1)
+    W, idx, _ = synth.random_params(L, m, k, seed=4)
+    W[::2, :] = 0.0
+    W[1::4, :] = np.where(np.arange(k) % 2 == 0, 0.5, -0.5).astype(np.float32)
+    W[3::8, ::3] = -0.0
+    lay.set_params(W=tens(W), idx=tens(idx))
+    lay.redistribute(1000)
+    s = state_of(lay)
+    z = np.zeros_like(W)
+    p = int(np.floor(F32(0.1) * k))
+    W2, idx2, _, _ = oracle.redistribute(W, idx, z, z, m, p, seed=5, step=1000)
+    assert (s["idx"] == idx2).all() and (s["W"] == W2).all()
+    pruned = (s["idx"] != idx)
+    assert (pruned[::2].sum(axis=1) == p).all() and pruned[::2, :p].all()
+
+
 def test_redistribution_config_errors():
     layer = L_()
     lay = make(100, 64, 8, prune_frac=0.05)          # floor(0.05*8) = 0
