@@ -166,8 +166,11 @@ ff_status fixedfanin_train_step(ff_layer* layer, const float* h, int32_t B,
 /* Same as train_step with HOST inputs/outputs (end-to-end path): copies h_host [B][m]
  * and the label CSR (host) into one of two workspace staging slots on a library-owned copy
  * stream (so that, with pinned memory, the next call's copy overlaps this call's kernels;
- * `stream` waits for the copy with an event), runs the fused step on `stream`, then copies
- * the loss (and dh if dh_host != NULL) back on `stream`.  The host inputs must stay
+ * `stream` waits for the copy with an event), runs the fused step on `stream`, then returns
+ * the loss (if loss_host != NULL) and dh (if dh_host != NULL) on `stream`.  A page-locked
+ * loss_host is written by a one-thread kernel store (mapped memory, no copy-engine
+ * operation); a pageable one by cudaMemcpyAsync.  dh_host == NULL skips the [B][m] copy-out
+ * of dh (it is still computed).  The host inputs must stay
  * unmodified, and the host outputs are valid, once `stream` is synchronized.
  * lbl_ptr_host[B] <= max_nnz (read on the host for the copy size).                      */
 ff_status fixedfanin_train_step_host(ff_layer* layer, const float* h_host, int32_t B,

@@ -1003,6 +1003,12 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
   }
 }
 
+// The host entry point's loss output: one store into page-locked host memory (mapped,
+// device-addressable), instead of a copy-engine D2H on the step's stream.
+__global__ void k_store_scalar(const float* __restrict__ src, float* dst) {
+  if (threadIdx.x == 0) { *dst = *src; __threadfence_system(); }
+}
+
 // Validation for set_params: idx in [0, m), distinct within each row (k <= 64).
 __global__ void k_validate_idx(const int* __restrict__ idx, int64_t L, int m, int k, int* err) {
   const int lane = threadIdx.x & 31;

@@ -361,10 +361,12 @@ ff_status csc_rebuild(ff_layer* l, cudaStream_t st) {
 
 // hd_ready: h is already in the h half of hd and (atomic mode) the dh half is zero (the
 // model step's dense forward wrote them); dh then stays in hd (dh may be NULL).
+// dh_optional (host entry point): dh == NULL skips only the [B][m] copy-out of dh.
 ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t* lbl_ptr, const int32_t* lbl_ids,
-                          float grad_scale, float lr, float* dh, float* loss, cudaStream_t st, bool hd_ready = false) {
+                          float grad_scale, float lr, float* dh, float* loss, cudaStream_t st, bool hd_ready = false,
+                          bool dh_optional = false) {
   if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
-  if ((!hd_ready && (!ptr_ok(h, B) || !ptr_ok(dh, B))) || lbl_ptr == nullptr)
+  if ((!hd_ready && (!ptr_ok(h, B) || (!dh_optional && !ptr_ok(dh, B)))) || lbl_ptr == nullptr)
     return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
   ff_status s = launch_prep(l, hd_ready ? nullptr : h, B, (!l->csc || l->split > 0) && !hd_ready, lbl_ptr, lbl_ids,
                             loss, st);
@@ -806,12 +808,27 @@ ff_status fixedfanin_train_step_host(ff_layer* l, const float* h_host, int32_t B
   if (nnz) FF_CUDA(cudaMemcpyAsync(lbl_stage + B + 1, lbl_ids_host, 4 * (size_t)nnz, cudaMemcpyHostToDevice, l->copy_st));
   FF_CUDA(cudaEventRecord(l->ev_ready[slot], l->copy_st));
   FF_CUDA(cudaStreamWaitEvent(st, l->ev_ready[slot], 0));
-  ff_status s = train_step_impl(l, h_stage, B, lbl_stage, lbl_stage + B + 1, grad_scale, lr, l->dh_stage,
-                                l->loss_scratch, st);
-  const int32_t launches = g_launches;
+  // dh is copied out to [B][m] only when the caller asks for it
+  ff_status s = train_step_impl(l, h_stage, B, lbl_stage, lbl_stage + B + 1, grad_scale, lr,
+                                dh_host ? l->dh_stage : nullptr, l->loss_scratch, st, false, true);
+  int32_t launches = g_launches;
   if (s != FF_OK) return s;
   FF_CUDA(cudaEventRecord(l->ev_free[slot], st));
-  if (loss_host) FF_CUDA(cudaMemcpyAsync(loss_host, l->loss_scratch, 4, cudaMemcpyDeviceToHost, st));
+  if (loss_host) {
+    // pinned (page-locked) host memory is device-addressable: one thread stores the loss
+    // there right after the step's last kernel, with no copy-engine operation on `stream`
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, loss_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        pa.devicePointer != nullptr;
+    if (!pinned) cudaGetLastError();       // clear a pageable-pointer query error
+    if (pinned) {
+      k_store_scalar<<<1, 32, 0, st>>>(l->loss_scratch, static_cast<float*>(pa.devicePointer));
+      FF_LAUNCHED();
+      ++launches;
+    } else {
+      FF_CUDA(cudaMemcpyAsync(loss_host, l->loss_scratch, 4, cudaMemcpyDeviceToHost, st));
+    }
+  }
   if (dh_host && hb) FF_CUDA(cudaMemcpyAsync(dh_host, l->dh_stage, hb, cudaMemcpyDeviceToHost, st));
   g_launches = launches;
   return FF_OK;

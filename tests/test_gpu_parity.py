@@ -486,6 +486,27 @@ def test_host_entry_point_double_buffering_over_many_steps(dh_mode):
         assert (sa[key] == sb[key]).all(), key
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_entry_point_loss_output(pinned):
+    """The loss of every host-entry step reaches host memory: page-locked (kernel store into
+    mapped memory) or pageable (cudaMemcpyAsync); dh_host = None skips only the copy-out."""
+    L, m, k, B = 2000, 512, 32, 32
+    a, b = make(L, m, k, B=B, seed=8), make(L, m, k, B=B, seed=8)
+    loss_host = torch.empty(1).pin_memory() if pinned else torch.empty(1)
+    loss = torch.zeros(1, device=dev())
+    for s in range(4):
+        h = synth.hidden_batch(B, m, step=s)
+        ptr, ids = synth.label_batch(B, L, 5.0, step=s)
+        loss_host.fill_(-1.0)
+        a.train_step_host(torch.from_numpy(h).pin_memory(), torch.from_numpy(ptr), torch.from_numpy(ids), 1e-3,
+                          loss_host=loss_host)
+        b.train_step(tens(h), tens(ptr), tens(ids), 1e-3, loss=loss)
+        torch.cuda.synchronize()
+        assert abs(loss_host.item() - loss.item()) <= 1e-5 * loss.item(), s
+    sa, sb = state_of(a), state_of(b)
+    assert (sa["W"] == sb["W"]).all() and (sa["vW"] == sb["vW"]).all()
+
+
 def test_csc_dh_is_deterministic_and_matches_atomic():
     L, m, k, B = 3000, 1024, 32, 32
     a, b = make(L, m, k, B=B, seed=2, dh_mode=1), make(L, m, k, B=B, seed=2, dh_mode=0)
