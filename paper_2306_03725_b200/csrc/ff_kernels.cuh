@@ -799,27 +799,44 @@ __global__ void k_csc_finish(const int* __restrict__ skeys, const int* __restric
 // ------------------------------------------------------------------------------ prep
 // hd[c][q2][r] = h[q2*32 + r][c] (0 for samples >= B), hd[c][q2][32 + r] = 0 (dh
 // accumulator), positives -> posmask bits, *loss = 0.  Grid: ceil(m/32) blocks of 32x8.
+// VEC (m % 4 == 0, 16-B aligned h): 16-B loads of h rows and 16-B stores of the lines,
+// through a conflict-free [32][33] shared tile (scalar smem accesses).
+template <bool VEC>
 __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float* __restrict__ hd, int zero_dh,
                        const int* __restrict__ lbl_ptr, const int* __restrict__ lbl_ids,
                        uint32_t* __restrict__ posmask, int64_t L_local, int64_t row_begin,
                        int64_t L_global, float* loss, int* err) {
   __shared__ float t[32][33];
-  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int c0 = blockIdx.x * 32;
   const int cstride = 64 * nb;
   if (h != nullptr) {
     for (int q2 = 0; q2 < nb; ++q2) {
-      for (int r = ty; r < 32; r += 8) {
-        const int b = q2 * 32 + r, c = c0 + tx;
-        t[r][tx] = (b < B && c < m) ? h[(int64_t)b * m + c] : 0.0f;
-      }
-      __syncthreads();
-      for (int r = ty; r < 32; r += 8) {
-        const int c = c0 + r;
-        if (c < m) {
-          float* line = hd + (int64_t)c * cstride + q2 * 64;
-          line[tx] = t[tx][r];
-          if (zero_dh) line[32 + tx] = 0.0f;
+      if (VEC) {
+        const int r = tid >> 3, c4 = tid & 7, b = q2 * 32 + r, c = c0 + 4 * c4;
+        const float4 v = (b < B && c < m) ? *reinterpret_cast<const float4*>(h + (int64_t)b * m + c)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        t[4 * c4][r] = v.x; t[4 * c4 + 1][r] = v.y; t[4 * c4 + 2][r] = v.z; t[4 * c4 + 3][r] = v.w;
+        __syncthreads();
+        const int cl = tid >> 3, q = tid & 7;
+        if (c0 + cl < m) {
+          float* line = hd + (int64_t)(c0 + cl) * cstride + q2 * 64;
+          *reinterpret_cast<float4*>(line + 4 * q) = make_float4(t[cl][4 * q], t[cl][4 * q + 1], t[cl][4 * q + 2], t[cl][4 * q + 3]);
+          if (zero_dh) *reinterpret_cast<float4*>(line + 32 + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else {
+        for (int r = ty; r < 32; r += 8) {
+          const int b = q2 * 32 + r, c = c0 + tx;
+          t[r][tx] = (b < B && c < m) ? h[(int64_t)b * m + c] : 0.0f;
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+          const int c = c0 + r;
+          if (c < m) {
+            float* line = hd + (int64_t)c * cstride + q2 * 64;
+            line[tx] = t[tx][r];
+            if (zero_dh) line[32 + tx] = 0.0f;
+          }
         }
       }
       __syncthreads();
@@ -839,11 +856,25 @@ __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float*
   if (loss != nullptr && blockIdx.x == 0 && tx == 0 && ty == 0) *loss = 0.0f;
 }
 
-// dh[b][c] = hd[c][b/32][32 + b%32] for b < B.  Grid ceil(m/32) x nb, 32x8 threads.
+// dh[b][c] = hd[c][b/32][32 + b%32] for b < B.  Grid ceil(m/32) x nb, 32x8 threads; VEC as
+// in k_prep (16-B line loads and 16-B dh row stores).
+template <bool VEC>
 __global__ void k_dh_out(const float* __restrict__ hd, int B, int m, int nb, float* __restrict__ dh) {
   __shared__ float t[32][33];
-  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int c0 = blockIdx.x * 32, q2 = blockIdx.y;
+  if (VEC) {
+    const int cl = tid >> 3, q = tid & 7;
+    const float4 v = (c0 + cl < m) ? *reinterpret_cast<const float4*>(hd + (int64_t)(c0 + cl) * 64 * nb + q2 * 64 + 32 + 4 * q)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    t[cl][4 * q] = v.x; t[cl][4 * q + 1] = v.y; t[cl][4 * q + 2] = v.z; t[cl][4 * q + 3] = v.w;
+    __syncthreads();
+    const int r = tid >> 3, c4 = tid & 7, b = q2 * 32 + r, c = c0 + 4 * c4;
+    if (b < B && c < m)
+      *reinterpret_cast<float4*>(dh + (int64_t)b * m + c) =
+          make_float4(t[4 * c4][r], t[4 * c4 + 1][r], t[4 * c4 + 2][r], t[4 * c4 + 3][r]);
+    return;
+  }
   for (int r = ty; r < 32; r += 8) {
     const int c = c0 + r;
     t[r][tx] = (c < m) ? hd[(int64_t)c * 64 * nb + q2 * 64 + 32 + tx] : 0.0f;

@@ -182,8 +182,10 @@ ff_status launch_prep(ff_layer* l, const float* h, int B, bool zero_dh, const in
                       const int* lbl_ids, float* loss, cudaStream_t st) {
   const int nb = nb_of(B);
   dim3 grid((l->cfg.m + 31) / 32), block(32, 8);
-  k_prep<<<grid, block, 0, st>>>(h, B, l->cfg.m, nb, l->hd, zero_dh ? 1 : 0, lbl_ptr, lbl_ids, l->posmask,
-                                 l->cfg.L_local, l->cfg.row_begin, l->cfg.L_global, loss, l->err);
+  const bool vec = (l->cfg.m & 3) == 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0;
+  (vec ? k_prep<true> : k_prep<false>)<<<grid, block, 0, st>>>(h, B, l->cfg.m, nb, l->hd, zero_dh ? 1 : 0, lbl_ptr,
+                                                                lbl_ids, l->posmask, l->cfg.L_local, l->cfg.row_begin,
+                                                                l->cfg.L_global, loss, l->err);
   FF_LAUNCHED();
   return FF_OK;
 }
@@ -191,7 +193,8 @@ ff_status launch_prep(ff_layer* l, const float* h, int B, bool zero_dh, const in
 ff_status launch_dh_out(ff_layer* l, int B, float* dh, cudaStream_t st) {
   const int nb = nb_of(B);
   dim3 grid((l->cfg.m + 31) / 32, nb), block(32, 8);
-  k_dh_out<<<grid, block, 0, st>>>(l->hd, B, l->cfg.m, nb, dh);
+  const bool vec = (l->cfg.m & 3) == 0 && (reinterpret_cast<uintptr_t>(dh) & 15) == 0;
+  (vec ? k_dh_out<true> : k_dh_out<false>)<<<grid, block, 0, st>>>(l->hd, B, l->cfg.m, nb, dh);
   FF_LAUNCHED();
   return FF_OK;
 }
