@@ -125,7 +125,8 @@ ff_status fixedfanin_set_params(ff_layer* layer, const float* W, const int32_t* 
                                 const float* mb, const float* vb, const int64_t* t_host,
                                 ff_stream_t stream);
 
-/* Copy the state into device arrays (any pointer may be NULL = skip); *t_host = Adam t. */
+/* Copy the state into device arrays (any pointer may be NULL = skip); *t_host = Adam t
+ * (read back from the device counter).  Synchronizes `stream`.                          */
 ff_status fixedfanin_get_params(ff_layer* layer, float* W, int32_t* idx, float* bias,
                                 float* mW, float* vW, float* mb, float* vb, int64_t* t_host,
                                 ff_stream_t stream);
@@ -157,7 +158,11 @@ ff_status fixedfanin_adam_step(ff_layer* layer, float lr, ff_stream_t stream);
 
 /* The fused training step: forward, BCE gradient, dW, db, dh (pre-update W) and Adam
  * (t += 1) in one pass over the label rows; y, g, dW are never written to HBM.
- * dh (device [B][m]) overwritten; loss as in backward (NULL = skip).                */
+ * dh (device [B][m]) overwritten; loss as in backward (NULL = skip).
+ * CUDA-graph capturable: it only enqueues kernels on `stream` (no host synchronisation),
+ * and the Adam step counter t and its bias corrections live on the device (advanced by the
+ * step's first kernel), so replays of a captured step take consecutive t.  A captured
+ * step reads h / labels from the captured addresses (copy new batches into them).      */
 ff_status fixedfanin_train_step(ff_layer* layer, const float* h, int32_t B,
                                 const int32_t* lbl_ptr, const int32_t* lbl_ids,
                                 float grad_scale, float lr, float* dh, float* loss,

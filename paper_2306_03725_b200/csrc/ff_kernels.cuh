@@ -47,6 +47,7 @@ struct RowArgs {
   float* y_out;               // forward: y[B][L]
   const float* y_in;          // backward: y[B][L]
   float* loss;                // device scalar (zeroed by prep) or nullptr
+  const float* rbc;           // train: device [rbc1, rbc2] of this step (written by k_prep), or nullptr
   int* err;
   AdamArgs adam;
   uint32_t check_finite;
@@ -249,8 +250,18 @@ __device__ __forceinline__ void row_dw_slots(const float (&dwp)[NG], int lane, f
 // blocks) and walks their rows one at a time, prefetching the next row's state.  Per-label
 // scalars (bias, its moments, the positive mask) are one coalesced vector per block
 // (lane i <-> row i) and the bias Adam update runs once per block, vectorized.
+// The Adam arguments of a training launch: the bias corrections of this step come from the
+// device (k_prep advanced the device step counter t and wrote them), so a captured step
+// replays with the right t.
+__device__ __forceinline__ AdamArgs step_adam(const RowArgs& a) {
+  AdamArgs ad = a.adam;
+  if (a.rbc != nullptr) { ad.rbc1 = a.rbc[0]; ad.rbc2 = a.rbc[1]; }
+  return ad;
+}
+
 template <int MODE, bool STORE_GRADS, int NG, bool CSC, bool FULL>
 __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_rows(RowArgs a) {
+  const AdamArgs adam = step_adam(a);
   constexpr int KPL = (NG + 7) / 8;                 // slots per lane (k <= 32 * KPL)
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -388,7 +399,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
         if (CSC && (uint32_t)c[e] >= a.split) a.wcsc[pe[e]] = gany ? w[e] : 0.0f;
         if (MODE == kModeBackward || STORE_GRADS) a.dW[r] = gW[e];
         if (MODE == kModeTrain) {
-          adam_update(w[e], mw[e], vw[e], gW[e], a.adam);
+          adam_update(w[e], mw[e], vw[e], gW[e], adam);
           st_stream(a.W + r, w[e], pol_s);
           st_stream(a.mW + r, mw[e], pol_s);
           st_stream(a.vW + r, vw[e], pol_s);
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       if (pm_v != 0u) a.posmask[j0 + lane] = 0u;      // self-clearing mask (chunk 0)
       if (MODE == kModeBackward || STORE_GRADS) a.db[j0 + lane] = db_v;
       if (MODE == kModeTrain) {                        // bias Adam, one row per lane
-        adam_update(bias_v, mb_v, vb_v, db_v, a.adam);
+        adam_update(bias_v, mb_v, vb_v, db_v, adam);
         st_stream(a.bias + j0 + lane, bias_v, pol_s);
         st_stream(a.mb + j0 + lane, mb_v, pol_s);
         st_stream(a.vb + j0 + lane, vb_v, pol_s);
@@ -465,6 +476,7 @@ __device__ __forceinline__ T* pin(T* p) { asm volatile("" : "+l"(p)); return p; 
 
 template <bool STORE_GRADS, int MODE>
 __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_train_ring(RowArgs a) {
+  const AdamArgs adam = step_adam(a);
   constexpr int NG = 8, D = RingCfg<MODE>::D;
   constexpr bool CSC = MODE != 0, HYB = MODE == 2;
   constexpr uint32_t kColFloats = 64;                   // hd column stride at nb = 1 (h | dh lines)
@@ -615,7 +627,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     if (lane == i) db_v = dbr;
     const uint32_t row = j * 32u + lane;
     if (STORE_GRADS) a.dW[row] = gW;
-    adam_update(st.w, st.mw, st.vw, gW, a.adam);
+    adam_update(st.w, st.mw, st.vw, gW, adam);
     st_na(W + row, st.w);
     st_na(mW + row, st.mw);
     st_na(vW + row, st.vw);
@@ -625,7 +637,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
         if (bv.pm != 0u) a.posmask[jl] = 0u;
         if (STORE_GRADS) a.db[jl] = db_v;
         float p = bv.bias, mo = bv.mb, ve = bv.vb;
-        adam_update(p, mo, ve, db_v, a.adam);
+        adam_update(p, mo, ve, db_v, adam);
         st_na(a.bias + jl, p);
         st_na(a.mb + jl, mo);
         st_na(a.vb + jl, ve);
@@ -805,9 +817,17 @@ template <bool VEC>
 __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float* __restrict__ hd, int zero_dh,
                        const int* __restrict__ lbl_ptr, const int* __restrict__ lbl_ids,
                        uint32_t* __restrict__ posmask, int64_t L_local, int64_t row_begin,
-                       int64_t L_global, float* loss, int* err) {
+                       int64_t L_global, float* loss, int* err, int64_t* t_dev, float* rbc, float beta1,
+                       float beta2) {
   __shared__ float t[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  if (t_dev != nullptr && blockIdx.x == 0 && tid == 0) {
+    // training step: t <- t + 1 and the Adam bias corrections 1/(1 - beta^t) (fp64, R6/R7)
+    const int64_t tn = *t_dev + 1;
+    *t_dev = tn;
+    rbc[0] = (float)(1.0 / (1.0 - pow((double)beta1, (double)tn)));
+    rbc[1] = (float)(1.0 / (1.0 - pow((double)beta2, (double)tn)));
+  }
   const int c0 = blockIdx.x * 32;
   const int cstride = 64 * nb;
   if (h != nullptr) {
@@ -887,11 +907,22 @@ __global__ void k_dh_out(const float* __restrict__ hd, int B, int m, int nb, flo
 }
 
 // ------------------------------------------------------------------------------ Adam
+// The device step counter of the unfused path (adam_step): as in k_prep.
+__global__ void k_step_t(int64_t* t_dev, float* rbc, float beta1, float beta2) {
+  if (threadIdx.x == 0) {
+    const int64_t tn = *t_dev + 1;
+    *t_dev = tn;
+    rbc[0] = (float)(1.0 / (1.0 - pow((double)beta1, (double)tn)));
+    rbc[1] = (float)(1.0 / (1.0 - pow((double)beta2, (double)tn)));
+  }
+}
+
 // Standalone Adam over W (with dW) and bias (with db).
 __global__ void k_adam(float* __restrict__ W, float* __restrict__ mW, float* __restrict__ vW,
                        const float* __restrict__ dW, int64_t n, float* __restrict__ bias,
                        float* __restrict__ mb, float* __restrict__ vb, const float* __restrict__ db,
-                       int64_t L, AdamArgs a) {
+                       int64_t L, AdamArgs a, const float* rbc) {
+  a.rbc1 = rbc[0]; a.rbc2 = rbc[1];                     // this step's bias corrections (k_step_t)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n + L; e += stride) {
     if (e < n) {

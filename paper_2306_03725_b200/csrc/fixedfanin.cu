@@ -157,6 +157,8 @@ struct ff_layer {
   int64_t tile_rows;                // CSC mode: labels per tile (multiple of 32)
   int ntiles;
   float* loss_scratch;
+  int64_t* t_dev;          // the authoritative Adam step counter (device; advanced by k_prep / k_step_t)
+  float* rbc_dev;          // [2] bias corrections of the current step
   uint32_t* posmask;
   int64_t t;
   bool grads_valid;
@@ -179,13 +181,15 @@ template <typename T>
 T* at(char* base, size_t off) { return reinterpret_cast<T*>(base + off); }
 
 ff_status launch_prep(ff_layer* l, const float* h, int B, bool zero_dh, const int* lbl_ptr,
-                      const int* lbl_ids, float* loss, cudaStream_t st) {
+                      const int* lbl_ids, float* loss, cudaStream_t st, bool step_t = false) {
   const int nb = nb_of(B);
   dim3 grid((l->cfg.m + 31) / 32), block(32, 8);
   const bool vec = (l->cfg.m & 3) == 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0;
   (vec ? k_prep<true> : k_prep<false>)<<<grid, block, 0, st>>>(h, B, l->cfg.m, nb, l->hd, zero_dh ? 1 : 0, lbl_ptr,
                                                                 lbl_ids, l->posmask, l->cfg.L_local, l->cfg.row_begin,
-                                                                l->cfg.L_global, loss, l->err);
+                                                                l->cfg.L_global, loss, l->err,
+                                                                step_t ? l->t_dev : nullptr, l->rbc_dev,
+                                                                l->cfg.beta1, l->cfg.beta2);
   FF_LAUNCHED();
   return FF_OK;
 }
@@ -372,13 +376,14 @@ ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t*
   if ((!hd_ready && (!ptr_ok(h, B) || (!dh_optional && !ptr_ok(dh, B)))) || lbl_ptr == nullptr)
     return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
   ff_status s = launch_prep(l, hd_ready ? nullptr : h, B, (!l->csc || l->split > 0) && !hd_ready, lbl_ptr, lbl_ids,
-                            loss, st);
+                            loss, st, true);
   if (s != FF_OK) return s;
   l->t += 1;
   RowArgs a = row_args(l, B);
   a.grad_scale = grad_scale;
   a.loss = loss;
-  a.adam = adam_args(l, lr, l->t);
+  a.adam = adam_args(l, lr, l->t);                // rbc1/rbc2 are replaced by the device's (a.rbc)
+  a.rbc = l->rbc_dev;
   const bool sg = (l->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
   const bool pipe = l->cfg.k == 32 && B <= 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE);
   if (pipe) {
@@ -592,6 +597,7 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->h_stage = at<float>(ws, lay.h_stage); l->lbl_stage = at<int>(ws, lay.lbl_stage);
   l->dh_stage = at<float>(ws, lay.dh_stage);
   l->err = at<int>(ws, lay.scalars); l->loss_scratch = at<float>(ws, lay.scalars + 4);
+  l->t_dev = at<int64_t>(ws, lay.scalars + 8); l->rbc_dev = at<float>(ws, lay.scalars + 16);
   l->csc = c.dh_mode != FF_DH_ATOMIC;
   l->split = c.dh_mode == FF_DH_HYBRID
                  ? (uint32_t)std::min<double>(c.m, std::floor((double)c.hybrid_frac * (double)c.m + 0.5)) : 0u;
@@ -675,7 +681,11 @@ ff_status fixedfanin_set_params(ff_layer* l, const float* W, const int32_t* idx,
   };
   FF_CUDA(cp(l->W, W, Lk)); FF_CUDA(cp(l->idx, idx, Lk)); FF_CUDA(cp(l->bias, bias, L4));
   FF_CUDA(cp(l->mW, mW, Lk)); FF_CUDA(cp(l->vW, vW, Lk)); FF_CUDA(cp(l->mb, mb, L4)); FF_CUDA(cp(l->vb, vb, L4));
-  if (t) l->t = *t;
+  if (t) {
+    l->t = *t;
+    FF_CUDA(cudaMemcpyAsync(l->t_dev, &l->t, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    FF_CUDA(cudaStreamSynchronize(st));                 // &l->t is host memory read asynchronously
+  }
   l->grads_valid = false;
   if (idx && l->cfg.L_local > 0) {
     FF_CUDA(cudaMemsetAsync(l->err, 0, sizeof(int), st));
@@ -706,8 +716,9 @@ ff_status fixedfanin_get_params(ff_layer* l, float* W, int32_t* idx, float* bias
   };
   FF_CUDA(cp(W, l->W, Lk)); FF_CUDA(cp(idx, l->idx, Lk)); FF_CUDA(cp(bias, l->bias, L4));
   FF_CUDA(cp(mW, l->mW, Lk)); FF_CUDA(cp(vW, l->vW, Lk)); FF_CUDA(cp(mb, l->mb, L4)); FF_CUDA(cp(vb, l->vb, L4));
-  if (t) *t = l->t;
+  if (t) FF_CUDA(cudaMemcpyAsync(t, l->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   FF_CUDA(cudaStreamSynchronize(st));
+  if (t) l->t = *t;
   return FF_OK;
 }
 
@@ -764,9 +775,11 @@ ff_status fixedfanin_adam_step(ff_layer* l, float lr, ff_stream_t stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   l->t += 1;
   const int64_t n = l->cfg.L_local * l->cfg.k;
+  k_step_t<<<1, 32, 0, st>>>(l->t_dev, l->rbc_dev, l->cfg.beta1, l->cfg.beta2);
+  FF_LAUNCHED();
   if (n > 0) {
     k_adam<<<l->nsm * 8, 256, 0, st>>>(l->W, l->mW, l->vW, l->dW, n, l->bias, l->mb, l->vb, l->db, l->cfg.L_local,
-                                       adam_args(l, lr, l->t));
+                                       adam_args(l, lr, l->t), l->rbc_dev);
     FF_LAUNCHED();
   }
   l->grads_valid = false;

@@ -507,6 +507,61 @@ def test_host_entry_point_loss_output(pinned):
     assert (sa["W"] == sb["W"]).all() and (sa["vW"] == sb["vW"]).all()
 
 
+@DH
+def test_train_step_cuda_graph_replay(dh_mode):
+    """The fused step is capturable: it only enqueues kernels on the caller's stream, and the
+    Adam step counter lives on the device (k_prep advances it), so N replays of one captured
+    step (inputs copied into static buffers) equal N eager steps bit for bit, t included, with
+    a redistribution between replays."""
+    L, m, k, B = 3000, 512, 32, 32
+    a, b = make(L, m, k, B=B, seed=6, dh_mode=dh_mode), make(L, m, k, B=B, seed=6, dh_mode=dh_mode)
+    batches = [synth.label_batch(B, L, 5.0, step=s) for s in range(6)]
+    hs = [tens(synth.hidden_batch(B, m, step=s)) for s in range(6)]
+    nnz_max = max(int(p_[-1]) for p_, _ in batches)
+    sh, sp = torch.zeros((B, m), device=dev()), torch.zeros(B + 1, dtype=torch.int32, device=dev())
+    si = torch.zeros(nnz_max, dtype=torch.int32, device=dev())
+    sdh, sloss = torch.empty((B, m), device=dev()), torch.zeros(1, device=dev())
+
+    def load(s):
+        sh.copy_(hs[s]); sp.copy_(tens(batches[s][0])); si[:len(batches[s][1])].copy_(tens(batches[s][1]))
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):                      # one eager step before capture (torch's rule)
+        load(0)
+        a.train_step(sh, sp, si, 1e-3, dh=sdh, loss=sloss)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        a.train_step(sh, sp, si, 1e-3, dh=sdh, loss=sloss)
+    # the capture did not run the step: a has taken exactly one step (t = 1)
+    losses_g = []
+    for s in range(1, 6):
+        load(s)
+        g.replay()
+        losses_g.append(sloss.clone())
+        if s == 3:
+            a.redistribute(1000)
+    loss_e = torch.zeros(1, device=dev())
+    losses_e = []
+    for s in range(6):
+        dh_e, _ = b.train_step(hs[s], tens(batches[s][0]), tens(batches[s][1]), 1e-3, loss=loss_e)
+        if s > 0:
+            losses_e.append(loss_e.clone())
+        if s == 3:
+            b.redistribute(1000)
+    torch.cuda.synchronize()
+    sa, sb = state_of(a), state_of(b)
+    assert sa["t"] == sb["t"] == 6
+    for key in ("W", "bias", "mW", "vW", "idx", "mb", "vb"):
+        assert (sa[key] == sb[key]).all(), key
+    if dh_mode == 1:                                   # CSC: deterministic dh and loss order
+        assert torch.equal(sdh, dh_e)
+    else:                                              # atomic reductions: order-dependent rounding
+        assert dh_close(sdh.cpu(), dh_e.cpu())
+    assert all(abs(x.item() - y.item()) <= 1e-6 * abs(y.item()) for x, y in zip(losses_g, losses_e))
+
+
 def test_csc_dh_is_deterministic_and_matches_atomic():
     L, m, k, B = 3000, 1024, 32, 32
     a, b = make(L, m, k, B=B, seed=2, dh_mode=1), make(L, m, k, B=B, seed=2, dh_mode=0)
