@@ -1322,12 +1322,16 @@ __device__ __forceinline__ void warp_topk_pop(float (&ts)[kTopkMax], int (&ti)[k
     }
   }
 }
-__global__ void __launch_bounds__(256) k_merge_topk_block(const float* __restrict__ in_s, const int* __restrict__ in_i,
+#ifndef FF_MERGE_THREADS
+#define FF_MERGE_THREADS 1024
+#endif
+constexpr int kMergeThreads = FF_MERGE_THREADS;                  // <= 1024 (warp 0 merges <= 32 lists)
+__global__ void __launch_bounds__(kMergeThreads) k_merge_topk_block(const float* __restrict__ in_s, const int* __restrict__ in_i,
                                                           int nlist, int64_t list_stride, int64_t sample_stride,
                                                           int Kin, int K, float* __restrict__ out_s,
                                                           int* __restrict__ out_i) {
-  __shared__ float ws_s[8][kTopkMax];
-  __shared__ int ws_i[8][kTopkMax];
+  __shared__ float ws_s[kMergeThreads / 32][kTopkMax];
+  __shared__ int ws_i[kMergeThreads / 32][kTopkMax];
   const int b = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
   float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll

@@ -427,7 +427,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
     FF_CUDA(cudaLaunchKernel(predict_kernel(l->cfg.k), dim3(l->grid_pred), dim3(kRowThreads), args, 0, st));
   }
   ++g_launches;
-  k_merge_topk_block<<<B, 256, 0, st>>>(l->cand_s, l->cand_i, nlist, (int64_t)ldh * kTopkMax, kTopkMax, kTopkMax, K,
+  k_merge_topk_block<<<B, kMergeThreads, 0, st>>>(l->cand_s, l->cand_i, nlist, (int64_t)ldh * kTopkMax, kTopkMax, kTopkMax, K,
                                         scores, ids);
   FF_LAUNCHED();
   return FF_OK;
