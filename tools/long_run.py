@@ -34,4 +34,5 @@ for mode, name in ((FF_DH_ATOMIC, "atomic"), (FF_DH_CSC, "csc")):
     finite = all(bool(torch.isfinite(st[k]).all().item()) for k in ("W", "bias", "mW", "vW"))
     print(f"{name}: {steps} steps ({steps // 1000} redistributions) in {dt:.2f} s wall = {B * steps / dt:.0f} samples/s; "
           f"rows with k distinct in-range indices: {distinct and in_range}; finite state: {finite}; "
+          f"device Adam t = {st['t']} (expected {steps}); "
           f"loss at each redistribution: {[round(x, 2) for x in losses]}")
