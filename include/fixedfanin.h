@@ -71,6 +71,8 @@ typedef enum {
 #define FF_FLAG_STORE_GRADS 2u   /* fused train_step also stores dW/db (for get_grads/tests)  */
 #define FF_FLAG_NO_PIPE 4u       /* use the generic fused kernel even where the pipelined one
                                     applies (k = 32, B <= 32); same results, for A/B tests     */
+#define FF_STEP_AUTO UINT64_MAX  /* dense forward / model step `step`: key the dropout on the dense
+                                  layer's device Adam counter + 1 (CUDA-graph capturable)      */
 #define FF_FLAG_DENSE_SIMT 8u    /* ff_dense_config.flags: FP32 FMA forward instead of the
                                     tcgen05 3xTF32 tensor-core forward (B <= 32), for A/B tests */
 
@@ -273,7 +275,9 @@ ff_status fixedfanin_dense_get_params(ff_dense* dense, float* Wd, float* bd, flo
  * (u >> 8) * 2^-24 >= p for u = word f of the Philox stream (ctr = (f/4, b, step, 3),
  * key = seed), kept values scaled by fp32(1/(1-p))), else xt = x;
  * z[b][c] = bd[c] + sum_f xt[b][f] Wd[f][c] (f ascending); h = max(z, 0).  Writes h
- * [B][m] if h != NULL and keeps xt and h for the backward.  0 <= B <= max_batch.         */
+ * [B][m] if h != NULL and keeps xt and h for the backward.  0 <= B <= max_batch.
+ * step == FF_STEP_AUTO: the key is the dense layer's device Adam counter + 1 (the step the
+ * following backward_adam takes), read on the device.                                    */
 ff_status fixedfanin_dense_forward(ff_dense* dense, const float* x, int32_t B, uint64_t step,
                                    int32_t train, float* h, ff_stream_t stream);
 
@@ -291,7 +295,9 @@ ff_status fixedfanin_dense_get_grads(ff_dense* dense, float* dWd, float* dbd, ff
 /* One training step of the whole architecture on one GPU (unsharded `layer`, same m):
  * dense forward with dropout (step keys the masks) -> the fixed fan-in layer's fused
  * train_step -> dense backward + Adam.  h and dh never leave the layer's internal
- * h|dh column lines (no [B][m] round trip).  loss as in fixedfanin_train_step.           */
+ * h|dh column lines (no [B][m] round trip).  loss as in fixedfanin_train_step.
+ * With step == FF_STEP_AUTO the step is CUDA-graph capturable: both layers' Adam counters
+ * and the dropout key live on the device (the layer's k_prep advances both counters).    */
 ff_status fixedfanin_model_train_step(ff_dense* dense, ff_layer* layer, const float* x, int32_t B,
                                       uint64_t step, const int32_t* lbl_ptr,
                                       const int32_t* lbl_ids, float grad_scale, float lr,

@@ -39,7 +39,11 @@ __device__ __forceinline__ void st_na4(float* a, float4 v) {
 // Philox stream (ctr = (f/4, b, step, 3), key = seed) has (u >> 8) * 2^-24 >= p, else 0.
 // train = 0: xT = x (inference, no dropout).  Samples B..ldx-1 are 0.  Thread per (b, f/4).
 __global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, float p, float scale, int train,
-                            uint32_t step, uint32_t key0, uint32_t key1, float* __restrict__ xT) {
+                            uint32_t step, uint32_t key0, uint32_t key1, float* __restrict__ xT,
+                            const int64_t* __restrict__ t_auto) {
+  // t_auto (FF_STEP_AUTO): the step key is the dense layer's device counter + 1, i.e. the
+  // Adam step this forward belongs to (read before k_prep / k_step_t advance it)
+  if (t_auto != nullptr) step = (uint32_t)(*t_auto + 1);
   const int nq = (d + 3) / 4;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)ldx * nq;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -474,7 +478,8 @@ __global__ void __launch_bounds__(kDenseBwdThreads, 2) k_dense_bwd_adam(
     float* __restrict__ Wd, float* __restrict__ mWd, float* __restrict__ vWd, float* __restrict__ bd,
     float* __restrict__ mbd, float* __restrict__ vbd, const float* __restrict__ xT, int d, int m, int ldw, int ldx,
     int nb, const float* __restrict__ hd, int cstride, AdamArgs adam, float* __restrict__ dWd,
-    float* __restrict__ dbd, int rows_per_cta) {
+    float* __restrict__ dbd, int rows_per_cta, const float* __restrict__ rbc) {
+  adam.rbc1 = rbc[0]; adam.rbc2 = rbc[1];                         // this step's bias corrections (device t)
   __shared__ __align__(16) float dzs[32][128];
   __shared__ __align__(16) float xs[kDenseBwdBlk][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -606,7 +611,8 @@ __global__ void __launch_bounds__(kDenseBwdThreads, 2) k_dense_bwd_adam_b32(
     float* __restrict__ Wd, float* __restrict__ mWd, float* __restrict__ vWd, float* __restrict__ bd,
     float* __restrict__ mbd, float* __restrict__ vbd, const float* __restrict__ xT, int d, int m, int ldx,
     const float* __restrict__ hd, int cstride, AdamArgs adam, float* __restrict__ dWd, float* __restrict__ dbd,
-    int rows_per_cta) {
+    int rows_per_cta, const float* __restrict__ rbc) {
+  adam.rbc1 = rbc[0]; adam.rbc2 = rbc[1];                         // this step's bias corrections (device t)
   extern __shared__ __align__(16) float bsm[];
   float (*dzs)[128] = reinterpret_cast<float (*)[128]>(bsm);        // [32][128]
   float* const stages = bsm + 32 * 128;

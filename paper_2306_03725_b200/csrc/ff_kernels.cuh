@@ -818,7 +818,7 @@ __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float*
                        const int* __restrict__ lbl_ptr, const int* __restrict__ lbl_ids,
                        uint32_t* __restrict__ posmask, int64_t L_local, int64_t row_begin,
                        int64_t L_global, float* loss, int* err, int64_t* t_dev, float* rbc, float beta1,
-                       float beta2) {
+                       float beta2, int64_t* t2_dev, float* rbc2, float beta1d, float beta2d) {
   __shared__ float t[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   if (t_dev != nullptr && blockIdx.x == 0 && tid == 0) {
@@ -827,6 +827,13 @@ __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float*
     *t_dev = tn;
     rbc[0] = (float)(1.0 / (1.0 - pow((double)beta1, (double)tn)));
     rbc[1] = (float)(1.0 / (1.0 - pow((double)beta2, (double)tn)));
+  }
+  if (t2_dev != nullptr && blockIdx.x == 0 && tid == 32) {
+    // whole-architecture step: the dense layer's own counter (R28), after its dropout read it
+    const int64_t tn = *t2_dev + 1;
+    *t2_dev = tn;
+    rbc2[0] = (float)(1.0 / (1.0 - pow((double)beta1d, (double)tn)));
+    rbc2[1] = (float)(1.0 / (1.0 - pow((double)beta2d, (double)tn)));
   }
   const int c0 = blockIdx.x * 32;
   const int cstride = 64 * nb;

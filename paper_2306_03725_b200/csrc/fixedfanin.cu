@@ -180,8 +180,12 @@ int ring_mode(const ff_layer* l) { return !l->csc ? 0 : l->split > 0 ? 2 : 1; }
 template <typename T>
 T* at(char* base, size_t off) { return reinterpret_cast<T*>(base + off); }
 
+// the dense layer's step counter, advanced by k_prep of a whole-architecture step
+struct DenseT { int64_t* t; float* rbc; float beta1, beta2; };
+
 ff_status launch_prep(ff_layer* l, const float* h, int B, bool zero_dh, const int* lbl_ptr,
-                      const int* lbl_ids, float* loss, cudaStream_t st, bool step_t = false) {
+                      const int* lbl_ids, float* loss, cudaStream_t st, bool step_t = false,
+                      const DenseT* dt = nullptr) {
   const int nb = nb_of(B);
   dim3 grid((l->cfg.m + 31) / 32), block(32, 8);
   const bool vec = (l->cfg.m & 3) == 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0;
@@ -189,7 +193,9 @@ ff_status launch_prep(ff_layer* l, const float* h, int B, bool zero_dh, const in
                                                                 lbl_ids, l->posmask, l->cfg.L_local, l->cfg.row_begin,
                                                                 l->cfg.L_global, loss, l->err,
                                                                 step_t ? l->t_dev : nullptr, l->rbc_dev,
-                                                                l->cfg.beta1, l->cfg.beta2);
+                                                                l->cfg.beta1, l->cfg.beta2, dt ? dt->t : nullptr,
+                                                                dt ? dt->rbc : nullptr, dt ? dt->beta1 : 0.0f,
+                                                                dt ? dt->beta2 : 0.0f);
   FF_LAUNCHED();
   return FF_OK;
 }
@@ -371,12 +377,12 @@ ff_status csc_rebuild(ff_layer* l, cudaStream_t st) {
 // dh_optional (host entry point): dh == NULL skips only the [B][m] copy-out of dh.
 ff_status train_step_impl(ff_layer* l, const float* h, int32_t B, const int32_t* lbl_ptr, const int32_t* lbl_ids,
                           float grad_scale, float lr, float* dh, float* loss, cudaStream_t st, bool hd_ready = false,
-                          bool dh_optional = false) {
+                          bool dh_optional = false, const DenseT* dt = nullptr) {
   if (B < 0 || B > l->cfg.max_batch) return fail(FF_ERR_ARG, "B=%d outside [0, max_batch=%d]", B, l->cfg.max_batch);
   if ((!hd_ready && (!ptr_ok(h, B) || (!dh_optional && !ptr_ok(dh, B)))) || lbl_ptr == nullptr)
     return fail(FF_ERR_ARG, "null h/dh/lbl_ptr");
   ff_status s = launch_prep(l, hd_ready ? nullptr : h, B, (!l->csc || l->split > 0) && !hd_ready, lbl_ptr, lbl_ids,
-                            loss, st, true);
+                            loss, st, true, dt);
   if (s != FF_OK) return s;
   l->t += 1;
   RowArgs a = row_args(l, B);
@@ -436,7 +442,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
 
 // ============================================================ NEXT-2: the intermediate layer
 struct DenseLayout {
-  size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, zpart, cnt, hd, x_stage, total;
+  size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, zpart, cnt, hd, x_stage, scal, total;
 };
 int ldw_of(int m) { return (m + 127) / 128 * 128; }   // Wd is stored in 128-column tiles
 DenseLayout dense_layout_of(const ff_dense_config& c) {
@@ -453,6 +459,7 @@ DenseLayout dense_layout_of(const ff_dense_config& c) {
   o.cnt = take(4 * (size_t)(ldw_of(c.m) / 128));
   o.hd = take(8 * (size_t)c.m * ldx);     // own h|dh lines for the standalone forward/backward
   o.x_stage = take(4 * (size_t)c.max_batch * (size_t)c.d);
+  o.scal = take(kAlign);           // [0] int64 Adam t (device, authoritative), [8] float rbc[2]
   o.total = off;
   return o;
 }
@@ -494,7 +501,9 @@ struct ff_dense {
   unsigned* cnt;
   int ldw;
   int nsm;
-  int64_t t;
+  int64_t t;            // host mirror of *t_dev
+  int64_t* t_dev;       // Adam step counter (R28), advanced on the device (CUDA-graph capturable)
+  float* rbc_dev;       // [2] bias corrections of the current step
   int fwd_B;            // batch of the last training forward (-1: none since the last backward)
   bool grads_valid;
 };
@@ -511,7 +520,8 @@ ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, 
     const int64_t work = (int64_t)ldx * ((n->cfg.d + 3) / 4);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 4096));
     k_dropout_T<<<grid, 256, 0, st>>>(x, B, n->cfg.d, ldx, p, scale, (train && p > 0.0f) ? 1 : 0, (uint32_t)step,
-                                      (uint32_t)n->cfg.seed, (uint32_t)(n->cfg.seed >> 32), n->xT);
+                                      (uint32_t)n->cfg.seed, (uint32_t)(n->cfg.seed >> 32), n->xT,
+                                      step == FF_STEP_AUTO ? n->t_dev : nullptr);
     FF_LAUNCHED();
   }
   if (nb == 1 && !(n->cfg.flags & FF_FLAG_DENSE_SIMT)) {          // tensor cores (tcgen05, 3xTF32)
@@ -532,10 +542,15 @@ ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, 
 }
 
 // backward + Adam from the h|dh lines of `hd` (t += 1)
-ff_status dense_backward_impl(ff_dense* n, int B, float lr, const float* hd, cudaStream_t st) {
+// t_done: this step's k_prep already advanced the dense counter (whole-architecture step)
+ff_status dense_backward_impl(ff_dense* n, int B, float lr, const float* hd, cudaStream_t st, bool t_done = false) {
   const int nb = nb_of(B), ldx = 32 * nb;
   n->t += 1;
-  const AdamArgs a = adam_args_of(n->cfg.beta1, n->cfg.beta2, n->cfg.eps, lr, n->t);
+  if (!t_done) {
+    k_step_t<<<1, 32, 0, st>>>(n->t_dev, n->rbc_dev, n->cfg.beta1, n->cfg.beta2);
+    FF_LAUNCHED();
+  }
+  const AdamArgs a = adam_args_of(n->cfg.beta1, n->cfg.beta2, n->cfg.eps, lr, n->t);   // rbc from the device
   const bool sg = (n->cfg.flags & FF_FLAG_STORE_GRADS) != 0;
   // feature ranges per column tile: about 4 CTAs per SM in total, whole 16-feature blocks
   const int gx = (n->ldw + 127) / 128;
@@ -545,11 +560,12 @@ ff_status dense_backward_impl(ff_dense* n, int B, float lr, const float* hd, cud
   if (nb == 1)
     k_dense_bwd_adam_b32<<<grid, kDenseBwdThreads, kDenseBwd1Smem, st>>>(
         n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d, n->cfg.m, ldx, hd, 64 * nb, a,
-        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows);
+        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows, n->rbc_dev);
   else
     k_dense_bwd_adam<<<grid, kDenseBwdThreads, 0, st>>>(n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d,
                                                         n->cfg.m, n->ldw, ldx, nb, hd, 64 * nb, a,
-                                                        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows);
+                                                        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows,
+                                                        n->rbc_dev);
   FF_LAUNCHED();
   n->grads_valid = sg;
   n->fwd_B = -1;
@@ -997,6 +1013,7 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
   n->bd = at<float>(ws, lay.bd); n->mbd = at<float>(ws, lay.mbd); n->vbd = at<float>(ws, lay.vbd);
   n->dbd = at<float>(ws, lay.dbd);
   n->xT = at<float>(ws, lay.xT); n->hd = at<float>(ws, lay.hd); n->x_stage = at<float>(ws, lay.x_stage);
+  n->t_dev = at<int64_t>(ws, lay.scal); n->rbc_dev = at<float>(ws, lay.scal + 8);
   n->zpart = at<float>(ws, lay.zpart); n->cnt = at<unsigned>(ws, lay.cnt);
   n->ldw = ldw_of(c.m);
   n->t = 0; n->fwd_B = -1; n->grads_valid = false;
@@ -1051,7 +1068,10 @@ ff_status fixedfanin_dense_set_params(ff_dense* n, const float* Wd, const float*
   };
   FF_CUDA(cp2(n->Wd, Wd)); FF_CUDA(cp2(n->mWd, mWd)); FF_CUDA(cp2(n->vWd, vWd));
   FF_CUDA(cp1(n->bd, bd)); FF_CUDA(cp1(n->mbd, mbd)); FF_CUDA(cp1(n->vbd, vbd));
-  if (t) n->t = *t;
+  if (t) {
+    n->t = *t;
+    FF_CUDA(cudaMemcpyAsync(n->t_dev, &n->t, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  }
   n->grads_valid = false;
   FF_CUDA(cudaStreamSynchronize(st));
   return FF_OK;
@@ -1075,8 +1095,9 @@ ff_status fixedfanin_dense_get_params(ff_dense* n, float* Wd, float* bd, float* 
   };
   FF_CUDA(cp2(Wd, n->Wd)); FF_CUDA(cp2(mWd, n->mWd)); FF_CUDA(cp2(vWd, n->vWd));
   FF_CUDA(cp1(bd, n->bd)); FF_CUDA(cp1(mbd, n->mbd)); FF_CUDA(cp1(vbd, n->vbd));
-  if (t) *t = n->t;
+  if (t) FF_CUDA(cudaMemcpyAsync(t, n->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   FF_CUDA(cudaStreamSynchronize(st));
+  if (t) n->t = *t;
   return FF_OK;
 }
 
@@ -1141,10 +1162,11 @@ ff_status fixedfanin_model_train_step(ff_dense* n, ff_layer* l, const float* x, 
   ff_status s = dense_forward_impl(n, x, B, step, true, l->hd, nullptr, st);
   if (s != FF_OK) return s;
   int32_t nl = g_launches;
-  s = train_step_impl(l, nullptr, B, lbl_ptr, lbl_ids, grad_scale, lr, nullptr, loss, st, true);
+  const DenseT dt{n->t_dev, n->rbc_dev, n->cfg.beta1, n->cfg.beta2};
+  s = train_step_impl(l, nullptr, B, lbl_ptr, lbl_ids, grad_scale, lr, nullptr, loss, st, true, false, &dt);
   if (s != FF_OK) return s;
   nl += g_launches;
-  s = dense_backward_impl(n, B, lr, l->hd, st);
+  s = dense_backward_impl(n, B, lr, l->hd, st, true);
   g_launches += nl;
   return s;
 }

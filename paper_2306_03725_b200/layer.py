@@ -20,6 +20,7 @@ FF_FLAG_CHECK_FINITE = 1
 FF_FLAG_STORE_GRADS = 2
 FF_FLAG_NO_PIPE = 4
 FF_FLAG_DENSE_SIMT = 8
+FF_STEP_AUTO = 2 ** 64 - 1     # dropout keyed on the dense layer's device Adam counter + 1
 FF_DH_ATOMIC, FF_DH_CSC, FF_DH_HYBRID = 0, 1, 2
 FF_LOSS_BCE, FF_LOSS_SQH = 0, 1
 FF_MAX_FANIN, FF_MAX_BATCH, FF_MAX_TOPK = 64, 1024, 8

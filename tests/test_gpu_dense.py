@@ -280,3 +280,57 @@ def test_model_full_size_amazon_670k_sampled(dh_mode):
     assert_close(dbd[cols], rbd, Abd, "dense dbd cols")
     Wdr, _, _ = oracle.adam(d0["Wd"][:, cols], dWd[:, cols], d0["mWd"][:, cols], d0["vWd"][:, cols], 1, F32(1e-3), **ADAM)
     assert_close(d1["Wd"][:, cols], Wdr, adam_A(d0["Wd"][:, cols], Wdr), "Wd' cols")
+
+
+@pytest.mark.parametrize("dh_mode", [1, 0])
+def test_model_step_cuda_graph_replay(dh_mode):
+    """The whole-architecture step is capturable with step = FF_STEP_AUTO: both Adam counters
+    and the dropout step key live on the device, so replays of one captured step equal eager
+    steps with explicit steps 1, 2, ... (CSC: bit-identical; atomic: dh rounding order)."""
+    layer = L_()
+    L, m, k, B, d = 2000, 1024, 32, 32, 64
+    runs = []
+    for graph in (True, False):
+        lay = make(L, m, k, B=B, seed=42, dh_mode=dh_mode)
+        dn = make_dense(d, m, B=B, seed=43, dropout=0.1)
+        xs = [tens(synth.feature_batch(B, d, step=s)) for s in range(5)]
+        lb = [synth.label_batch(B, L, 5.0, step=s) for s in range(5)]
+        nnz = max(int(p_[-1]) for p_, _ in lb)
+        sx = torch.zeros((B, d), device=dev()); sp = torch.zeros(B + 1, dtype=torch.int32, device=dev())
+        si = torch.zeros(nnz, dtype=torch.int32, device=dev()); loss = torch.zeros(1, device=dev())
+
+        def load(s):
+            sx.copy_(xs[s]); sp.copy_(tens(lb[s][0])); si[:len(lb[s][1])].copy_(tens(lb[s][1]))
+        if graph:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                load(0)
+                layer.model_train_step(dn, lay, sx, layer.FF_STEP_AUTO, sp, si, F32(1e-3), loss=loss)
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                layer.model_train_step(dn, lay, sx, layer.FF_STEP_AUTO, sp, si, F32(1e-3), loss=loss)
+            for s in range(1, 5):
+                load(s)
+                g.replay()
+        else:
+            for s in range(5):
+                load(s)
+                layer.model_train_step(dn, lay, sx, s + 1, sp, si, F32(1e-3), loss=loss)
+        torch.cuda.synchronize()
+        runs.append((state_of(lay), dstate(dn), float(loss.item())))
+    (sa, da, la), (sb, db_, lb_) = runs
+    assert sa["t"] == sb["t"] == 5 and da["t"] == db_["t"] == 5
+    if dh_mode == 1:
+        for key in ("W", "bias", "mW", "vW", "idx"):
+            assert (sa[key] == sb[key]).all(), key
+        for key in ("Wd", "bd", "mWd", "vWd"):
+            assert (da[key] == db_[key]).all(), key
+        assert abs(la - lb_) <= 1e-6 * abs(lb_)          # the loss sum is an atomic reduction
+    else:
+        for key in ("Wd", "W"):
+            ref = (db_ if key == "Wd" else sb)[key]
+            got = (da if key == "Wd" else sa)[key]
+            assert np.allclose(got, ref, rtol=1e-4, atol=1e-6), key
+        assert abs(la - lb_) <= 1e-5 * abs(lb_)
