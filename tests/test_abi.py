@@ -110,3 +110,24 @@ def test_dense_workspace_size_matches_layout_model():
     assert sizes[1] - sizes[0] == 4 * d * m                     # dWd
     core = 3 * 4 * d * m + 4 * 4 * m + 4 * d * 32 + 8 * m * 32 + 4 * B * d
     assert core <= sizes[0] <= core + 2 * 4 * m * 32 + 4 * (m // 128) + 16 * 256
+
+
+def test_python_constants_match_header_defines():
+    """The binding's FF_* constants equal the header's #defines and enum values."""
+    import os
+    import re
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "fixedfanin.h")).read()
+    defines = {k: v for k, v in re.findall(r"#define\s+(FF_\w+)\s+(\w+)", hdr)}
+    enums = {k: int(v) for k, v in re.findall(r"\b(FF_\w+)\s*=\s*(\d+)", hdr)}
+    checked = 0
+    for name, val in defines.items():
+        if not hasattr(L, name):
+            continue
+        want = 2 ** 64 - 1 if val == "UINT64_MAX" else int(val.rstrip("uU"), 0)
+        assert getattr(L, name) == want, name
+        checked += 1
+    for name, val in enums.items():
+        if hasattr(L, name):
+            assert getattr(L, name) == val, name
+            checked += 1
+    assert checked >= 8
