@@ -122,6 +122,31 @@ def test_forward_parity(L, m, k, B):
 DH = pytest.mark.parametrize("dh_mode", [0, 1, 2], ids=["atomic", "csc", "hybrid"])
 
 
+@pytest.mark.parametrize("m,offset", [(257, 0), (258, 0), (256, 1), (256, 0)])
+def test_transpose_kernels_scalar_and_vector_paths(m, offset):
+    """k_prep / k_dh_out take 16-B vector paths only when m % 4 == 0 and h / dh are 16-B
+    aligned: odd widths and a misaligned (offset) h / dh view run the scalar paths.  Forward
+    y and backward dh against the oracle either way."""
+    L, k, B = 500, 16, 32
+    lay = make(L, m, k, B=B, seed=9)
+    W, idx, bias = synth.random_params(L, m, k, seed=m + offset)
+    lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    h = synth.hidden_batch(B, m, step=5)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=5)
+    hb = torch.zeros(B * m + offset, device=dev())
+    hb[offset:].copy_(tens(h).reshape(-1))
+    hv = hb[offset:].view(B, m)                        # data_ptr() % 16 != 0 when offset = 1
+    y = lay.forward(hv)
+    yr, Ay = oracle.forward(W, idx, bias, h)
+    assert_close(y.cpu().numpy(), yr, Ay, "y")
+    db_ = torch.zeros(B * m + offset, device=dev())
+    dh = db_[offset:].view(B, m)
+    lay.backward(hv, y, tens(ptr), tens(ids), dh=dh)
+    g, _ = oracle.loss_grad("bce", y.cpu().numpy().astype(np.float64), ptr, ids, F32(1.0 / B))
+    dhr, Adh = oracle.input_grad(W, idx, g, m)
+    assert_close(dh.cpu().numpy(), dhr, Adh, "dh")
+
+
 LOSS = pytest.mark.parametrize("loss", ["bce", "sqh"])
 
 
