@@ -252,6 +252,37 @@ def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k):
         assert s1["t"] == step + 1
 
 
+@pytest.mark.parametrize("t0", [41, 999, 123456])
+def test_set_params_t_drives_the_device_step_counter(t0):
+    """set_params(t) reaches the device counter: the next fused step and the next unfused
+    adam_step use the bias corrections of t0 + 1 and t0 + 2 (R6, R7), and get_params reads
+    the counter back."""
+    L, m, k, B = 800, 256, 32, 32
+    layer = L_()
+    lay = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, seed=5)
+    rng = np.random.default_rng(t0)
+    mW = (rng.random((L, k)) * 1e-3).astype(np.float32); vW = (rng.random((L, k)) * 1e-6).astype(np.float32)
+    lay.set_params(mW=tens(mW), vW=tens(vW), t=t0)
+    assert state_of(lay)["t"] == t0
+    s0 = state_of(lay)
+    h = synth.hidden_batch(B, m, step=1)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=1)
+    lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
+    dW, _ = lay.get_grads()
+    s1 = state_of(lay)
+    assert s1["t"] == t0 + 1
+    Wr, mr, vr = oracle.adam(s0["W"], dW.cpu().numpy(), s0["mW"], s0["vW"], t0 + 1, F32(1e-3), **ADAM)
+    assert_close(s1["W"], Wr, adam_A(s0["W"], Wr), "W' (fused)")
+    y = lay.forward(tens(h))
+    lay.backward(tens(h), y, tens(ptr), tens(ids))
+    dW2, _ = lay.get_grads()
+    lay.adam_step(F32(1e-3))
+    s2 = state_of(lay)
+    assert s2["t"] == t0 + 2
+    Wr2, _, _ = oracle.adam(s1["W"], dW2.cpu().numpy(), s1["mW"], s1["vW"], t0 + 2, F32(1e-3), **ADAM)
+    assert_close(s2["W"], Wr2, adam_A(s1["W"], Wr2), "W' (unfused)")
+
+
 @DH
 def test_free_running_tiny_run_matches_oracle(dh_mode):
     """tiny config of BASELINE.json: 5 Adam steps + 1 redistribution, then predict K = 5.
