@@ -334,3 +334,26 @@ def test_model_step_cuda_graph_replay(dh_mode):
             got = (da if key == "Wd" else sa)[key]
             assert np.allclose(got, ref, rtol=1e-4, atol=1e-6), key
         assert abs(la - lb_) <= 1e-5 * abs(lb_)
+
+
+def test_dense_auto_step_equals_explicit_steps():
+    """Standalone dense layer: forward(step = FF_STEP_AUTO) keys the dropout on the device
+    counter + 1 and backward_adam advances it (k_step_t), so three AUTO steps equal three
+    steps with explicit keys 1, 2, 3: same h, same Wd / moments, t = 3."""
+    layer = L_()
+    d, m, B = 64, 512, 32
+    a = make_dense(d, m, B=B, seed=21, dropout=0.2)
+    b = make_dense(d, m, B=B, seed=21, dropout=0.2)
+    for s in range(3):
+        x = tens(synth.feature_batch(B, d, step=s))
+        dh = tens(synth.feature_batch(B, m, step=10 + s) * np.float32(0.01))
+        ha = a.forward(x, step=layer.FF_STEP_AUTO, train=True)
+        hb = b.forward(x, step=s + 1, train=True)
+        assert torch.equal(ha, hb), s
+        a.backward_adam(dh, F32(1e-3))
+        b.backward_adam(dh, F32(1e-3))
+    torch.cuda.synchronize()
+    da, db_ = dstate(a), dstate(b)
+    assert da["t"] == db_["t"] == 3
+    for key in ("Wd", "bd", "mWd", "vWd"):
+        assert (da[key] == db_[key]).all(), key
