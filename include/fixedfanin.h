@@ -319,6 +319,9 @@ ff_status fixedfanin_check(ff_layer* layer, ff_stream_t stream);
  * and returns the summed kernel milliseconds and the number of timed launches.        */
 ff_status fixedfanin_profile_begin(ff_layer* layer, int32_t max_launches);
 ff_status fixedfanin_profile_end(ff_layer* layer, double* kernel_ms_host, int32_t* launches_host);
+/* paused != 0: launches are not timed until resumed (host flag, no synchronisation), so a
+ * benchmark can time a sample of its steps and keep event recording out of the others.   */
+ff_status fixedfanin_profile_pause(ff_layer* layer, int32_t paused);
 
 /* Number of kernel launches the last API call enqueued (host counter, for benchmarks). */
 int32_t fixedfanin_last_launch_count(void);

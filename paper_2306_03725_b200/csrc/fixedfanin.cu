@@ -171,6 +171,7 @@ struct ff_layer {
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int stage_slot = 0;
   int prof_used = 0;
+  bool prof_paused = false;
 };
 
 namespace {
@@ -310,7 +311,7 @@ int block_rows(int64_t rows, int grid, int threads) {
 // One row-kernel launch, bracketed by a profiling event pair while profiling is on.
 ff_status timed_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads, int smem) {
   a.br = block_rows(a.j_end - a.j_begin, grid, threads);
-  const bool timed = 2 * (l->prof_used + 1) <= (int)l->prof_ev.size();
+  const bool timed = !l->prof_paused && 2 * (l->prof_used + 1) <= (int)l->prof_ev.size();
   if (timed) FF_CUDA(cudaEventRecord(l->prof_ev[2 * l->prof_used], st));
   ff_status s = launch_rows(fn, grid, a, st, threads, smem);
   if (s != FF_OK) return s;
@@ -945,6 +946,14 @@ ff_status fixedfanin_profile_begin(ff_layer* l, int32_t max_launches) {
   l->prof_ev.assign(2 * (size_t)max_launches, nullptr);
   for (auto& e : l->prof_ev) FF_CUDA(cudaEventCreate(&e));
   l->prof_used = 0;
+  l->prof_paused = false;
+  return FF_OK;
+}
+
+ff_status fixedfanin_profile_pause(ff_layer* l, int32_t paused) {
+  g_launches = 0;
+  if (!l) return fail(FF_ERR_ARG, "layer is NULL");
+  l->prof_paused = paused != 0;
   return FF_OK;
 }
 

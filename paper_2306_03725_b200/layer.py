@@ -34,7 +34,7 @@ EXPORTS = [
     "fixedfanin_predict_topk", "fixedfanin_score_shortlist", "fixedfanin_merge_topk", "fixedfanin_check",
     "fixedfanin_precision_at_k",
     "fixedfanin_profile_begin",
-    "fixedfanin_profile_end", "fixedfanin_last_launch_count",
+    "fixedfanin_profile_end", "fixedfanin_profile_pause", "fixedfanin_last_launch_count",
     "fixedfanin_last_error",
     # NEXT-2: the intermediate layer and the whole architecture
     "fixedfanin_dense_workspace_size", "fixedfanin_dense_create", "fixedfanin_dense_destroy",
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
             "fixedfanin_check": [P, P],
             "fixedfanin_profile_begin": [P, i32],
             "fixedfanin_profile_end": [P, P, P],
+            "fixedfanin_profile_pause": [P, i32],
             "fixedfanin_dense_workspace_size": [P, P],
             "fixedfanin_dense_create": [P, P, ctypes.c_size_t, P, P],
             "fixedfanin_dense_destroy": [P],
@@ -293,6 +294,9 @@ class FixedFanInLayer:
 
     def profile_begin(self, max_launches: int):
         _check(lib().fixedfanin_profile_begin(self._h, int(max_launches)))
+
+    def profile_pause(self, paused: bool):
+        _check(lib().fixedfanin_profile_pause(self._h, 1 if paused else 0))
 
     def profile_end(self):
         """-> (summed fused-kernel milliseconds, number of timed launches)"""
