@@ -48,6 +48,8 @@ def args_():
     p.add_argument("--batch", type=int, default=0,
                    help="override the shape's mini-batch B (default: the paper's 32, P:685); for batch sweeps")
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    p.add_argument("--repeats", type=int, default=5,
+                   help="timed windows of --steps steps each; the median window is reported (SURVEY §8(d).3)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--flags", type=int, default=0, help="extra ff_config.flags (A/B experiments)")
     p.add_argument("--loss", default="bce", choices=["bce", "sqh"],
@@ -157,40 +159,78 @@ def alg_bytes_predict(L, k, B, m):
 
 
 # ----------------------------------------------------------------------------- cpu baseline
-def oracle_sample_rate(shape, rows, steps, data):
-    """Time the fp64 oracle (as it stands, single thread) on the first `rows` label rows of
-    the workload; return samples/s scaled to the full label count."""
+def host_cores():
+    return len(os.sched_getaffinity(0))
+
+
+def oracle_timed(shape, data, steps, warmup, step_budget_s):
+    """Time the fp64 oracle as it stands, in its OpenMP timing mode on every host core
+    (SURVEY §8(d).4), for `steps` steps after `warmup` untimed ones.  Each step runs the
+    full label count when one full step fits `step_budget_s`, else the first `rows` label
+    rows (a bounded sample; rows chosen from a probe step on L/32 rows).  Returns
+    (rows, measured seconds per step of what ran, threads)."""
     import oracle
-    st = oracle.State.create(rows, shape.m, shape.k, seed=42)
-    t0 = time.perf_counter()
-    for s in range(steps):
-        h, ptr, ids = data[s % len(data)]
+    oracle.build()
+    cores = host_cores()
+    oracle.set_threads(cores)
+    try:
+        probe = max(1, shape.L // 32)
+        st = oracle.State.create(probe, shape.m, shape.k, seed=42)
+        t0 = time.perf_counter()
+        h, ptr, ids = data[0]
         oracle.train_step(st, h, ptr, ids, 1.0 / shape.B, LR)
-    dt = (time.perf_counter() - t0) / steps
-    return shape.B / (dt * shape.L / rows), dt
+        t_full = (time.perf_counter() - t0) * shape.L / probe
+        rows = shape.L if t_full <= step_budget_s else max(1, int(shape.L * step_budget_s / t_full))
+        st = oracle.State.create(rows, shape.m, shape.k, seed=42)
+        for s in range(warmup):
+            h, ptr, ids = data[s % len(data)]
+            oracle.train_step(st, h, ptr, ids, 1.0 / shape.B, LR)
+        t0 = time.perf_counter()
+        for s in range(steps):
+            h, ptr, ids = data[(warmup + s) % len(data)]
+            oracle.train_step(st, h, ptr, ids, 1.0 / shape.B, LR)
+        dt = (time.perf_counter() - t0) / max(steps, 1)
+    finally:
+        oracle.set_threads(1)
+    return rows, dt, cores
+
+
+def cpu_line(shape, rows, dt, cores, steps, warmup):
+    """The measured oracle numbers: ms per step of what ran; samples/s of the workload (the
+    full label count, so a sampled run's rate is scaled by L / rows and says so)."""
+    full = rows == shape.L
+    value = shape.B / (dt * shape.L / rows)
+    sample = (f"{'all' if full else f'first {rows} of'} {shape.L} label rows, m={shape.m}, k={shape.k}, "
+              f"B={shape.B}; fp64 oracle (OpenMP timing mode, {cores} threads), {warmup} warm-up + {steps} timed "
+              f"steps of {dt * 1e3:.1f} ms each" + ("" if full else f", rate scaled x{shape.L / rows:.2f} to all rows"))
+    out = {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle", "sample": sample,
+           "rows_per_step": rows, "ms_per_step_measured": dt * 1e3}
+    if not full:
+        out["extrapolated_full_L"] = {"ms_per_step": dt * 1e3 * shape.L / rows, "value": value}
+    return out
 
 
 def run_reference(a, shape, world, rank):
+    """This tier's reference arm: the fp64 CPU oracle, on rank 0 only (other ranks exit)."""
     if rank != 0:
         return
     from paper_2306_03725_b200 import synth
-    rows = max(1, shape.L // 128)
     data = [(synth.hidden_batch(shape.B, shape.m, step=s), *synth.label_batch(shape.B, shape.L, shape.avg_pos, step=s))
             for s in range(N_BATCHES)]
-    import oracle
-    oracle.build()
-    if a.warmup:
-        oracle_sample_rate(shape, rows, max(1, min(a.warmup, 3)), data)
-    v, dt = oracle_sample_rate(shape, rows, a.steps, data)
-    sample = (f"first {rows} of {shape.L} label rows (1/128), m={shape.m}, k={shape.k}, B={shape.B}; "
-              f"{a.steps} oracle steps of {dt * 1e3:.1f} ms, scaled x{shape.L / rows:.1f} to all rows")
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3 * shape.L / rows,
+    # the whole --steps K --warmup W run is bounded to ~150 s of oracle work
+    budget = 150.0 / max(1, a.steps + a.warmup)
+    rows, dt, cores = oracle_timed(shape, data, a.steps, a.warmup, budget)
+    cb = cpu_line(shape, rows, dt, cores, a.steps, a.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "samples/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": shape.name, "L": shape.L, "m": shape.m, "k": shape.k,
-                                              "B": shape.B},
-            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle", "sample": sample},
-            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic: h = ReLU(N(0,1)), Zipf(1.0) sparse labels, Philox-initialized W/idx (no dataset)",
+            "config": {"workload": shape.name, "L": shape.L, "m": shape.m, "k": shape.k, "B": shape.B,
+                       "rows_per_step": rows},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if rows < shape.L:
+        line["extrapolated_full_L"] = cb["extrapolated_full_L"]
     print(json.dumps(line), flush=True)
 
 
@@ -302,14 +342,17 @@ def run_ours(a, shape, world, rank, local_rank):
     from paper_2306_03725_b200.sharded import OverlappedTrainer
     trainer = OverlappedTrainer(layer, h_dev, ptr_dev, ids_dev, LR, B, shape.m, dev, loss=loss)
 
+    n_redist = 0
+
     def step(s):
-        nonlocal t_global, launches
+        nonlocal t_global, launches, n_redist
         trainer.step(s % N_BATCHES, (s + 1) % N_BATCHES)     # h broadcast / dh all-reduce overlapped
         launches += last_launch_count()
         t_global += 1
         if t_global % REDIST_EVERY == 0:
             layer.redistribute(t_global)
             launches += last_launch_count()
+            n_redist += 1
 
     def barrier():
         if world > 1:
@@ -327,27 +370,45 @@ def run_ours(a, shape, world, rank, local_rank):
         step(s)
     trainer.finish()
     barrier()
-    launches = 0
-    # the row kernel is timed by CUDA events around its launches on every PROF_EVERY-th step of
-    # the timed loop (each event pair costs the step ~6 us; tools/prof_overhead.py)
-    eng.profile_begin(a.steps * 16)
+    # The global step counter drives the redistribution cadence ("every 1000 training
+    # steps").  A window of K >= 1000 steps crosses its multiples naturally; a shorter window
+    # is placed so that it crosses exactly one (t_global starts K/2 before a multiple of
+    # 1000): such a window then carries one redistribution per K steps, more than the
+    # amortised 1/1000 (conservative; `redistribution` reports the amortised share).
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        barrier()
-        e0.record(stream)
-        for s in range(a.steps):
-            if PROF_EVERY > 1:
-                eng.profile_pause(s % PROF_EVERY != 0)
-            step(a.warmup + s)
-        trainer.finish()                                     # every collective inside the timed region
-        e1.record(stream)
-        barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1))
-    k_ms, k_n = eng.profile_end()
-    n_prof = len(range(0, a.steps, PROF_EVERY))          # profiled steps
-    k_step_ms = max_over_ranks(k_ms / n_prof)            # fused row kernel time per step (all its launches)
-    launches_per_step = k_n / n_prof
-    gpu_launches = launches
+    windows, redist_per_window, launch_counts = [], [], []
+    k_ms_tot, k_n_tot, n_prof = 0.0, 0, 0
+    samplers = []
+    for rep in range(max(1, a.repeats)):
+        if a.steps < REDIST_EVERY:
+            t_global = REDIST_EVERY * (rep + 1) - a.steps // 2
+        launches, n_redist = 0, 0
+        # the row kernel is timed by CUDA events around its launches on every PROF_EVERY-th step
+        # of the timed loop (each event pair costs the step ~6 us; tools/prof_overhead.py)
+        eng.profile_begin(a.steps * 16)
+        sampler = ClockSampler(local_rank)
+        with sampler:
+            barrier()
+            e0.record(stream)
+            for s in range(a.steps):
+                if PROF_EVERY > 1:
+                    eng.profile_pause(s % PROF_EVERY != 0)
+                step(a.warmup + s)
+            trainer.finish()                                     # every collective inside the timed region
+            e1.record(stream)
+            barrier()
+        windows.append(max_over_ranks(e0.elapsed_time(e1)))
+        k_ms, k_n = eng.profile_end()
+        k_ms_tot += k_ms; k_n_tot += k_n; n_prof += len(range(0, a.steps, PROF_EVERY))
+        redist_per_window.append(n_redist)
+        launch_counts.append(launches)
+        samplers.append(sampler)
+    med = sorted(range(len(windows)), key=lambda i: windows[i])[len(windows) // 2]
+    clk = samplers[med]                                   # clocks of the reported window
+    ms = windows[med]
+    k_step_ms = max_over_ranks(k_ms_tot / n_prof)        # fused row kernel time per step (all its launches)
+    launches_per_step = k_n_tot / n_prof
+    gpu_launches = launch_counts[med]
 
     # ---- end to end through the public API with host buffers (H2D inputs, D2H loss)
     n_e2e = a.e2e_steps or a.steps
@@ -357,12 +418,15 @@ def run_ours(a, shape, world, rank, local_rank):
     loss_pin = torch.zeros(1).pin_memory()
     h2d = B * shape.m * 4 + int(np.mean([4 * (B + 1 + len(d[2])) for d in data]))
     d2h = 4
+    dh_pin = torch.empty((B, shape.m)).pin_memory()
+    want_dh = False                       # second e2e pass: the step's [B][m] dh output comes back too
 
     def step_e2e(s):
         nonlocal t_global
         i = s % N_BATCHES
         if world == 1:
-            eng.train_step_host(h_pin[i], ptr_pin[i], ids_pin[i], LR, loss_host=loss_pin)
+            eng.train_step_host(h_pin[i], ptr_pin[i], ids_pin[i], LR, loss_host=loss_pin,
+                                dh_host=dh_pin if want_dh else None)
         else:
             h_dev[i].copy_(h_pin[i], non_blocking=True)
             ptr_dev[i].copy_(ptr_pin[i], non_blocking=True)
@@ -370,6 +434,8 @@ def run_ours(a, shape, world, rank, local_rank):
             layer.broadcast_h(h_dev[i])
             layer.train_step(h_dev[i], ptr_dev[i], ids_dev[i], LR, dh=dh, loss=loss)
             loss_pin.copy_(loss, non_blocking=True)
+            if want_dh:
+                dh_pin.copy_(dh, non_blocking=True)
         t_global += 1
         if t_global % REDIST_EVERY == 0:
             layer.redistribute(t_global)
@@ -384,6 +450,16 @@ def run_ours(a, shape, world, rank, local_rank):
         e1.record(stream)
         barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    want_dh = True
+    for s in range(3):
+        step_e2e(s)
+    barrier()
+    e0.record(stream)
+    for s in range(n_e2e):
+        step_e2e(s)
+    e1.record(stream)
+    barrier()
+    ms_e2e_dh = max_over_ranks(e0.elapsed_time(e1))
 
     # ---- inference: fused forward + top-K (row a8), K = 5 (P@1/3/5)
     K = 5
@@ -498,8 +574,12 @@ def run_ours(a, shape, world, rank, local_rank):
                    "avg_pos": shape.avg_pos, "parallelism": f"label-shard x{world}", "dh_mode": a.dh_mode,
                    "hybrid_frac": (a.hybrid_frac or 0.5) if a.dh_mode == "hybrid" else None,
                    "loss": a.loss, "margin_bias": a.margin_bias, "grad_skip_fraction": skip_fraction,
-                   "redistribution": f"every {REDIST_EVERY} steps inside the timed region (global step counter)",
+                   "redistribution": (f"at every multiple of {REDIST_EVERY} of the global step counter; "
+                                      f"{redist_per_window[med]} inside the reported window of {a.steps} steps"
+                                      + (" (window placed to cross one multiple)" if a.steps < REDIST_EVERY else "")),
                    "l2": "no flush: per-step state stream 617 MB >> 126 MB L2 (inputs larger than L2)"},
+        "repeats": {"windows_ms_per_step": [w / a.steps for w in windows], "reported": "median",
+                    "redistributions_per_window": redist_per_window},
         "clocks": {"sm_mhz": c1["sm_mhz"], "sm_max_mhz": c1["sm_max_mhz"], "reasons": c1["reasons"],
                    "samples": c1["samples"]},
         "hbm_step": {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / a.steps * 1e-3) / 1e9,
@@ -508,15 +588,27 @@ def run_ours(a, shape, world, rank, local_rank):
                 "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ms_e2e / n_e2e,
                 "path": "fixedfanin_train_step_host (C ABI, pinned host buffers)" if world == 1 else
                         "torch H2D + ShardedLayer.train_step + D2H loss", "clocks_sm_mhz": c2["sm_mhz"]},
+        "e2e_with_dh": {"value": B * n_e2e / (ms_e2e_dh * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h + 4 * B * shape.m, "steps": n_e2e,
+                        "ms_per_step": ms_e2e_dh / n_e2e,
+                        "note": "as e2e, plus the step's dh [B][m] copied back to pinned host memory every step"},
         "gpu_launches": gpu_launches,
-        "roofline": {"bound": "hbm", "kernel": "k_train_ring (fused fwd/BCE/dW/db/dh-or-g/Adam row pass)",
+        # `bound` names the roof the ncu evidence shows binding (profiles/r01d_ncu_train_ring_atomic.txt:
+        # L1->XBAR request path ~89% busy, DRAM ~13%); achieved / peak / frac stay the north star's
+        # HBM fraction (algorithmic bytes), and `binding` relates the same launch to its on-chip roof.
+        "roofline": {"bound": "l2", "kernel": "k_train_ring (fused fwd/BCE/dW/db/dh-or-g/Adam row pass)",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "hbm_frac": achieved / peak, "traffic": traffic,
+                     "binding": {"roof": "L2 gather + reduction path (random 128-B lines)",
+                                 "achieved_gbs": onchip / (k_step_ms * 1e-3) / 1e9,
+                                 "ceiling_gbs": ONCHIP_CEILING_GBS.get(a.dh_mode),
+                                 "frac": (onchip / (k_step_ms * 1e-3) / 1e9 / ONCHIP_CEILING_GBS[a.dh_mode]
+                                          if a.dh_mode in ONCHIP_CEILING_GBS else None)},
                      "alg_bytes_per_launch": kb / launches_per_step, "launches_per_step": launches_per_step,
                      "avg_launch_ms": k_step_ms / launches_per_step,
                      "kernel_share_of_step": k_step_ms / (ms / a.steps),
                      "timing": f"CUDA events around each launch on the launching stream, every {PROF_EVERY}th timed step "
-                               f"({n_prof} of {a.steps})"},
+                               f"({n_prof} of {a.steps * max(1, a.repeats)} over {max(1, a.repeats)} windows)"},
         "onchip": {"l2_bytes_per_step": onchip, "l2_gbs": onchip / (ms / a.steps * 1e-3) / 1e9,
                    "kernel_gbs": onchip / (k_step_ms * 1e-3) / 1e9,
                    "ceiling_gbs": ONCHIP_CEILING_GBS.get(a.dh_mode),
@@ -553,13 +645,9 @@ def run_ours(a, shape, world, rank, local_rank):
         "note": "dense figures for a dense m x L last layer of the same width (P:37-45 quotes 10.7 GiB "
                 "/ >40 GiB for Amazon-3M at 1024 hidden)"}
     if world == 1 and not a.no_cpu_baseline:
-        import oracle
-        oracle.build()
-        rows = shape.L // 8
-        v, dt = oracle_sample_rate(shape, rows, 2, data)
-        line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
-                                "sample": f"first {rows} of {shape.L} label rows (1/8), m={shape.m}, k={shape.k}, "
-                                          f"B={B}; 2 fp64 oracle steps of {dt:.2f} s, scaled x8 to all rows"}
+        # ~10-30 s of CPU work: 1 warm-up + 3 timed steps, each full-size if it fits 6 s
+        rows, dt, cores = oracle_timed(shape, data, 3, 1, 6.0)
+        line["cpu_baseline"] = cpu_line(shape, rows, dt, cores, 3, 1)
     print(json.dumps(line), flush=True)
 
 

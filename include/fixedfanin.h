@@ -90,7 +90,8 @@ typedef enum {
 typedef struct {
     int64_t L_global;    /* total labels, 1 <= L_global < 2^31 (32-bit label ids)   */
     int64_t row_begin;   /* first global label row owned by this handle                         */
-    int64_t L_local;     /* rows owned, 0 <= L_local, row_begin + L_local <= L_global           */
+    int64_t L_local;     /* rows owned, 0 <= L_local, row_begin + L_local <= L_global,          */
+                         /* L_local * k < 2^31 (32-bit connection offsets; else FF_ERR_CONFIG)  */
     int32_t m;           /* width of h, 1 <= m < 2^31                                           */
     int32_t k;           /* connections per label, 1 <= k <= min(m, FF_MAX_FANIN)               */
     int32_t max_batch;   /* largest B that will be passed, 1..FF_MAX_BATCH                      */

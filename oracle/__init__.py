@@ -26,7 +26,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 def build(force: bool = False) -> str:
     """Compile oracle.c (plain C, -O2, single thread) into liboracle.so."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-fopenmp", "-shared", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -47,6 +47,10 @@ def lib():
         L.oracle_input_grad.argtypes = [i64, i32, i32, i32, P, P, P, P, P]
         L.oracle_adam.argtypes = [i64, P, P, P, P, i64, f64, f64, f64, f64]
         L.oracle_philox4x32_10.argtypes = [P, P, P]
+        L.oracle_set_threads.argtypes = [i32]
+        L.oracle_set_threads.restype = None
+        L.oracle_get_threads.argtypes = []
+        L.oracle_get_threads.restype = i32
         L.oracle_init.argtypes = [i64, i64, i32, i32, u64, f32, P, P]
         L.oracle_redistribute.argtypes = [i64, i64, i32, i32, i32, u64, u64, P, P, P, P]
         L.oracle_topk.argtypes = [i64, i64, i32, P, i32, P, P]
@@ -78,6 +82,16 @@ def _f64(a) -> np.ndarray:
 
 def _i32(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def set_threads(n: int) -> None:
+    """Timing mode: share the label loops over n OpenMP threads (1 = the
+    plain sequential loops the parity tests use).  Only bench.py's CPU legs set n > 1."""
+    lib().oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().oracle_get_threads())
 
 
 # --------------------------------------------------------------------------- steps

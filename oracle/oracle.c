@@ -29,6 +29,21 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ------------------------------------------------------------------------- */
+/* Timing mode: with oracle_set_threads(n > 1) the loops over labels (and
+ * over Adam's elements) are shared by n OpenMP threads.  Every output element is still
+ * computed by one thread in the loop order written below, so y, g, dW, db and Adam are
+ * bit-identical to the 1-thread run; Alg. 2's dh is accumulated in per-thread private
+ * arrays over contiguous label ranges and summed in thread order (a different, fixed fp64
+ * summation order), and the loss total is an OpenMP sum.  The default is 1 thread: the
+ * parity tests run the plain sequential loops.                                          */
+static int g_threads = 1;
+void oracle_set_threads(int32_t n) { g_threads = n > 1 ? n : 1; }
+int32_t oracle_get_threads(void) { return g_threads; }
 
 /* ------------------------------------------------------------------------- */
 /* Alg. 1: score of label `label` for instance `instance`:
@@ -42,6 +57,7 @@ void oracle_forward(int64_t L, int32_t m, int32_t k, int32_t B,
                     const double* h, double* y, double* Ay)
 {
     for (int32_t instance = 0; instance < B; ++instance) {
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t label = 0; label < L; ++label) {
             double value = bias[label];
             double avalue = fabs(bias[label]);
@@ -114,6 +130,7 @@ void oracle_bce_grad(int64_t L, int64_t row_begin, int32_t B, const double* y,
 {
     double total = 0.0;
     for (int32_t b = 0; b < B; ++b) {
+        #pragma omp parallel for schedule(static) reduction(+ : total) if (g_threads > 1) num_threads(g_threads)
         for (int64_t j = 0; j < L; ++j) {
             double yy = y[(int64_t)b * L + j];
             int t = is_positive(lbl_ptr, lbl_ids, b, row_begin + j);
@@ -134,6 +151,7 @@ void oracle_sqh_grad(int64_t L, int64_t row_begin, int32_t B, const double* y,
 {
     double total = 0.0;
     for (int32_t b = 0; b < B; ++b) {
+        #pragma omp parallel for schedule(static) reduction(+ : total) if (g_threads > 1) num_threads(g_threads)
         for (int64_t j = 0; j < L; ++j) {
             double yy = y[(int64_t)b * L + j];
             double t = is_positive(lbl_ptr, lbl_ids, b, row_begin + j) ? 1.0 : -1.0;
@@ -157,6 +175,7 @@ void oracle_weight_grad(int64_t L, int32_t m, int32_t k, int32_t B,
                         const int32_t* idx, const double* h, const double* g,
                         double* dW, double* AdW, double* db, double* Adb)
 {
+    #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
     for (int64_t label = 0; label < L; ++label) {
         for (int32_t weight_idx = 0; weight_idx < k; ++weight_idx) {
             int32_t source = idx[label * k + weight_idx];
@@ -192,6 +211,44 @@ void oracle_input_grad(int64_t L, int32_t m, int32_t k, int32_t B,
 {
     memset(dh, 0, sizeof(double) * (size_t)B * (size_t)m);
     if (Adh) memset(Adh, 0, sizeof(double) * (size_t)B * (size_t)m);
+#ifdef _OPENMP
+    if (g_threads > 1) {
+        /* timing mode: thread r owns labels [r L / n, (r+1) L / n) and a private dh (and Adh);
+         * the partials are summed in thread order.                                        */
+        const int n = g_threads;
+        const size_t Bm = (size_t)B * (size_t)m;
+        double* part = (double*)calloc((size_t)n * Bm * (Adh ? 2 : 1), sizeof(double));
+        if (part) {
+            #pragma omp parallel num_threads(n)
+            {
+                const int r = omp_get_thread_num();
+                double* pd = part + (size_t)r * Bm;
+                double* pa = Adh ? part + (size_t)(n + r) * Bm : NULL;
+                for (int32_t instance = 0; instance < B; ++instance) {
+                    for (int64_t label = L * r / n; label < L * (r + 1) / n; ++label) {
+                        double out = g[(int64_t)instance * L + label];
+                        for (int32_t weight_idx = 0; weight_idx < k; ++weight_idx) {
+                            int32_t source = idx[label * k + weight_idx];
+                            double weight = W[label * k + weight_idx];
+                            pd[(int64_t)instance * m + source] += weight * out;
+                            if (pa) pa[(int64_t)instance * m + source] += fabs(weight * out);
+                        }
+                    }
+                }
+                #pragma omp barrier
+                #pragma omp for schedule(static)
+                for (int64_t e = 0; e < (int64_t)Bm; ++e) {
+                    for (int q = 0; q < n; ++q) {
+                        dh[e] += part[(size_t)q * Bm + e];
+                        if (Adh) Adh[e] += part[(size_t)(n + q) * Bm + e];
+                    }
+                }
+            }
+            free(part);
+            return;
+        }
+    }
+#endif
     for (int32_t instance = 0; instance < B; ++instance) {
         for (int64_t label = 0; label < L; ++label) {
             double out = g[(int64_t)instance * L + label];
@@ -215,6 +272,7 @@ void oracle_adam(int64_t n, double* p, const double* q, double* mo, double* ve,
 {
     double bc1 = 1.0 - pow(beta1, (double)t);
     double bc2 = 1.0 - pow(beta2, (double)t);
+    #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
     for (int64_t e = 0; e < n; ++e) {
         mo[e] = beta1 * mo[e] + (1.0 - beta1) * q[e];
         ve[e] = beta2 * ve[e] + (1.0 - beta2) * q[e] * q[e];

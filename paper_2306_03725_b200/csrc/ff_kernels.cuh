@@ -1045,7 +1045,8 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
     }
     const bool pruned0 = (pm0 >> lane) & 1u, pruned1 = (pm1 >> lane) & 1u;
     const uint32_t grow = (uint32_t)(row_begin + j);
-    int acc = -1, na = 0;                              // accepted draws: lane q holds draw q (p <= 32)
+    // accepted draws: draw q is held by lane q & 31 in register q >> 5 (p <= 63 since p < k <= 64)
+    int acc[2] = {-1, -1}, na = 0;
     for (uint32_t n = 0; na < p; ++n) {
       const U4 v = philox(n, grow, step, kDomRegrow, key0, key1);
 #pragma unroll
@@ -1054,9 +1055,10 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
           const int cand = lemire_draw(word_of(v, wi), (uint32_t)m, thr);
           if (cand >= 0) {
             const bool taken = __ballot_sync(kFull, (act[0] && c[0] == cand) || (act[1] && c[1] == cand) ||
-                                                    (lane < na && acc == cand)) != 0u;
+                                                    (lane < na && acc[0] == cand) ||
+                                                    (lane + 32 < na && acc[1] == cand)) != 0u;
             if (!taken) {
-              if (lane == na) acc = cand;
+              if (lane == (na & 31)) acc[na >> 5] = cand;
               ++na;
             }
           }
@@ -1065,8 +1067,10 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
     }
     const int order0 = __popc(pm0 & ((1u << lane) - 1u));
     const int order1 = __popc(pm0) + __popc(pm1 & ((1u << lane) - 1u));
-    const int new0 = __shfl_sync(kFull, acc, order0 & 31);
-    const int new1 = __shfl_sync(kFull, acc, order1 & 31);
+    const int a00 = __shfl_sync(kFull, acc[0], order0 & 31), a01 = __shfl_sync(kFull, acc[1], order0 & 31);
+    const int a10 = __shfl_sync(kFull, acc[0], order1 & 31), a11 = __shfl_sync(kFull, acc[1], order1 & 31);
+    const int new0 = order0 < 32 ? a00 : a01;
+    const int new1 = order1 < 32 ? a10 : a11;
     if (pruned0) { const int64_t el = j * k + lane; idx[el] = new0; W[el] = 0.0f; mW[el] = 0.0f; vW[el] = 0.0f; }
     if (pruned1) { const int64_t el = j * k + lane + 32; idx[el] = new1; W[el] = 0.0f; mW[el] = 0.0f; vW[el] = 0.0f; }
   }

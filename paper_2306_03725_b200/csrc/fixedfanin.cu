@@ -118,8 +118,11 @@ ff_status validate(const ff_config* c) {
   if (c->dh_mode != FF_DH_ATOMIC && c->dh_mode != FF_DH_CSC && c->dh_mode != FF_DH_HYBRID)
     return fail(FF_ERR_CONFIG, "dh_mode=%d is not FF_DH_ATOMIC, FF_DH_CSC or FF_DH_HYBRID", c->dh_mode);
   if (!(c->hybrid_frac >= 0.0f && c->hybrid_frac <= 1.0f)) return fail(FF_ERR_CONFIG, "hybrid_frac outside [0, 1]");
-  if (c->dh_mode != FF_DH_ATOMIC && c->L_local * (int64_t)c->k >= (int64_t(1) << 31))
-    return fail(FF_ERR_CONFIG, "CSC mode needs L_local*k < 2^31");
+  // the row kernels address W / idx / moments (and the CSC entries) with 32-bit connection
+  // offsets j*k + i: every mode needs L_local*k < 2^31 (60 GB of state per shard at the limit)
+  if (c->L_local * (int64_t)c->k >= (int64_t(1) << 31))
+    return fail(FF_ERR_CONFIG, "L_local*k = %lld connections per shard >= 2^31 (shard the labels further)",
+                (long long)(c->L_local * (int64_t)c->k));
   if (c->prune_frac < 0.0f || c->prune_frac >= 1.0f) return fail(FF_ERR_CONFIG, "prune_frac outside [0, 1)");
   if (c->loss != FF_LOSS_BCE && c->loss != FF_LOSS_SQH) return fail(FF_ERR_CONFIG, "loss=%d unknown", c->loss);
   if (c->beta1 < 0.0f || c->beta1 >= 1.0f || c->beta2 < 0.0f || c->beta2 >= 1.0f || c->eps < 0.0f)
@@ -873,6 +876,9 @@ ff_status fixedfanin_redistribute(ff_layer* l, uint64_t step, ff_stream_t stream
   const int p = (int)std::floor((double)l->cfg.prune_frac * (double)l->cfg.k);
   if (p < 1) return fail(FF_ERR_CONFIG, "prune count floor(%g*%d) = %d < 1", l->cfg.prune_frac, l->cfg.k, p);
   if (l->cfg.m - l->cfg.k < p) return fail(FF_ERR_CONFIG, "m - k = %d < prune count %d", l->cfg.m - l->cfg.k, p);
+  // stored gradients belong to the pre-call connections (a regrown slot's dW would be applied
+  // to a different column): invalidate them in every dh mode
+  l->grads_valid = false;
   if (l->cfg.L_local == 0) return FF_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_redistribute<<<l->grid_rows, 256, 0, st>>>(l->W, l->idx, l->mW, l->vW, l->cfg.L_local, l->cfg.row_begin, l->cfg.m,

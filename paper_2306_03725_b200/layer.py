@@ -313,8 +313,10 @@ def merge_topk(scores, ids, stream=None):
     P, B, K = scores.shape
     out_s = torch.empty((B, K), dtype=torch.float32, device=scores.device)
     out_i = torch.empty((B, K), dtype=torch.int32, device=scores.device)
-    _check(lib().fixedfanin_merge_topk(_ptr(scores.contiguous()), _ptr(ids.contiguous()), P, B, K, _ptr(out_s),
-                                       _ptr(out_i), _stream(stream)))
+    # the contiguous copies stay bound until the (asynchronous) kernel was enqueued on `stream`:
+    # a temporary freed inside the argument list could hand its block to the next temporary
+    sc, ic = scores.contiguous(), ids.contiguous()
+    _check(lib().fixedfanin_merge_topk(_ptr(sc), _ptr(ic), P, B, K, _ptr(out_s), _ptr(out_i), _stream(stream)))
     return out_s, out_i
 
 
@@ -324,8 +326,9 @@ def precision_at_k(ids, lbl_ptr, lbl_ids, stream=None):
     B, K = ids.shape
     hits = torch.empty(B, dtype=torch.int32, device=ids.device)
     mean = torch.empty(1, dtype=torch.float32, device=ids.device)
-    _check(lib().fixedfanin_precision_at_k(_ptr(ids.contiguous()), B, K, _ptr(lbl_ptr), _ptr(lbl_ids), _ptr(hits),
-                                           _ptr(mean), _stream(stream)))
+    ic, pc, lc = ids.contiguous(), lbl_ptr.contiguous(), lbl_ids.contiguous()     # bound: see merge_topk
+    _check(lib().fixedfanin_precision_at_k(_ptr(ic), B, K, _ptr(pc), _ptr(lc), _ptr(hits), _ptr(mean),
+                                           _stream(stream)))
     return hits, mean
 
 
@@ -388,8 +391,13 @@ class DenseLayer:
                                                  _ptr(vbd), ctypes.byref(tt) if tt is not None else None,
                                                  _stream(stream)))
 
-    def forward(self, x, step=0, train=True, h=None, stream=None):
+    def forward(self, x, step=None, train=True, h=None, stream=None):
+        """step keys the dropout mask (R25).  None: FF_STEP_AUTO for a training forward (the
+        device Adam counter + 1, so consecutive training steps draw fresh masks), 0 for
+        inference (no dropout is applied then)."""
         B = x.shape[0]
+        if step is None:
+            step = FF_STEP_AUTO if train else 0
         if h is None:
             h = torch.empty((B, self.m), dtype=torch.float32, device=self.device)
         _check(lib().fixedfanin_dense_forward(self._h, _ptr(x), B, int(step), 1 if train else 0, _ptr(h),
@@ -409,8 +417,11 @@ class DenseLayer:
 def model_train_step(dense: DenseLayer, layer: FixedFanInLayer, x, step, lbl_ptr, lbl_ids, lr, grad_scale=None,
                      loss=None, stream=None):
     """One step of the whole architecture (dropout -> dense -> ReLU -> fixed fan-in -> loss ->
-    backward through both layers -> Adam on both) through fixedfanin_model_train_step."""
+    backward through both layers -> Adam on both) through fixedfanin_model_train_step.
+    step keys the dropout mask; None = FF_STEP_AUTO (the dense layer's device counter + 1)."""
     B = x.shape[0]
+    if step is None:
+        step = FF_STEP_AUTO
     gs = 1.0 / max(B, 1) if grad_scale is None else grad_scale
     _check(lib().fixedfanin_model_train_step(dense._h, layer._h, _ptr(x), B, int(step), _ptr(lbl_ptr), _ptr(lbl_ids),
                                              gs, lr, _ptr(loss), _stream(stream)))

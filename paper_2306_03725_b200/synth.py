@@ -64,6 +64,12 @@ def hidden_batch(B: int, m: int, step: int = 0, seed: int = DATA_SEED) -> np.nda
     return np.maximum(z, np.float32(0.0))
 
 
+def signed_hidden_batch(B: int, m: int, step: int = 0, seed: int = DATA_SEED, scale: float = 1.0) -> np.ndarray:
+    """h[B][m] float32 = scale * N(0,1) without the ReLU: signed inputs for the parity tests
+    of regimes a post-ReLU h never reaches (negative h, saturated logits)."""
+    return (_rng(seed, step, 5).standard_normal((B, m), dtype=np.float32) * np.float32(scale)).astype(np.float32)
+
+
 def feature_batch(B: int, d: int, step: int = 0, seed: int = DATA_SEED) -> np.ndarray:
     """x[B][d] float32 ~ N(0,1): stand-in for the fixed dense embeddings (no dataset)."""
     return _rng(seed, step, 3).standard_normal((B, d), dtype=np.float32)

@@ -55,11 +55,21 @@ def test_workspace_size_matches_layout_model():
     (dict(L_global=10, m=64, k=8, max_topk=9), "max_topk"),
     (dict(L_global=2 ** 31, m=64, k=8), "L_global"),
     (dict(L_global=10, m=64, k=8, prune_frac=1.0), "prune_frac"),
+    # 32-bit connection offsets in every dh mode: 2^26 rows x 32 = 2^31
+    (dict(L_global=2 ** 26, m=64, k=32), "connections per shard"),
+    (dict(L_global=2 ** 26, m=64, k=32, dh_mode=L.FF_DH_CSC), "connections per shard"),
+    (dict(L_global=2 ** 30, m=64, k=64, row_begin=2 ** 20, L_local=2 ** 25), "connections per shard"),
 ])
 def test_bad_configs_rejected(kw, msg):
     with pytest.raises(L.FFError) as e:
         L.workspace_size(L.LayerConfig(**kw))
     assert e.value.status == L.FF_ERR_CONFIG and msg in str(e.value)
+
+
+def test_largest_shard_below_the_offset_limit_is_accepted():
+    """L_local * k = 2^31 - 32 connections: the last shard size the 32-bit offsets allow."""
+    n = L.workspace_size(L.LayerConfig(L_global=2 ** 26 - 1, m=64, k=32, max_batch=32))
+    assert n >= 5 * 4 * (2 ** 31 - 32)
 
 
 def test_create_without_gpu_fails_loudly():

@@ -70,6 +70,22 @@ def adam_A(W_old, W_new_ref):
     return np.abs(W_old) + np.abs(np.asarray(W_new_ref) - W_old)
 
 
+def assert_adam_update(W_old, W_new, W_ref, what):
+    """Direct check of the Adam update u = p - p' itself (not only of p' = p - u at the scale
+    of |p| + |u|): |(p'_gpu - p) - (p'_ref - p)| <= 1e-4 |u_ref| + 2 ulp_fp32(p, p'), the last
+    term being the fp32 rounding of the subtraction p - u on the GPU."""
+    W_old = np.asarray(W_old, dtype=np.float32)
+    W_new = np.asarray(W_new, dtype=np.float32)
+    d_gpu = W_new.astype(np.float64) - W_old.astype(np.float64)      # exact in fp64
+    u_ref = np.asarray(W_ref, dtype=np.float64) - W_old.astype(np.float64)
+    ulp = np.maximum(np.spacing(np.abs(W_old)), np.spacing(np.abs(W_new))).astype(np.float64)
+    err = np.abs(d_gpu - u_ref)
+    bound = 1e-4 * np.abs(u_ref) + 2 * ulp
+    bad = err > bound
+    assert not bad.any(), (f"{what}: {bad.sum()} updates off, worst err {err[bad].max():.3e} "
+                           f"vs bound {bound[bad][err[bad].argmax()]:.3e}")
+
+
 def state_of(lay):
     p = lay.get_params()
     return {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in p.items()}
@@ -186,6 +202,8 @@ def test_backward_and_adam_parity(L, m, k, B, dh_mode, loss):
     assert_close(s["mW"], mr, 0, "mW'")
     assert_close(s["vW"], vr, 1e-30, "vW'")
     assert_close(s["bias"], br, adam_A(bias, br), "bias'")
+    assert_adam_update(W, s["W"], Wr, "W update")
+    assert_adam_update(bias, s["bias"], br, "bias update")
     assert s["t"] == 1
 
 
@@ -249,6 +267,9 @@ def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k):
         Wr, mr, vr = oracle.adam(s0["W"], dW.cpu().numpy(), s0["mW"], s0["vW"], s0["t"] + 1, F32(1e-3), **ADAM)
         assert_close(s1["W"], Wr, adam_A(s0["W"], Wr), "W'")
         assert_close(s1["mW"], mr, 0, "m'"); assert_close(s1["vW"], vr, 1e-30, "v'")
+        assert_adam_update(s0["W"], s1["W"], Wr, f"W update step {step}")
+        br, _, _ = oracle.adam(s0["bias"], db.cpu().numpy(), s0["mb"], s0["vb"], s0["t"] + 1, F32(1e-3), **ADAM)
+        assert_adam_update(s0["bias"], s1["bias"], br, f"bias update step {step}")
         assert s1["t"] == step + 1
 
 
@@ -273,6 +294,7 @@ def test_set_params_t_drives_the_device_step_counter(t0):
     assert s1["t"] == t0 + 1
     Wr, mr, vr = oracle.adam(s0["W"], dW.cpu().numpy(), s0["mW"], s0["vW"], t0 + 1, F32(1e-3), **ADAM)
     assert_close(s1["W"], Wr, adam_A(s0["W"], Wr), "W' (fused)")
+    assert_adam_update(s0["W"], s1["W"], Wr, "W update (fused, t0 + 1)")
     y = lay.forward(tens(h))
     lay.backward(tens(h), y, tens(ptr), tens(ids))
     dW2, _ = lay.get_grads()
@@ -281,6 +303,7 @@ def test_set_params_t_drives_the_device_step_counter(t0):
     assert s2["t"] == t0 + 2
     Wr2, _, _ = oracle.adam(s1["W"], dW2.cpu().numpy(), s1["mW"], s1["vW"], t0 + 2, F32(1e-3), **ADAM)
     assert_close(s2["W"], Wr2, adam_A(s1["W"], Wr2), "W' (unfused)")
+    assert_adam_update(s1["W"], s2["W"], Wr2, "W update (unfused, t0 + 2)")
 
 
 @DH
@@ -304,9 +327,20 @@ def test_free_running_tiny_run_matches_oracle(dh_mode):
     W2, idx2, m2, v2 = oracle.redistribute(s["W"], s["idx"], s["mW"], s["vW"], m, p, seed=42, step=5)
     s2 = state_of(lay)
     assert (s2["idx"] == idx2).all() and (s2["W"] == W2).all() and (s2["mW"] == m2).all() and (s2["vW"] == v2).all()
-    # and the free-running oracle state agrees except at near-ties of |W|
+    # and the free-running oracle (its own fp64 state) agrees except at near-ties of |W|
+    # (SURVEY §8(c).4): the regrow draws and the pre-call sets are identical (same Philox key,
+    # same idx), so a row can only differ if the p-th and (p+1)-th smallest |W| swap places
+    # between the fp32 and fp64 runs, i.e. if their fp64 gap is within the two elements'
+    # R19 error bound after 5 steps: 1e-4 (|W| + 5 lr) each.
     Wf, idxf, _, _ = oracle.redistribute(st.W, st.idx, st.mW, st.vW, m, p, seed=42, step=5)
-    assert (idxf == s2["idx"]).mean() > 0.999
+    rows = np.where((idxf != s2["idx"]).any(axis=1))[0]
+    lr5 = 5 * F32(1e-3)
+    for j in rows:
+        a = np.sort(np.abs(st.W[j]))
+        gap = a[p] - a[p - 1]
+        tol = 1e-4 * (a[p] + lr5) + 1e-4 * (a[p - 1] + lr5)
+        assert gap <= tol, f"row {j}: pruned set differs without a near-tie (gap {gap:.3e} > {tol:.3e})"
+    print(f"free-running redistribution: {len(rows)} of {L} rows differ, all at near-ties of |W|")
     # one more step after the redistribution: dh must use the new connections (CSC rebuilt)
     s2 = state_of(lay)
     st2 = oracle.State(s2["W"].astype(np.float64), s2["idx"], s2["bias"].astype(np.float64),
@@ -835,3 +869,187 @@ def test_precision_at_k_matches_oracle(B, K, npos):
     assert (hits.cpu().numpy() == ref_h).all()
     ref = oracle.precision_at_k(top.astype(np.int64), ptr, ids)
     assert abs(mean.item() - ref) <= 1e-6 * max(ref, 1e-30)
+
+
+# ------------------------------------------- top-K against the fp64 oracle (gap-guarded)
+def _topk_gap_guarded(ids_gpu, y64, Ay, K):
+    """SURVEY §8(c).2 #20 against the fp64 scores.  With s_0 >= s_1 >= ... the oracle's
+    ordered scores of a sample and tol_r = 1e-4 (A_r + A_{r+1}) the R19 bound of two
+    neighbours: where the K-th / (K+1)-th gap exceeds tol the GPU's top-K id SET equals the
+    oracle's top-K of the fp64 y, and every rank r whose gaps to both neighbours exceed their
+    tol holds the oracle's id exactly.  A sample where any of these gaps is within tol is a
+    near-tie: counted, and its ids must still be a valid top-K (every returned score within
+    the bound of the oracle's K-th, K distinct ids).  Returns the number of near-tie samples."""
+    _, oid = oracle.topk(y64, K + 1)
+    near = 0
+    for b in range(y64.shape[0]):
+        o = oid[b]
+        s = y64[b, o]
+        sep = s[:-1] - s[1:] > 1e-4 * (Ay[b, o[:-1]] + Ay[b, o[1:]])      # gap r / r+1 is unambiguous
+        if sep[K - 1]:
+            assert set(ids_gpu[b].tolist()) == set(o[:K].tolist()), f"sample {b}: {ids_gpu[b]} vs {o[:K]}"
+        for r in range(K):
+            if sep[r] and (r == 0 or sep[r - 1]):
+                assert ids_gpu[b, r] == o[r], f"sample {b} rank {r}: {ids_gpu[b]} vs fp64 top-K {o[:K]}"
+        if not sep.all():
+            near += 1
+            kth = s[K - 1] - 1e-4 * Ay[b, o[K - 1]]
+            assert (y64[b, ids_gpu[b]] + 1e-4 * Ay[b, ids_gpu[b]] >= kth).all(), f"sample {b}: invalid top-K"
+            assert len(set(ids_gpu[b].tolist())) == K
+    return near
+
+
+@pytest.mark.parametrize("L,m,k,B,K", [(5000, 512, 32, 32, 5), (3001, 300, 32, 7, 8), (4000, 1024, 16, 70, 5),
+                                        (2000, 4096, 64, 32, 3), (200003, 4096, 32, 32, 5), (3000, 1024, 32, 1024, 5)])
+def test_predict_topk_vs_fp64_oracle_gap_guarded(L, m, k, B, K):
+    lay = make(L, m, k, B=B, seed=13)
+    h = synth.hidden_batch(B, m, step=11)
+    _, ids = lay.predict_topk(tens(h), K)
+    s = state_of(lay)
+    y64, Ay = oracle.forward(s["W"], s["idx"], s["bias"], h)      # fp64 scores of the GPU's params
+    near = _topk_gap_guarded(ids.cpu().numpy(), y64, Ay, K)
+    print(f"top-{K} vs fp64 oracle: {B - near} of {B} samples without a near-tie, {near} near-ties")
+    assert near <= max(2, B // 4)           # sanity: ties within the 1e-4 bound stay a minority
+
+
+def test_predict_topk_vs_fp64_oracle_full_amazon_670k():
+    """BASELINE.json's Amazon-670K shape in the bench's predict configuration (k = 32, B = 32,
+    the pipelined kernel), after one training step so that bias and W are not at init."""
+    shape = synth.SHAPES["amazon-670k"]
+    L, m, k, B = shape.L, shape.m, shape.k, shape.B
+    lay = make(L, m, k, B=B, seed=42)
+    ptr, lid = synth.label_batch(B, L, shape.avg_pos, step=0)
+    lay.train_step(tens(synth.hidden_batch(B, m, step=0)), tens(ptr), tens(lid), F32(1e-3))
+    h = synth.hidden_batch(B, m, step=3)
+    _, ids = lay.predict_topk(tens(h), 5)
+    s = state_of(lay)
+    y64, Ay = oracle.forward(s["W"], s["idx"], s["bias"], h)
+    near = _topk_gap_guarded(ids.cpu().numpy(), y64, Ay, 5)
+    print(f"Amazon-670K top-5 vs fp64 oracle: {B - near} of {B} samples without a near-tie, {near} near-ties")
+    assert near <= B // 4
+
+
+# ------------------------------------------- saturated-logit BCE regime, signed h (R5)
+SAT_BIAS = np.array([-60.0, -25.0, 0.0, 25.0, 60.0], np.float32)
+
+
+@LOSS
+@DH
+@pytest.mark.parametrize("k,B", [(32, 32), (16, 32), (32, 20), (13, 40)])
+def test_saturated_logits_and_signed_h_lockstep(dh_mode, loss, k, B):
+    """biases of +-25 and +-60 with positives and negatives on each, W scale 2
+    and signed (non-ReLU) h, so that y reaches |y| ~ 65.  For a positive with y >~ 17 the naive
+    fp32 sigma(y) - 1 is exactly 0 while the true gradient is -s sigma(-y) ~ 1e-26 (R5): dW,
+    db (sums of such terms) and the loss are compared with the oracle at R19, the Adam state
+    in lockstep, the update directly.  Runs the pipelined (k = 32, B <= 32) and generic kernels."""
+    layer = L_()
+    L, m = 1500, 512
+    lay = make(L, m, k, B=max(B, 32), seed=17, dh_mode=dh_mode, loss=loss_id(loss), flags=layer.FF_FLAG_STORE_GRADS)
+    W, idx, _ = synth.random_params(L, m, k, seed=21, scale=2.0)
+    bias = SAT_BIAS[np.arange(L) % len(SAT_BIAS)]
+    lay.set_params(W=tens(W), idx=tens(idx), bias=tens(bias))
+    h = synth.signed_hidden_batch(B, m, step=3)
+    ptr, ids = synth.random_labels_uniform(B, L, 60, seed=5)      # ~60 positives per sample: every bias class
+    st = oracle.State(W.astype(np.float64), idx, bias.astype(np.float64), np.zeros((L, k)), np.zeros((L, k)),
+                      np.zeros(L), np.zeros(L), 0)
+    y = lay.forward(tens(h)).cpu().numpy()
+    loss_t = torch.zeros(1, device=dev())
+    dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3), loss=loss_t)
+    dW, db = (x.cpu().numpy() for x in lay.get_grads())
+    r = oracle.train_step(st, h, ptr, ids, F32(1.0 / B), F32(1e-3), loss=loss, **ADAM)
+    assert np.abs(r.y).max() > 40                                  # the saturated regime is reached
+    posmask = np.zeros((B, L), bool)
+    for b in range(B):
+        posmask[b, ids[ptr[b]:ptr[b + 1]]] = True
+    if loss == "bce":
+        sat_pos = posmask & (r.y > 17)                             # sigma(y) - 1 == 0 in fp32 here
+        assert sat_pos.sum() > 50 and (r.g[sat_pos] != 0).all()
+    assert_close(y, r.y, r.Ay, "y")
+    assert_close(dW, r.dW, r.AdW, "dW")
+    assert_close(db, r.db, r.Adb, "db")
+    assert_close(dh.cpu().numpy(), r.dh, r.Adh, "dh")
+    assert abs(loss_t.item() - r.loss) <= RTOL * abs(r.loss)
+    s1 = state_of(lay)
+    Wr, mr, vr = oracle.adam(W, dW, np.zeros((L, k)), np.zeros((L, k)), 1, F32(1e-3), **ADAM)
+    br, mbr, vbr = oracle.adam(bias, db, np.zeros(L), np.zeros(L), 1, F32(1e-3), **ADAM)
+    assert_close(s1["W"], Wr, adam_A(W, Wr), "W'")
+    assert_close(s1["mW"], mr, 0, "mW'")
+    assert_close(s1["vW"], vr, 1e-30, "vW'")
+    assert_close(s1["bias"], br, adam_A(bias, br), "bias'")
+    assert_adam_update(W, s1["W"], Wr, "W update")
+    assert_adam_update(bias, s1["bias"], br, "bias update")
+
+
+# ------------------------------------------------------------ FF_FLAG_CHECK_FINITE
+@DH
+@pytest.mark.parametrize("k,B", [(32, 32), (16, 32), (32, 100)])
+@pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan])
+def test_check_finite_reports_nonfinite_scores(dh_mode, k, B, bad):
+    """with FF_FLAG_CHECK_FINITE a non-finite score (an inf / NaN in h reaches
+    every label connected to that column) raises FF_ERR_NONFINITE at the next check(), which
+    clears it; without the flag the same step reports nothing."""
+    layer = L_()
+    L, m = 2000, 256
+    h = synth.hidden_batch(B, m, step=1)
+    h[B // 2, 17] = bad
+    ptr, ids = synth.label_batch(B, L, 5.0, step=1)
+    flagged = make(L, m, k, B=B, seed=3, dh_mode=dh_mode, flags=layer.FF_FLAG_CHECK_FINITE)
+    plain = make(L, m, k, B=B, seed=3, dh_mode=dh_mode)
+    flagged.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
+    with pytest.raises(layer.FFError) as e:
+        flagged.check()
+    assert e.value.status == layer.FF_ERR_NONFINITE
+    flagged.check()                                                # cleared
+    plain.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
+    plain.check()
+    hf = synth.hidden_batch(B, m, step=2)                          # finite input: no report
+    flagged.train_step(tens(hf), tens(ptr), tens(ids), F32(1e-3))
+    # (the previous step left non-finite weights in the rows that saw the inf: fresh layer)
+    fresh = make(L, m, k, B=B, seed=3, dh_mode=dh_mode, flags=layer.FF_FLAG_CHECK_FINITE)
+    fresh.train_step(tens(hf), tens(ptr), tens(ids), F32(1e-3))
+    fresh.check()
+    y = fresh.forward(tens(hf))
+    fresh.backward(tens(h), y, tens(ptr), tens(ids))              # unfused backward: y finite, h not
+    fresh.check()                                                  # scores are checked, finite here
+    y[B // 2, 5] = bad
+    fresh.backward(tens(hf), y, tens(ptr), tens(ids))
+    with pytest.raises(layer.FFError) as e:
+        fresh.check()
+    assert e.value.status == layer.FF_ERR_NONFINITE
+
+
+# ------------------------------------------- redistribution with more than 32 pruned slots
+@pytest.mark.parametrize("L,m,k,frac", [(500, 4096, 64, 0.6), (300, 200, 64, 0.99), (400, 1000, 48, 0.8)])
+def test_redistribution_more_than_32_pruned_slots(L, m, k, frac):
+    """p = floor(frac k) up to 63 (k = 64): the regrow draws beyond the 32nd are held
+    in a second register per lane; bit-exact vs the oracle and k distinct indices per row."""
+    lay = make(L, m, k, seed=19, prune_frac=frac)
+    W, idx, _ = synth.random_params(L, m, k, seed=8)
+    rng = np.random.default_rng(2)
+    mW, vW = rng.random((L, k)).astype(np.float32), rng.random((L, k)).astype(np.float32)
+    lay.set_params(W=tens(W), idx=tens(idx), mW=tens(mW), vW=tens(vW))
+    lay.redistribute(1000)
+    s = state_of(lay)
+    p = int(np.floor(F32(frac) * k))
+    assert p > 32
+    W2, idx2, m2, v2 = oracle.redistribute(W, idx, mW, vW, m, p, seed=19, step=1000)
+    assert (s["idx"] == idx2).all()
+    assert (s["W"] == W2).all() and (s["mW"] == m2).all() and (s["vW"] == v2).all()
+    assert all(len(set(r)) == k for r in s["idx"])
+    lay.set_params(idx=tens(s["idx"]))                              # round trip: no duplicate rejected
+
+
+def test_redistribute_invalidates_stored_gradients():
+    """backward -> redistribute -> adam_step must not apply the old connections'
+    gradients to the regrown slots: the Adam step after a redistribution is refused."""
+    layer = L_()
+    L, m, k, B = 300, 256, 16, 32
+    lay = make(L, m, k, B=B, seed=4)
+    h = tens(synth.hidden_batch(B, m, step=1))
+    ptr, ids = synth.label_batch(B, L, 5.0, step=1)
+    y = lay.forward(h)
+    lay.backward(h, y, tens(ptr), tens(ids))
+    lay.redistribute(1000)
+    with pytest.raises(layer.FFError) as e:
+        lay.adam_step(1e-3)
+    assert e.value.status == layer.FF_ERR_STATE

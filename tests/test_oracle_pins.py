@@ -559,3 +559,27 @@ def test_model_step_updates_both_layers_with_their_own_t():
     nz = np.abs(r.dWd) > 1e-6
     assert np.allclose(moved[nz], 1e-3, rtol=1e-2) and (moved[r.dWd == 0] == 0).all()
     assert (np.abs(st.W - W0) > 0).any()
+
+
+def test_threaded_timing_mode_equals_sequential_oracle():
+    """the OpenMP timing mode (bench.py's cpu_baseline and reference arm)
+    computes the same step: y, g, dW, db and the Adam state bit-identical to the sequential
+    loops, dh and the loss equal up to the fp64 summation order."""
+    import os
+    L, m, k, B = 3001, 512, 16, 32
+    h = synth.hidden_batch(B, m, step=1)
+    ptr, ids = synth.label_batch(B, L, 5.0, step=1)
+    a = oracle.State.create(L, m, k, seed=42)
+    b = a.copy()
+    oracle.set_threads(1)
+    ra = oracle.train_step(a, h, ptr, ids, 1.0 / B, 1e-3)
+    try:
+        oracle.set_threads(max(2, min(8, len(os.sched_getaffinity(0)))))
+        rb = oracle.train_step(b, h, ptr, ids, 1.0 / B, 1e-3)
+    finally:
+        oracle.set_threads(1)
+    for x, y in ((ra.y, rb.y), (ra.g, rb.g), (ra.dW, rb.dW), (ra.db, rb.db), (a.W, b.W), (a.mW, b.mW),
+                 (a.vW, b.vW), (a.bias, b.bias)):
+        assert np.array_equal(x, y)
+    assert np.abs(ra.dh - rb.dh).max() <= 1e-12 * ra.Adh.max()
+    assert abs(ra.loss - rb.loss) <= 1e-12 * abs(ra.loss)
