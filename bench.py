@@ -51,6 +51,8 @@ def args_():
     p.add_argument("--repeats", type=int, default=5,
                    help="timed windows of --steps steps each; the median window is reported (SURVEY §8(d).3)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--train-only", action="store_true",
+                   help="dev A/B sweeps: time the training windows only (no e2e / predict / model / extra sections)")
     p.add_argument("--flags", type=int, default=0, help="extra ff_config.flags (A/B experiments)")
     p.add_argument("--loss", default="bce", choices=["bce", "sqh"],
                    help="bce (north star) or the paper's squared hinge with implicit negative mining (P:526-551)")
@@ -410,6 +412,13 @@ def run_ours(a, shape, world, rank, local_rank):
     launches_per_step = k_n_tot / n_prof
     gpu_launches = launch_counts[med]
 
+    if a.train_only:
+        if rank == 0:
+            print(json.dumps({"ms_per_step": ms / a.steps, "value": B * a.steps / (ms * 1e-3),
+                              "windows_ms_per_step": [w / a.steps for w in windows],
+                              "row_kernel_ms_per_step": k_step_ms, "row_launches_per_step": launches_per_step,
+                              "dh_mode": a.dh_mode, "loss": a.loss, "B": B, "shape": shape.name}), flush=True)
+        return
     # ---- end to end through the public API with host buffers (H2D inputs, D2H loss)
     n_e2e = a.e2e_steps or a.steps
     h_pin = [torch.from_numpy(d[0]).pin_memory() for d in data]

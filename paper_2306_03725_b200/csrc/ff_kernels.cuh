@@ -37,9 +37,10 @@ struct RowArgs {
   float* dW; float* db;
   uint32_t* posmask;          // [nb][L] bit (b & 31) of word [b>>5][j]: is row_begin+j a positive of b
   float* hd;                  // [m][nb][64]: h line | dh line per column and 32-sample chunk
-  const int* pos;             // CSC mode: CSC position of connection e = j*k + i
-  float* wcsc;                // CSC mode: pre-update W in CSC order
-  float* gT;                  // CSC mode: g[j - j_begin][nb][32] (per-label gradient lines of the tile)
+  float* gT;                  // CSC mode: one record per label row of the tile, rs floats each:
+                              //   [q2*32 + r] = g[q2*32 + r][j] (gradient line of chunk q2),
+                              //   [32*nb + i] = pre-update W[j][i] (0 if the row's gradient is all zero)
+  int rs;                     // CSC mode: record stride in floats = 32*nb + 32*ceil(k/32)
   int64_t j_begin, j_end;     // label rows processed by this launch (a tile; multiple of 32)
   int br;                     // rows per warp block (32, 16, 8 or 4): smaller for small L
   int64_t L; int k; int B; int nb; int cstride;   // cstride = 64*nb floats per column
@@ -277,9 +278,9 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
   float loss_acc = 0.0f;
 
   float w_n[KPL], mw_n[KPL], vw_n[KPL];
-  int c_n[KPL], p_n[KPL];
+  int c_n[KPL];
 #pragma unroll
-  for (int e = 0; e < KPL; ++e) { w_n[e] = mw_n[e] = vw_n[e] = 0.f; c_n[e] = p_n[e] = 0; }
+  for (int e = 0; e < KPL; ++e) { w_n[e] = mw_n[e] = vw_n[e] = 0.f; c_n[e] = 0; }
   auto prefetch_row = [&](int64_t jj) {
     const int64_t row = jj * k;
 #pragma unroll
@@ -288,7 +289,6 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
         const int64_t r = row + lane + 32 * e;
         w_n[e] = ld_stream(a.W + r, pol_s);
         c_n[e] = ld_stream_ro(a.idx + r, pol_s);
-        if (CSC && MODE != kModeForward) p_n[e] = ld_stream_ro(a.pos + r, pol_s);
         if (MODE == kModeTrain) { mw_n[e] = ld_stream(a.mW + r, pol_s); vw_n[e] = ld_stream(a.vW + r, pol_s); }
       }
     }
@@ -310,9 +310,9 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
     for (int i = 0; i < nl; ++i) {
       const int64_t j = j0 + i;
       float w[KPL], mw[KPL], vw[KPL];
-      int c[KPL], pe[KPL];
+      int c[KPL];
 #pragma unroll
-      for (int e = 0; e < KPL; ++e) { w[e] = w_n[e]; mw[e] = mw_n[e]; vw[e] = vw_n[e]; c[e] = c_n[e]; pe[e] = p_n[e]; }
+      for (int e = 0; e < KPL; ++e) { w[e] = w_n[e]; mw[e] = mw_n[e]; vw[e] = vw_n[e]; c[e] = c_n[e]; }
       if (i + 1 < nl) prefetch_row(j + 1);
       else if (blk + nw < nblk) prefetch_row(jb + (blk + nw) * br);
       const int64_t row = j * k;
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
         dbr = q2 == 0 ? dbc : dbr + dbc;
         if (CSC) {
           // CSC mode: publish g[., j] (one 128-B line per chunk); dh is pulled later (k_dh_csc)
-          st_hint(a.gT + ((j - jb) * nb + q2) * 32 + 4 * bq + gq, g, pol_l);
+          st_hint(a.gT + (j - jb) * a.rs + q2 * 32 + 4 * bq + gq, g, pol_l);
           if (a.split != 0u) {                        // hybrid: columns < split by red
             const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
@@ -387,8 +387,6 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       }
       if (MODE == kModeForward) continue;
 
-      // pre-update W in CSC order for k_dh_csc; 0 when the row's gradient is all zero, so the
-      // column pass skips the gather (its contribution w*g is exactly zero anyway)
       float gW[KPL];
       row_dw_slots<NG>(dwp, lane, gW);
       if (lane == i) db_v = dbr;                      // lane i <-> row j0 + i
@@ -396,7 +394,9 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
       for (int e = 0; e < KPL; ++e) {
         if (!act[e]) continue;
         const int64_t r = row + lane + 32 * e;
-        if (CSC && (uint32_t)c[e] >= a.split) a.wcsc[pe[e]] = gany ? w[e] : 0.0f;
+        // pre-update W into the row's record for k_dh_csc (one coalesced line); 0 when the row's
+        // gradient is all zero, so the column pass may skip the gather (w*g is exactly 0 anyway)
+        if (CSC) a.gT[(j - jb) * a.rs + 32 * nb + lane + 32 * e] = gany ? w[e] : 0.0f;
         if (MODE == kModeBackward || STORE_GRADS) a.dW[r] = gW[e];
         if (MODE == kModeTrain) {
           adam_update(w[e], mw[e], vw[e], gW[e], adam);
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
   const int B = a.B;
   float* const hb = pin(a.hd + 4 * bq);
   float* const W = a.W; float* const mW = a.mW; float* const vW = a.vW;
-  const int* const idx = a.idx; const int* const pos = a.pos;
+  const int* const idx = a.idx;
   const float grad_scale = a.grad_scale;
   const bool want_loss = a.loss != nullptr, check = a.check_finite != 0, sqh = a.sqh != 0;
   const uint32_t split = a.split;
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
   auto row_of = [&](Cur c) { return jb32 + c; };
   auto i_of = [&](Cur c) { return (int)((c - r_lo) & 31u); };
 
-  struct St { float w, mw, vw; int c, pe; };
+  struct St { float w, mw, vw; int c; };
   auto load_st = [&](Cur cu, St& st) {
     if (live(cu)) {
       const uint32_t row = row_of(cu) * 32u + lane;
@@ -521,7 +521,6 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
       st.c = ld_na_ro(idx + row);
       st.mw = ld_na(mW + row);
       st.vw = ld_na(vW + row);
-      if (CSC) st.pe = ld_na_ro(pos + row);
     }
   };
   struct Bv { float bias, mb, vb; uint32_t pm; };
@@ -604,8 +603,11 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
 #pragma unroll
     for (int q = 0; q < NG; ++q) dwp[q] = dw_partial(g4, hv[q]);
     if (CSC) {
-      st_hint(a.gT + (size_t)((j - jb32) * 32u + b), g, pol_l);
-      if (!HYB || (uint32_t)st.c >= split) a.wcsc[(uint32_t)st.pe] = gany ? st.w : 0.0f;   // 0: column pass skips
+      // the row's record: its gradient line and (at +32 floats) its pre-update weights, two
+      // coalesced 128-B lines (0 weights when the row's gradient is all zero)
+      float* const rec = a.gT + (size_t)(j - jb32) * (uint32_t)a.rs;
+      st_hint(rec + b, g, pol_l);
+      st_hint(rec + 32 + lane, gany ? st.w : 0.0f, pol_l);
       if (HYB) {                                         // hybrid: columns < split by red
         const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
@@ -655,79 +657,104 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
 
 // ---------------------------------------------------------------------- CSC dh pull
 // Alg. 2 as a gather over the transposed (CSC) index: for every column c,
-//   dh[b][c] = sum_{p in col c} wcsc[p] * g[b][ent_row[p]]
+//   dh[b][c] = sum_{p in col c} W_old[j_p][i_p] * g[b][j_p]
 // with entries in (label tile, column, row) order — deterministic, no atomics.  The
-// transposed index is split by label tile so that the gT lines a launch gathers were
-// written by the row launch just before it (L2-resident).  Tile t covers col_ptr segments
-// [t*m + c]; tile 0 writes the dh half of hd, later tiles accumulate into it.
-// Warp per column (grid-stride); lane (gq, bq) takes entry 4u + gq of each 32-entry batch
-// and samples 4bq..4bq+3 (one 16-B slice of the 128-B g line).
-template <bool NB1>
-__global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr, const int* __restrict__ ent_row,
-                                                const float* __restrict__ wcsc, const float* __restrict__ gT,
-                                                int m, int nb_rt, int tile, int64_t j_begin, float* __restrict__ hd,
-                                                int c_begin) {
+// transposed index is split by label tile so that the records a launch gathers were
+// written by the row launch just before it (L2-resident).  Entry p is the packed
+// (row within the tile << 6) | slot; the row pass left, per row of the tile, one record of
+// rs floats: the gradient line of each 32-sample chunk, then the row's pre-update weights.
+// So the column pass reads the entry stream coalesced and, per entry, one 128-B gradient
+// line plus the one 32-B sector holding W_old[j][i] — the hand-off of the pre-update
+// weights costs the row pass one coalesced line per row instead of k scattered stores.
+// Tile t covers col_ptr segments [t*m + c]; tile 0 writes the dh half of hd, later tiles
+// accumulate into it.  Warp per column (grid-stride); lane (gq, bq) takes entry 4u + gq of
+// each 32-entry batch and samples 4bq..4bq+3 (one 16-B slice of the 128-B g line).
+// SKIPZ (squared hinge): a zero weight (a row whose gradient is all zero) skips the gather;
+// the weight is then loaded before the gathers instead of beside them.
+template <bool NB1, bool SKIPZ>
+__global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr, const int* __restrict__ ent,
+                                                const float* __restrict__ gT, int rs, int m, int nb_rt, int tile,
+                                                float* __restrict__ hd, int c_begin) {
   const int nb = NB1 ? 1 : nb_rt;
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const uint64_t pol_l = policy_evict_last();
   const int* cp = col_ptr + (int64_t)tile * m;
-  const int jb = (int)j_begin;
-  const uint32_t gstride = 32u * (uint32_t)nb;               // floats per gT row
+  const uint32_t rsu = (uint32_t)rs, woff = 32u * (uint32_t)nb;
+  // one batch of up to 32 entries [p, p + 32) of a column ending at pend, for chunk q2:
+  // returns the lane's 4-sample partial sums added to acc
+  auto batch = [&](int er, bool ok, int p, int pend, int q2, float4& acc) {
+    const bool tail = p + 32 > pend;
+    const uint32_t rec = (uint32_t)er >> 6;
+    const float* gb = gT + q2 * 32 + 4 * bq;
+    float wv = 0.0f;
+    if (SKIPZ && ok) wv = ld_na(gT + (size_t)rec * rsu + woff + ((uint32_t)er & 63u));
+    float4 gv[8]; float ww[8];
+    if (SKIPZ) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t grow = (uint32_t)__shfl_sync(kFull, (int)rec, 4 * u + gq);
+      gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const bool live = !tail || p + 4 * u + gq < pend;
+      if (live && (!SKIPZ || ww[u] != 0.0f)) gv[u] = ld_line4(col_line(gb, grow, rsu), pol_l);
+    }
+    if (!SKIPZ) {
+      // issued after the gathers: the weight load and the gathers are in flight together
+      if (ok) wv = ld_na(gT + (size_t)rec * rsu + woff + ((uint32_t)er & 63u));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
+    }
+    float2 a01 = lo2(acc), a23 = hi2(acc);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a01 = ffma2(bc2(ww[u]), lo2(gv[u]), a01);
+      a23 = ffma2(bc2(ww[u]), hi2(gv[u]), a23);
+    }
+    acc = make_float4(a01.x, a01.y, a23.x, a23.y);
+  };
+  auto finish = [&](int c, int q2, float4 acc) {
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1) {
+      acc.x += __shfl_xor_sync(kFull, acc.x, o); acc.y += __shfl_xor_sync(kFull, acc.y, o);
+      acc.z += __shfl_xor_sync(kFull, acc.z, o); acc.w += __shfl_xor_sync(kFull, acc.w, o);
+    }
+    if (gq == 0) {
+      float4* dst = reinterpret_cast<float4*>(hd + (int64_t)c * 64 * nb + q2 * 64 + 32 + 4 * bq);
+      if (tile > 0) {
+        const float4 o = *dst;
+        acc = make_float4(o.x + acc.x, o.y + acc.y, o.z + acc.z, o.w + acc.w);
+      }
+      *dst = acc;
+    }
+  };
   if (NB1) {
-    // B <= 32: the entries (row, weight) of the next batch — in this column, or the first
-    // batch of the warp's next column — are loaded while the current batch's gathers run, so
-    // the entry stream's DRAM latency is not exposed once per batch.  Same per-lane order of
-    // the FMAs and the same final reduction as below: bit-identical dh.
-    const float* gb = gT + 4 * bq;
-    auto load_ent = [&](int p, int pend, int& jr, float& wv) {
-      const bool ok = p + lane < pend;
-      jr = ok ? ld_na_ro(ent_row + p + lane) : jb;
-      wv = ok ? ld_na(wcsc + p + lane) : 0.0f;
+    // B <= 32: the entries of the next batch — in this column, or the first batch of the
+    // warp's next column — are loaded while the current batch's gathers run, so the entry
+    // stream's DRAM latency is not exposed once per batch.
+    auto load_ent = [&](int p, int pend, int& er, bool& ok) {
+      ok = p + lane < pend;
+      er = ok ? ld_na_ro(ent + p + lane) : 0;
     };
     int c = c_begin + (int)global_warp();
-    int p0 = 0, p1 = 0, jr_n = jb; float wv_n = 0.0f;
-    if (c < m) { p0 = cp[c]; p1 = cp[c + 1]; load_ent(p0, p1, jr_n, wv_n); }
+    int p0 = 0, p1 = 0, er_n = 0;
+    bool ok_n = false;
+    if (c < m) { p0 = cp[c]; p1 = cp[c + 1]; load_ent(p0, p1, er_n, ok_n); }
     for (; c < m; c += nw) {
       const int cn = c + nw;
       int q0 = 0, q1 = 0;
       if (cn < m) { q0 = cp[cn]; q1 = cp[cn + 1]; }
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int p = p0; p < p1; p += 32) {
-        const int jr = jr_n; const float wv = wv_n;
-        if (p + 32 < p1) load_ent(p + 32, p1, jr_n, wv_n);        // next batch, same column
-        else if (cn < m) load_ent(q0, q1, jr_n, wv_n);            // first batch of the next column
-        const bool tail = p + 32 > p1;
-        float4 gv[8]; float ww[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t grow = (uint32_t)(__shfl_sync(kFull, jr, 4 * u + gq) - jb);
-          ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
-          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if ((!tail || p + 4 * u + gq < p1) && ww[u] != 0.0f) gv[u] = ld_line4(col_line(gb, grow, gstride), pol_l);
-        }
-        float2 a01 = lo2(acc), a23 = hi2(acc);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          a01 = ffma2(bc2(ww[u]), lo2(gv[u]), a01);
-          a23 = ffma2(bc2(ww[u]), hi2(gv[u]), a23);
-        }
-        acc = make_float4(a01.x, a01.y, a23.x, a23.y);
+        const int er = er_n; const bool ok = ok_n;
+        if (p + 32 < p1) load_ent(p + 32, p1, er_n, ok_n);        // next batch, same column
+        else if (cn < m) load_ent(q0, q1, er_n, ok_n);            // first batch of the next column
+        batch(er, ok, p, p1, 0, acc);
       }
-      if (p0 == p1 && cn < m) load_ent(q0, q1, jr_n, wv_n);        // empty column: prefetch here
-#pragma unroll
-      for (int o = 8; o <= 16; o <<= 1) {
-        acc.x += __shfl_xor_sync(kFull, acc.x, o); acc.y += __shfl_xor_sync(kFull, acc.y, o);
-        acc.z += __shfl_xor_sync(kFull, acc.z, o); acc.w += __shfl_xor_sync(kFull, acc.w, o);
-      }
-      if (gq == 0) {
-        float4* dst = reinterpret_cast<float4*>(hd + (int64_t)c * 64 + 32 + 4 * bq);
-        if (tile > 0) {
-          const float4 o = *dst;
-          acc = make_float4(o.x + acc.x, o.y + acc.y, o.z + acc.z, o.w + acc.w);
-        }
-        *dst = acc;
-      }
+      if (p0 == p1 && cn < m) load_ent(q0, q1, er_n, ok_n);        // empty column: prefetch here
+      finish(c, 0, acc);
       p0 = q0; p1 = q1;
     }
     return;
@@ -735,47 +762,13 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
   for (int c = c_begin + (int)global_warp(); c < m; c += nw) {
     const int p0 = cp[c], p1 = cp[c + 1];
     for (int q2 = 0; q2 < nb; ++q2) {
-      const float* gb = gT + q2 * 32 + 4 * bq;                // this lane's slice of chunk q2
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      auto batch = [&](int p, bool tail) {
-        const bool ok = !tail || p + lane < p1;
-        const int jr = ok ? ld_na_ro(ent_row + p + lane) : jb;
-        const float wv = ok ? ld_na(wcsc + p + lane) : 0.0f;
-        float4 gv[8]; float ww[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t grow = (uint32_t)(__shfl_sync(kFull, jr, 4 * u + gq) - jb);
-          ww[u] = __shfl_sync(kFull, wv, 4 * u + gq);
-          // entries with a zero weight contribute exactly zero: no gather (this is how the
-          // implicit negative mining reaches the column pass: the row pass publishes 0 for
-          // rows whose gradient is all zero)
-          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if ((!tail || p + 4 * u + gq < p1) && ww[u] != 0.0f) gv[u] = ld_line4(col_line(gb, grow, gstride), pol_l);
-        }
-        float2 a01 = lo2(acc), a23 = hi2(acc);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          a01 = ffma2(bc2(ww[u]), lo2(gv[u]), a01);
-          a23 = ffma2(bc2(ww[u]), hi2(gv[u]), a23);
-        }
-        acc = make_float4(a01.x, a01.y, a23.x, a23.y);
-      };
-      int p = p0;
-      for (; p + 32 <= p1; p += 32) batch(p, false);
-      if (p < p1) batch(p, true);
-#pragma unroll
-      for (int o = 8; o <= 16; o <<= 1) {
-        acc.x += __shfl_xor_sync(kFull, acc.x, o); acc.y += __shfl_xor_sync(kFull, acc.y, o);
-        acc.z += __shfl_xor_sync(kFull, acc.z, o); acc.w += __shfl_xor_sync(kFull, acc.w, o);
+      for (int p = p0; p < p1; p += 32) {
+        const bool ok = p + lane < p1;
+        const int er = ok ? ld_na_ro(ent + p + lane) : 0;
+        batch(er, ok, p, p1, q2, acc);
       }
-      if (gq == 0) {
-        float4* dst = reinterpret_cast<float4*>(hd + (int64_t)c * 64 * nb + q2 * 64 + 32 + 4 * bq);
-        if (tile > 0) {
-          const float4 o = *dst;
-          acc = make_float4(o.x + acc.x, o.y + acc.y, o.z + acc.z, o.w + acc.w);
-        }
-        *dst = acc;
-      }
+      finish(c, q2, acc);
     }
   }
 }
@@ -790,16 +783,16 @@ __global__ void k_csc_keys(const int* __restrict__ idx, int64_t n, int k, int m,
     vals[e] = (int)e;
   }
 }
-// CSC build step 2: ent_row[p] = row of the p-th entry, pos[e] = p; col_ptr over the key
-// space [0, nkeys] from the sorted keys (col_ptr[q] = first p with key >= q).
+// CSC build step 2: ent[p] = (row within its tile << 6) | slot of the p-th entry; col_ptr
+// over the key space [0, nkeys] from the sorted keys (col_ptr[q] = first p with key >= q).
 __global__ void k_csc_finish(const int* __restrict__ skeys, const int* __restrict__ svals, int64_t n, int k,
-                             int nkeys, int* __restrict__ ent_row, int* __restrict__ pos, int* __restrict__ col_ptr) {
+                             int64_t tile_rows, int nkeys, int* __restrict__ ent, int* __restrict__ col_ptr) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int e = svals[p];
     const int key = skeys[p];
     const int prev = p > 0 ? skeys[p - 1] : -1;
-    ent_row[p] = e / k;
-    pos[e] = (int)p;
+    const int j = e / k, i = e - j * k;
+    ent[p] = (int)(((int64_t)j % tile_rows) << 6) | i;
     for (int c = prev + 1; c <= key; ++c) col_ptr[c] = (int)p;
     if (p == n - 1)
       for (int c = key + 1; c <= nkeys; ++c) col_ptr[c] = (int)n;

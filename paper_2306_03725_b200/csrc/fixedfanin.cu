@@ -55,18 +55,23 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct Layout {   // byte offsets into the workspace
   size_t W, idx, mW, vW, dW, bias, mb, vb, db, posmask, hd, cand_s, cand_i,
       h_stage, lbl_stage, dh_stage, scalars,
-      ent_row, pos, wcsc, gT, col_ptr, sort_keys, sort_tmp, sort_tmp_bytes,   // CSC mode only
+      ent, sort_keys2, gT, col_ptr, sort_keys, sort_tmp, sort_tmp_bytes,   // CSC mode only
       total;
 };
 
 int nb_of(int B) { return (B + 31) / 32; }
 
-// CSC mode label tile: the g lines of one tile (tile_rows * 128 B * nb) stay L2-resident
+// CSC mode: one record per label row of a tile, rs floats: the row's gradient line per
+// 32-sample chunk, then its pre-update weights (ceil(k/32) lines).
+int csc_rec_stride(int max_batch, int k) { return 32 * nb_of(max_batch) + 32 * ((k + 31) / 32); }
+// CSC mode label tile: the records of one tile (tile_rows * 4 rs B) stay L2-resident
 // between the row launch that writes them and the column launch that gathers them.
-constexpr size_t kCscTileBytes = size_t(32) << 20;
+#ifndef FF_CSC_TILE_MB
+#define FF_CSC_TILE_MB 64
+#endif
+constexpr size_t kCscTileBytes = size_t(FF_CSC_TILE_MB) << 20;
 size_t csc_tile_cap(const ff_config& c) {
-  const size_t nbm = (size_t)nb_of(c.max_batch);
-  const size_t cap = kCscTileBytes / (128 * nbm) / 32 * 32;
+  const size_t cap = kCscTileBytes / (4 * (size_t)csc_rec_stride(c.max_batch, c.k)) / 32 * 32;
   return std::max<size_t>(std::min<size_t>(cap, ((size_t)c.L_local + 31) / 32 * 32), 32);
 }
 
@@ -88,10 +93,10 @@ Layout layout_of(const ff_config& c) {
   o.dh_stage = take(4 * (size_t)c.max_batch * m);
   o.scalars = take(kAlign);       // [0] int err, [1] float loss
   if (c.dh_mode != FF_DH_ATOMIC) {          // CSC and hybrid
-    o.ent_row = take(4 * Lk); o.pos = take(4 * Lk); o.wcsc = take(4 * Lk); o.sort_keys = take(4 * Lk);
+    o.ent = take(4 * Lk); o.sort_keys2 = take(4 * Lk); o.sort_keys = take(4 * Lk);
     // tiles are >= cap/2 rows (create rounds the cap down to whole row-kernel waves, or keeps it)
     const size_t lt = csc_tile_cap(c), ntile = (2 * L + lt - 1) / lt + 1;
-    o.gT = take(4 * lt * ldh);      // g lines of one label tile
+    o.gT = take(4 * lt * (size_t)csc_rec_stride(c.max_batch, c.k));      // records of one label tile
     o.col_ptr = take(4 * (std::max<size_t>(ntile, 1) * m + 1));
     o.sort_tmp_bytes = (size_t(8) << 20) + 2 * Lk;
     o.sort_tmp = take(o.sort_tmp_bytes);
@@ -150,9 +155,10 @@ struct ff_layer {
   char* ws;
   float *W, *mW, *vW, *dW, *bias, *mb, *vb, *db, *hd, *cand_s, *h_stage, *dh_stage;
   int *idx, *cand_i, *lbl_stage, *err;
-  int *ent_row, *pos, *col_ptr;     // CSC mode
-  float *wcsc, *gT;
-  int* sort_keys;
+  int *ent, *col_ptr;               // CSC mode
+  float* gT;
+  int rs;                           // CSC mode: record stride (floats)
+  int *sort_keys, *sort_keys2;
   void* sort_tmp;
   bool csc;                         // CSC or hybrid dh
   uint32_t split;                   // hybrid: columns [0, split) by red, [split, m) by the CSC pull; else 0
@@ -232,7 +238,7 @@ RowArgs row_args(ff_layer* l, int B) {
   a.dW = l->dW; a.db = l->db; a.posmask = l->posmask; a.hd = l->hd;
   a.L = l->cfg.L_local; a.k = l->cfg.k; a.B = B; a.nb = nb_of(B); a.cstride = 64 * a.nb;
   a.err = l->err;
-  a.pos = l->pos; a.wcsc = l->wcsc; a.gT = l->gT;
+  a.gT = l->gT; a.rs = l->rs;
   a.j_begin = 0; a.j_end = l->cfg.L_local;
   a.check_finite = (l->cfg.flags & FF_FLAG_CHECK_FINITE) ? 1u : 0u;
   a.sqh = l->cfg.loss == FF_LOSS_SQH ? 1 : 0;
@@ -292,12 +298,10 @@ bool ptr_ok(const void* p, int64_t n) { return n == 0 || p != nullptr; }
 // CSC mode: dh of one label tile = pull over the transposed index (after the row kernel
 // published that tile's g lines and pre-update weights).
 ff_status launch_dh_csc(ff_layer* l, int B, int tile, cudaStream_t st) {
-  if (B <= 32)
-    k_dh_csc<true><<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent_row, l->wcsc, l->gT, l->cfg.m, 1, tile,
-                                                 (int64_t)tile * l->tile_rows, l->hd, (int)l->split);
-  else
-    k_dh_csc<false><<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent_row, l->wcsc, l->gT, l->cfg.m, nb_of(B), tile,
-                                                  (int64_t)tile * l->tile_rows, l->hd, (int)l->split);
+  const bool skipz = l->cfg.loss == FF_LOSS_SQH;      // zero gradients are exact only for the squared hinge
+  auto fn = B <= 32 ? (skipz ? k_dh_csc<true, true> : k_dh_csc<true, false>)
+                    : (skipz ? k_dh_csc<false, true> : k_dh_csc<false, false>);
+  fn<<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent, l->gT, l->rs, l->cfg.m, nb_of(B), tile, l->hd, (int)l->split);
   FF_LAUNCHED();
   return FF_OK;
 }
@@ -339,6 +343,7 @@ ff_status run_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, int B, cud
       if (s != FF_OK) return s;
     }
   }
+
   return FF_OK;
 }
 
@@ -348,9 +353,9 @@ ff_status run_rows(ff_layer* l, const void* fn, int grid, RowArgs& a, int B, cud
 ff_status csc_rebuild(ff_layer* l, cudaStream_t st) {
   const int64_t n = l->cfg.L_local * l->cfg.k;
   int* keysA = l->sort_keys;
-  int* keysB = reinterpret_cast<int*>(l->wcsc);
+  int* keysB = l->sort_keys2;
   int* valsA = reinterpret_cast<int*>(l->dW);
-  int* valsB = l->ent_row;
+  int* valsB = l->ent;
   const int nkeys = l->ntiles * l->cfg.m;
   int end_bit = 1;
   while ((1ll << end_bit) < (long long)nkeys) ++end_bit;
@@ -370,7 +375,7 @@ ff_status csc_rebuild(ff_layer* l, cudaStream_t st) {
     ++g_launches;
   }
   k_csc_finish<<<l->nsm * 8, 256, 0, st>>>(reinterpret_cast<const int*>(dk.Current()), dv.Current(), n, l->cfg.k,
-                                           nkeys, l->ent_row, l->pos, l->col_ptr);
+                                           l->tile_rows, nkeys, l->ent, l->col_ptr);
   FF_LAUNCHED();
   l->grads_valid = false;
   return FF_OK;
@@ -622,9 +627,10 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->split = c.dh_mode == FF_DH_HYBRID
                  ? (uint32_t)std::min<double>(c.m, std::floor((double)c.hybrid_frac * (double)c.m + 0.5)) : 0u;
   if (l->csc) {
-    l->ent_row = at<int>(ws, lay.ent_row); l->pos = at<int>(ws, lay.pos); l->wcsc = at<float>(ws, lay.wcsc);
+    l->ent = at<int>(ws, lay.ent); l->sort_keys2 = at<int>(ws, lay.sort_keys2);
     l->gT = at<float>(ws, lay.gT); l->col_ptr = at<int>(ws, lay.col_ptr); l->sort_tmp = ws + lay.sort_tmp;
     l->sort_keys = at<int>(ws, lay.sort_keys);
+    l->rs = csc_rec_stride(c.max_batch, c.k);
   }
   l->t = 0; l->grads_valid = false;
   int dev = 0;
@@ -634,7 +640,7 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->grid_train = occupancy_grid(row_kernel<kModeTrain, false>(c.k, l->csc), l->nsm, kRowThreads);
   l->grid_fwd = occupancy_grid(row_kernel<kModeForward, false>(c.k, false), l->nsm, kRowThreads);
   l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k, l->csc), l->nsm, kRowThreads);
-  l->grid_csc = occupancy_grid((const void*)k_dh_csc<true>, l->nsm, 256);
+  l->grid_csc = occupancy_grid((const void*)k_dh_csc<true, false>, l->nsm, 256);
   for (int sg = 0; sg < 2; ++sg)
     for (int cs = 0; cs < 3; ++cs)
       if (cudaFuncSetAttribute(ring_kernel(sg, cs), cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem_of(cs)) !=
@@ -670,7 +676,7 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   }
   if (l->csc) {
     ff_status s2 = csc_rebuild(l, st);
-    if (s2 != FF_OK) { delete l; return s2; }
+    if (s2 != FF_OK) { fixedfanin_destroy(l); return s2; }
   }
   *out = l;
   return FF_OK;
@@ -684,6 +690,7 @@ ff_status fixedfanin_destroy(ff_layer* l) {
       if (l->ev_free[i]) cudaEventDestroy(l->ev_free[i]);
     }
     if (l->copy_st) cudaStreamDestroy(l->copy_st);
+
   }
   delete l;
   return FF_OK;
