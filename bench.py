@@ -378,7 +378,7 @@ def run_ours(a, shape, world, rank, local_rank):
     # 1000): such a window then carries one redistribution per K steps, more than the
     # amortised 1/1000 (conservative; `redistribution` reports the amortised share).
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    windows, redist_per_window, launch_counts = [], [], []
+    windows, own_windows, host_ms, redist_per_window, launch_counts = [], [], [], [], []
     k_ms_tot, k_n_tot, n_prof = 0.0, 0, 0
     samplers = []
     for rep in range(max(1, a.repeats)):
@@ -392,14 +392,17 @@ def run_ours(a, shape, world, rank, local_rank):
         with sampler:
             barrier()
             e0.record(stream)
+            t_h0 = time.perf_counter()
             for s in range(a.steps):
                 if PROF_EVERY > 1:
                     eng.profile_pause(s % PROF_EVERY != 0)
                 step(a.warmup + s)
             trainer.finish()                                     # every collective inside the timed region
+            host_ms.append((time.perf_counter() - t_h0) * 1e3 / a.steps)   # enqueue time (no sync yet)
             e1.record(stream)
             barrier()
-        windows.append(max_over_ranks(e0.elapsed_time(e1)))
+        own_windows.append(e0.elapsed_time(e1))
+        windows.append(max_over_ranks(own_windows[-1]))
         k_ms, k_n = eng.profile_end()
         k_ms_tot += k_ms; k_n_tot += k_n; n_prof += len(range(0, a.steps, PROF_EVERY))
         redist_per_window.append(n_redist)
@@ -412,6 +415,27 @@ def run_ours(a, shape, world, rank, local_rank):
     launches_per_step = k_n_tot / n_prof
     gpu_launches = launch_counts[med]
 
+    # ---- N > 1: where a rank's step goes: the same steps with the shard's
+    # compute only (no collectives) and the collectives only (h broadcast + dh all-reduce),
+    # each timed on this rank's stream; gathered to rank 0
+    per_rank = None
+    if world > 1:
+        def timed(fn):
+            barrier()
+            e0.record(stream)
+            for s in range(a.steps):
+                fn(s)
+            e1.record(stream)
+            barrier()
+            return e0.elapsed_time(e1) / a.steps
+        compute_ms = timed(lambda s: eng.train_step(h_dev[s % N_BATCHES], ptr_dev[s % N_BATCHES], ids_dev[s % N_BATCHES],
+                                                    LR, dh=dh, loss=loss))
+        comm_ms = timed(lambda s: (dist.broadcast(h_dev[s % N_BATCHES], src=0), dist.all_reduce(dh)))
+        rec = {"rank": rank, "L_local": L_local, "step_ms": own_windows[med] / a.steps,
+               "row_kernel_ms": k_ms_tot / n_prof, "compute_only_ms": compute_ms, "comm_only_ms": comm_ms,
+               "exposed_comm_ms": own_windows[med] / a.steps - compute_ms, "host_enqueue_ms": host_ms[med]}
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, rec)
     if a.train_only:
         if rank == 0:
             print(json.dumps({"ms_per_step": ms / a.steps, "value": B * a.steps / (ms * 1e-3),
@@ -437,25 +461,31 @@ def run_ours(a, shape, world, rank, local_rank):
             eng.train_step_host(h_pin[i], ptr_pin[i], ids_pin[i], LR, loss_host=loss_pin,
                                 dh_host=dh_pin if want_dh else None)
         else:
-            h_dev[i].copy_(h_pin[i], non_blocking=True)
+            # the producer rank's h reaches the device by H2D and the other ranks by the
+            # broadcast inside trainer.step; every rank copies its labels; the dh all-reduce of
+            # this step overlaps the next step (OverlappedTrainer)
+            if rank == 0:
+                h_dev[i].copy_(h_pin[i], non_blocking=True)
             ptr_dev[i].copy_(ptr_pin[i], non_blocking=True)
             ids_dev[i].copy_(ids_pin[i], non_blocking=True)
-            layer.broadcast_h(h_dev[i])
-            layer.train_step(h_dev[i], ptr_dev[i], ids_dev[i], LR, dh=dh, loss=loss)
+            dh_s = trainer.step(i, None)
             loss_pin.copy_(loss, non_blocking=True)
             if want_dh:
-                dh_pin.copy_(dh, non_blocking=True)
+                trainer.finish()
+                dh_pin.copy_(dh_s, non_blocking=True)
         t_global += 1
         if t_global % REDIST_EVERY == 0:
             layer.redistribute(t_global)
 
     for s in range(3):
         step_e2e(s)
+    trainer.finish()
     with ClockSampler(local_rank) as clk2:
         barrier()
         e0.record(stream)
         for s in range(n_e2e):
             step_e2e(s)
+        trainer.finish()
         e1.record(stream)
         barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
@@ -466,6 +496,7 @@ def run_ours(a, shape, world, rank, local_rank):
     e0.record(stream)
     for s in range(n_e2e):
         step_e2e(s)
+    trainer.finish()
     e1.record(stream)
     barrier()
     ms_e2e_dh = max_over_ranks(e0.elapsed_time(e1))
@@ -596,7 +627,9 @@ def run_ours(a, shape, world, rank, local_rank):
         "e2e": {"value": B * n_e2e / (ms_e2e * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ms_e2e / n_e2e,
                 "path": "fixedfanin_train_step_host (C ABI, pinned host buffers)" if world == 1 else
-                        "torch H2D + ShardedLayer.train_step + D2H loss", "clocks_sm_mhz": c2["sm_mhz"]},
+                        "torch H2D (h on the producer rank, labels on every rank) + OverlappedTrainer step "
+                        "(h broadcast, fused step, dh all-reduce overlapped with the next step) + D2H loss",
+                "clocks_sm_mhz": c2["sm_mhz"]},
         "e2e_with_dh": {"value": B * n_e2e / (ms_e2e_dh * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h + 4 * B * shape.m, "steps": n_e2e,
                         "ms_per_step": ms_e2e_dh / n_e2e,
@@ -632,6 +665,12 @@ def run_ours(a, shape, world, rank, local_rank):
                    "note": ("h 128-B line gather + dh 128-B red.v4 per connection" if a.dh_mode == "atomic" else
                             "h 128-B line gather (row pass) + g 128-B line gather (CSC column pass) per connection")
                            + "; measured ceilings (profiles/r01_l2bench.txt): gather ~19.9 TB/s, red ~6.3-6.6 TB/s"},
+        "host_enqueue_ms_per_step": host_ms[med],
+        "per_rank": per_rank,
+        "comm": ({"backend": dist.get_backend(), "comm_nranks": dist.get_world_size(),
+                  "collectives_per_step": "broadcast h (4 B m) + all_reduce dh (4 B m), overlapped with the next "
+                                          "step (OverlappedTrainer)",
+                  "nccl_debug": os.environ.get("NCCL_DEBUG")} if world > 1 else None),
         "predict": {"value": B * n_pred / (ms_pred * 1e-3), "unit": "samples/s", "K": K,
                     "ms_per_batch": ms_pred / n_pred,
                     "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,
@@ -683,6 +722,10 @@ def main():
         gpu = local_rank % torch.cuda.device_count()
         torch.cuda.set_device(gpu)
         if backend == "nccl":
+            # NCCL's communicator log (stderr) carries the nranks of every communicator
+            if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", "NONE", ""):
+                os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
         else:
             dist.init_process_group(backend)

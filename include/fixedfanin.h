@@ -235,30 +235,37 @@ ff_status fixedfanin_merge_topk(const float* in_scores, const int32_t* in_ids, i
  * -> ReLU (R18) -> the fixed fan-in layer.  Readings R25-R28.
  * Layouts: x float [B][d] (d = feature dimension: 512 Slice / 768 Cascade),
  *          Wd float [d][m] (input-feature major), bd float [m], h and dh float [B][m].
- * One ff_dense handle = one replica of the dense layer (it is not label-sharded: under
- * label sharding every rank holds the same replica and feeds it the all-reduced dh).
+ * One ff_dense handle = the dense layer or one column shard of it (col_begin, m_global):
+ * under label sharding rank r owns the columns [m_global r / P, m_global (r+1) / P) of Wd,
+ * bd and their Adam state; h is all-gathered and dh reduce-scattered.
  * Same conventions as above: caller-owned workspace, async on `stream`, status codes.
  * ====================================================================================== */
 typedef struct ff_dense ff_dense;
 
 typedef struct {
     int32_t d;           /* input feature dimension, >= 1                                       */
-    int32_t m;           /* output width = the fixed fan-in layer's m, >= 1                     */
+    int32_t m;           /* output columns of this handle, >= 1 (the fixed fan-in layer's m,   */
+                         /* or a column shard of it: see col_begin / m_global)                  */
     int32_t max_batch;   /* largest B, 1..FF_MAX_BATCH                                          */
-    int32_t reserved;    /* 0                                                                   */
+    int32_t col_begin;   /* column shard: this handle owns the global columns  */
+                         /* [col_begin, col_begin + m) of Wd, bd; 0 for the whole layer          */
     uint64_t seed;       /* Philox key: Wd init (domain 4, R27) and dropout masks (domain 3, R25) */
     float init_scale;    /* Wd ~ U(-a, a); 0 -> a = fp32(sqrt(6 / (d + m))) (Glorot uniform, R27) */
     float dropout;       /* input dropout rate p in [0, 1) (0.1 Amazon-670K)         */
     float beta1, beta2, eps;   /* Adam; 0 -> 0.9 / 0.999 / 1e-8 (R6)                            */
     uint32_t flags;      /* FF_FLAG_STORE_GRADS: keep dWd/dbd for fixedfanin_dense_get_grads    */
+    int32_t m_global;    /* width of the whole layer (0 -> m); col_begin + m <= m_global.  The   */
+                         /* init draws global column c's word and the Glorot scale uses m_global,*/
+                         /* so the column shards of a layer concatenate to the unsharded layer  */
 } ff_dense_config;
 
 /* Bytes of device workspace for `cfg` (host-only).  FF_ERR_CONFIG on a bad config.       */
 ff_status fixedfanin_dense_workspace_size(const ff_dense_config* cfg, size_t* bytes_host);
 
 /* Carve `workspace` (>= workspace_size bytes, 256-B aligned) and initialize on `stream`:
- * Wd[f][c] = a * (2 * ((u >> 8) * 2^-24) - 1) in fp32, u = word c of the Philox stream
- * (ctr = (c/4, f, 0, 4), key = seed) (R27); bd = moments = 0; t = 0.                     */
+ * Wd[f][c] = a * (2 * ((u >> 8) * 2^-24) - 1) in fp32, u = word g of the Philox stream
+ * (ctr = (g/4, f, 0, 4), key = seed), g = col_begin + c the global column (R27); bd =
+ * moments = 0; t = 0.                                                                    */
 ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, size_t bytes,
                                   ff_stream_t stream, ff_dense** out_host);
 ff_status fixedfanin_dense_destroy(ff_dense* dense);

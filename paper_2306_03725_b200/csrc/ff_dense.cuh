@@ -752,17 +752,24 @@ __global__ void k_dh_in(const float* __restrict__ dh, int B, int m, int nb, floa
 // Dense init (reading R27): Wd[f][c] = a * (2 * ((u >> 8) * 2^-24) - 1) in fp32, u = word c
 // of the stream (ctr = (c/4, f, 0, 4), key = seed); pad columns and bd, moments = 0.
 // Thread per (tile, feature, 4 columns), tiled layout.
-__global__ void k_dense_init(float* __restrict__ Wd, int d, int m, int ldw, uint32_t key0, uint32_t key1, float a) {
+__global__ void k_dense_init(float* __restrict__ Wd, int d, int m, int ldw, int col_begin, uint32_t key0, uint32_t key1,
+                             float a) {
   const int64_t n4 = (int64_t)d * (ldw / 4);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / ((int64_t)d * 32);
     const int f = (int)((e / 32) % d), cq = (int)(e % 32);
     const int c = (int)t * 128 + 4 * cq;
-    const U4 v = philox((uint32_t)(c / 4), (uint32_t)f, 0u, 4u, key0, key1);
+    // global column g = col_begin + c + u draws word g % 4 of the block (g / 4, f, 0, 4) (R27):
+    // a column shard reproduces its columns of the whole layer
+    const uint32_t g0 = (uint32_t)(col_begin + c);
+    const U4 v0 = philox(g0 / 4, (uint32_t)f, 0u, 4u, key0, key1);
+    const U4 v1 = (g0 & 3u) ? philox(g0 / 4 + 1, (uint32_t)f, 0u, 4u, key0, key1) : v0;
     float out[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const float unit = __fmul_rn((float)(word_of(v, u) >> 8), 1.0f / 16777216.0f);
+      const uint32_t g = g0 + (uint32_t)u;
+      const uint32_t word = (g / 4 == g0 / 4) ? word_of(v0, (int)(g & 3u)) : word_of(v1, (int)(g & 3u));
+      const float unit = __fmul_rn((float)(word >> 8), 1.0f / 16777216.0f);
       const float centered = __fsub_rn(__fmul_rn(2.0f, unit), 1.0f);
       out[u] = c + u < m ? __fmul_rn(a, centered) : 0.0f;
     }

@@ -479,6 +479,9 @@ ff_status dense_validate(const ff_dense_config* c) {
   if (c->max_batch < 1 || c->max_batch > FF_MAX_BATCH)
     return fail(FF_ERR_CONFIG, "max_batch=%d outside [1, %d]", c->max_batch, FF_MAX_BATCH);
   if (!(c->dropout >= 0.0f && c->dropout < 1.0f)) return fail(FF_ERR_CONFIG, "dropout outside [0, 1)");
+  if (c->col_begin < 0 || c->m_global < 0 || (int64_t)c->col_begin + c->m > (c->m_global ? c->m_global : INT32_MAX))
+    return fail(FF_ERR_CONFIG, "column shard [%d, %lld) outside [0, m_global=%d)", c->col_begin,
+                (long long)c->col_begin + c->m, c->m_global);
   if (c->beta1 < 0.0f || c->beta1 >= 1.0f || c->beta2 < 0.0f || c->beta2 >= 1.0f || c->eps < 0.0f)
     return fail(FF_ERR_CONFIG, "Adam hyper-parameters out of range");
   return FF_OK;
@@ -488,7 +491,8 @@ ff_dense_config dense_defaults(const ff_dense_config& in) {
   if (c.beta1 == 0.0f) c.beta1 = 0.9f;
   if (c.beta2 == 0.0f) c.beta2 = 0.999f;
   if (c.eps == 0.0f) c.eps = 1e-8f;
-  if (c.init_scale == 0.0f) c.init_scale = (float)std::sqrt(6.0 / ((double)c.d + (double)c.m));
+  if (c.m_global == 0) c.m_global = c.col_begin + c.m;
+  if (c.init_scale == 0.0f) c.init_scale = (float)std::sqrt(6.0 / ((double)c.d + (double)c.m_global));
   return c;
 }
 AdamArgs adam_args_of(float beta1, float beta2, float eps, float lr, int64_t t) {
@@ -1058,7 +1062,7 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
   if (e != cudaSuccess) { delete n; return fail(FF_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); }
   const int64_t work = (int64_t)c.d * (n->ldw / 4);
   k_dense_init<<<(int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8192)), 256, 0, st>>>(
-      n->Wd, c.d, c.m, n->ldw, (uint32_t)c.seed, (uint32_t)(c.seed >> 32), c.init_scale);
+      n->Wd, c.d, c.m, n->ldw, c.col_begin, (uint32_t)c.seed, (uint32_t)(c.seed >> 32), c.init_scale);
   e = cudaGetLastError();
   if (e != cudaSuccess) { delete n; return fail(FF_ERR_CUDA, "init launch: %s", cudaGetErrorString(e)); }
   ++g_launches;

@@ -63,9 +63,10 @@ class ff_config(ctypes.Structure):
 
 class ff_dense_config(ctypes.Structure):
     _fields_ = [
-        ("d", ctypes.c_int32), ("m", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("d", ctypes.c_int32), ("m", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("col_begin", ctypes.c_int32),
         ("seed", ctypes.c_uint64), ("init_scale", ctypes.c_float), ("dropout", ctypes.c_float),
         ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("flags", ctypes.c_uint32),
+        ("m_global", ctypes.c_int32),
     ]
 
 
@@ -335,7 +336,8 @@ def precision_at_k(ids, lbl_ptr, lbl_ids, stream=None):
 # ------------------------------------------------------------------ NEXT-2
 @dataclass
 class DenseConfig:
-    """The intermediate layer of the proposed architecture (Fig. 2)."""
+    """The intermediate layer of the proposed architecture (Fig. 2), or the column
+    shard [col_begin, col_begin + m) of a layer m_global wide."""
     d: int
     m: int
     max_batch: int = 32
@@ -346,10 +348,12 @@ class DenseConfig:
     beta2: float = 0.999
     eps: float = 1e-8
     flags: int = 0
+    col_begin: int = 0
+    m_global: int = 0
 
     def c(self) -> ff_dense_config:
-        return ff_dense_config(self.d, self.m, self.max_batch, 0, self.seed, self.init_scale, self.dropout,
-                               self.beta1, self.beta2, self.eps, self.flags)
+        return ff_dense_config(self.d, self.m, self.max_batch, self.col_begin, self.seed, self.init_scale, self.dropout,
+                               self.beta1, self.beta2, self.eps, self.flags, self.m_global)
 
 
 class DenseLayer:

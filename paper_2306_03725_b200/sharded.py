@@ -46,11 +46,14 @@ class ShardedLayer:
             dist.broadcast(h, src=src, group=self.group)
         return h
 
-    def train_step(self, h, lbl_ptr, lbl_ids, lr, grad_scale=None, dh=None, loss=None, reduce_loss=False):
-        """Fused step on this shard, then dh all-reduce.  Returns (dh, loss)."""
+    def train_step(self, h, lbl_ptr, lbl_ids, lr, grad_scale=None, dh=None, loss=None, reduce_loss=False,
+                   reduce_dh=True):
+        """Fused step on this shard, then dh all-reduce (reduce_dh=False: return this shard's
+        partial dh, for a caller that reduce-scatters it).  Returns (dh, loss)."""
         dh, loss = self.engine.train_step(h, lbl_ptr, lbl_ids, lr, grad_scale=grad_scale, dh=dh, loss=loss)
         if self.world > 1:
-            dist.all_reduce(dh, op=dist.ReduceOp.SUM, group=self.group)
+            if reduce_dh:
+                dist.all_reduce(dh, op=dist.ReduceOp.SUM, group=self.group)
             if reduce_loss and loss is not None:
                 dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=self.group)
         return dh, loss
@@ -101,7 +104,8 @@ class OverlappedTrainer:
             self.bcast[i_cur] = None
         elif L.world > 1:
             dist.broadcast(self.h[i_cur], src=0, group=L.group)
-        self.prefetch(i_next)
+        if i_next is not None:                          # None: the caller fills the next slot itself
+            self.prefetch(i_next)
         slot = self.s & 1
         if self.ar[slot] is not None:
             self.ar[slot].wait()
@@ -124,21 +128,32 @@ class OverlappedTrainer:
 
 
 class ShardedModel:
-    """The whole proposed architecture (Fig. 2) under label sharding (NEXT-2):
-    every rank holds a replica of the dense intermediate layer (``dense``: the CUDA
-    ``DenseLayer`` by default) and one label shard of the fixed fan-in layer.
+    """The whole proposed architecture (Fig. 2) under label sharding (NEXT-2,
+    SURVEY §8(f)2): rank r owns one label shard of the fixed fan-in layer AND the column shard
+    [m r / P, m (r+1) / P) of the dense intermediate layer (Wd, bd and their Adam state), so
+    the dense layer's bytes per rank fall as 1/P like the sparse layer's.
 
-    Per step: the features x (replicated; broadcast from rank 0) go through the replica's
-    dropout + dense forward — identical on every rank, because the dropout mask is keyed on
-    (seed, step, sample) (reading R25) — the shard's fused step yields its partial dh, the
-    dh all-reduce sums the shards, and every replica applies the same dense backward + Adam
-    to the same summed dh, so the replicas stay identical without another collective."""
+    Per step (x replicated, broadcast from rank 0):
+      1. dropout + dense forward of this rank's columns: h_r = ReLU(dropout(x) Wd[:, cols] + bd)
+         — the dropout mask is keyed on (seed, step, sample, feature) (R25), identical on
+         every rank;
+      2. all_gather of the column shards -> the full h [B][m];
+      3. the label shard's fused step -> this shard's partial dh [B][m];
+      4. reduce_scatter of the partial dh -> dh[:, cols] summed over the label shards;
+      5. dense backward + Adam of this rank's columns (dWd[:, cols] = xt^T (dh_r [h_r > 0])).
+    Bytes on the wire per step: 4 B m (P-1)/P for each of the all-gather and the
+    reduce-scatter (the same as the dh all-reduce they replace)."""
 
     def __init__(self, layer: ShardedLayer, dense=None, d: int | None = None, device=None, **dense_cfg):
         self.layer = layer
+        m, P, r = layer.m, layer.world, layer.rank
+        self.cols = [shard_rows(m, q, P) for q in range(P)]
+        self.col_begin, self.col_end = self.cols[r]
+        self.mc = max(e - b for b, e in self.cols)            # padded shard width of the collectives
         if dense is None:
             from .layer import DenseConfig, DenseLayer
-            dense = DenseLayer(DenseConfig(d=d, m=layer.m, **dense_cfg), device=device)
+            dense = DenseLayer(DenseConfig(d=d, m=self.col_end - self.col_begin, col_begin=self.col_begin,
+                                           m_global=m, **dense_cfg), device=device)
         self.dense = dense
 
     def broadcast_x(self, x: torch.Tensor, src: int = 0) -> torch.Tensor:
@@ -146,12 +161,43 @@ class ShardedModel:
             dist.broadcast(x, src=src, group=self.layer.group)
         return x
 
-    def train_step(self, x, step, lbl_ptr, lbl_ids, lr, grad_scale=None, dh=None, loss=None, reduce_loss=False):
-        h = self.dense.forward(x, step=step, train=True)
-        dh, loss = self.layer.train_step(h, lbl_ptr, lbl_ids, lr, grad_scale=grad_scale, dh=dh, loss=loss,
-                                         reduce_loss=reduce_loss)
-        self.dense.backward_adam(dh, lr)
-        return dh, loss
+    def gather_h(self, h_r: torch.Tensor) -> torch.Tensor:
+        """[B][m_r] column shards of every rank -> the full h [B][m] (all_gather)."""
+        L = self.layer
+        if L.world == 1:
+            return h_r
+        B, mr = h_r.shape
+        send = h_r
+        if mr < self.mc:
+            send = torch.zeros((B, self.mc), dtype=h_r.dtype, device=h_r.device)
+            send[:, :mr] = h_r
+        out = torch.empty((L.world * B, self.mc), dtype=h_r.dtype, device=h_r.device)
+        dist.all_gather_into_tensor(out, send.contiguous(), group=L.group)
+        out = out.view(L.world, B, self.mc)
+        return torch.cat([out[q, :, :e - b] for q, (b, e) in enumerate(self.cols)], dim=1)
+
+    def scatter_dh(self, dh: torch.Tensor) -> torch.Tensor:
+        """This label shard's partial dh [B][m] -> dh[:, own columns] summed over the label
+        shards (reduce_scatter)."""
+        L = self.layer
+        if L.world == 1:
+            return dh
+        B = dh.shape[0]
+        inp = torch.zeros((L.world, B, self.mc), dtype=dh.dtype, device=dh.device)
+        for q, (b, e) in enumerate(self.cols):
+            inp[q, :, :e - b] = dh[:, b:e]
+        out = torch.empty((B, self.mc), dtype=dh.dtype, device=dh.device)
+        dist.reduce_scatter_tensor(out, inp.view(L.world * B, self.mc), op=dist.ReduceOp.SUM, group=L.group)
+        return out[:, :self.col_end - self.col_begin].contiguous()
+
+    def train_step(self, x, step, lbl_ptr, lbl_ids, lr, grad_scale=None, loss=None, reduce_loss=False):
+        """One step (1-5 above).  Returns (dh of this rank's columns, loss)."""
+        h = self.gather_h(self.dense.forward(x, step=step, train=True))
+        dh, loss = self.layer.train_step(h, lbl_ptr, lbl_ids, lr, grad_scale=grad_scale, loss=loss,
+                                         reduce_loss=reduce_loss, reduce_dh=False)
+        dh_r = self.scatter_dh(dh)
+        self.dense.backward_adam(dh_r, lr)
+        return dh_r, loss
 
     def predict_topk(self, x, K: int):
-        return self.layer.predict_topk(self.dense.forward(x, train=False), K)
+        return self.layer.predict_topk(self.gather_h(self.dense.forward(x, train=False)), K)

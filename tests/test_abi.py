@@ -99,6 +99,8 @@ def test_merge_topk_argument_validation():
     (dict(d=16, m=64, dropout=1.0), "dropout"),
     (dict(d=16, m=64, dropout=-0.1), "dropout"),
     (dict(d=16, m=64, beta1=1.0), "Adam"),
+    (dict(d=16, m=64, col_begin=10, m_global=70), "column shard"),     # [10, 74) outside [0, 70)
+    (dict(d=16, m=64, col_begin=-1, m_global=70), "column shard"),
 ])
 def test_bad_dense_configs_rejected(kw, msg):
     c = L.DenseConfig(**kw).c()

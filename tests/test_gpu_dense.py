@@ -327,7 +327,9 @@ def test_model_step_cuda_graph_replay(dh_mode):
             assert (sa[key] == sb[key]).all(), key
         for key in ("Wd", "bd", "mWd", "vWd"):
             assert (da[key] == db_[key]).all(), key
-        assert abs(la - lb_) <= 1e-6 * abs(lb_)          # the loss sum is an atomic reduction
+        # the loss is an fp32 atomicAdd of per-CTA partial sums (B L = 64,000 terms) in arrival
+        # order: the two runs agree to fp32 summation-order rounding, ~1e-6 relative
+        assert abs(la - lb_) <= 1e-5 * abs(lb_)
     else:
         for key in ("Wd", "W"):
             ref = (db_ if key == "Wd" else sb)[key]
@@ -357,3 +359,57 @@ def test_dense_auto_step_equals_explicit_steps():
     assert da["t"] == db_["t"] == 3
     for key in ("Wd", "bd", "mWd", "vWd"):
         assert (da[key] == db_[key]).all(), key
+
+
+@pytest.mark.parametrize("P,d,m,B", [(2, 64, 512, 32), (3, 37, 203, 7), (4, 512, 4100, 32), (3, 48, 1000, 70)])
+def test_column_shards_concatenate_to_the_unsharded_layer(P, d, m, B):
+    """SURVEY §8(f)2 on one GPU: P virtual column shards [m r / P, m (r+1) / P) of the dense
+    layer (col_begin, m_global): their Philox init, training forward (same dropout mask) and
+    backward + Adam on the dh columns are bit-identical to the unsharded layer's columns (the
+    arithmetic of a column does not depend on the others), over two steps."""
+    layer = L_()
+    full = make_dense(d, m, B=B, seed=23, dropout=0.1)
+    cols = [(m * r // P, m * (r + 1) // P) for r in range(P)]
+    shards = [make_dense(d, e - b, B=B, seed=23, dropout=0.1, col_begin=b, m_global=m) for b, e in cols]
+    sf = dstate(full)
+    assert (np.concatenate([dstate(s)["Wd"] for s in shards], axis=1).view(np.uint32) == sf["Wd"].view(np.uint32)).all()
+    for step in (1, 2):
+        x = tens(synth.feature_batch(B, d, step=step))
+        hf = full.forward(x, step=step, train=True)
+        hs = [s.forward(x, step=step, train=True) for s in shards]
+        assert torch.equal(torch.cat(hs, dim=1), hf), step
+        dh = tens(synth.signed_hidden_batch(B, m, step=20 + step, scale=0.01))
+        full.backward_adam(dh, F32(1e-3))
+        for s, (b, e) in zip(shards, cols):
+            s.backward_adam(dh[:, b:e].contiguous(), F32(1e-3))
+    torch.cuda.synchronize()
+    sf = dstate(full)
+    cat = [dstate(s) for s in shards]
+    for key, ax in (("Wd", 1), ("mWd", 1), ("vWd", 1), ("bd", 0), ("mbd", 0), ("vbd", 0)):
+        assert (np.concatenate([c[key] for c in cat], axis=ax) == sf[key]).all(), key
+
+
+def test_sharded_model_world1_equals_model_step_composition():
+    """ShardedModel with one rank runs the unsharded layer through the standalone calls:
+    its state after two steps equals forward + train_step + backward_adam composed by hand,
+    bit for bit (CSC dh: deterministic summation order)."""
+    from paper_2306_03725_b200.sharded import ShardedLayer, ShardedModel
+    L, m, k, d, B = 3000, 512, 32, 64, 32
+    sm = ShardedModel(ShardedLayer(L, m, k, device=dev(), max_batch=B, seed=9, dh_mode=1), d=d, device=dev(), seed=3,
+                      dropout=0.1, max_batch=B)
+    lay = make(L, m, k, B=B, seed=9, dh_mode=1)
+    dn = make_dense(d, m, B=B, seed=3, dropout=0.1)
+    for step in (1, 2):
+        x = tens(synth.feature_batch(B, d, step=step))
+        ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        sm.train_step(x, step, tens(ptr), tens(ids), F32(1e-3))
+        h = dn.forward(x, step=step, train=True)
+        dh, _ = lay.train_step(h, tens(ptr), tens(ids), F32(1e-3))
+        dn.backward_adam(dh, F32(1e-3))
+    torch.cuda.synchronize()
+    a, b = dstate(sm.dense), dstate(dn)
+    for key in ("Wd", "bd", "mWd", "vWd"):
+        assert (a[key] == b[key]).all(), key
+    sa, sb = state_of(sm.layer.engine), state_of(lay)
+    for key in ("W", "idx", "bias", "mW", "vW"):
+        assert (sa[key] == sb[key]).all(), key

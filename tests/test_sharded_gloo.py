@@ -194,10 +194,15 @@ D_FEAT, P_DROP, DSEED = 12, 0.2, 5
 
 
 class OracleDense:
-    """CPU stand-in for DenseLayer (same method signatures) backed by the oracle."""
+    """CPU stand-in for DenseLayer (same method signatures) backed by the oracle: the column
+    shard [c0, c1) of the dense layer (its columns of the whole layer's Glorot init; the
+    oracle's dense arithmetic is per column, so a slice of its inputs is the shard)."""
 
-    def __init__(self):
-        self.ds = oracle.DenseState.create(D_FEAT, M, DSEED)
+    def __init__(self, c0=0, c1=M):
+        full = oracle.DenseState.create(D_FEAT, M, DSEED)
+        sl = slice(c0, c1)
+        self.ds = oracle.DenseState(full.Wd[:, sl].copy(), full.bd[sl].copy(), full.mWd[:, sl].copy(),
+                                    full.vWd[:, sl].copy(), full.mbd[sl].copy(), full.vbd[sl].copy(), 0)
         self.xt = self.z = None
 
     def forward(self, x, step=0, train=True):
@@ -222,8 +227,10 @@ def _worker_model(rank, world, port, results):
         from paper_2306_03725_b200.sharded import ShardedModel
         rb, re_ = shard_rows(L, rank, world)
         eng = OracleEngine(L, M, K_FAN, rb, re_, SEED)
+        c0, c1 = shard_rows(M, rank, world)                 # this rank's dense columns
         model = ShardedModel(ShardedLayer(L, M, K_FAN, rank=rank, world=world, engine=eng, merge_fn=cpu_merge),
-                             dense=OracleDense())
+                             dense=OracleDense(c0, c1))
+        assert (model.col_begin, model.col_end) == (c0, c1)
         out = {}
         for step in range(3):
             x = torch.from_numpy(synth.feature_batch(B, D_FEAT, step=step).astype(np.float64))
@@ -244,11 +251,12 @@ def _worker_model(rank, world, port, results):
         dist.destroy_process_group()
 
 
-def test_two_rank_gloo_model_matches_unsharded_oracle():
-    """ShardedModel over 2 gloo ranks (dense replica per rank + label shards + dh all-reduce)
-    == the unsharded oracle.model_train_step: identical dense replicas, shard rows, losses
-    and merged top-K."""
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_model_matches_unsharded_oracle(world):
+    """ShardedModel over 2 and 3 gloo ranks (dense layer column-sharded, h
+    all-gathered, dh reduce-scattered; fixed fan-in layer label-sharded) == the unsharded
+    oracle.model_train_step: the ranks' Wd column shards concatenate to the unsharded Wd,
+    their label rows to W; identical losses and merged top-K."""
     mgr = mp.Manager()
     results = mgr.dict()
     mp.spawn(_worker_model, args=(world, _free_port(), results), nprocs=world, join=True)
@@ -260,8 +268,9 @@ def test_two_rank_gloo_model_matches_unsharded_oracle():
         r = oracle.model_train_step(ds, st, x, step, P_DROP, DSEED, ptr, ids, 1.0 / B, 1e-2)
         for rank in range(world):
             assert results[rank][f"loss{step}"] == pytest.approx(r.sparse.loss, rel=1e-12)
-    for rank in range(world):
-        np.testing.assert_allclose(results[rank]["Wd"], ds.Wd, rtol=0, atol=1e-12)
+    Wd_cat = np.concatenate([results[r]["Wd"] for r in range(world)], axis=1)
+    assert Wd_cat.shape == ds.Wd.shape and results[0]["Wd"].shape[1] == shard_rows(M, 0, world)[1]
+    np.testing.assert_allclose(Wd_cat, ds.Wd, rtol=0, atol=1e-12)
     np.testing.assert_allclose(np.concatenate([results[r]["W"] for r in range(world)]), st.W, rtol=0, atol=1e-12)
     _, _, h = oracle.dense_forward(ds.Wd, ds.bd, synth.feature_batch(B, D_FEAT, step=9).astype(np.float64))
     y, _ = oracle.forward(st.W, st.idx, st.bias, h)

@@ -171,6 +171,52 @@ __global__ void k_gbulk(const int* __restrict__ idx, const float* __restrict__ h
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (acc == 12345.f) out[0] = acc;
 }
+// gather + split reductions: lines of connection group gq < SPLIT go through red.v4 (LSU ->
+// L1 -> XBAR), the others are staged in smem and leave through the TMA engine as one
+// cp.reduce.async.bulk of 128 B each — two egress paths at once, if they are separate
+template <int SPLIT>
+__global__ void k_gsplit(const int* __restrict__ idx, const float* __restrict__ hT, float* dhT, long nconn, float* out) {
+  extern __shared__ float sm[];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, gq = lane >> 3, bq = lane & 7;
+  long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  long nw = (gridDim.x * (long)blockDim.x) >> 5;
+  float acc = 0.f;
+  int it = 0;
+  for (long r = warp; r * 32 < nconn; r += nw, ++it) {
+    float* buf = sm + (wib * 2 + (it & 1)) * 1024;
+    int c = __ldg(idx + r * 32 + lane);
+    float4 v[8]; int cc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { cc[i] = __shfl_sync(~0u, c, i * 4 + gq);
+      v[i] = __ldg(reinterpret_cast<const float4*>(hT + (long)cc[i] * 32 + 4 * bq)); }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += v[i].x + v[i].y + v[i].z + v[i].w;
+    float s = __shfl_xor_sync(~0u, acc, 1) * 1e-30f;
+    if (gq < SPLIT) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) red_v4(dhT + (long)cc[i] * 32 + 4 * bq, make_float4(s, s, s, s));
+    }
+    if (SPLIT < 4) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      if (gq >= SPLIT) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<float4*>(buf + (i * 4 + gq) * 32 + 4 * bq) = make_float4(s, s, s, s);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if ((lane & 3) >= SPLIT) {      // connection `lane` has group lane & 3
+        uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + lane * 32);
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 128;"
+                     :: "l"(dhT + (long)c * 32), "r"(sa) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (SPLIT < 4) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (acc == 12345.f) out[0] = acc;
+}
 __global__ void k_stream(const float4* __restrict__ a, long n4, float* out) {
   float acc = 0.f;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += gridDim.x * (long)blockDim.x) {
@@ -223,6 +269,24 @@ int main(int argc, char** argv) {
     snprintf(nm, 64, "gather v4+bulk red g=%d", grid);
     CK(cudaFuncSetAttribute(k_gbulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
     timeit(nm, 2 * gbytes, [&] { k_gbulk<<<grid, tpb, 16 * 4096>>>(idx, hT, dhT, nconn, out); });
+  }
+  for (int bpsm : {4, 8}) {
+    int grid = nsm * bpsm; char nm[64];
+    CK(cudaFuncSetAttribute(k_gsplit<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    CK(cudaFuncSetAttribute(k_gsplit<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    CK(cudaFuncSetAttribute(k_gsplit<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    CK(cudaFuncSetAttribute(k_gsplit<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    CK(cudaFuncSetAttribute(k_gsplit<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    snprintf(nm, 64, "gather+red split 4/4 LSU g=%d", grid);
+    timeit(nm, 2 * gbytes, [&] { k_gsplit<4><<<grid, 256, 16 * 4096>>>(idx, hT, dhT, nconn, out); });
+    snprintf(nm, 64, "gather+red split 3/4 LSU g=%d", grid);
+    timeit(nm, 2 * gbytes, [&] { k_gsplit<3><<<grid, 256, 16 * 4096>>>(idx, hT, dhT, nconn, out); });
+    snprintf(nm, 64, "gather+red split 2/4 LSU g=%d", grid);
+    timeit(nm, 2 * gbytes, [&] { k_gsplit<2><<<grid, 256, 16 * 4096>>>(idx, hT, dhT, nconn, out); });
+    snprintf(nm, 64, "gather+red split 1/4 LSU g=%d", grid);
+    timeit(nm, 2 * gbytes, [&] { k_gsplit<1><<<grid, 256, 16 * 4096>>>(idx, hT, dhT, nconn, out); });
+    snprintf(nm, 64, "gather+red split 0/4 LSU g=%d", grid);
+    timeit(nm, 2 * gbytes, [&] { k_gsplit<0><<<grid, 256, 16 * 4096>>>(idx, hT, dhT, nconn, out); });
   }
   timeit("hbm read 1GiB", (double)nbig, [&] { k_stream<<<nsm * 8, 512>>>(big, nbig / 16, out); });
   timeit("hbm copy 1GiB", 2.0 * nbig, [&] { k_copy<<<nsm * 8, 512>>>(big, big2, nbig / 16); });
