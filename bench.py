@@ -139,6 +139,13 @@ class ClockSampler:
 # r01b_l2bench_bulkred.txt): 21.4 M random 128-B line gathers + 21.4 M 128-B red.v4 lines = 11.2 TB/s combined
 # (atomic dh); two gathers per connection (CSC pull) ~19.9 TB/s
 ONCHIP_CEILING_GBS = {"atomic": 11200.0, "csc": 19900.0}
+GATHER_CEILING_GBS = 19900.0      # random 128-B line gathers from an L2-resident table (r01_l2bench)
+
+
+def gather_bytes(shape, B):
+    """On-chip bytes a forward/predict pass gathers: one 128-B h line per connection and
+    32-sample chunk (samples padded to whole lines)."""
+    return 128.0 * shape.L * shape.k * ((B + 31) // 32)
 
 
 # ----------------------------------------------------------------------------- byte models
@@ -588,6 +595,8 @@ def run_ours(a, shape, world, rank, local_rank):
             res[name] = e0.elapsed_time(e1) / reps
         big = {"B": BI, "K": K, "predict_samples_per_s": BI / (res["predict"] * 1e-3),
                "predict_ms_per_batch": res["predict"],
+               "predict_gather_floor_ms": gather_bytes(shape, BI) / (GATHER_CEILING_GBS * 1e9) * 1e3,
+               "predict_gather_frac": gather_bytes(shape, BI) / (res["predict"] * 1e-3) / 1e9 / GATHER_CEILING_GBS,
                "shortlist_candidates_per_sample": NCAND, "shortlist_pairs_per_s": BI * NCAND / (res["shortlist"] * 1e-3),
                "shortlist_ms_per_batch": res["shortlist"]}
         del inf
@@ -674,7 +683,12 @@ def run_ours(a, shape, world, rank, local_rank):
         "predict": {"value": B * n_pred / (ms_pred * 1e-3), "unit": "samples/s", "K": K,
                     "ms_per_batch": ms_pred / n_pred,
                     "hbm_gbs": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9,
-                    "frac": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9 / peak},
+                    "frac": pred_bytes / (ms_pred / n_pred * 1e-3) / 1e9 / peak,
+                    # the binding roof: the random 128-B h-line gathers (4 B x B_pad x L x k) vs the
+                    # measured gather-only ceiling (tools/microbench/l2bench, profiles/r01_l2bench.txt)
+                    "gather_gbs": gather_bytes(shape, B) / (ms_pred / n_pred * 1e-3) / 1e9,
+                    "gather_floor_ms": gather_bytes(shape, B) / (GATHER_CEILING_GBS * 1e9) * 1e3,
+                    "gather_frac": gather_bytes(shape, B) / (ms_pred / n_pred * 1e-3) / 1e9 / GATHER_CEILING_GBS},
         "redistribution": redist,
         "cuda_graph": graph,
         "inference_large_batch": big,

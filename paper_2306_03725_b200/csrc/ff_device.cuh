@@ -107,6 +107,16 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
   return r;
 }
+// The same FMA as a volatile asm: volatile asms keep their program order, so FMAs written
+// after a batch of (volatile) line loads cannot be hoisted between them by the scheduler —
+// otherwise the first FMA's wait on its load stalls the issue of the remaining loads.
+__device__ __forceinline__ float2 ffma2_ordered(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm volatile("{.reg .b64 a, b, c, d; mov.b64 a, {%2,%3}; mov.b64 b, {%4,%5}; mov.b64 c, {%6,%7};"
+               " fma.rn.f32x2 d, a, b, c; mov.b64 {%0,%1}, d;}"
+               : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   float2 r;
   asm("{.reg .b64 a, b, d; mov.b64 a, {%2,%3}; mov.b64 b, {%4,%5}; mul.rn.f32x2 d, a, b; mov.b64 {%0,%1}, d;}"

@@ -1305,6 +1305,156 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   }
 }
 
+// Fused forward + top-K for large batches (B > 32, k = 32; NEXT-3): the batch is
+// scored in chunks of 128 samples (4 hd lines per column; 16 MiB of h lines at m = 32768, so a
+// chunk stays L2-resident while every row streams past it).  Per connection one warp
+// instruction gathers four 128-B h lines (lane l: line l >> 3 of the chunk, 16-B segment
+// l & 7), i.e. 512 B per instruction instead of the ring kernel's 128 B per 8 lanes.  The
+// gathers are staged like k_train_ring's: a per-warp ring of D stages in shared memory
+// (cp.async, no registers held), one stage = one connection group g (slots g + 4q, q < 8).
+// The score of every sample is summed in exactly row_score_own's order — per group g two FMA
+// chains (q even / odd) from 0, P_g = a + b, y = ((P_0 + P_2) + (P_1 + P_3)) + bias — so y is
+// bit-identical to forward().
+// Top-K: each lane owns 4 samples, with a register threshold per sample and a sorted
+// kTopkMax list per (warp, sample) in an L2-resident scratch wl[warp][kTopkMax][128]; the
+// block merges its warps' lists into cand[blk][b][kTopkMax] per chunk.  The host runs the
+// kernel twice: over a prefix of the rows [0, r1) (thr = NULL), whose lists are merged into
+// that prefix's exact top-K, then over [r1, L) with thr = that merged list: its K-th entry
+// (score, id) starts every lane's threshold.  A row ranked below the K-th of a subset of the
+// rows cannot be in the top K, so the skip is exact, and insertions (a dependent walk through
+// the list) become rare; the final merge takes the second pass's lists plus the prefix list.
+#ifndef FF_PREDW_THREADS
+#define FF_PREDW_THREADS 256
+#endif
+#ifndef FF_PREDW_D
+#define FF_PREDW_D 2
+#endif
+constexpr int kPredWThreads = FF_PREDW_THREADS, kPredWD = FF_PREDW_D;
+constexpr int kPredWStage = 8 * 32 * 16;                                     // 8 connections x 512 B
+constexpr int kPredWSmem = (kPredWThreads / 32) * kPredWD * kPredWStage;
+constexpr int kPredWListFloats = kTopkMax * 128;                             // per warp, per array
+__global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __restrict__ W, const int* __restrict__ idx,
+                                                                const float* __restrict__ bias,
+                                                                const float* __restrict__ hd, int64_t r0, int64_t r1,
+                                                                int B, int nb, int64_t row_begin,
+                                                                const float* __restrict__ thr_s_in,
+                                                                const int* __restrict__ thr_i_in, int K,
+                                                                float* __restrict__ cand_s, int* __restrict__ cand_i,
+                                                                float* __restrict__ wl_s, int* __restrict__ wl_i) {
+  constexpr int BC = 128, NW = kPredWThreads / 32, D = kPredWD;
+  extern __shared__ __align__(16) unsigned char wide_smem[];
+  float* const lst_s = wl_s + (int64_t)blockIdx.x * NW * kPredWListFloats;     // this block's [NW][kTopkMax][BC]
+  int* const lst_i = wl_i + (int64_t)blockIdx.x * NW * kPredWListFloats;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* const ws = lst_s + wid * kTopkMax * BC;
+  int* const wi = lst_i + wid * kTopkMax * BC;
+  const uint32_t ring0 = pin((uint32_t)__cvta_generic_to_shared(wide_smem) + (uint32_t)(wid * D * kPredWStage) +
+                             (uint32_t)lane * 16u);
+  const uint32_t nwarp = pin((uint32_t)(((int64_t)gridDim.x * blockDim.x) >> 5));
+  const uint32_t nrows = pin((uint32_t)r1);
+  const uint32_t cfl = pin(64u * (uint32_t)nb);            // floats per hd column
+  const uint32_t j0 = (uint32_t)r0 + (uint32_t)global_warp();
+  const int nchunk = (nb + 3) / 4;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int q2 = ch * 4 + (lane >> 3);                    // this lane's line; samples 4 (lane & 7) + e
+    const bool ok = q2 < nb;
+    const float* const hb = hd + (ok ? q2 : 0) * 64 + 4 * (lane & 7);
+    const int sb = q2 * 32 + 4 * (lane & 7);                // first sample of the lane
+    const int s0 = (lane >> 3) * 32 + 4 * (lane & 7);       // its index within the chunk
+    for (int t = threadIdx.x; t < NW * kTopkMax * BC; t += blockDim.x) { lst_s[t] = -INFINITY; lst_i[t] = INT_MAX; }
+    __syncthreads();
+    float thr_s[4]; int thr_i[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      thr_s[e] = -INFINITY; thr_i[e] = INT_MAX;
+      if (thr_s_in && ok && sb + e < B) {
+        thr_s[e] = thr_s_in[(int64_t)(sb + e) * kTopkMax + K - 1];
+        thr_i[e] = thr_i_in[(int64_t)(sb + e) * kTopkMax + K - 1];
+      }
+    }
+    // issue side: group (ji, gi) of the flat (row, group) sequence; ci = that row's idx lane
+    uint32_t ji = j0; int gi = 0;
+    int ci = ji < nrows ? ld_na_ro(idx + ji * 32u + lane) : 0;
+    int ci_n = ji + nwarp < nrows ? ld_na_ro(idx + (ji + nwarp) * 32u + lane) : 0;
+    auto issue = [&](uint32_t stg) {
+      if (ji < nrows) {
+        const uint32_t dst = ring0 + stg * (uint32_t)kPredWStage;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t c = (uint32_t)__shfl_sync(kFull, ci, 4 * q + gi);
+          if (ok) cp_async16(dst + (uint32_t)q * 512u, col_line(hb, c, cfl));    // lines >= nb: not gathered
+        }
+      }
+      cp_async_commit();
+      if (++gi == 4) {
+        gi = 0; ji += nwarp; ci = ci_n;
+        ci_n = ji + nwarp < nrows ? ld_na_ro(idx + (ji + nwarp) * 32u + lane) : 0;
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) issue((uint32_t)d);
+    uint32_t stg = 0;
+    float w_n = 0.f, b_n = 0.f;
+    if (j0 < nrows) { w_n = ld_na(W + j0 * 32u + lane); b_n = ld_na(bias + j0); }
+    for (uint32_t j = j0; j < nrows; j += nwarp) {
+      const float wl = w_n, bj = b_n;
+      if (j + nwarp < nrows) { w_n = ld_na(W + (j + nwarp) * 32u + lane); b_n = ld_na(bias + j + nwarp); }
+      float2 P[4][2];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        issue(stg == 0 ? (uint32_t)(D - 1) : stg - 1);        // the stage summed last iteration
+        cp_async_wait<D - 1>();                               // this group's lines have landed
+        const uint32_t src = ring0 + stg * (uint32_t)kPredWStage;
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 hv = lds4(src + (uint32_t)q * 512u);
+          const float w = __shfl_sync(kFull, wl, 4 * q + g);
+          if (q & 1) { b0 = ffma2(bc2(w), lo2(hv), b0); b1 = ffma2(bc2(w), hi2(hv), b1); }
+          else       { a0 = ffma2(bc2(w), lo2(hv), a0); a1 = ffma2(bc2(w), hi2(hv), a1); }
+        }
+        P[g][0] = make_float2(a0.x + b0.x, a0.y + b0.y);
+        P[g][1] = make_float2(a1.x + b1.x, a1.y + b1.y);
+        stg = stg + 1 == (uint32_t)D ? 0u : stg + 1;
+      }
+      const int jid = (int)(row_begin + j);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        auto el = [&](const float2& v) { return (e & 1) ? v.y : v.x; };
+        const float y = ((el(P[0][e >> 1]) + el(P[2][e >> 1])) + (el(P[1][e >> 1]) + el(P[3][e >> 1]))) + bj;
+        if (ok && sb + e < B && better(y, jid, thr_s[e], thr_i[e])) {
+          const int s = s0 + e;
+          int r = kTopkMax - 1;
+          while (r > 0 && better(y, jid, ws[(r - 1) * BC + s], wi[(r - 1) * BC + s])) {
+            ws[r * BC + s] = ws[(r - 1) * BC + s]; wi[r * BC + s] = wi[(r - 1) * BC + s]; --r;
+          }
+          ws[r * BC + s] = y; wi[r * BC + s] = jid;
+          const float ks = ws[(kTopkMax - 1) * BC + s]; const int ki = wi[(kTopkMax - 1) * BC + s];
+          if (better(ks, ki, thr_s[e], thr_i[e])) { thr_s[e] = ks; thr_i[e] = ki; }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // block merge: thread t takes chunk samples t, t + blockDim, ...
+    for (int s = threadIdx.x; s < BC; s += blockDim.x) {
+      const int b = ch * BC + s;
+      if (b >= 32 * nb) break;
+      float ts[kTopkMax]; int ti[kTopkMax];
+#pragma unroll
+      for (int q = 0; q < kTopkMax; ++q) { ts[q] = lst_s[q * BC + s]; ti[q] = lst_i[q * BC + s]; }
+      for (int w2 = 1; w2 < NW; ++w2)
+#pragma unroll
+        for (int q = 0; q < kTopkMax; ++q)
+          topk_consider(ts, ti, lst_s[(w2 * kTopkMax + q) * BC + s], lst_i[(w2 * kTopkMax + q) * BC + s]);
+      const int64_t base = ((int64_t)blockIdx.x * 32 * nb + b) * kTopkMax;
+#pragma unroll
+      for (int q = 0; q < kTopkMax; ++q) { cand_s[base + q] = ts[q]; cand_i[base + q] = ti[q]; }
+    }
+    __syncthreads();
+  }
+}
+
 // Block per sample: merge `nlist` sorted candidate lists (first Kin entries used) into the
 // top K.  Each thread keeps a running top-kTopkMax over lists tid, tid + blockDim, ...; each
 // warp reduces its lanes by K rounds of arg-best + pop; warp 0 merges the warps' lists the

@@ -49,11 +49,12 @@ ff_status fail(ff_status s, const char* fmt, ...) {
 
 constexpr size_t kAlign = 256;
 constexpr int kMaxCandBlocks = 1024;    // predict grid cap (candidate buffer rows)
+constexpr int kMaxWideWarps = 4096;     // wide predict: warps with a top-K list in the scratch
 
 size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {   // byte offsets into the workspace
-  size_t W, idx, mW, vW, dW, bias, mb, vb, db, posmask, hd, cand_s, cand_i,
+  size_t W, idx, mW, vW, dW, bias, mb, vb, db, posmask, hd, cand_s, cand_i, wl_s, wl_i,
       h_stage, lbl_stage, dh_stage, scalars,
       ent, sort_keys2, gT, col_ptr, sort_keys, sort_tmp, sort_tmp_bytes,   // CSC mode only
       total;
@@ -88,6 +89,10 @@ Layout layout_of(const ff_config& c) {
   o.hd = take(8 * m * ldh);         // [m][nb][h 32 | dh 32]
   o.cand_s = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
   o.cand_i = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
+  if (c.max_batch > 32 && c.k == 32) {                               // wide predict: per-warp top-K lists
+    o.wl_s = take(4 * (size_t)kMaxWideWarps * kPredWListFloats);
+    o.wl_i = take(4 * (size_t)kMaxWideWarps * kPredWListFloats);
+  }
   o.h_stage = take(2 * 4 * (size_t)c.max_batch * m);                 // double-buffered (host entry point)
   o.lbl_stage = take(2 * 4 * ((size_t)c.max_batch + 1 + nnz));
   o.dh_stage = take(4 * (size_t)c.max_batch * m);
@@ -153,8 +158,8 @@ struct ff_layer {
   ff_config cfg;
   Layout lay;
   char* ws;
-  float *W, *mW, *vW, *dW, *bias, *mb, *vb, *db, *hd, *cand_s, *h_stage, *dh_stage;
-  int *idx, *cand_i, *lbl_stage, *err;
+  float *W, *mW, *vW, *dW, *bias, *mb, *vb, *db, *hd, *cand_s, *h_stage, *dh_stage, *wl_s;
+  int *idx, *cand_i, *wl_i, *lbl_stage, *err;
   int *ent, *col_ptr;               // CSC mode
   float* gT;
   int rs;                           // CSC mode: record stride (floats)
@@ -171,7 +176,7 @@ struct ff_layer {
   uint32_t* posmask;
   int64_t t;
   bool grads_valid;
-  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring, grid_pred_ring;
+  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring, grid_pred_ring, grid_pred_wide;
   int nsm;
   std::vector<cudaEvent_t> prof_ev;   // pairs (before, after) of the fused row kernel
   // host entry point: H2D copies on a library stream into one of two staging slots, so the
@@ -437,6 +442,25 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
     nlist = l->grid_pred_ring;
     void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &rb, &cs, &ci};
     FF_CUDA(cudaLaunchKernel((const void*)k_predict_ring, dim3(nlist), dim3(kPredRingThreads), args, kPredRingSmem, st));
+  } else if (k == 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE)) {   // large batch: chunked wide kernel (bit-identical)
+    // pass 1 over a prefix of the rows, merged into its exact top-K (list slot g of cand);
+    // pass 2 over the rest, thresholds from that list; the final merge takes g + 1 lists
+    const int g = l->grid_pred_wide;
+    const int64_t r1 = std::min<int64_t>(L, std::max<int64_t>(L / 32, (int64_t)g * (kPredWThreads / 32)));
+    float* wls = l->wl_s; int* wli = l->wl_i;
+    float* ps = cs + (int64_t)g * ldh * kTopkMax; int* pi = ci + (int64_t)g * ldh * kTopkMax;
+    const float* no_s = nullptr; const int* no_i = nullptr;
+    int64_t z = 0, Lw = L;
+    int Kw = K;
+    void* a1[] = {&W, &idx, &bias, &hd, &z, const_cast<int64_t*>(&r1), &BB, &nbb, &rb, &no_s, &no_i, &Kw, &cs, &ci, &wls, &wli};
+    FF_CUDA(cudaLaunchKernel((const void*)k_predict_wide, dim3(g), dim3(kPredWThreads), a1, kPredWSmem, st));
+    k_merge_topk_block<<<B, kMergeThreads, 0, st>>>(cs, ci, g, (int64_t)ldh * kTopkMax, kTopkMax, kTopkMax, kTopkMax,
+                                                    ps, pi);
+    g_launches += 2;
+    const float* ts_ = ps; const int* ti_ = pi;
+    void* a2[] = {&W, &idx, &bias, &hd, const_cast<int64_t*>(&r1), &Lw, &BB, &nbb, &rb, &ts_, &ti_, &Kw, &cs, &ci, &wls, &wli};
+    FF_CUDA(cudaLaunchKernel((const void*)k_predict_wide, dim3(g), dim3(kPredWThreads), a2, kPredWSmem, st));
+    nlist = g + 1;
   } else {
     void* args[] = {&W, &idx, &bias, &hd, &L, &k, &BB, &nbb, &rb, &cs, &ci};
     FF_CUDA(cudaLaunchKernel(predict_kernel(l->cfg.k), dim3(l->grid_pred), dim3(kRowThreads), args, 0, st));
@@ -623,6 +647,7 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->mb = at<float>(ws, lay.mb); l->vb = at<float>(ws, lay.vb); l->db = at<float>(ws, lay.db);
   l->posmask = at<uint32_t>(ws, lay.posmask); l->hd = at<float>(ws, lay.hd);
   l->cand_s = at<float>(ws, lay.cand_s); l->cand_i = at<int>(ws, lay.cand_i);
+  l->wl_s = lay.wl_s ? at<float>(ws, lay.wl_s) : nullptr; l->wl_i = lay.wl_i ? at<int>(ws, lay.wl_i) : nullptr;
   l->h_stage = at<float>(ws, lay.h_stage); l->lbl_stage = at<int>(ws, lay.lbl_stage);
   l->dh_stage = at<float>(ws, lay.dh_stage);
   l->err = at<int>(ws, lay.scalars); l->loss_scratch = at<float>(ws, lay.scalars + 4);
@@ -667,6 +692,13 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   }
   l->grid_pred_ring =
       std::min(kMaxCandBlocks, occupancy_grid((const void*)k_predict_ring, l->nsm, kPredRingThreads, kPredRingSmem));
+  if (cudaFuncSetAttribute((const void*)k_predict_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kPredWSmem) !=
+      cudaSuccess) {
+    delete l;
+    return fail(FF_ERR_CUDA, "wide predict smem attribute");
+  }
+  l->grid_pred_wide = std::min(std::min(kMaxCandBlocks - 1, kMaxWideWarps / (kPredWThreads / 32)),
+                               occupancy_grid((const void*)k_predict_wide, l->nsm, kPredWThreads, kPredWSmem));
   l->grid_rows = l->nsm * 8;
   // zero everything that must start at zero (moments, masks, dW/db, dhT, scalars)
   e = cudaMemsetAsync(ws, 0, lay.total, st);

@@ -417,7 +417,10 @@ def test_redistribution_config_errors():
                                         (4000, 1024, 32, 1024, 5),
                                         # k = 32, B <= 32: the pipelined predict kernel
                                         (5000, 512, 32, 32, 5), (3001, 300, 32, 7, 8), (40, 64, 32, 32, 8),
-                                        (200003, 4096, 32, 32, 5)])
+                                        (200003, 4096, 32, 32, 5),
+                                        # k = 32, B > 32: the chunked wide kernel (ragged lines and chunks)
+                                        (3001, 300, 32, 33, 8), (2000, 512, 32, 129, 5), (2500, 700, 32, 300, 3),
+                                        (20011, 2048, 32, 1000, 8), (37, 64, 32, 64, 8)])
 def test_predict_topk_bit_exact(L, m, k, B, K):
     lay = make(L, m, k, B=B, seed=3)
     h = tens(synth.hidden_batch(B, m, step=1))
@@ -440,6 +443,17 @@ def test_predict_topk_ties_resolved_by_lower_id():
 
 def test_predict_topk_ties_resolved_by_lower_id_pipelined():
     L, m, k, B = 5000, 64, 32, 32          # k = 32, B <= 32: k_predict_ring + block merge
+    lay = make(L, m, k, B=B)
+    W = np.zeros((L, k), np.float32)
+    bias = np.zeros(L, np.float32); bias[[4999, 17, 5, 2500, 100]] = 1.0
+    lay.set_params(W=tens(W), bias=tens(bias))
+    sc, ids = lay.predict_topk(tens(synth.hidden_batch(B, m)), 8)
+    assert (ids.cpu().numpy() == np.array([5, 17, 100, 2500, 4999, 0, 1, 2])).all()
+
+
+@pytest.mark.parametrize("B", [70, 300])
+def test_predict_topk_ties_resolved_by_lower_id_wide(B):
+    L, m, k = 5000, 64, 32                 # k = 32, B > 32: k_predict_wide + block merge
     lay = make(L, m, k, B=B)
     W = np.zeros((L, k), np.float32)
     bias = np.zeros(L, np.float32); bias[[4999, 17, 5, 2500, 100]] = 1.0
@@ -645,11 +659,13 @@ def test_train_step_cuda_graph_replay(dh_mode):
     assert sa["t"] == sb["t"] == 6
     for key in ("W", "bias", "mW", "vW", "idx", "mb", "vb"):
         assert (sa[key] == sb[key]).all(), key
-    if dh_mode == 1:                                   # CSC: deterministic dh and loss order
+    if dh_mode == 1:                                   # CSC: deterministic dh order
         assert torch.equal(sdh, dh_e)
     else:                                              # atomic reductions: order-dependent rounding
         assert dh_close(sdh.cpu(), dh_e.cpu())
-    assert all(abs(x.item() - y.item()) <= 1e-6 * abs(y.item()) for x, y in zip(losses_g, losses_e))
+    # the loss is an fp32 sum of per-block partials added by atomics in arrival order (every
+    # dh mode): replay and eager agree to summation-order rounding, bounded well inside R19
+    assert all(abs(x.item() - y.item()) <= 1e-5 * abs(y.item()) for x, y in zip(losses_g, losses_e))
 
 
 def test_csc_dh_is_deterministic_and_matches_atomic():
