@@ -242,9 +242,9 @@ def test_fused_step_equals_unfused_path(L, m, k, B, dh_mode):
 
 @LOSS
 @DH
-@pytest.mark.parametrize("k", [16, 32, 64])
-def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k):
-    L, m, B = 1000, 256, 32
+@pytest.mark.parametrize("k,B", [(16, 32), (32, 32), (64, 32), (32, 16), (32, 5)])
+def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k, B):
+    L, m = 1000, 256
     layer = L_()
     lay = make(L, m, k, B=B, flags=layer.FF_FLAG_STORE_GRADS, seed=42, dh_mode=dh_mode, loss=loss_id(loss))
     for step in range(5):
@@ -254,13 +254,28 @@ def test_fused_step_lockstep_vs_oracle(dh_mode, loss, k):
                           s0["vb"].astype(np.float64), s0["t"])
         h = synth.hidden_batch(B, m, step=step)
         ptr, ids = synth.label_batch(B, L, 5.0, step=step)
+        y_gpu = lay.forward(tens(h)).cpu().numpy().astype(np.float64)     # = the fused step's y
         loss_t = torch.zeros(1, device=dev())
         dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3), loss=loss_t)
         dW, db = lay.get_grads()
         r = oracle.train_step(st, h, ptr, ids, F32(1.0 / B), F32(1e-3), loss=loss, **ADAM)
-        assert_close(dh.cpu().numpy(), r.dh, r.Adh, f"dh step {step}")
-        assert_close(dW.cpu().numpy(), r.dW, r.AdW, f"dW step {step}")
-        assert_close(db.cpu().numpy(), r.db, r.Adb, f"db step {step}")
+        assert_close(y_gpu, r.y, r.Ay, f"y step {step}")
+        if loss == "sqh":
+            # the hinge's zero/non-zero decision max(0, 1 - t'y) is taken on the kernel's y
+            # (fp32) on both sides; it may differ from the fp64 decision only at a margin tie
+            g2, _ = oracle.loss_grad(loss, y_gpu, ptr, ids, F32(1.0 / B))
+            flip = (g2 != 0) != (r.g != 0)
+            tp = -np.ones((B, L))                                       # t' = +-1
+            for b_ in range(B):
+                tp[b_, ids[ptr[b_]:ptr[b_ + 1]]] = 1.0
+            assert (np.abs(1 - tp * r.y)[flip] <= RTOL * r.Ay[flip]).all(), "hinge decision away from a tie"
+            dWr, AdWr, dbr, Adbr = oracle.weight_grad(s0["idx"], h, g2)
+            dhr, Adhr = oracle.input_grad(s0["W"], s0["idx"], g2, m)
+        else:
+            dWr, AdWr, dbr, Adbr, dhr, Adhr = r.dW, r.AdW, r.db, r.Adb, r.dh, r.Adh
+        assert_close(dh.cpu().numpy(), dhr, Adhr, f"dh step {step}")
+        assert_close(dW.cpu().numpy(), dWr, AdWr, f"dW step {step}")
+        assert_close(db.cpu().numpy(), dbr, Adbr, f"db step {step}")
         assert abs(loss_t.item() - r.loss) <= RTOL * r.loss
         # Adam applied by the oracle to the GPU's gradient: tight elementwise parity
         s1 = state_of(lay)
@@ -741,7 +756,9 @@ def test_csc_multi_tile_dh_and_grads():
 
 @LOSS
 @DH
-@pytest.mark.parametrize("L,m,B", [(5000, 1024, 32), (1234, 700, 19), (31, 64, 32), (70000, 4096, 32)])
+@pytest.mark.parametrize("L,m,B", [(5000, 1024, 32), (1234, 700, 19), (31, 64, 32), (70000, 4096, 32),
+                                   # B <= 16: padded samples in every line
+                                   (5000, 1024, 16), (1234, 700, 9), (33, 64, 1), (70000, 4096, 13)])
 def test_pipelined_step_equals_generic_step(L, m, B, dh_mode, loss):
     """k = 32, B <= 32 runs the software-pipelined fused kernel (cp.async shared-memory ring);
     FF_FLAG_NO_PIPE forces the generic one.  Both implement the same arithmetic: state and
@@ -951,7 +968,7 @@ SAT_BIAS = np.array([-60.0, -25.0, 0.0, 25.0, 60.0], np.float32)
 
 @LOSS
 @DH
-@pytest.mark.parametrize("k,B", [(32, 32), (16, 32), (32, 20), (13, 40)])
+@pytest.mark.parametrize("k,B", [(32, 32), (16, 32), (32, 20), (13, 40), (32, 12)])
 def test_saturated_logits_and_signed_h_lockstep(dh_mode, loss, k, B):
     """biases of +-25 and +-60 with positives and negatives on each, W scale 2
     and signed (non-ReLU) h, so that y reaches |y| ~ 65.  For a positive with y >~ 17 the naive
@@ -998,7 +1015,7 @@ def test_saturated_logits_and_signed_h_lockstep(dh_mode, loss, k, B):
 
 # ------------------------------------------------------------ FF_FLAG_CHECK_FINITE
 @DH
-@pytest.mark.parametrize("k,B", [(32, 32), (16, 32), (32, 100)])
+@pytest.mark.parametrize("k,B", [(32, 32), (16, 32), (32, 100), (32, 8)])
 @pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan])
 def test_check_finite_reports_nonfinite_scores(dh_mode, k, B, bad):
     """with FF_FLAG_CHECK_FINITE a non-finite score (an inf / NaN in h reaches
