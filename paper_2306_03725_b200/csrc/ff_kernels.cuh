@@ -1202,10 +1202,12 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
                                                                    const int* __restrict__ idx,
                                                                    const float* __restrict__ bias,
                                                                    const float* __restrict__ hd, int64_t L, int B,
-                                                                   int64_t row_begin, float* __restrict__ cand_s,
+                                                                   int nb, int q2, int64_t row_begin,
+                                                                   float* __restrict__ cand_s,
                                                                    int* __restrict__ cand_i) {
   constexpr int NG = 8, D = kPredRingD;
-  constexpr uint32_t kColFloats = 64, kStage = 8 * 32 * 16;
+  constexpr uint32_t kStage = 8 * 32 * 16;
+  const uint32_t kColFloats = pin(64u * (uint32_t)nb);   // hd column stride; this launch scores line q2
   extern __shared__ __align__(16) unsigned char ring_smem[];
   // per-warp candidate buffer [slot][lane] while scoring (conflict-free), reused as the
   // block-merge lists [lane][q] at the end (same per-warp 1-KB regions)
@@ -1218,14 +1220,14 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   // per-connection shuffles, the ring slot, the h-line base and the state pointers
   const uint32_t nwarp = pin((uint32_t)(((int64_t)gridDim.x * blockDim.x) >> 5));
   const uint32_t ring0 = pin((uint32_t)__cvta_generic_to_shared(ring_smem) + (uint32_t)wid * D * kStage + (uint32_t)lane * 16u);
-  const float* const hb = pin(hd + 4 * bq);
+  const float* const hb = pin(hd + q2 * 64 + 4 * bq);
   const float* const Wp = pin(W);
   const int* const idxp = pin(idx);
   const float* const biasp = pin(bias);
   int sl[NG];
 #pragma unroll
   for (int q = 0; q < NG; ++q) sl[q] = pin(4 * q + gq);
-  const int b = 4 * bq + gq;
+  const int b = q2 * 32 + 4 * bq + gq;                   // this lane's sample
   const uint32_t nrows = pin((uint32_t)L);
   float ts[kTopkMax]; int ti[kTopkMax];
 #pragma unroll
@@ -1299,7 +1301,7 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
     for (int w2 = 1; w2 < kPredRingThreads / 32; ++w2)
 #pragma unroll
       for (int q = 0; q < kTopkMax; ++q) topk_insert(ts, ti, ss[w2][lane][q], si[w2][lane][q]);
-    const int64_t base = ((int64_t)blockIdx.x * 32 + b) * kTopkMax;
+    const int64_t base = ((int64_t)blockIdx.x * 32 * nb + b) * kTopkMax;
 #pragma unroll
     for (int q = 0; q < kTopkMax; ++q) { cand_s[base + q] = ts[q]; cand_i[base + q] = ti[q]; }
   }

@@ -50,6 +50,7 @@ ff_status fail(ff_status s, const char* fmt, ...) {
 constexpr size_t kAlign = 256;
 constexpr int kMaxCandBlocks = 1024;    // predict grid cap (candidate buffer rows)
 constexpr int kMaxWideWarps = 4096;     // wide predict: warps with a top-K list in the scratch
+constexpr int kPredRingMaxLines = 3;    // predict: B <= 96 runs the ring kernel per 32-sample line
 
 size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -438,10 +439,15 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
   int64_t L = l->cfg.L_local, rb = l->cfg.row_begin; int k = l->cfg.k, BB = B, nbb = nb;
   float* cs = l->cand_s; int* ci = l->cand_i;
   int nlist = l->grid_pred;
-  if (k == 32 && nb == 1) {            // hot configuration: pipelined kernel (bit-identical scores)
+  if (k == 32 && (nb == 1 || (nb <= kPredRingMaxLines && !(l->cfg.flags & FF_FLAG_NO_PIPE)))) {
+    // hot configuration (B <= 32), and B <= 96: the pipelined kernel once per 32-sample line
+    // (bit-identical scores; below 4 lines the wide kernel would leave lanes idle)
     nlist = l->grid_pred_ring;
-    void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &rb, &cs, &ci};
-    FF_CUDA(cudaLaunchKernel((const void*)k_predict_ring, dim3(nlist), dim3(kPredRingThreads), args, kPredRingSmem, st));
+    for (int q2 = 0; q2 < nb; ++q2) {
+      void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &nbb, &q2, &rb, &cs, &ci};
+      FF_CUDA(cudaLaunchKernel((const void*)k_predict_ring, dim3(nlist), dim3(kPredRingThreads), args, kPredRingSmem, st));
+      if (q2 + 1 < nb) ++g_launches;
+    }
   } else if (k == 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE)) {   // large batch: chunked wide kernel (bit-identical)
     // pass 1 over a prefix of the rows, merged into its exact top-K (list slot g of cand);
     // pass 2 over the rest, thresholds from that list; the final merge takes g + 1 lists
