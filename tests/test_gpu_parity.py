@@ -945,16 +945,22 @@ def test_predict_topk_vs_fp64_oracle_gap_guarded(L, m, k, B, K):
     assert near <= max(2, B // 4)           # sanity: ties within the 1e-4 bound stay a minority
 
 
-def test_predict_topk_vs_fp64_oracle_full_amazon_670k():
-    """BASELINE.json's Amazon-670K shape in the bench's predict configuration (k = 32, B = 32,
-    the pipelined kernel), after one training step so that bias and W are not at init."""
+@pytest.mark.parametrize("B", [32, 64, 160])
+def test_predict_topk_vs_fp64_oracle_full_amazon_670k(B):
+    """BASELINE.json's Amazon-670K shape in the bench's predict configuration (k = 32, the
+    ring kernel at B = 32 and, per 32-sample line, at B = 64; the two-pass wide kernel at
+    B = 160: one full 128-sample chunk and a ragged one), after one training step so that bias
+    and W are not at init.  Checked against the fp64 oracle (gap-guarded) and bit-exactly
+    against the oracle's top-K of the GPU's own forward scores."""
     shape = synth.SHAPES["amazon-670k"]
-    L, m, k, B = shape.L, shape.m, shape.k, shape.B
-    lay = make(L, m, k, B=B, seed=42)
+    L, m, k = shape.L, shape.m, shape.k
+    lay = make(L, m, k, B=max(B, shape.B), seed=42)
     ptr, lid = synth.label_batch(B, L, shape.avg_pos, step=0)
     lay.train_step(tens(synth.hidden_batch(B, m, step=0)), tens(ptr), tens(lid), F32(1e-3))
     h = synth.hidden_batch(B, m, step=3)
-    _, ids = lay.predict_topk(tens(h), 5)
+    sc, ids = lay.predict_topk(tens(h), 5)
+    rs, rid = oracle.topk(lay.forward(tens(h)).cpu().numpy(), 5)            # bit-exact: same fp32 y
+    assert (ids.cpu().numpy() == rid).all() and (sc.cpu().numpy() == rs).all()
     s = state_of(lay)
     y64, Ay = oracle.forward(s["W"], s["idx"], s["bias"], h)
     near = _topk_gap_guarded(ids.cpu().numpy(), y64, Ay, 5)
