@@ -1,6 +1,7 @@
-"""Time the intermediate layer's forward (dropout + tcgen05 3xTF32 GEMM + bias/ReLU) and
-backward + Adam at d = 512, m = 32768, B = 32 (the bench's model config): ms per call over
-200 calls, CUDA events.  FIXEDFANIN_LIB selects a library variant."""
+"""Run the intermediate layer's forward (dropout + dense GEMM + bias/ReLU) and backward + Adam
+at d = 512, B = 32 (the bench's model config) for a given m, 200 times: a target for ncu
+(`gpu__time_duration` per kernel; tools/gpu_dense_var.sh) — the Python loop itself is
+host-bound (~21 us per call), so its event time is not the kernels'.  Usage: m [simt]."""
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -9,17 +10,12 @@ from paper_2306_03725_b200 import layer as L
 
 d, B = 512, 32
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-n = L.DenseLayer(L.DenseConfig(d=d, m=m, max_batch=B, seed=43, dropout=0.1), device="cuda")
+flags = L.FF_FLAG_DENSE_SIMT if "simt" in sys.argv else 0
+n = L.DenseLayer(L.DenseConfig(d=d, m=m, max_batch=B, seed=43, dropout=0.1, flags=flags), device="cuda")
 x = torch.from_numpy(synth.feature_batch(B, d, step=3)).cuda()
 dh = torch.randn(B, m, device="cuda") * 1e-3
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for name, fn in (("forward", lambda s: n.forward(x, step=s, train=True)),):
-    for s in range(10):
-        fn(s)
-    torch.cuda.synchronize()
-    e0.record()
-    for s in range(200):
-        fn(s)
-    e1.record()
-    e1.synchronize()
-    print(f"m={m} {name}: {e0.elapsed_time(e1) / 200 * 1e3:.1f} us per call", flush=True)
+for s in range(200):
+    n.forward(x, step=s + 1, train=True)
+    n.backward_adam(dh, 1e-3)
+torch.cuda.synchronize()
+print(f"m={m} done", flush=True)
