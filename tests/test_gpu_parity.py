@@ -508,6 +508,23 @@ def test_sharded_layers_are_p_invariant(P, dh_mode):
     assert torch.equal(mi, fi) and torch.equal(ms, fs)
 
 
+@pytest.mark.parametrize("P,B", [(2, 64), (3, 100), (8, 300)])
+def test_sharded_predict_is_p_invariant_large_batch(P, B):
+    """Label shards (row_begin > 0) through the per-line ring (B <= 96) and the two-pass wide
+    kernel (B > 96): merged shard top-K == the unsharded top-K, bit for bit."""
+    layer = L_()
+    L, m, k, K = 4001, 512, 32, 8
+    full = make(L, m, k, B=B, seed=19)
+    bounds = [L * r // P for r in range(P + 1)]
+    shards = [make(bounds[r + 1] - bounds[r], m, k, B=B, seed=19, L_global=L, row_begin=bounds[r],
+                   L_local=bounds[r + 1] - bounds[r]) for r in range(P)]
+    h = tens(synth.hidden_batch(B, m, step=6))
+    fs, fi = full.predict_topk(h, K)
+    parts = [s.predict_topk(h, K) for s in shards]
+    ms, mi = layer.merge_topk(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]))
+    assert torch.equal(mi, fi) and torch.equal(ms, fs)
+
+
 # ------------------------------------------------------------------- edge cases
 def test_label_id_out_of_range_reported():
     layer = L_()
