@@ -1183,6 +1183,15 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
   }
 }
 
+// Order-preserving int key of a score (atomicMax on floats of either sign) and its inverse.
+__device__ __forceinline__ int score_key(float f) { const int i = __float_as_int(f); return i >= 0 ? i : i ^ 0x7FFFFFFF; }
+__device__ __forceinline__ float key_score(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+constexpr int kKeyNegInf = (int)0x807FFFFF;                                   // score_key(-inf)
+__global__ void k_fill_i32(int* __restrict__ p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
 // Fused forward + running top-K for the hot configuration (k = 32, B <= 32), pipelined like
 // k_train_ring: the h-line gathers of the next D - 1 rows are in flight (cp.async into a
 // per-warp shared-memory ring) and the state (W, idx, bias) of row X + D is being loaded
@@ -1195,6 +1204,12 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
 #ifndef FF_PRED_RING_THREADS
 #define FF_PRED_RING_THREADS 128
 #endif
+#ifndef FF_PRED_XCH
+#define FF_PRED_XCH 16u             // rows between threshold exchanges (power of 2)
+#endif
+#ifndef FF_PRED_FLUSH_EVERY
+#define FF_PRED_FLUSH_EVERY 4u      // rows between candidate-buffer checks (1, 2, 4 or 8)
+#endif
 constexpr int kPredRingD = FF_PRED_RING_D;
 constexpr int kPredRingThreads = FF_PRED_RING_THREADS;
 constexpr int kPredRingSmem = (kPredRingThreads / 32) * kPredRingD * 8 * 32 * 16;
@@ -1204,7 +1219,8 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
                                                                    const float* __restrict__ hd, int64_t L, int B,
                                                                    int nb, int q2, int64_t row_begin,
                                                                    float* __restrict__ cand_s,
-                                                                   int* __restrict__ cand_i) {
+                                                                   int* __restrict__ cand_i,
+                                                                   int* __restrict__ gthr) {
   constexpr int NG = 8, D = kPredRingD;
   constexpr uint32_t kStage = 8 * 32 * 16;
   const uint32_t kColFloats = pin(64u * (uint32_t)nb);   // hd column stride; this launch scores line q2
@@ -1237,8 +1253,26 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   auto flush = [&]() {
     for (int q = 0; q < ncand; ++q) topk_consider(ts, ti, cbs[q * 32 + lane], cbi[q * 32 + lane]);
     ncand = 0;
-    thr_s = ts[kTopkMax - 1]; thr_i = ti[kTopkMax - 1];
+    if (better(ts[kTopkMax - 1], ti[kTopkMax - 1], thr_s, thr_i)) { thr_s = ts[kTopkMax - 1]; thr_i = ti[kTopkMax - 1]; }
   };
+  // Shared threshold per sample (gthr, an order-preserving int key): every 8 rows a lane
+  // publishes the kTopkMax-th score of its running list and adopts the best one published by
+  // any warp.  That score is the kTopkMax-th of some set of rows, so no row scoring below it
+  // can be in the top K <= kTopkMax: skipping y < it is exact (y == it is kept — its id may
+  // win the tie), and after the first rows almost no row reaches the candidate buffer.
+  int* const gp = gthr + b;
+  // (reading the shared value one exchange ahead, so that the load never stalls, measured
+  // slower: the stale value lets more lanes publish, and the publishes contend on B words)
+  auto exchange = [&]() {
+    if (b < B) {
+      const int g = *(volatile int*)gp;
+      const float own = ts[kTopkMax - 1];
+      if (own != -INFINITY && score_key(own) > g) atomicMax(gp, score_key(own));
+      const float gs = key_score(g);
+      if (gs > thr_s) { thr_s = gs; thr_i = INT_MAX; }
+    }
+  };
+  uint32_t it = 0;
 
   struct St { float w, bj; int c; };
   auto load_st = [&](uint32_t j, St& st) {
@@ -1288,7 +1322,17 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
     // divergent insertion per row); a full buffer in any lane flushes the warp's buffers
     const int jid = (int)(row_begin + j);
     if (b < B && better(y, jid, thr_s, thr_i)) { cbs[ncand * 32 + lane] = y; cbi[ncand * 32 + lane] = jid; ++ncand; }
+#if FF_PRED_FLUSH_EVERY == 1
     if (__any_sync(kFull, ncand == kTopkMax)) flush();
+    if ((++it & (FF_PRED_XCH - 1u)) == 0) exchange();
+#else
+    // checked every FF_PRED_FLUSH_EVERY rows: a lane appends at most one candidate per row, so
+    // a buffer holding more than kTopkMax - FF_PRED_FLUSH_EVERY is flushed before it can overflow
+    if ((++it & (FF_PRED_FLUSH_EVERY - 1u)) == 0) {
+      if (__any_sync(kFull, ncand > kTopkMax - FF_PRED_FLUSH_EVERY)) flush();
+      if ((it & (FF_PRED_XCH - 1u)) == 0) exchange();
+    }
+#endif
     stg = stg + 1 == (uint32_t)D ? 0u : stg + 1;
   }
   cp_async_wait<0>();
@@ -1485,7 +1529,10 @@ constexpr int kMergeThreads = FF_MERGE_THREADS;                  // <= 1024 (war
 __global__ void __launch_bounds__(kMergeThreads) k_merge_topk_block(const float* __restrict__ in_s, const int* __restrict__ in_i,
                                                           int nlist, int64_t list_stride, int64_t sample_stride,
                                                           int Kin, int K, float* __restrict__ out_s,
-                                                          int* __restrict__ out_i) {
+                                                          int* __restrict__ out_i, int* __restrict__ reset_thr) {
+  // the predict path's per-sample shared threshold is re-armed for the next call here (this
+  // kernel runs after every kernel that read it)
+  if (reset_thr != nullptr && threadIdx.x == 0) reset_thr[blockIdx.x] = kKeyNegInf;
   __shared__ float ws_s[kMergeThreads / 32][kTopkMax];
   __shared__ int ws_i[kMergeThreads / 32][kTopkMax];
   const int b = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;

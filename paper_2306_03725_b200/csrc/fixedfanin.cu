@@ -55,7 +55,7 @@ constexpr int kPredRingMaxLines = 3;    // predict: B <= 96 runs the ring kernel
 size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {   // byte offsets into the workspace
-  size_t W, idx, mW, vW, dW, bias, mb, vb, db, posmask, hd, cand_s, cand_i, wl_s, wl_i,
+  size_t W, idx, mW, vW, dW, bias, mb, vb, db, posmask, hd, cand_s, cand_i, pthr, wl_s, wl_i,
       h_stage, lbl_stage, dh_stage, scalars,
       ent, sort_keys2, gT, col_ptr, sort_keys, sort_tmp, sort_tmp_bytes,   // CSC mode only
       total;
@@ -90,6 +90,7 @@ Layout layout_of(const ff_config& c) {
   o.hd = take(8 * m * ldh);         // [m][nb][h 32 | dh 32]
   o.cand_s = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
   o.cand_i = take(4 * (size_t)kMaxCandBlocks * ldh * kTopkMax);
+  o.pthr = take(4 * ldh);                                            // predict ring: shared per-sample thresholds
   if (c.max_batch > 32 && c.k == 32) {                               // wide predict: per-warp top-K lists
     o.wl_s = take(4 * (size_t)kMaxWideWarps * kPredWListFloats);
     o.wl_i = take(4 * (size_t)kMaxWideWarps * kPredWListFloats);
@@ -160,7 +161,7 @@ struct ff_layer {
   Layout lay;
   char* ws;
   float *W, *mW, *vW, *dW, *bias, *mb, *vb, *db, *hd, *cand_s, *h_stage, *dh_stage, *wl_s;
-  int *idx, *cand_i, *wl_i, *lbl_stage, *err;
+  int *idx, *cand_i, *pthr, *wl_i, *lbl_stage, *err;
   int *ent, *col_ptr;               // CSC mode
   float* gT;
   int rs;                           // CSC mode: record stride (floats)
@@ -444,7 +445,8 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
     // (bit-identical scores; below 4 lines the wide kernel would leave lanes idle)
     nlist = l->grid_pred_ring;
     for (int q2 = 0; q2 < nb; ++q2) {
-      void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &nbb, &q2, &rb, &cs, &ci};
+      int* gt = l->pthr;
+      void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &nbb, &q2, &rb, &cs, &ci, &gt};
       FF_CUDA(cudaLaunchKernel((const void*)k_predict_ring, dim3(nlist), dim3(kPredRingThreads), args, kPredRingSmem, st));
       if (q2 + 1 < nb) ++g_launches;
     }
@@ -461,7 +463,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
     void* a1[] = {&W, &idx, &bias, &hd, &z, const_cast<int64_t*>(&r1), &BB, &nbb, &rb, &no_s, &no_i, &Kw, &cs, &ci, &wls, &wli};
     FF_CUDA(cudaLaunchKernel((const void*)k_predict_wide, dim3(g), dim3(kPredWThreads), a1, kPredWSmem, st));
     k_merge_topk_block<<<B, kMergeThreads, 0, st>>>(cs, ci, g, (int64_t)ldh * kTopkMax, kTopkMax, kTopkMax, kTopkMax,
-                                                    ps, pi);
+                                                    ps, pi, nullptr);
     g_launches += 2;
     const float* ts_ = ps; const int* ti_ = pi;
     void* a2[] = {&W, &idx, &bias, &hd, const_cast<int64_t*>(&r1), &Lw, &BB, &nbb, &rb, &ts_, &ti_, &Kw, &cs, &ci, &wls, &wli};
@@ -473,7 +475,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
   }
   ++g_launches;
   k_merge_topk_block<<<B, kMergeThreads, 0, st>>>(l->cand_s, l->cand_i, nlist, (int64_t)ldh * kTopkMax, kTopkMax, kTopkMax, K,
-                                        scores, ids);
+                                                  scores, ids, l->pthr);         // also re-arms the ring's thresholds
   FF_LAUNCHED();
   return FF_OK;
 }
@@ -653,6 +655,7 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->mb = at<float>(ws, lay.mb); l->vb = at<float>(ws, lay.vb); l->db = at<float>(ws, lay.db);
   l->posmask = at<uint32_t>(ws, lay.posmask); l->hd = at<float>(ws, lay.hd);
   l->cand_s = at<float>(ws, lay.cand_s); l->cand_i = at<int>(ws, lay.cand_i);
+  l->pthr = at<int>(ws, lay.pthr);
   l->wl_s = lay.wl_s ? at<float>(ws, lay.wl_s) : nullptr; l->wl_i = lay.wl_i ? at<int>(ws, lay.wl_i) : nullptr;
   l->h_stage = at<float>(ws, lay.h_stage); l->lbl_stage = at<int>(ws, lay.lbl_stage);
   l->dh_stage = at<float>(ws, lay.dh_stage);
@@ -709,6 +712,11 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   // zero everything that must start at zero (moments, masks, dW/db, dhT, scalars)
   e = cudaMemsetAsync(ws, 0, lay.total, st);
   if (e != cudaSuccess) { delete l; return fail(FF_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); }
+  {                                                    // predict thresholds start at score_key(-inf)
+    const int n = 32 * nb_of(c.max_batch);
+    k_fill_i32<<<(n + 255) / 256, 256, 0, st>>>(l->pthr, n, kKeyNegInf);
+    ++g_launches;
+  }
   if (c.L_local > 0) {
     k_init<<<l->grid_rows, 256, 0, st>>>(l->W, l->idx, l->bias, l->mW, l->vW, l->mb, l->vb, c.L_local, c.row_begin,
                                          c.m, c.k, (uint32_t)c.seed, (uint32_t)(c.seed >> 32), c.init_scale);

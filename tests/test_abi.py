@@ -42,7 +42,7 @@ def test_workspace_size_matches_layout_model():
     Lk = 670091 * 32
     state = 5 * 4 * Lk + 4 * 4 * 670091 + 4 * 670091          # W idx mW vW dW, bias mb vb db, posmask
     # hd (h|dh lines), top-K candidates, double-buffered h and label staging + dh staging (host entry point)
-    scratch = 2 * 4 * 32768 * 32 + 2 * 4 * 1024 * 32 * 8 + 3 * 4 * 32 * 32768 + 2 * 4 * (33 + 64 * 32)
+    scratch = 2 * 4 * 32768 * 32 + 2 * 4 * 1024 * 32 * 8 + 4 * 32 + 3 * 4 * 32 * 32768 + 2 * 4 * (33 + 64 * 32)
     assert state <= n <= state + scratch + 32 * 256
     assert n % 256 == 0
 
