@@ -993,6 +993,9 @@ __global__ void k_init(float* __restrict__ W, int* __restrict__ idx, float* __re
 // uniform on [0,m) that are accepted when not in the pre-call row set and not yet accepted;
 // the q-th accepted index goes to the q-th pruned slot in ascending slot order; W = mW =
 // vW = 0 there.
+// K64: k in (32, 64] (a second slot per lane); otherwise k <= 32 and the second half is
+// compiled out (the hot configuration k = 32: ~40% fewer instructions per row).
+template <bool K64>
 __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, float* __restrict__ mW,
                                float* __restrict__ vW, int64_t L, int64_t row_begin, int m, int k,
                                int p, uint32_t step, uint32_t key0, uint32_t key1) {
@@ -1003,8 +1006,8 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t thr = (uint32_t)(0x100000000ull % (uint64_t)m);
   bool act[2];
-#pragma unroll
-  for (int e = 0; e < 2; ++e) act[e] = lane + 32 * e < k;
+  act[0] = lane < k;
+  act[1] = K64 && lane + 32 < k;
   float w_n[2] = {0.0f, 0.0f}; int c_n[2] = {-1, -1};
   auto load = [&](int64_t jj) {
 #pragma unroll
@@ -1013,7 +1016,17 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
   };
   int64_t j = global_warp();
   if (j < L) load(j);
+  // the first Philox block (n = 0) of the warp's next 32 rows, one row per lane: draw words
+  // for row j + i nw come from lane i by shuffle (usually all p draws come from it); further
+  // blocks (n >= 1) are computed by the whole warp when a row needs them
+  U4 pre{0u, 0u, 0u, 0u};
+  int i_pre = 32;
   for (; j < L; j += nw) {
+    if (i_pre == 32) {
+      pre = philox(0u, (uint32_t)(row_begin + j + (int64_t)lane * nw), step, kDomRegrow, key0, key1);
+      i_pre = 0;
+    }
+    const int src_lane = i_pre++;
     int c[2]; uint32_t key[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -1041,7 +1054,13 @@ __global__ void k_redistribute(float* __restrict__ W, int* __restrict__ idx, flo
     // accepted draws: draw q is held by lane q & 31 in register q >> 5 (p <= 63 since p < k <= 64)
     int acc[2] = {-1, -1}, na = 0;
     for (uint32_t n = 0; na < p; ++n) {
-      const U4 v = philox(n, grow, step, kDomRegrow, key0, key1);
+      U4 v;
+      if (n == 0) {
+        v.x = __shfl_sync(kFull, pre.x, src_lane); v.y = __shfl_sync(kFull, pre.y, src_lane);
+        v.z = __shfl_sync(kFull, pre.z, src_lane); v.w = __shfl_sync(kFull, pre.w, src_lane);
+      } else {
+        v = philox(n, grow, step, kDomRegrow, key0, key1);
+      }
 #pragma unroll
       for (int wi = 0; wi < 4; ++wi) {
         if (na < p) {

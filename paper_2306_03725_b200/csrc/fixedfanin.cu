@@ -938,7 +938,7 @@ ff_status fixedfanin_redistribute(ff_layer* l, uint64_t step, ff_stream_t stream
   l->grads_valid = false;
   if (l->cfg.L_local == 0) return FF_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  k_redistribute<<<l->grid_rows, 256, 0, st>>>(l->W, l->idx, l->mW, l->vW, l->cfg.L_local, l->cfg.row_begin, l->cfg.m,
+  (l->cfg.k > 32 ? k_redistribute<true> : k_redistribute<false>)<<<l->grid_rows, 256, 0, st>>>(l->W, l->idx, l->mW, l->vW, l->cfg.L_local, l->cfg.row_begin, l->cfg.m,
                                                l->cfg.k, p, (uint32_t)step, (uint32_t)l->cfg.seed,
                                                (uint32_t)(l->cfg.seed >> 32));
   FF_LAUNCHED();
