@@ -478,7 +478,7 @@ def test_predict_topk_ties_resolved_by_lower_id_wide(B):
 
 
 @DH
-@pytest.mark.parametrize("P", [2, 3, 8])
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
 def test_sharded_layers_are_p_invariant(P, dh_mode):
     """Virtual sharding on one GPU: P handles with row offsets reproduce the unsharded
     state, scores and (after merge) top-K bit-exactly (rows are independent)."""
