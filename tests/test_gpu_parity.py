@@ -395,6 +395,67 @@ def test_redistribution_bit_exact(L, m, k, frac, step):
     assert all(len(set(r)) == k for r in s["idx"])
 
 
+@pytest.mark.parametrize("k,frac", [(16, 0.1), (32, 0.1), (32, 0.25)])
+def test_hundred_train_redistribute_cycles(k, frac):
+    """SPEC acceptance criterion 3 on the GPU: 100 interleaved train / redistribute
+    cycles.  Every redistribution is checked in lockstep against the oracle's on the GPU's
+    pre-call state (bit-exact W, idx, moments), and afterwards every row still has k distinct
+    in-range indices, the regrown slots have zero weight and moments, the untouched slots are
+    bitwise unchanged, and the pruned slots were the row's p smallest (|W|, slot) keys (R9)."""
+    L, m, B = 300, 256, 16
+    lay = make(L, m, k, B=B, seed=23, prune_frac=frac)
+    p = int(np.floor(F32(frac) * k))
+    for cyc in range(100):
+        h = synth.hidden_batch(B, m, step=cyc)
+        ptr, ids = synth.label_batch(B, L, 5.0, step=cyc)
+        lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-2))
+        s0 = state_of(lay)
+        lay.redistribute(1000 * (cyc + 1))
+        s1 = state_of(lay)
+        W2, idx2, m2, v2 = oracle.redistribute(s0["W"], s0["idx"], s0["mW"], s0["vW"], m, p, seed=23,
+                                               step=1000 * (cyc + 1))
+        assert (s1["idx"] == idx2).all() and (s1["W"] == W2).all(), cyc
+        assert (s1["mW"] == m2).all() and (s1["vW"] == v2).all(), cyc
+        changed = s1["idx"] != s0["idx"]
+        assert (changed.sum(axis=1) == p).all(), cyc                          # exactly p regrown per row
+        assert ((s1["idx"] >= 0) & (s1["idx"] < m)).all()
+        assert all(len(set(r)) == k for r in s1["idx"])                       # k distinct
+        assert (s1["W"][changed] == 0).all() and (s1["mW"][changed] == 0).all() and (s1["vW"][changed] == 0).all()
+        keep = ~changed
+        assert (s1["W"][keep].view(np.uint32) == s0["W"][keep].view(np.uint32)).all()   # survivors untouched
+        for j in range(0, L, 7):                                              # sort-oracle check of the pruned set
+            keys = sorted(range(k), key=lambda i: (np.float32(abs(s0["W"][j, i])), i))
+            assert set(np.nonzero(changed[j])[0]) == set(keys[:p]), (cyc, j)
+        # freshness (R10): a regrown index was not in the row before the call
+        for j in range(0, L, 11):
+            assert not (set(s1["idx"][j][changed[j]]) & set(s0["idx"][j])), (cyc, j)
+
+
+def test_column_independence():
+    """changing one label row's weights and indices changes that label's scores only
+    (bit-exact for every other label), in the forward and in the fused step's state."""
+    L, m, k, B = 2000, 512, 32, 32
+    a = make(L, m, k, B=B, seed=31)
+    b = make(L, m, k, B=B, seed=31)
+    s = state_of(b)
+    j0 = 777
+    W, idx = s["W"].copy(), s["idx"].copy()
+    W[j0] = -W[j0] * np.float32(1.5)
+    idx[j0] = np.random.default_rng(3).choice(m, size=k, replace=False).astype(np.int32)
+    b.set_params(W=tens(W), idx=tens(idx))
+    h = tens(synth.hidden_batch(B, m, step=1))
+    ya, yb = a.forward(h).cpu().numpy(), b.forward(h).cpu().numpy()
+    other = np.arange(L) != j0
+    assert (ya[:, other].view(np.uint32) == yb[:, other].view(np.uint32)).all()
+    assert (ya[:, j0] != yb[:, j0]).any()
+    ptr, ids = synth.label_batch(B, L, 5.0, step=1)
+    a.train_step(h, tens(ptr), tens(ids), F32(1e-3))
+    b.train_step(h, tens(ptr), tens(ids), F32(1e-3))
+    sa, sb = state_of(a), state_of(b)
+    for key in ("W", "mW", "vW", "bias", "mb", "vb"):
+        assert (sa[key][other] == sb[key][other]).all(), key
+
+
 @pytest.mark.parametrize("k", [16, 32, 48])
 def test_redistribution_all_ties(k):
     """Rows whose |W| are all equal (incl. +-0): the p lowest slots are pruned (R9)."""

@@ -319,6 +319,23 @@ def test_redistribution_invariants_vs_sort(L, m, k, p):
     _check_redistribution(W, idx, mW, vW, W2, idx2, m2, v2, m, p)
 
 
+def test_hundred_train_redistribute_cycles_keep_the_invariants():
+    """SPEC acceptance criterion 3 on the oracle: 100 interleaved train / prune-and-
+    regrow cycles on a random model; after every cycle each row has k distinct in-range
+    indices, regrown slots have zero weight and moments, survivors are untouched and dominate
+    the pruned slots in |W| (the sort-oracle check)."""
+    L, m, k, B = 60, 48, 8, 4
+    p = 2
+    st = oracle.State.create(L, m, k, seed=7)
+    for cyc in range(100):
+        h = synth.hidden_batch(B, m, step=cyc)
+        ptr, ids = synth.label_batch(B, L, 2.0, step=cyc)
+        oracle.train_step(st, h, ptr, ids, 1.0 / B, 1e-2)
+        W, idx, mW, vW = st.W.copy(), st.idx.copy(), st.mW.copy(), st.vW.copy()
+        st.W, st.idx, st.mW, st.vW = oracle.redistribute(W, idx, mW, vW, m, p, seed=7, step=1000 * (cyc + 1))
+        _check_redistribution(W, idx, mW, vW, st.W, st.idx, st.mW, st.vW, m, p)
+
+
 def test_redistribution_all_equal_prunes_lowest_slots_and_single_zero():
     W = np.ones((4, 8)); W[1] = -1; W[2, 5] = 0.0   # row 2: the single zero-magnitude entry (S:216)
     idx = np.tile(np.arange(8, dtype=np.int32), (4, 1))
