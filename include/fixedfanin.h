@@ -195,7 +195,9 @@ ff_status fixedfanin_redistribute(ff_layer* layer, uint64_t step, ff_stream_t st
 
 /* Top-K prediction: per instance the K labels of this shard with the largest
  * scores, ordered by (score desc, global id asc) (R15).  scores [B][K] float,
- * ids [B][K] int32 GLOBAL ids.  1 <= K <= min(max_topk, L_local).                      */
+ * ids [B][K] int32 GLOBAL ids.  1 <= K <= min(max_topk, L_local).  A NaN score never
+ * enters the top K; with FF_FLAG_CHECK_FINITE a non-finite score raises FF_ERR_NONFINITE
+ * at the next fixedfanin_check.                                                         */
 ff_status fixedfanin_predict_topk(ff_layer* layer, const float* h, int32_t B, int32_t K,
                                   float* scores, int32_t* ids, ff_stream_t stream);
 

@@ -1145,7 +1145,8 @@ template <int NG, bool FULL>
 __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict__ W, const int* __restrict__ idx,
                                                          const float* __restrict__ bias, const float* __restrict__ hd,
                                                          int64_t L, int k, int B, int nb, int64_t row_begin,
-                                                         float* __restrict__ cand_s, int* __restrict__ cand_i) {
+                                                         float* __restrict__ cand_s, int* __restrict__ cand_i,
+                                                         int* __restrict__ err) {
   __shared__ float ss[kRowThreads / 32][32][kTopkMax];
   __shared__ int si[kRowThreads / 32][32][kTopkMax];
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7, wid = threadIdx.x >> 5;
@@ -1185,6 +1186,7 @@ __global__ void __launch_bounds__(kRowThreads) k_predict(const float* __restrict
       row_spread_k<NG, KPL>(w, c, gq, ws, cs);
       row_gather<NG, FULL>(hb, cs, cfl, k, gq, pol_l, hv);
       const float y = row_score_own<NG>(ws, hv, gq, bj);
+      if (err != nullptr && b < B && !isfinite(y)) atomicOr(err, kErrNonFinite);   // FF_FLAG_CHECK_FINITE (R15)
       if (b < B) topk_consider(ts, ti, y, (int)(row_begin + j));
     }
 #pragma unroll
@@ -1232,6 +1234,7 @@ __global__ void k_fill_i32(int* __restrict__ p, int n, int v) {
 constexpr int kPredRingD = FF_PRED_RING_D;
 constexpr int kPredRingThreads = FF_PRED_RING_THREADS;
 constexpr int kPredRingSmem = (kPredRingThreads / 32) * kPredRingD * 8 * 32 * 16;
+template <bool CHECK>                                    // FF_FLAG_CHECK_FINITE: report non-finite scores
 __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* __restrict__ W,
                                                                    const int* __restrict__ idx,
                                                                    const float* __restrict__ bias,
@@ -1239,7 +1242,7 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
                                                                    int nb, int q2, int64_t row_begin,
                                                                    float* __restrict__ cand_s,
                                                                    int* __restrict__ cand_i,
-                                                                   int* __restrict__ gthr) {
+                                                                   int* __restrict__ gthr, int* __restrict__ err) {
   constexpr int NG = 8, D = kPredRingD;
   constexpr uint32_t kStage = 8 * 32 * 16;
   const uint32_t kColFloats = pin(64u * (uint32_t)nb);   // hd column stride; this launch scores line q2
@@ -1340,6 +1343,7 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
     // candidates better than the lane's current K-th best are appended to its buffer (no
     // divergent insertion per row); a full buffer in any lane flushes the warp's buffers
     const int jid = (int)(row_begin + j);
+    if (CHECK && b < B && !isfinite(y)) atomicOr(err, kErrNonFinite);              // FF_FLAG_CHECK_FINITE (R15)
     if (b < B && better(y, jid, thr_s, thr_i)) { cbs[ncand * 32 + lane] = y; cbi[ncand * 32 + lane] = jid; ++ncand; }
 #if FF_PRED_FLUSH_EVERY == 1
     if (__any_sync(kFull, ncand == kTopkMax)) flush();
@@ -1405,7 +1409,8 @@ __global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __r
                                                                 const float* __restrict__ thr_s_in,
                                                                 const int* __restrict__ thr_i_in, int K,
                                                                 float* __restrict__ cand_s, int* __restrict__ cand_i,
-                                                                float* __restrict__ wl_s, int* __restrict__ wl_i) {
+                                                                float* __restrict__ wl_s, int* __restrict__ wl_i,
+                                                                int* __restrict__ err) {
   constexpr int BC = 128, NW = kPredWThreads / 32, D = kPredWD;
   extern __shared__ __align__(16) unsigned char wide_smem[];
   float* const lst_s = wl_s + (int64_t)blockIdx.x * NW * kPredWListFloats;     // this block's [NW][kTopkMax][BC]
@@ -1487,6 +1492,7 @@ __global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __r
       for (int e = 0; e < 4; ++e) {
         auto el = [&](const float2& v) { return (e & 1) ? v.y : v.x; };
         const float y = ((el(P[0][e >> 1]) + el(P[2][e >> 1])) + (el(P[1][e >> 1]) + el(P[3][e >> 1]))) + bj;
+        if (err != nullptr && ok && sb + e < B && !isfinite(y)) atomicOr(err, kErrNonFinite);   // (R15)
         if (ok && sb + e < B && better(y, jid, thr_s[e], thr_i[e])) {
           const int s = s0 + e;
           int r = kTopkMax - 1;

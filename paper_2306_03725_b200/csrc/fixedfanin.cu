@@ -439,6 +439,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
   const float* W = l->W; const int* idx = l->idx; const float* bias = l->bias; const float* hd = l->hd;
   int64_t L = l->cfg.L_local, rb = l->cfg.row_begin; int k = l->cfg.k, BB = B, nbb = nb;
   float* cs = l->cand_s; int* ci = l->cand_i;
+  int* perr = (l->cfg.flags & FF_FLAG_CHECK_FINITE) ? l->err : nullptr;     // NaN/inf scores reported (R15)
   int nlist = l->grid_pred;
   if (k == 32 && (nb == 1 || (nb <= kPredRingMaxLines && !(l->cfg.flags & FF_FLAG_NO_PIPE)))) {
     // hot configuration (B <= 32), and B <= 96: the pipelined kernel once per 32-sample line
@@ -446,8 +447,9 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
     nlist = l->grid_pred_ring;
     for (int q2 = 0; q2 < nb; ++q2) {
       int* gt = l->pthr;
-      void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &nbb, &q2, &rb, &cs, &ci, &gt};
-      FF_CUDA(cudaLaunchKernel((const void*)k_predict_ring, dim3(nlist), dim3(kPredRingThreads), args, kPredRingSmem, st));
+      void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &nbb, &q2, &rb, &cs, &ci, &gt, &perr};
+      FF_CUDA(cudaLaunchKernel(perr ? (const void*)k_predict_ring<true> : (const void*)k_predict_ring<false>, dim3(nlist),
+                               dim3(kPredRingThreads), args, kPredRingSmem, st));
       if (q2 + 1 < nb) ++g_launches;
     }
   } else if (k == 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE)) {   // large batch: chunked wide kernel (bit-identical)
@@ -460,17 +462,17 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
     const float* no_s = nullptr; const int* no_i = nullptr;
     int64_t z = 0, Lw = L;
     int Kw = K;
-    void* a1[] = {&W, &idx, &bias, &hd, &z, const_cast<int64_t*>(&r1), &BB, &nbb, &rb, &no_s, &no_i, &Kw, &cs, &ci, &wls, &wli};
+    void* a1[] = {&W, &idx, &bias, &hd, &z, const_cast<int64_t*>(&r1), &BB, &nbb, &rb, &no_s, &no_i, &Kw, &cs, &ci, &wls, &wli, &perr};
     FF_CUDA(cudaLaunchKernel((const void*)k_predict_wide, dim3(g), dim3(kPredWThreads), a1, kPredWSmem, st));
     k_merge_topk_block<<<B, kMergeThreads, 0, st>>>(cs, ci, g, (int64_t)ldh * kTopkMax, kTopkMax, kTopkMax, kTopkMax,
                                                     ps, pi, nullptr);
     g_launches += 2;
     const float* ts_ = ps; const int* ti_ = pi;
-    void* a2[] = {&W, &idx, &bias, &hd, const_cast<int64_t*>(&r1), &Lw, &BB, &nbb, &rb, &ts_, &ti_, &Kw, &cs, &ci, &wls, &wli};
+    void* a2[] = {&W, &idx, &bias, &hd, const_cast<int64_t*>(&r1), &Lw, &BB, &nbb, &rb, &ts_, &ti_, &Kw, &cs, &ci, &wls, &wli, &perr};
     FF_CUDA(cudaLaunchKernel((const void*)k_predict_wide, dim3(g), dim3(kPredWThreads), a2, kPredWSmem, st));
     nlist = g + 1;
   } else {
-    void* args[] = {&W, &idx, &bias, &hd, &L, &k, &BB, &nbb, &rb, &cs, &ci};
+    void* args[] = {&W, &idx, &bias, &hd, &L, &k, &BB, &nbb, &rb, &cs, &ci, &perr};
     FF_CUDA(cudaLaunchKernel(predict_kernel(l->cfg.k), dim3(l->grid_pred), dim3(kRowThreads), args, 0, st));
   }
   ++g_launches;
@@ -694,13 +696,15 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
     l->ntiles = (int)std::max<int64_t>(1, (c.L_local + l->tile_rows - 1) / l->tile_rows);
   }
   l->grid_pred = std::min(kMaxCandBlocks, occupancy_grid(predict_kernel(c.k), l->nsm, kRowThreads));
-  if (cudaFuncSetAttribute((const void*)k_predict_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, kPredRingSmem) !=
-      cudaSuccess) {
+  if (cudaFuncSetAttribute((const void*)k_predict_ring<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kPredRingSmem) != cudaSuccess ||
+      cudaFuncSetAttribute((const void*)k_predict_ring<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kPredRingSmem) != cudaSuccess) {
     delete l;
     return fail(FF_ERR_CUDA, "pipelined predict smem attribute");
   }
   l->grid_pred_ring =
-      std::min(kMaxCandBlocks, occupancy_grid((const void*)k_predict_ring, l->nsm, kPredRingThreads, kPredRingSmem));
+      std::min(kMaxCandBlocks, occupancy_grid((const void*)k_predict_ring<false>, l->nsm, kPredRingThreads, kPredRingSmem));
   if (cudaFuncSetAttribute((const void*)k_predict_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kPredWSmem) !=
       cudaSuccess) {
     delete l;

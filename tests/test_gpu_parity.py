@@ -1135,6 +1135,28 @@ def test_check_finite_reports_nonfinite_scores(dh_mode, k, B, bad):
     assert e.value.status == layer.FF_ERR_NONFINITE
 
 
+@pytest.mark.parametrize("B", [32, 64, 300])
+def test_check_finite_reports_nonfinite_predict_scores(B):
+    """R15 / SURVEY c.2 #15: with FF_FLAG_CHECK_FINITE a NaN score seen by the predict kernels
+    (ring, per-line ring, wide) raises FF_ERR_NONFINITE at the next check(); the NaN label never
+    enters the top K, and without the flag nothing is reported."""
+    layer = L_()
+    L, m, k = 3000, 256, 32
+    flagged = make(L, m, k, B=B, seed=4, flags=layer.FF_FLAG_CHECK_FINITE)
+    plain = make(L, m, k, B=B, seed=4)
+    bias = np.zeros(L, np.float32); bias[1234] = np.nan
+    for lay in (flagged, plain):
+        lay.set_params(bias=tens(bias))
+    h = tens(synth.hidden_batch(B, m, step=2))
+    _, ids = flagged.predict_topk(h, 5)
+    with pytest.raises(layer.FFError) as e:
+        flagged.check()
+    assert e.value.status == layer.FF_ERR_NONFINITE
+    assert not (ids.cpu().numpy() == 1234).any()
+    plain.predict_topk(h, 5)
+    plain.check()
+
+
 # ------------------------------------------- redistribution with more than 32 pruned slots
 @pytest.mark.parametrize("L,m,k,frac", [(500, 4096, 64, 0.6), (300, 200, 64, 0.99), (400, 1000, 48, 0.8)])
 def test_redistribution_more_than_32_pruned_slots(L, m, k, frac):
