@@ -777,12 +777,15 @@ def test_csc_dh_is_deterministic_and_matches_atomic():
     assert dh_close(d1, d3)
 
 
-@pytest.mark.parametrize("shape_name,dh_modes", [("wiki10-31k", (0,)), ("wiki-500k", (0,)), ("amazon-670k", (1, 0, 2)),
-                                                  ("amazon-3m", (1, 0)), ("amazon-670k-k64-m65k", (0, 1))])
-def test_full_size_sampled_parity(shape_name, dh_modes):
+@pytest.mark.parametrize("shape_name,dh_modes,loss", [("wiki10-31k", (0,), "bce"), ("wiki-500k", (0,), "bce"),
+                                                       ("amazon-670k", (1, 0, 2), "bce"), ("amazon-3m", (1, 0), "bce"),
+                                                       ("amazon-670k-k64-m65k", (0, 1), "bce"),
+                                                       ("amazon-670k", (0, 1), "sqh")])
+def test_full_size_sampled_parity(shape_name, dh_modes, loss):
     """BASELINE.json's shapes in the bench's launch configuration: one fused step checked on
     sampled label rows (y, dW, db, W') and on the full dh (the oracle's Alg. 2 over every
-    connection), lockstep (R20)."""
+    connection), lockstep (R20); the squared hinge (the paper's loss, with its exact-zero
+    skips) at Amazon-670K as well, its margin decisions taken on the kernel's y."""
     layer = L_()
     shape = synth.SHAPES[shape_name]
     L, m, k, B = shape.L, shape.m, shape.k, shape.B
@@ -791,7 +794,7 @@ def test_full_size_sampled_parity(shape_name, dh_modes):
     rng = np.random.default_rng(5)
     rows = np.sort(rng.choice(L, 256, replace=False))
     for dh_mode in dh_modes:
-        lay = make(L, m, k, B=B, seed=42, flags=layer.FF_FLAG_STORE_GRADS, dh_mode=dh_mode)
+        lay = make(L, m, k, B=B, seed=42, flags=layer.FF_FLAG_STORE_GRADS, dh_mode=dh_mode, loss=loss_id(loss))
         s0 = state_of(lay)
         y = lay.forward(tens(h)).cpu().numpy().astype(np.float64)
         dh, _ = lay.train_step(tens(h), tens(ptr), tens(ids), F32(1e-3))
@@ -799,7 +802,7 @@ def test_full_size_sampled_parity(shape_name, dh_modes):
         s1 = state_of(lay)
         yr, Ay = oracle.forward(s0["W"][rows], s0["idx"][rows], s0["bias"][rows], h)
         assert_close(y[:, rows], yr, Ay, "y rows")
-        g, _ = oracle.bce_grad(y, ptr, ids, F32(1.0 / B))
+        g, _ = oracle.loss_grad(loss, y, ptr, ids, F32(1.0 / B))
         dWr, AdW, dbr, Adb = oracle.weight_grad(s0["idx"][rows], h, g[:, rows])
         assert_close(dW[rows], dWr, AdW, "dW rows")
         assert_close(db[rows], dbr, Adb, "db rows")
