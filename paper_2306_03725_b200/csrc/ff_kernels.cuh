@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
           if (gnz && c < split) red_add4(col_line(hb, c, kColFloats) + 32, dh_contrib(ws[q], g4), pol_l);
         }
       }
-    } else {
+    } else if (!sqh || gany) {                           // (squared hinge: an all-zero row reduces nothing)
       const bool gnz = (g4.x != 0.0f) | (g4.y != 0.0f) | (g4.z != 0.0f) | (g4.w != 0.0f);
 #pragma unroll
       for (int q = 0; q < NG; ++q) {
@@ -624,8 +624,14 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
         if (gnz) red_add4(col_line(hb, c, kColFloats) + 32, dh_contrib(ws[q], g4), pol_l);
       }
     }
-    const float gW = row_dw_slot<NG>(dwp, lane);
-    const float dbr = row_db_chunk(g4);
+    // implicit negative mining (squared hinge): a row whose gradient is exactly zero
+    // for every sample has dW = db = 0 — the transpose-reduce is skipped (warp-uniform branch;
+    // the same values up to the sign of zero, which Adam does not see)
+    float gW = 0.0f, dbr = 0.0f;
+    if (!sqh || gany) {
+      gW = row_dw_slot<NG>(dwp, lane);
+      dbr = row_db_chunk(g4);
+    }
     if (lane == i) db_v = dbr;
     const uint32_t row = j * 32u + lane;
     if (STORE_GRADS) a.dW[row] = gW;
