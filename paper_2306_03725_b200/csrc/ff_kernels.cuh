@@ -445,9 +445,19 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 #ifndef FF_ATOM_RING_MINB
 #define FF_ATOM_RING_MINB 4
 #endif
+#ifndef FF_SQH_RING_D
+#define FF_SQH_RING_D 2
+#endif
+#ifndef FF_SQH_RING_MINB
+#define FF_SQH_RING_MINB 5
+#endif
+// MODE 3 = atomic dh with the squared hinge: the same code as MODE 0, tuned separately — with
+// most reductions skipped the kernel is latency-bound and prefers 2 stages at 5 CTAs/SM
+// (0.250 vs 0.265 ms at 100% skips), where the BCE step, bound by the reductions, does not care.
 template <int MODE> struct RingCfg {
-  static constexpr int D = MODE == 1 ? FF_CSC_RING_D : FF_ATOM_RING_D;                 // ring stages per warp
-  static constexpr int kMinBlocks = MODE == 1 ? FF_CSC_RING_MINB : FF_ATOM_RING_MINB;  // CTAs per SM (registers)
+  static constexpr int D = MODE == 1 ? FF_CSC_RING_D : MODE == 3 ? FF_SQH_RING_D : FF_ATOM_RING_D;  // stages per warp
+  static constexpr int kMinBlocks = MODE == 1 ? FF_CSC_RING_MINB : MODE == 3 ? FF_SQH_RING_MINB
+                                                                              : FF_ATOM_RING_MINB;  // CTAs per SM
 };
 constexpr int kRingThreads = 128;
 constexpr int kRingStageBytes = 8 * 32 * 16;            // 8 registers x 32 lanes x 16 B = 32 h lines
@@ -478,7 +488,7 @@ template <bool STORE_GRADS, int MODE>
 __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_train_ring(RowArgs a) {
   const AdamArgs adam = step_adam(a);
   constexpr int NG = 8, D = RingCfg<MODE>::D;
-  constexpr bool CSC = MODE != 0, HYB = MODE == 2;
+  constexpr bool CSC = MODE == 1 || MODE == 2, HYB = MODE == 2;
   constexpr uint32_t kColFloats = 64;                   // hd column stride at nb = 1 (h | dh lines)
   extern __shared__ __align__(16) unsigned char ring_smem[];
   const int lane = pin((int)(threadIdx.x & 31)), gq = pin(lane >> 3), bq = pin(lane & 7);

@@ -192,7 +192,9 @@ struct ff_layer {
 
 namespace {
 
-int ring_mode(const ff_layer* l) { return !l->csc ? 0 : l->split > 0 ? 2 : 1; }
+int ring_mode(const ff_layer* l) {
+  return !l->csc ? (l->cfg.loss == FF_LOSS_SQH ? 3 : 0) : l->split > 0 ? 2 : 1;
+}
 
 template <typename T>
 T* at(char* base, size_t off) { return reinterpret_cast<T*>(base + off); }
@@ -280,12 +282,14 @@ const void* predict_kernel(int k) {
 // ring kernel MODE: 0 atomic, 1 CSC, 2 hybrid
 int ring_mode(const ff_layer* l);
 const void* ring_kernel(bool sg, int mode) {
-  if (sg) return mode == 2 ? (const void*)k_train_ring<true, 2> : mode == 1 ? (const void*)k_train_ring<true, 1>
-                                                                           : (const void*)k_train_ring<true, 0>;
-  return mode == 2 ? (const void*)k_train_ring<false, 2> : mode == 1 ? (const void*)k_train_ring<false, 1>
-                                                                     : (const void*)k_train_ring<false, 0>;
+  if (sg) return mode == 3 ? (const void*)k_train_ring<true, 3> : mode == 2 ? (const void*)k_train_ring<true, 2>
+               : mode == 1 ? (const void*)k_train_ring<true, 1> : (const void*)k_train_ring<true, 0>;
+  return mode == 3 ? (const void*)k_train_ring<false, 3> : mode == 2 ? (const void*)k_train_ring<false, 2>
+       : mode == 1 ? (const void*)k_train_ring<false, 1> : (const void*)k_train_ring<false, 0>;
 }
-int ring_smem_of(int mode) { return mode == 2 ? ring_smem<2>() : mode == 1 ? ring_smem<1>() : ring_smem<0>(); }
+int ring_smem_of(int mode) {
+  return mode == 3 ? ring_smem<3>() : mode == 2 ? ring_smem<2>() : mode == 1 ? ring_smem<1>() : ring_smem<0>();
+}
 
 ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads = kRowThreads, int smem = 0) {
   void* args[] = {&a};
@@ -682,7 +686,7 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k, l->csc), l->nsm, kRowThreads);
   l->grid_csc = occupancy_grid((const void*)k_dh_csc<true, false>, l->nsm, 256);
   for (int sg = 0; sg < 2; ++sg)
-    for (int cs = 0; cs < 3; ++cs)
+    for (int cs = 0; cs < 4; ++cs)
       if (cudaFuncSetAttribute(ring_kernel(sg, cs), cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem_of(cs)) !=
           cudaSuccess) {
         delete l;
