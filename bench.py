@@ -246,6 +246,41 @@ def run_reference(a, shape, world, rank):
 # ----------------------------------------------------------------------------- NEXT-2
 
 
+def run_sqh(shape, dev, stream, e0, e1, h_dev, ptr_dev, ids_dev, margin=3.0, steps=300):
+    """the paper's squared-hinge loss with implicit negative mining
+     on the same batches, the label biases set to -margin so that almost every
+    (sample, label) gradient is exactly zero (engineered margins, SURVEY d.1); samples/s and
+    the fraction of exact-zero gradients on the first batch."""
+    import torch
+    from paper_2306_03725_b200 import synth
+    from paper_2306_03725_b200.layer import FixedFanInLayer, LayerConfig, FF_LOSS_SQH
+    B = shape.B
+    lay = FixedFanInLayer(LayerConfig(L_global=shape.L, m=shape.m, k=shape.k, max_batch=B, seed=synth.PARAM_SEED,
+                                      loss=FF_LOSS_SQH), device=dev)
+    lay.set_params(bias=torch.full((shape.L,), -margin, dtype=torch.float32, device=dev))
+    y = lay.forward(h_dev[0])
+    t = -torch.ones_like(y)
+    p_, i_ = ptr_dev[0].cpu().numpy(), ids_dev[0].cpu().numpy()
+    for b in range(B):
+        t[b, torch.from_numpy(i_[p_[b]:p_[b + 1]].astype(np.int64)).to(dev)] = 1.0
+    skip = float(((t * y) >= 1.0).float().mean().item())
+    del y, t
+    dh = torch.empty((B, shape.m), device=dev)
+    n = len(h_dev)
+    for s in range(20):
+        lay.train_step(h_dev[s % n], ptr_dev[s % n], ids_dev[s % n], LR, dh=dh)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for s in range(steps):
+        lay.train_step(h_dev[s % n], ptr_dev[s % n], ids_dev[s % n], LR, dh=dh)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del lay
+    return {"loss": "squared hinge (P:526-529)", "margin_bias": margin, "grad_skip_fraction": skip,
+            "value": B / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms, "steps": steps}
+
+
 def run_model(eng, shape, dev, stream, e0, e1, d=512, dropout=0.1, steps=100):
     """the whole proposed architecture (Fig. 2): 512-d Slice-like features
      -> 10% input dropout -> dense Wd -> ReLU -> the fixed fan-in layer, one
@@ -571,7 +606,7 @@ def run_ours(a, shape, world, rank, local_rank):
         del g
 
     # ---- NEXT-3: large-batch inference and shortlist scoring, one GPU
-    big = model = None
+    big = model = sqh = None
     if world == 1:
         from paper_2306_03725_b200.layer import FixedFanInLayer, LayerConfig
         BI, NCAND = 1024, 100
@@ -601,6 +636,8 @@ def run_ours(a, shape, world, rank, local_rank):
                "shortlist_ms_per_batch": res["shortlist"]}
         del inf
         model = run_model(eng, shape, dev, stream, e0, e1)
+        if a.loss == "bce" and not a.train_only:
+            sqh = run_sqh(shape, dev, stream, e0, e1, h_dev, ptr_dev, ids_dev)
 
     if rank != 0:
         return
@@ -693,6 +730,7 @@ def run_ours(a, shape, world, rank, local_rank):
         "cuda_graph": graph,
         "inference_large_batch": big,
         "model": model if world == 1 else None,
+        "sqh": (dict(sqh, ratio_to_bce_step=sqh["ms_per_step"] / (ms / a.steps)) if sqh else None),
     }
     # NEXT-4 memory report: this layer's device bytes vs the dense/COO formats of P:37-45
     Lk = shape.L * shape.k
