@@ -1416,7 +1416,10 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
 #endif
 constexpr int kPredWThreads = FF_PREDW_THREADS, kPredWD = FF_PREDW_D;
 constexpr int kPredWStage = 8 * 32 * 16;                                     // 8 connections x 512 B
-constexpr int kPredWSmem = (kPredWThreads / 32) * kPredWD * kPredWStage;
+#ifndef FF_PREDW_XPOSE
+#define FF_PREDW_XPOSE 1
+#endif
+constexpr int kPredWSmem = (kPredWThreads / 32) * (kPredWD * kPredWStage + (FF_PREDW_XPOSE ? 3 * 128 : 0));
 constexpr int kPredWListFloats = kTopkMax * 128;                             // per warp, per array
 __global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __restrict__ W, const int* __restrict__ idx,
                                                                 const float* __restrict__ bias,
@@ -1460,6 +1463,33 @@ __global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __r
     }
     // issue side: group (ji, gi) of the flat (row, group) sequence; ci = that row's idx lane
     uint32_t ji = j0; int gi = 0;
+#if FF_PREDW_XPOSE
+    // a row's indices / weights are handed to the lanes through shared memory, transposed so
+    // that group g's eight slots g + 4q are one 32-B run ([g][q]): two broadcast LDS.128 per
+    // group instead of eight shuffles.  Index rows alternate between two buffers by row parity.
+    const uint32_t xp0 = (uint32_t)__cvta_generic_to_shared(wide_smem) + (uint32_t)(NW * D * kPredWStage) +
+                         (uint32_t)(wid * 3 * 128);                 // cbuf[2][32] | wbuf[32] (ints/floats)
+    const uint32_t xslot = (uint32_t)(((lane & 3) * 8 + (lane >> 2)) * 4);
+    uint32_t ipar = 0;                                              // parity of row ji's index buffer
+    auto sts32 = [](uint32_t a, uint32_t v) { asm volatile("st.shared.b32 [%0], %1;" :: "r"(a), "r"(v) : "memory"); };
+    auto lds4u = [](uint32_t a) { uint4 v; asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory"); return v; };
+    if (ji < nrows) sts32(xp0 + xslot, (uint32_t)ld_na_ro(idx + ji * 32u + lane));
+    int ci_n = ji + nwarp < nrows ? ld_na_ro(idx + (ji + nwarp) * 32u + lane) : 0;
+    __syncwarp();
+    auto issue = [&](uint32_t stg) {
+      if (ji < nrows) {
+        const uint32_t dst = ring0 + stg * (uint32_t)kPredWStage;
+        const uint32_t cb = xp0 + ipar * 128u + (uint32_t)gi * 32u;
+        const uint4 c0 = lds4u(cb), c1 = lds4u(cb + 16u);
+        const uint32_t cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (ok) cp_async16(dst + (uint32_t)q * 512u, col_line(hb, cc[q], cfl));   // lines >= nb: not gathered
+      }
+      cp_async_commit();
+      if (++gi == 4) { gi = 0; ji += nwarp; ipar ^= 1u; }
+    };
+#else
     int ci = ji < nrows ? ld_na_ro(idx + ji * 32u + lane) : 0;
     int ci_n = ji + nwarp < nrows ? ld_na_ro(idx + (ji + nwarp) * 32u + lane) : 0;
     auto issue = [&](uint32_t stg) {
@@ -1477,6 +1507,7 @@ __global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __r
         ci_n = ji + nwarp < nrows ? ld_na_ro(idx + (ji + nwarp) * 32u + lane) : 0;
       }
     };
+#endif
 #pragma unroll
     for (int d = 0; d < D - 1; ++d) issue((uint32_t)d);
     uint32_t stg = 0;
@@ -1485,6 +1516,14 @@ __global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __r
     for (uint32_t j = j0; j < nrows; j += nwarp) {
       const float wl = w_n, bj = b_n;
       if (j + nwarp < nrows) { w_n = ld_na(W + (j + nwarp) * 32u + lane); b_n = ld_na(bias + j + nwarp); }
+#if FF_PREDW_XPOSE
+      // this row's weights, and the next row's indices (issued during this row's last group)
+      __syncwarp();                                        // the previous row's reads are done
+      sts32(xp0 + 256u + xslot, __float_as_uint(wl));
+      sts32(xp0 + (ipar ^ 1u) * 128u + xslot, (uint32_t)ci_n);   // (the issue side is on row j here, D <= 4)
+      ci_n = j + 2u * nwarp < nrows ? ld_na_ro(idx + (j + 2u * nwarp) * 32u + lane) : 0;
+      __syncwarp();
+#endif
       float2 P[4][2];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -1492,10 +1531,18 @@ __global__ void __launch_bounds__(kPredWThreads) k_predict_wide(const float* __r
         cp_async_wait<D - 1>();                               // this group's lines have landed
         const uint32_t src = ring0 + stg * (uint32_t)kPredWStage;
         float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+#if FF_PREDW_XPOSE
+        const uint4 w0 = lds4u(xp0 + 256u + (uint32_t)g * 32u), w1 = lds4u(xp0 + 256u + (uint32_t)g * 32u + 16u);
+        const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#endif
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float4 hv = lds4(src + (uint32_t)q * 512u);
+#if FF_PREDW_XPOSE
+          const float w = __uint_as_float(wv[q]);
+#else
           const float w = __shfl_sync(kFull, wl, 4 * q + g);
+#endif
           if (q & 1) { b0 = ffma2(bc2(w), lo2(hv), b0); b1 = ffma2(bc2(w), hi2(hv), b1); }
           else       { a0 = ffma2(bc2(w), lo2(hv), a0); a1 = ffma2(bc2(w), hi2(hv), a1); }
         }
