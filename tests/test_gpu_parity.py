@@ -527,6 +527,22 @@ def test_predict_topk_ties_resolved_by_lower_id_pipelined():
     assert (ids.cpu().numpy() == np.array([5, 17, 100, 2500, 4999, 0, 1, 2])).all()
 
 
+def test_predict_shared_thresholds_rearm_between_calls():
+    """The ring kernel's shared per-sample thresholds are re-armed by each call's merge: calls
+    with different batches and inputs in any order (B = 64, 16, 64 on other data, 300 on the
+    wide path) give exactly the top-K of a fresh layer."""
+    L, m, k, K = 6000, 512, 32, 5
+    lay = make(L, m, k, B=300, seed=27)
+    for B, step in ((64, 1), (16, 2), (64, 3), (300, 4), (32, 1)):
+        h = tens(synth.hidden_batch(B, m, step=step))
+        fresh = make(L, m, k, B=300, seed=27)
+        s1, i1 = lay.predict_topk(h, K)
+        s2, i2 = fresh.predict_topk(h, K)
+        assert torch.equal(i1, i2) and torch.equal(s1, s2), (B, step)
+        rs, rid = oracle.topk(lay.forward(h).cpu().numpy(), K)
+        assert (i1.cpu().numpy() == rid).all(), (B, step)
+
+
 @pytest.mark.parametrize("B", [70, 300])
 def test_predict_topk_ties_resolved_by_lower_id_wide(B):
     L, m, k = 5000, 64, 32                 # k = 32, B > 32: k_predict_wide + block merge
