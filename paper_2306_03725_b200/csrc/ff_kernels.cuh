@@ -687,6 +687,9 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
 // each 32-entry batch and samples 4bq..4bq+3 (one 16-B slice of the 128-B g line).
 // SKIPZ (squared hinge): a zero weight (a row whose gradient is all zero) skips the gather;
 // the weight is then loaded before the gathers instead of beside them.
+#ifndef FF_CSC_PLAIN
+#define FF_CSC_PLAIN 1            // g-line gathers without the L2 policy operand (1% faster CSC step)
+#endif
 template <bool NB1, bool SKIPZ>
 __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr, const int* __restrict__ ent,
                                                 const float* __restrict__ gT, int rs, int m, int nb_rt, int tile,
@@ -715,7 +718,11 @@ __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr,
       const uint32_t grow = (uint32_t)__shfl_sync(kFull, (int)rec, 4 * u + gq);
       gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       const bool live = !tail || p + 4 * u + gq < pend;
+#if FF_CSC_PLAIN
+      if (live && (!SKIPZ || ww[u] != 0.0f)) gv[u] = ld_line4_plain(col_line(gb, grow, rsu));
+#else
       if (live && (!SKIPZ || ww[u] != 0.0f)) gv[u] = ld_line4(col_line(gb, grow, rsu), pol_l);
+#endif
     }
     if (!SKIPZ) {
       // issued after the gathers: the weight load and the gathers are in flight together
