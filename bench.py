@@ -697,6 +697,14 @@ def run_ours(a, shape, world, rank, local_rank):
                      "kernel_share_of_step": k_step_ms / (ms / a.steps),
                      "timing": f"CUDA events around each launch on the launching stream, every {PROF_EVERY}th timed step "
                                f"({n_prof} of {a.steps * max(1, a.repeats)} over {max(1, a.repeats)} windows)"},
+        # SURVEY §8(d).2's third ceiling: FP32 issue.  3 B L k FMAs per step (forward, dW, dh
+        # contributions) in the row kernel against 148 SMs x 128 FP32 lanes x the max SM clock
+        # (FFMA2 issues two lanes' worth per instruction; nominal ~74 TFLOP/s)
+        "fp32": {"fma_per_step": 3.0 * B * L_local * shape.k,
+                 "kernel_tfma_s": 3.0 * B * L_local * shape.k / (k_step_ms * 1e-3) / 1e12,
+                 "peak_tfma_s": 148 * 128 * 1.965e9 / 1e12,
+                 "frac": 3.0 * B * L_local * shape.k / (k_step_ms * 1e-3) / (148 * 128 * 1.965e9),
+                 "peak_source": "derived: 148 SMs x 128 FP32 FMA lanes x 1965 MHz"},
         "onchip": {"l2_bytes_per_step": onchip, "l2_gbs": onchip / (ms / a.steps * 1e-3) / 1e9,
                    "kernel_gbs": onchip / (k_step_ms * 1e-3) / 1e9,
                    "ceiling_gbs": ONCHIP_CEILING_GBS.get(a.dh_mode),
