@@ -306,15 +306,27 @@ def run_model(eng, shape, dev, stream, e0, e1, d=512, dropout=0.1, steps=100):
     h = torch.empty((B, shape.m), device=dev)
     dh = torch.from_numpy(synth.hidden_batch(B, shape.m, step=5) * np.float32(1e-3)).to(dev)
     res = {}
-    for name, fn in (("fwd", lambda: dn.forward(xs[0], step=1, train=True, h=h)),
-                     ("bwd", lambda: (dn.forward(xs[0], step=1, train=True, h=h), dn.backward_adam(dh, LR)))):
-        fn()
-        e0.record(stream)
-        for _ in range(20):
+    # the dense kernels alone, timed as CUDA-graph replays of 20 calls (a Python loop of these
+    # calls is host-bound at ~20 us per call, longer than the forward itself)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for name, fn in (("fwd", lambda: dn.forward(xs[0], step=1, train=True, h=h)),
+                         ("bwd", lambda: (dn.forward(xs[0], step=1, train=True, h=h), dn.backward_adam(dh, LR)))):
             fn()
-        e1.record(stream)
-        e1.synchronize()
-        res[name] = e0.elapsed_time(e1) / 20
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(20):
+                    fn()
+            g.replay()
+            e0.record(side)
+            for _ in range(5):
+                g.replay()
+            e1.record(side)
+            e1.synchronize()
+            res[name] = e0.elapsed_time(e1) / 100
+            del g
+    torch.cuda.current_stream().wait_stream(side)
     res["bwd"] -= res["fwd"]
     peak, peak_src = peaks()
     bwd_bytes = 24 * d * shape.m + 8 * d * 32 + 8 * shape.m * 32 + 4 * B * shape.m
@@ -328,8 +340,10 @@ def run_model(eng, shape, dev, stream, e0, e1, d=512, dropout=0.1, steps=100):
                           "achieved_gbs": fwd_bytes / (res["fwd"] * 1e-3) / 1e9, "peak_gbs": peak,
                           "frac": fwd_bytes / (res["fwd"] * 1e-3) / 1e9 / peak,
                           "tflops_3xtf32": 3 * fwd_flops / (res["fwd"] * 1e-3) / 1e12,
-                          "note": "dropout kernel + tcgen05 kind::tf32 3xTF32 GEMM (M = 128 columns, N = 32 samples) + "
-                                  "bias/ReLU epilogue from TMEM; bytes = read Wd + write the h|dh lines"},
+                          "note": "CUDA-graph replay: dropout kernel + k_dense_fwd_tma (TMA-fed tcgen05 kind::tf32 3xTF32, "
+                                  "M = 128 columns, N = 64 [x_hi | x_lo] + N = 32, bias/ReLU epilogue from TMEM); "
+                                  "bytes = read Wd + write the h|dh lines; bound by shared-memory bandwidth "
+                                  "(DESIGN.md 6c)"},
             "dense_bwd_adam": {"ms": res["bwd"], "bound": "hbm", "alg_bytes": bwd_bytes,
                                "achieved_gbs": bwd_bytes / (res["bwd"] * 1e-3) / 1e9, "peak_gbs": peak,
                                "peak_source": peak_src, "frac": bwd_bytes / (res["bwd"] * 1e-3) / 1e9 / peak,

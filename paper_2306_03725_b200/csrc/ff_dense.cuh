@@ -16,6 +16,8 @@
 //       the paper's B = 32 the layer is a 32-row GEMM whose backward + Adam is bound by
 //       streaming Wd and its moments (24 B per weight), not by FMAs.
 #pragma once
+#include <cuda.h>   // CUtensorMap
+#include <cstdio>
 #include "ff_device.cuh"
 #include "ff_kernels.cuh"   // cp.async helpers
 
@@ -38,9 +40,11 @@ __device__ __forceinline__ void st_na4(float* a, float4 v) {
 // Input dropout (reading R25): xT[f][b] = x[b][f] * scale if word f of the
 // Philox stream (ctr = (f/4, b, step, 3), key = seed) has (u >> 8) * 2^-24 >= p, else 0.
 // train = 0: xT = x (inference, no dropout).  Samples B..ldx-1 are 0.  Thread per (b, f/4).
+// xTlo (tensor-core forward, may be NULL): xT - (xT with the 13 low mantissa bits cleared),
+// the exact lo part of the 3xTF32 split (k_dense_fwd_tma).
 __global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, float p, float scale, int train,
                             uint32_t step, uint32_t key0, uint32_t key1, float* __restrict__ xT,
-                            const int64_t* __restrict__ t_auto) {
+                            const int64_t* __restrict__ t_auto, float* __restrict__ xTlo) {
   // t_auto (FF_STEP_AUTO): the step key is the dense layer's device counter + 1, i.e. the
   // Adam step this forward belongs to (read before k_prep / k_step_t advance it)
   if (t_auto != nullptr) step = (uint32_t)(*t_auto + 1);
@@ -65,6 +69,7 @@ __global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, 
         }
       }
       xT[(int64_t)f * ldx + b] = val;
+      if (xTlo != nullptr) xTlo[(int64_t)f * ldx + b] = val - __uint_as_float(__float_as_uint(val) & 0xFFFFE000u);
     }
   }
 }
@@ -243,46 +248,71 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
 }
 
 // ------------------------------------------------------------------ tensor-core forward
-// The same forward on the 5th-generation tensor cores (tcgen05, kind::tf32) for B <= 32:
-// per CTA D[128 columns][32 samples] (fp32, in TMEM) += A[128][8] . B[8][32] per 8-feature
-// block, A = Wd^T (the 128-column tile) and B = xT, both K-major in shared memory (no
-// swizzle: 8-row x 16-B core matrices; tools/microbench/tcprobe.cu checks the layout) —
-// fp32 accuracy from 3xTF32: a = a_hi + a_lo exactly with a_hi = a truncated to tf32, and
-// a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (the dropped a_lo.b_lo and the tf32 truncation of
-// the lo parts are <= ~2^-20 relative).  Warp-specialised: each of the 256 producer threads
-// converts its share of a 32-feature stage (loaded into registers one stage ahead; 2 CTAs per
-// SM) into the hi/lo tiles of one of two shared-memory buffers and arrives on the buffer's
-// "full" mbarrier; lane 0 of warp 8 waits on it, issues the 3 x 4 MMAs of the stage and
-// commits them to the buffer's "empty" mbarrier, which lets the producers refill it.  Epilogue: warps 0-3 read their
-// 32 TMEM lanes (= columns) x 32 columns (= samples) with tcgen05.ld, add the bias, apply
-// ReLU and write the h|dh lines.  Summation order differs from the SIMT kernel (tensor-core
-// internal), within the R19 tolerance.
-#ifndef FF_TC_FCH
-#define FF_TC_FCH 32
+// The forward on the 5th-generation tensor cores (tcgen05, kind::tf32) for B <= 32, fed by
+// TMA: per 128-column tile D[128 columns][32 samples] (fp32, in TMEM) = sum over 8-feature
+// blocks of A[128][8] . B[8][32], A = Wd^T and B = xT read in place from their HBM layouts:
+// both are MN-major (the tile's 128 columns, resp. the 32 samples, contiguous per feature),
+// which kind::tf32 accepts only in the 128-B swizzle with 32-B atoms (descriptor layout 1,
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; tools/microbench/tcprobe_mn.cu pins LBO = 4096 B
+// between 32-column groups and SBO = 512 B between 4-feature groups).
+// fp32 accuracy from 3xTF32: a = a_hi + a_lo exactly, a_hi = a with the 13 low mantissa bits
+// cleared; a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (the dropped a_lo.b_lo and the tf32
+// truncation of the lo parts are <= ~2^-20 relative).  The tensor core itself truncates fp32
+// operands to tf32 (tcprobe_mn: 1 + 3*2^-12 -> 1), so the raw TMA tiles ARE the hi operands;
+// A's lo tile is computed per stage (elementwise, at the same swizzled offsets) and xT's lo
+// once per forward by k_dropout_T.  Per 8-feature block two MMAs: A_hi . [x_hi | x_lo] (one
+// N = 64 MMA: x_lo is the next 32-sample atom) and A_lo . x_hi (N = 32), into separate TMEM
+// columns that the epilogue sums in a fixed order.  tools/microbench/tcrate.cu: an M = 128
+// MMA costs max(67, N / 2) cycles, so this is ~134 cycles per block (vs ~200 for three N = 32
+// MMAs).
+// Persistent, one CTA per SM over the column tiles, warp-specialised, no CTA barrier in the
+// loop: warp 0 = TMA producer into a ring of kTmStages stages (A raw 16 KB + x hi/lo 8 KB,
+// plus the stage's 16-KB A-lo slot); warps 2-5 = lo converters; warp 1 = MMA issuer (8 MMAs
+// per 32-feature stage, commit -> the stage's "empty" barrier); warps 6-9 = epilogue from one
+// of two TMEM accumulator sets (the next tile's MMAs run while a tile's epilogue drains):
+// bias, ReLU, h|dh lines through a per-warp shared-memory transpose (4 full 128-B lines per
+// store instruction) and h_out.  Each column's result depends only on its own Wd column and
+// xT, so column shards are bit-identical to the unsharded layer.
+// What bounds it (profiles/r02_dense_fwd_tma.txt): shared-memory bandwidth —
+// per stage the TMA writes 24 KB, the converters read 16 and write 16 KB, the MMAs read 44 KB
+// (~100 KB at 128 B/clock = ~780 cycles; a clock64 trace of block 0 shows ~830 per stage).
+// Split raw/lo rings, two MMA-issuing warps and L2 prefetch ahead of the ring were measured
+// slower.
+#ifndef FF_TM_STAGES
+#define FF_TM_STAGES 5
 #endif
-constexpr int kTcThreads = 256, kTcFch = FF_TC_FCH;                // features per stage
-constexpr int kTcAbytes = kTcFch * 128 * 4, kTcBbytes = kTcFch * 32 * 4;          // 32 KB, 8 KB
-constexpr int kTcBuf = 2 * kTcAbytes + 2 * kTcBbytes;                              // hi/lo A, hi/lo B: 80 KB
-constexpr int kTcSmem = 2 * kTcBuf + 1024 + 64;                                    // 2 buffers + align + barriers
-constexpr int kTcAu = kTcFch / 8, kTcBu = kTcFch / 32;       // 16-B chunks per thread per stage (A, B)
-static_assert(kTcFch % 32 == 0 && kTcFch <= 64, "tcgen05 forward stage size");
+constexpr int kTmStages = FF_TM_STAGES;
+constexpr int kTmThreads = 320;                                  // 10 warps
+constexpr uint32_t kTmA = 16384, kTmX = 4096;                    // A tile (32 f x 128 c), x tile (32 f x 32 b)
+constexpr uint32_t kTmStage = 2 * kTmA + 2 * kTmX;              // A raw | A lo | x hi | x lo = 40 KB
+constexpr uint32_t kTmTx = kTmA + 2 * kTmX;                      // TMA bytes per stage
+constexpr uint32_t kTmEpi = 4 * 32 * 33 * 4;                     // epilogue transpose buffers
+constexpr uint32_t kTmTileCols = 96;                             // TMEM columns per tile: [hi.hi | hi.lo] + lo.hi
+constexpr uint32_t kTmAlloc = 256;                               // two tile accumulator sets
+constexpr int kTmSmem = 1024 + kTmStages * kTmStage + kTmEpi + 256;
 
-// shared-memory matrix descriptor, K-major, no swizzle: LBO = byte distance between the two
-// 4-element K halves of an 8-K MMA step, SBO = byte distance between 8-row groups
-__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// shared-memory matrix descriptor (sm_100): start, LBO, SBO (16-B units), version 1, layout
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;                                         // version (sm_100); layout 0 = no swizzle
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
   return d;
 }
-// kind::tf32, D f32, A/B tf32 K-major, M = 128, N = 32
-constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// kind::tf32, D f32, A and B tf32 MN-major (bits 15, 16), M = 128, N = n
+__host__ __device__ constexpr uint32_t tm_idesc(uint32_t n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+template <uint32_t N>
 __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-               :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
+               :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(tm_idesc(N)), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t mbar, uint32_t parity) {
   uint32_t ok;
@@ -291,31 +321,57 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t mbar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) { while (!mbar_try_wait(mbar, parity)) {} }
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               :: "r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t mbar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(mbar) : "memory");
+}
 
-__global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float* __restrict__ Wd, const float* __restrict__ bd,
-                                                                 const float* __restrict__ xT, int d, int m, int ldx,
-                                                                 int B, float* __restrict__ hd, int cstride, int zero_dh,
+#ifdef FF_TM_TRACE
+__device__ long long g_tm_trace[5][96];   // block 0: TMA issue, landed, MMAs issued, -, slot free
+#define TM_TR(r, i) do { if (blockIdx.x == 0 && (i) < 96) g_tm_trace[r][i] = clock64(); } while (0)
+#else
+#define TM_TR(r, i) do { } while (0)
+#endif
+
+// mW: Wd as a 3-D tensor {128 columns, d features, tiles} (box 32 x 32 x 1); mX / mXl: xT and
+// its lo part {32 samples, d} (box 32 x 32).  Out-of-range features (d % 32 != 0) read as 0.
+__global__ void __launch_bounds__(kTmThreads, 1) k_dense_fwd_tma(const __grid_constant__ CUtensorMap mW,
+                                                                 const __grid_constant__ CUtensorMap mX,
+                                                                 const __grid_constant__ CUtensorMap mXl,
+                                                                 const float* __restrict__ bd, int d, int m, int B,
+                                                                 float* __restrict__ hd, int cstride, int zero_dh,
                                                                  float* __restrict__ h_out) {
-  // warp-specialised: warps 0-7 produce the operand tiles, warp 8 issues the MMAs; per buffer
-  // a "full" mbarrier (256 producer arrivals) and an "empty" one (the MMAs' tcgen05.commit),
-  // so no CTA-wide barrier sits in the stage loop
-  extern __shared__ __align__(16) unsigned char tsm[];      // aligned up to 1024 B below (kTcSmem has the slack)
+  extern __shared__ __align__(16) unsigned char tsm[];
   const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(tsm) + 1023u) & ~1023u;
-  const uint32_t mbar0 = sbase + 2 * kTcBuf;                      // empty[0], empty[1]
-  const uint32_t full0 = mbar0 + 16, tptr_s = mbar0 + 32;         // full[0], full[1]; TMEM address
+  const uint32_t epi0 = sbase + kTmStages * kTmStage;
+  const uint32_t bar0 = epi0 + kTmEpi;                            // full[S] | conv[S] | empty[S] | tfull[2] | tempty[2] | tmem
+  auto full = [&](uint32_t s) { return bar0 + 8u * s; };
+  auto conv = [&](uint32_t s) { return bar0 + 8u * (kTmStages + s); };
+  auto empty = [&](uint32_t s) { return bar0 + 8u * (2 * kTmStages + s); };
+  const uint32_t tfull0 = bar0 + 8u * (3 * kTmStages), tempty0 = tfull0 + 16, tptr_s = tempty0 + 16;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int ct = blockIdx.x * 128;
-  const int nst = (d + kTcFch - 1) / kTcFch;
-  if (w == 0) {                                                   // TMEM: 32 columns (N = 32 fp32)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" :: "r"(tptr_s) : "memory");
+  const int ntiles = (m + 127) / 128, nst = (d + 31) / 32;
+  if (w == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(tptr_s), "n"(kTmAlloc) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar0) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar0 + 8) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(full0), "r"(kTcThreads) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(full0 + 8), "r"(kTcThreads) : "memory");
+    for (uint32_t s = 0; s < (uint32_t)kTmStages; ++s) { mbar_init(full(s), 1); mbar_init(conv(s), 4); mbar_init(empty(s), 1); }
+    mbar_init(tfull0, 1); mbar_init(tfull0 + 8, 1); mbar_init(tempty0, 4); mbar_init(tempty0 + 8, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mX) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mXl) : "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -323,144 +379,146 @@ __global__ void __launch_bounds__(kTcThreads + 32, 2) k_dense_fwd_tc(const float
   uint32_t tmem_d;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(tmem_d) : "r"(tptr_s) : "memory");
 
-  if (w == kTcThreads / 32) {                                     // ===== MMA issuer
+  if (w == 0) {                                                   // ===== TMA producer
     if (lane == 0) {
-      for (int st = 0; st < nst; ++st) {
-        const int b = st & 1;
-        const uint32_t buf = sbase + (uint32_t)b * kTcBuf;
-        const uint32_t A_hi = buf, A_lo = buf + kTcAbytes, B_hi = buf + 2 * kTcAbytes, B_lo = B_hi + kTcBbytes;
-        mbar_wait(full0 + 8u * b, (uint32_t)((st >> 1) & 1));     // the producers filled buffer b
+      uint32_t i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int st = 0; st < nst; ++st, ++i) {
+          const uint32_t s = i % kTmStages;
+          if (i >= (uint32_t)kTmStages) { mbar_wait(empty(s), ((i / kTmStages) - 1) & 1u); TM_TR(4, i - kTmStages); }
+          TM_TR(0, i);
+          const uint32_t stg = sbase + s * kTmStage;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(full(s)), "r"(kTmTx) : "memory");
+#pragma unroll
+          for (int g = 0; g < 4; ++g) tma_load_3d(stg + (uint32_t)g * 4096u, &mW, 32 * g, 32 * st, t, full(s));
+          tma_load_2d(stg + 2 * kTmA, &mX, 0, 32 * st, full(s));
+          tma_load_2d(stg + 2 * kTmA + kTmX, &mXl, 0, 32 * st, full(s));
+        }
+    }
+  } else if (w == 1) {                                            // ===== MMA issuer
+    if (lane == 0) {
+      uint32_t i = 0;
+      int tl = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        const int acc = tl & 1;
+        if (tl >= 2) mbar_wait(tempty0 + 8u * acc, (uint32_t)(((tl >> 1) - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int nkb = min(kTcFch / 8, (d - st * kTcFch + 7) / 8);
-        for (int kb = 0; kb < nkb; ++kb) {
-          const uint64_t ah = umma_desc_kmajor(A_hi + kb * 4096, 2048, 128), al = umma_desc_kmajor(A_lo + kb * 4096, 2048, 128);
-          const uint64_t bh = umma_desc_kmajor(B_hi + kb * 1024, 512, 128), bl = umma_desc_kmajor(B_lo + kb * 1024, 512, 128);
-          tc_mma_tf32(tmem_d, ah, bh, (st > 0 || kb > 0) ? 1u : 0u);
-          tc_mma_tf32(tmem_d, ah, bl, 1u);
-          tc_mma_tf32(tmem_d, al, bh, 1u);
+        const uint32_t dhh = tmem_d + kTmTileCols * (uint32_t)acc, dlh = dhh + 64;
+        for (int st = 0; st < nst; ++st, ++i) {
+          const uint32_t s = i % kTmStages, par = (i / kTmStages) & 1u;
+          const uint32_t Ah = sbase + s * kTmStage, Al = Ah + kTmA, Xh = Ah + 2 * kTmA;
+          mbar_wait(full(s), par);
+          mbar_wait(conv(s), par);
+          TM_TR(2, i);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {                        // 8 features = two 4-row groups = 1 KB
+            const uint64_t xh = umma_desc(Xh + kb * 1024u, 4096, 512, 1);
+            const uint32_t accu = (st > 0 || kb > 0) ? 1u : 0u;
+            tc_mma_tf32<64>(dhh, umma_desc(Ah + kb * 1024u, 4096, 512, 1), xh, accu);   // [hi.hi | hi.lo]
+            tc_mma_tf32<32>(dlh, umma_desc(Al + kb * 1024u, 4096, 512, 1), xh, accu);   // lo.hi
+          }
+          tc_commit(empty(s));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                     :: "r"(mbar0 + 8u * b) : "memory");
+        tc_commit(tfull0 + 8u * acc);
       }
     }
-  } else {                                                        // ===== producers
-    // this thread's share of a stage: (column, 4 features) quads of Wd^T and (sample,
-    // 4 features) quads of xT — K-major 16-B chunks, read as 4 coalesced scalar loads each
-    // two register sets: while stage st is converted from one, the loads of stage st + 1 are
-    // landing in the other; the set just converted is refilled with stage st + 2
-    float4 wr0[kTcAu], xr0[kTcBu], wr1[kTcAu], xr1[kTcBu];
-    // thread tid owns column c = tid % 128 of A (K quads kq = 2u + tid / 128) and sample
-    // tid % 32 of B (K quads 8u + tid / 32): per stage, loads at fixed strides from two bases
-    static_assert(kTcThreads % 128 == 0, "column ownership");
-    const float* const wcol = Wd + (int64_t)blockIdx.x * d * 128 + (tid & 127) + (int64_t)(4 * (tid >> 7)) * 128;
-    const float* const xcol = xT + (tid & 31) + (int64_t)(4 * (tid >> 5)) * ldx;
-    auto load_stage = [&](int st, float4 (&wr)[kTcAu], float4 (&xr)[kTcBu]) {
-      const int f0 = st * kTcFch;
-      const float* wp = wcol + (int64_t)f0 * 128;
-      const float* xp = xcol + (int64_t)f0 * ldx;
-      if (f0 + kTcFch <= d) {                                     // full stage: unguarded
+  } else if (w < 6) {                                             // ===== A lo converters (128 threads)
+    const uint32_t ct = (uint32_t)(tid - 64) * 16u;
+    uint32_t i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int st = 0; st < nst; ++st, ++i) {
+        const uint32_t s = i % kTmStages;
+        mbar_wait(full(s), (i / kTmStages) & 1u);
+        if (ct == 0) TM_TR(1, i);
+        const uint32_t raw = sbase + s * kTmStage + ct;
 #pragma unroll
-        for (int u = 0; u < kTcAu; ++u)
-          wr[u] = make_float4(wp[(8 * u + 0) * 128], wp[(8 * u + 1) * 128], wp[(8 * u + 2) * 128], wp[(8 * u + 3) * 128]);
-#pragma unroll
-        for (int u = 0; u < kTcBu; ++u) {
-          const float* q = xp + (int64_t)(32 * u) * ldx;
-          xr[u] = make_float4(q[0], q[ldx], q[2 * ldx], q[3 * ldx]);
+        for (int j = 0; j < 8; ++j) {
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(raw + j * 2048u));
+          const float l0 = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          const float l1 = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          const float l2 = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          const float l3 = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(raw + kTmA + j * 2048u), "f"(l0), "f"(l1), "f"(l2), "f"(l3) : "memory");
         }
-      } else {
-#pragma unroll
-        for (int u = 0; u < kTcAu; ++u) {
-          const int fb = f0 + 8 * u + 4 * (tid >> 7);
-          float t[4];
-#pragma unroll
-          for (int i2 = 0; i2 < 4; ++i2) t[i2] = fb + i2 < d ? wp[(8 * u + i2) * 128] : 0.0f;
-          wr[u] = make_float4(t[0], t[1], t[2], t[3]);
-        }
-#pragma unroll
-        for (int u = 0; u < kTcBu; ++u) {
-          const int fb = f0 + 32 * u + 4 * (tid >> 5);
-          float t[4];
-#pragma unroll
-          for (int i2 = 0; i2 < 4; ++i2) t[i2] = fb + i2 < d ? xp[(int64_t)(32 * u + i2) * ldx] : 0.0f;
-          xr[u] = make_float4(t[0], t[1], t[2], t[3]);
-        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy stores -> tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(conv(s));
       }
-    };
-    auto split_store = [&](uint32_t hi_addr, uint32_t lo_addr, float4 v) {
-      // hi = a with the 13 low mantissa bits cleared (exactly a tf32 value; one LOP3), lo = a - hi
-      // exactly; the tensor core truncates lo to tf32 (<= 2^-21 |a|), a_lo.b_lo is dropped (<= 2^-20)
-      const uint32_t h0 = __float_as_uint(v.x) & 0xFFFFE000u, h1 = __float_as_uint(v.y) & 0xFFFFE000u;
-      const uint32_t h2 = __float_as_uint(v.z) & 0xFFFFE000u, h3 = __float_as_uint(v.w) & 0xFFFFE000u;
-      const float l0 = v.x - __uint_as_float(h0), l1 = v.y - __uint_as_float(h1);
-      const float l2 = v.z - __uint_as_float(h2), l3 = v.w - __uint_as_float(h3);
-      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(hi_addr), "r"(h0), "r"(h1), "r"(h2), "r"(h3) : "memory");
-      asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(lo_addr), "f"(l0), "f"(l1), "f"(l2), "f"(l3) : "memory");
-    };
-    auto produce = [&](int st, float4 (&wr)[kTcAu], float4 (&xr)[kTcBu]) {
-      const int b = st & 1;
-      const uint32_t buf = sbase + (uint32_t)b * kTcBuf;
-      const uint32_t A_hi = buf, A_lo = buf + kTcAbytes, B_hi = buf + 2 * kTcAbytes, B_lo = B_hi + kTcBbytes;
-      if (st >= 2) mbar_wait(mbar0 + 8u * b, (uint32_t)(((st - 2) >> 1) & 1));   // MMAs of stage st-2 done
-      // K-major core matrices: A chunk (column c, K quad kq) at kq*2048 + c*16 (SBO 128 B per
-      // 8 columns, LBO 2048 B per K quad); B chunk (sample b, kq) at kq*512 + b*16
+  } else {                                                        // ===== epilogue (TMEM lane quarter w % 4)
+    const int q = w & 3;
+    const uint32_t ebuf = epi0 + (uint32_t)(w - 6) * (32u * 33u * 4u);
+    int tl = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+      const int acc = tl & 1;
+      mbar_wait(tfull0 + 8u * acc, (uint32_t)((tl >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float z[32];
+#pragma unroll 1
+      for (uint32_t sl = 0; sl < kTmTileCols / 32; ++sl) {         // hi.hi + hi.lo + lo.hi, in that order
+        uint32_t v[32];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                       "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                       "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                       "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                     : "r"(tmem_d + ((uint32_t)(32 * q) << 16) + kTmTileCols * (uint32_t)acc + 32u * sl));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int u = 0; u < kTcAu; ++u) {
-        const int e = u * kTcThreads + tid, c = e & 127, kq = e >> 7;
-        const uint32_t off = (uint32_t)(kq * 2048 + c * 16);
-        split_store(A_hi + off, A_lo + off, wr[u]);
+        for (int s2 = 0; s2 < 32; ++s2) z[s2] = sl == 0 ? __uint_as_float(v[s2]) : z[s2] + __uint_as_float(v[s2]);
       }
-#pragma unroll
-      for (int u = 0; u < kTcBu; ++u) {
-        const int e = u * kTcThreads + tid, bb = e & 31, kq = e >> 5;
-        const uint32_t off = (uint32_t)(kq * 512 + bb * 16);
-        split_store(B_hi + off, B_lo + off, xr[u]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy stores -> tensor core
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(full0 + 8u * b) : "memory");
-      if (st + 2 < nst) load_stage(st + 2, wr, xr);                  // refill this set: two stages in flight
-    };
-    load_stage(0, wr0, xr0);
-    if (nst > 1) load_stage(1, wr1, xr1);
-    for (int st = 0; st < nst; st += 2) {
-      produce(st, wr0, xr0);
-      if (st + 1 < nst) produce(st + 1, wr1, xr1);
-    }
-  }
-  mbar_wait(mbar0 + 8u * ((nst - 1) & 1), (uint32_t)(((nst - 1) >> 1) & 1));      // all MMAs done
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (w < 4) {
-    uint32_t v[32];
-    const uint32_t taddr = tmem_d + ((uint32_t)(32 * w) << 16);
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-                   "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-                   "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int c = ct + 32 * w + lane;                              // TMEM lane = column
-    if (c < m) {
-      const float bj = bd[c];
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8u * acc);             // this accumulator set may be overwritten
+      const int cbase = t * 128 + 32 * q, c = cbase + lane;       // TMEM lane = column
+      const float bj = c < m ? bd[c] : 0.0f;
       float h[32];
 #pragma unroll
-      for (int s2 = 0; s2 < 32; ++s2) h[s2] = s2 < B ? fmaxf(__uint_as_float(v[s2]) + bj, 0.0f) : 0.0f;
-      float* line = hd + (int64_t)c * cstride;
-#pragma unroll
-      for (int s4 = 0; s4 < 32; s4 += 4) {
-        *reinterpret_cast<float4*>(line + s4) = make_float4(h[s4], h[s4 + 1], h[s4 + 2], h[s4 + 3]);
-        if (zero_dh) *reinterpret_cast<float4*>(line + 32 + s4) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      if (h_out != nullptr) {
+      for (int s2 = 0; s2 < 32; ++s2) h[s2] = s2 < B ? fmaxf(z[s2] + bj, 0.0f) : 0.0f;
+      if (h_out != nullptr && c < m) {
 #pragma unroll
         for (int s2 = 0; s2 < 32; ++s2)
           if (s2 < B) h_out[(int64_t)s2 * m + c] = h[s2];
       }
+      // transpose through shared memory: row = column (lane), 33-float pitch (conflict-free)
+#pragma unroll
+      for (int s2 = 0; s2 < 32; ++s2)
+        asm volatile("st.shared.f32 [%0], %1;" :: "r"(ebuf + (uint32_t)(lane * 33 + s2) * 4u), "f"(h[s2]) : "memory");
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {                               // 4 lines per instruction, 8 lanes per line
+        const int li = 4 * r + (lane >> 3), sg = lane & 7;
+        float4 o;
+        const uint32_t a = ebuf + (uint32_t)(li * 33 + 4 * sg) * 4u;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o.x) : "r"(a) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o.y) : "r"(a + 4) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o.z) : "r"(a + 8) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o.w) : "r"(a + 12) : "memory");
+        const int cl = cbase + li;
+        if (cl < m) {
+          float* line = hd + (int64_t)cl * cstride + 4 * sg;
+          *reinterpret_cast<float4*>(line) = o;
+          if (zero_dh) *reinterpret_cast<float4*>(line + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      __syncwarp();                                               // ebuf is rewritten by the next tile
     }
   }
+#ifdef FF_TM_TRACE
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) {
+    const long long t0 = g_tm_trace[0][0];
+    const int n = min(96, nst * ((ntiles - 1) / (int)gridDim.x + 1));
+    for (int i = 0; i < n; ++i)
+      printf("TMTRACE %d issue %lld landed %lld mma %lld free %lld\n", i, g_tm_trace[0][i] - t0,
+             g_tm_trace[1][i] - t0, g_tm_trace[2][i] - t0, i + kTmStages < n ? g_tm_trace[4][i] - t0 : -1ll);
+  }
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" :: "r"(tmem_d) : "memory");
+  if (w == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_d), "n"(kTmAlloc) : "memory");
 }
 
 // Backward + Adam: dz[b][c] = dh[b][c] * [h[b][c] > 0] (ReLU'(0) = 0, R26);

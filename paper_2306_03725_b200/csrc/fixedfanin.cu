@@ -4,6 +4,7 @@
 #include "fixedfanin.h"
 #include "ff_kernels.cuh"
 #include "ff_dense.cuh"
+#include <cudaTypedefs.h>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -489,7 +490,7 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
 
 // ============================================================ NEXT-2: the intermediate layer
 struct DenseLayout {
-  size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, zpart, cnt, hd, x_stage, scal, total;
+  size_t Wd, mWd, vWd, dWd, bd, mbd, vbd, dbd, xT, xTlo, zpart, cnt, hd, x_stage, scal, total;
 };
 int ldw_of(int m) { return (m + 127) / 128 * 128; }   // Wd is stored in 128-column tiles
 DenseLayout dense_layout_of(const ff_dense_config& c) {
@@ -502,6 +503,7 @@ DenseLayout dense_layout_of(const ff_dense_config& c) {
   o.dWd = (c.flags & FF_FLAG_STORE_GRADS) ? take(4 * dw) : 0;
   o.bd = take(4 * w); o.mbd = take(4 * w); o.vbd = take(4 * w); o.dbd = take(4 * w);
   o.xT = take(4 * (size_t)c.d * ldx);
+  o.xTlo = take(4 * (size_t)c.d * 32);                      // lo part of xT (tensor-core forward, B <= 32)
   o.zpart = take(2 * 4 * (size_t)ldw_of(c.m) * 32);        // split-feature forward partials (B <= 32)
   o.cnt = take(4 * (size_t)(ldw_of(c.m) / 128));
   o.hd = take(8 * (size_t)c.m * ldx);     // own h|dh lines for the standalone forward/backward
@@ -548,8 +550,9 @@ struct ff_dense {
   ff_dense_config cfg;
   DenseLayout lay;
   char* ws;
-  float *Wd, *mWd, *vWd, *dWd, *bd, *mbd, *vbd, *dbd, *xT, *hd, *x_stage, *zpart;
+  float *Wd, *mWd, *vWd, *dWd, *bd, *mbd, *vbd, *dbd, *xT, *xTlo, *hd, *x_stage, *zpart;
   unsigned* cnt;
+  CUtensorMap tmW, tmX, tmXl;   // TMA maps of Wd, xT and xTlo (k_dense_fwd_tma), encoded at create
   int ldw;
   int nsm;
   int64_t t;            // host mirror of *t_dev
@@ -560,6 +563,47 @@ struct ff_dense {
 };
 
 namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+// Wd: {128 columns, d features, tiles} over the tiled layout [ldw/128][d][128]; xT, xTlo:
+// {32 samples, d} (the B <= 32 layout, ldx = 32).  Box 32 x 32 (x 1); features >= d read 0.
+const char* encode_dense_maps(ff_dense* n) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (enc == nullptr) return "cuTensorMapEncodeTiled unavailable";
+  const cuuint64_t d = (cuuint64_t)n->cfg.d;
+  const cuuint32_t es[3] = {1, 1, 1};
+  {
+    const cuuint64_t dims[3] = {128, d, (cuuint64_t)(n->ldw / 128)};
+    const cuuint64_t strides[2] = {128 * 4, d * 128 * 4};
+    const cuuint32_t box[3] = {32, 32, 1};
+    if (enc(&n->tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, n->Wd, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return "Wd map";
+  }
+  const cuuint64_t dims[2] = {32, d};
+  const cuuint64_t strides[1] = {32 * 4};
+  const cuuint32_t box[2] = {32, 32};
+  if (enc(&n->tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, n->xT, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS ||
+      enc(&n->tmXl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, n->xTlo, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+    return "xT map";
+  return nullptr;
+}
 
 // dropout + forward into `hd` (the dense layer's own lines or a fixed fan-in layer's)
 ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, bool train, float* hd,
@@ -572,12 +616,13 @@ ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, 
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 4096));
     k_dropout_T<<<grid, 256, 0, st>>>(x, B, n->cfg.d, ldx, p, scale, (train && p > 0.0f) ? 1 : 0, (uint32_t)step,
                                       (uint32_t)n->cfg.seed, (uint32_t)(n->cfg.seed >> 32), n->xT,
-                                      step == FF_STEP_AUTO ? n->t_dev : nullptr);
+                                      step == FF_STEP_AUTO ? n->t_dev : nullptr, nb == 1 ? n->xTlo : nullptr);
     FF_LAUNCHED();
   }
-  if (nb == 1 && !(n->cfg.flags & FF_FLAG_DENSE_SIMT)) {          // tensor cores (tcgen05, 3xTF32)
-    k_dense_fwd_tc<<<(n->ldw + 127) / 128, kTcThreads + 32, kTcSmem, st>>>(n->Wd, n->bd, n->xT, n->cfg.d, n->cfg.m, ldx, B,
-                                                                      hd, 64 * nb, 1, h_out);
+  if (nb == 1 && !(n->cfg.flags & FF_FLAG_DENSE_SIMT)) {          // tensor cores (tcgen05 + TMA, 3xTF32)
+    const int grid = std::min(n->ldw / 128, n->nsm);               // persistent: one CTA per SM
+    k_dense_fwd_tma<<<grid, kTmThreads, kTmSmem, st>>>(n->tmW, n->tmX, n->tmXl, n->bd, n->cfg.d, n->cfg.m, B, hd, 64,
+                                                       1, h_out);
     FF_LAUNCHED();
     if (train) n->fwd_B = B;
     return FF_OK;
@@ -1092,7 +1137,7 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
   n->dWd = (c.flags & FF_FLAG_STORE_GRADS) ? at<float>(ws, lay.dWd) : nullptr;
   n->bd = at<float>(ws, lay.bd); n->mbd = at<float>(ws, lay.mbd); n->vbd = at<float>(ws, lay.vbd);
   n->dbd = at<float>(ws, lay.dbd);
-  n->xT = at<float>(ws, lay.xT); n->hd = at<float>(ws, lay.hd); n->x_stage = at<float>(ws, lay.x_stage);
+  n->xT = at<float>(ws, lay.xT); n->xTlo = at<float>(ws, lay.xTlo); n->hd = at<float>(ws, lay.hd); n->x_stage = at<float>(ws, lay.x_stage);
   n->t_dev = at<int64_t>(ws, lay.scal); n->rbc_dev = at<float>(ws, lay.scal + 8);
   n->zpart = at<float>(ws, lay.zpart); n->cnt = at<unsigned>(ws, lay.cnt);
   n->ldw = ldw_of(c.m);
@@ -1107,10 +1152,15 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
           cudaSuccess ||
       cudaFuncSetAttribute((const void*)k_dense_bwd_adam_b32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kDenseBwd1Smem) != cudaSuccess ||
-      cudaFuncSetAttribute((const void*)k_dense_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem) !=
+      cudaFuncSetAttribute((const void*)k_dense_fwd_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmSmem) !=
           cudaSuccess) {
     delete n;
     return fail(FF_ERR_CUDA, "dense forward smem attribute");
+  }
+  {
+    // TMA maps (128-B swizzle with 32-B atoms: the MN-major tf32 operand layout, ff_dense.cuh)
+    const char* why = encode_dense_maps(n);
+    if (why) { delete n; return fail(FF_ERR_CUDA, "dense forward tensor maps: %s", why); }
   }
   cudaError_t e = cudaMemsetAsync(ws, 0, lay.total, st);
   if (e != cudaSuccess) { delete n; return fail(FF_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); }

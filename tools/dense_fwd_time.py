@@ -19,3 +19,20 @@ for s in range(200):
     n.backward_adam(dh, 1e-3)
 torch.cuda.synchronize()
 print(f"m={m} done", flush=True)
+# CUDA-graph replay of 50 forwards (no host cost between launches): dropout + forward per call
+s = torch.cuda.Stream()
+h = torch.empty(B, m, device="cuda")
+with torch.cuda.stream(s):
+    n.forward(x, step=1, train=True, h=h)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(50):
+            n.forward(x, step=1, train=True, h=h)
+    g.replay(); g.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(10):
+        g.replay()
+    e1.record(s)
+    e1.synchronize()
+print(f"m={m} graph-timed forward (dropout + dense): {e0.elapsed_time(e1) / 500 * 1e3:.2f} us per call", flush=True)
