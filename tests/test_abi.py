@@ -110,8 +110,9 @@ def test_bad_dense_configs_rejected(kw, msg):
 
 
 def test_dense_workspace_size_matches_layout_model():
-    """Wd, mWd, vWd in 128-column tiles (+ dWd with FF_FLAG_STORE_GRADS), bias vectors, xT,
-    the split-forward scratch, the h|dh lines and the x staging."""
+    """Wd, mWd, vWd in 128-column tiles (+ dWd with FF_FLAG_STORE_GRADS), bias vectors, xT and
+    its tf32 lo part (the TMA forward), the split-forward scratch, the h|dh lines and the x
+    staging."""
     d, m, B = 512, 32768, 32
     sizes = []
     for flags in (0, L.FF_FLAG_STORE_GRADS):
@@ -120,7 +121,7 @@ def test_dense_workspace_size_matches_layout_model():
         assert L.lib().fixedfanin_dense_workspace_size(ctypes.byref(c), ctypes.byref(n)) == L.FF_OK
         sizes.append(n.value)
     assert sizes[1] - sizes[0] == 4 * d * m                     # dWd
-    core = 3 * 4 * d * m + 4 * 4 * m + 4 * d * 32 + 8 * m * 32 + 4 * B * d
+    core = 3 * 4 * d * m + 4 * 4 * m + 2 * 4 * d * 32 + 8 * m * 32 + 4 * B * d
     assert core <= sizes[0] <= core + 2 * 4 * m * 32 + 4 * (m // 128) + 16 * 256
 
 
