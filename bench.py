@@ -618,6 +618,27 @@ def run_ours(a, shape, world, rank, local_rank):
         graph = {"ms_per_step": ms_g, "samples_per_s": B / (ms_g * 1e-3), "steps": n_g,
                  "note": "one captured fixedfanin_train_step replayed on static buffers (redistribution not included)"}
         del g
+    elif dist.get_backend() == "nccl":
+        # N > 1: the sharded steps WITH their collectives in one graph (sharded.GraphedSteps:
+        # per step the h broadcast, the shard's fused step and the async dh all-reduce, which
+        # overlaps the next step inside the graph); NCCL collectives are capturable, gloo's not
+        from paper_2306_03725_b200.sharded import GraphedSteps
+        gs = GraphedSteps(layer, h_dev, ptr_dev, ids_dev, LR, B, shape.m, dev, loss=loss)
+        n_rep = max(1, 200 // gs.K)
+        for _ in range(2):
+            gs.replay()
+        barrier()
+        e0.record(stream)
+        for _ in range(n_rep):
+            gs.replay()
+        e1.record(stream)
+        barrier()
+        ms_g = max_over_ranks(e0.elapsed_time(e1) / (n_rep * gs.K))
+        graph = {"ms_per_step": ms_g, "samples_per_s": B / (ms_g * 1e-3), "steps": n_rep * gs.K,
+                 "steps_per_graph": gs.K,
+                 "note": "sharded.GraphedSteps: K steps (h broadcast + fused step + async dh all-reduce each) per "
+                         "captured graph, max over ranks (redistribution not included)"}
+        del gs
 
     # ---- NEXT-3: large-batch inference and shortlist scoring, one GPU
     big = model = sqh = None

@@ -127,6 +127,53 @@ class OverlappedTrainer:
                 self.bcast[i] = None
 
 
+class GraphedSteps:
+    """K consecutive label-sharded training steps, collectives included, captured once in one
+    CUDA graph and replayed: per step j the h broadcast of slot j, the shard's
+    fused step (fixedfanin_train_step) into dh[j], and the async dh all-reduce of dh[j], which
+    overlaps the compute of step j + 1 inside the graph (NCCL's stream forks from and joins the
+    capture stream); the graph joins every all-reduce at its end.  One graph launch replaces
+    K x (broadcast + 3 kernels + all-reduce) host enqueues.
+
+    The caller owns the K static input slots h[j] [B][m], ptr[j] and ids[j] (fixed capacity)
+    and refills them between replays; the learning rate is baked in at capture, the Adam step
+    counter lives on the device and advances per replayed step.  Construction runs the K steps
+    once eagerly (NCCL communicator set-up and lazy allocations must happen outside the
+    capture), so it trains K steps.  NCCL collectives are graph-capturable, gloo's are not:
+    ``collectives`` defaults to world > 1 and needs the NCCL backend; True with one rank
+    exercises the capture path on one GPU."""
+
+    def __init__(self, layer: "ShardedLayer", h, ptr, ids, lr, B, m, device, loss=None, collectives=None):
+        self.layer, self.h, self.ptr, self.ids, self.lr, self.loss = layer, h, ptr, ids, lr, loss
+        self.K = len(h)
+        self.dh = [torch.empty((B, m), device=device) for _ in range(self.K)]
+        self.collectives = layer.world > 1 if collectives is None else collectives
+        self.stream = torch.cuda.Stream(device=device)
+        self.stream.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(self.stream):
+            self._steps()                                     # eager pass: communicators, allocations
+        torch.cuda.current_stream(device).wait_stream(self.stream)
+        torch.cuda.synchronize(device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._steps()
+
+    def _steps(self):
+        L, works = self.layer, []
+        for j in range(self.K):
+            if self.collectives:
+                dist.broadcast(self.h[j], src=0, group=L.group)
+            L.engine.train_step(self.h[j], self.ptr[j], self.ids[j], self.lr, dh=self.dh[j], loss=self.loss)
+            if self.collectives:
+                works.append(dist.all_reduce(self.dh[j], op=dist.ReduceOp.SUM, group=L.group, async_op=True))
+        for w in works:
+            w.wait()
+
+    def replay(self):
+        """Run the K captured steps (on the current stream's device; ordered after prior work)."""
+        self.graph.replay()
+
+
 class ShardedModel:
     """The whole proposed architecture (Fig. 2) under label sharding (NEXT-2,
     SURVEY §8(f)2): rank r owns one label shard of the fixed fan-in layer AND the column shard
