@@ -1440,6 +1440,99 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
   }
 }
 
+// The same fused forward + running top-K for k = 32, B <= 32 (per 32-sample line q2) with the
+// h-line gathers loaded straight into registers (ld.global.v4) instead of through
+// k_predict_ring's cp.async shared-memory ring, which moves every gathered byte through
+// shared memory twice (the LDGSTS write and the LDS read: 8 KB per row, ~150 us per launch
+// at 128 B/clock per SM); register gathers reach 19.9 TB/s vs 11-17.7 TB/s for LDGSTS
+// (profiles/r01_gatherbench.txt).  Latency is hidden by occupancy (24 warps/SM at 80
+// registers) with the next row's W/idx/bias prefetched.  Measured (profiles/r02_pred_reg.txt):
+// 0.197 vs 0.213 ms at B = 32; a variant that also keeps the next row's 8 lines in flight
+// (64 more registers, 16 warps/SM) took 0.27-0.30 ms, and one with the top-K lists in shared
+// memory (64 registers, 32 warps/SM) 0.21-0.23 ms.  Same score arithmetic (row_score_own):
+// bit-identical y.  Candidates go straight into the lane's register top-K list when they beat
+// the lane's threshold (the max of its own K-th best and the per-sample shared threshold of
+// k_predict_ring, exchanged every FF_PRED_XCH rows), which after the first rows is rare.
+// Output: the block's merged lists in cand[blk][32 nb][kTopkMax], like the ring.
+#ifndef FF_PRED_REG_THREADS
+#define FF_PRED_REG_THREADS 128
+#endif
+#ifndef FF_PRED_REG_MINB
+#define FF_PRED_REG_MINB 6
+#endif
+constexpr int kPredRegThreads = FF_PRED_REG_THREADS;
+template <bool CHECK>
+__global__ void __launch_bounds__(kPredRegThreads, FF_PRED_REG_MINB) k_predict_reg(const float* __restrict__ W,
+                                                                                   const int* __restrict__ idx,
+                                                                                   const float* __restrict__ bias,
+                                                                                   const float* __restrict__ hd, int64_t L,
+                                                                                   int B, int nb, int q2, int64_t row_begin,
+                                                                                   float* __restrict__ cand_s,
+                                                                                   int* __restrict__ cand_i,
+                                                                                   int* __restrict__ gthr, int* __restrict__ err) {
+  constexpr int NG = 8;
+  __shared__ float ss[kPredRegThreads / 32][32][kTopkMax];
+  __shared__ int si[kPredRegThreads / 32][32][kTopkMax];
+  const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7, wid = threadIdx.x >> 5;
+  const uint32_t kColFloats = pin(64u * (uint32_t)nb);
+  const uint32_t nwarp = pin((uint32_t)(((int64_t)gridDim.x * blockDim.x) >> 5));
+  const float* const hb = pin(hd + q2 * 64 + 4 * bq);
+  int sl[NG];
+#pragma unroll
+  for (int q = 0; q < NG; ++q) sl[q] = pin(4 * q + gq);
+  const int b = q2 * 32 + 4 * bq + gq;
+  const uint32_t nrows = pin((uint32_t)L);
+  float ts[kTopkMax]; int ti[kTopkMax];
+#pragma unroll
+  for (int q = 0; q < kTopkMax; ++q) { ts[q] = -INFINITY; ti[q] = INT_MAX; }
+  float thr_s = -INFINITY; int thr_i = INT_MAX;
+  int* const gp = gthr + b;
+  auto exchange = [&]() {
+    if (b < B) {
+      const int g = *(volatile int*)gp;
+      const float own = ts[kTopkMax - 1];
+      if (own != -INFINITY && score_key(own) > g) atomicMax(gp, score_key(own));
+      const float gs = key_score(g);
+      if (gs > thr_s) { thr_s = gs; thr_i = INT_MAX; }
+    }
+  };
+  uint32_t j = (uint32_t)global_warp(), it = 0;
+  float w = 0.f, bj = 0.f; int c = 0;
+  if (j < nrows) { w = ld_na(W + j * 32u + lane); c = ld_na_ro(idx + j * 32u + lane); bj = ld_na(bias + j); }
+  while (j < nrows) {
+    float4 hv[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q)
+      hv[q] = ld_line4_plain(col_line(hb, (uint32_t)__shfl_sync(kFull, c, sl[q]), kColFloats));
+    const uint32_t jn = j + nwarp;                       // the next row's state, in flight meanwhile
+    float wn = 0.f, bjn = 0.f; int cn = 0;
+    if (jn < nrows) { wn = ld_na(W + jn * 32u + lane); cn = ld_na_ro(idx + jn * 32u + lane); bjn = ld_na(bias + jn); }
+    float ws[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) ws[q] = __shfl_sync(kFull, w, sl[q]);
+    const float y = row_score_own<NG>(ws, hv, gq, bj);
+    const int jid = (int)(row_begin + j);
+    if (CHECK && b < B && !isfinite(y)) atomicOr(err, kErrNonFinite);              // FF_FLAG_CHECK_FINITE (R15)
+    if (b < B && better(y, jid, thr_s, thr_i)) {
+      topk_insert(ts, ti, y, jid);
+      if (better(ts[kTopkMax - 1], ti[kTopkMax - 1], thr_s, thr_i)) { thr_s = ts[kTopkMax - 1]; thr_i = ti[kTopkMax - 1]; }
+    }
+    if ((++it & (FF_PRED_XCH - 1u)) == 0) exchange();
+    j = jn; w = wn; c = cn; bj = bjn;
+  }
+#pragma unroll
+  for (int q = 0; q < kTopkMax; ++q) { ss[wid][lane][q] = ts[q]; si[wid][lane][q] = ti[q]; }
+  __syncthreads();
+  if (wid == 0) {
+    for (int w2 = 1; w2 < kPredRegThreads / 32; ++w2)
+#pragma unroll
+      for (int q = 0; q < kTopkMax; ++q) topk_insert(ts, ti, ss[w2][lane][q], si[w2][lane][q]);
+    const int64_t base = ((int64_t)blockIdx.x * 32 * nb + b) * kTopkMax;
+#pragma unroll
+    for (int q = 0; q < kTopkMax; ++q) { cand_s[base + q] = ts[q]; cand_i[base + q] = ti[q]; }
+  }
+}
+
 // Fused forward + top-K for large batches (B > 32, k = 32; NEXT-3): the batch is
 // scored in chunks of 128 samples (4 hd lines per column; 16 MiB of h lines at m = 32768, so a
 // chunk stays L2-resident while every row streams past it).  Per connection one warp

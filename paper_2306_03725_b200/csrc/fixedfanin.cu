@@ -50,6 +50,9 @@ ff_status fail(ff_status s, const char* fmt, ...) {
 
 constexpr size_t kAlign = 256;
 constexpr int kMaxCandBlocks = 1024;    // predict grid cap (candidate buffer rows)
+#ifndef FF_PRED_REG
+#define FF_PRED_REG 1                    // B <= 96 predict: 1 = register gathers (k_predict_reg), 0 = cp.async ring
+#endif
 constexpr int kMaxWideWarps = 4096;     // wide predict: warps with a top-K list in the scratch
 constexpr int kPredRingMaxLines = 3;    // predict: B <= 96 runs the ring kernel per 32-sample line
 
@@ -179,7 +182,7 @@ struct ff_layer {
   uint32_t* posmask;
   int64_t t;
   bool grads_valid;
-  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring, grid_pred_ring, grid_pred_wide;
+  int grid_train, grid_fwd, grid_bwd, grid_pred, grid_rows, grid_ring, grid_pred_ring, grid_pred_wide, grid_pred_reg;
   int nsm;
   std::vector<cudaEvent_t> prof_ev;   // pairs (before, after) of the fused row kernel
   // host entry point: H2D copies on a library stream into one of two staging slots, so the
@@ -449,12 +452,21 @@ ff_status predict_impl(ff_layer* l, const float* h, int32_t B, int32_t K, float*
   if (k == 32 && (nb == 1 || (nb <= kPredRingMaxLines && !(l->cfg.flags & FF_FLAG_NO_PIPE)))) {
     // hot configuration (B <= 32), and B <= 96: the pipelined kernel once per 32-sample line
     // (bit-identical scores; below 4 lines the wide kernel would leave lanes idle)
+#if FF_PRED_REG
+    nlist = l->grid_pred_reg;
+#else
     nlist = l->grid_pred_ring;
+#endif
     for (int q2 = 0; q2 < nb; ++q2) {
       int* gt = l->pthr;
       void* args[] = {&W, &idx, &bias, &hd, &L, &BB, &nbb, &q2, &rb, &cs, &ci, &gt, &perr};
+#if FF_PRED_REG
+      FF_CUDA(cudaLaunchKernel(perr ? (const void*)k_predict_reg<true> : (const void*)k_predict_reg<false>,
+                               dim3(nlist), dim3(kPredRegThreads), args, 0, st));
+#else
       FF_CUDA(cudaLaunchKernel(perr ? (const void*)k_predict_ring<true> : (const void*)k_predict_ring<false>, dim3(nlist),
                                dim3(kPredRingThreads), args, kPredRingSmem, st));
+#endif
       if (q2 + 1 < nb) ++g_launches;
     }
   } else if (k == 32 && !(l->cfg.flags & FF_FLAG_NO_PIPE)) {   // large batch: chunked wide kernel (bit-identical)
@@ -754,6 +766,10 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   }
   l->grid_pred_ring =
       std::min(kMaxCandBlocks, occupancy_grid((const void*)k_predict_ring<false>, l->nsm, kPredRingThreads, kPredRingSmem));
+#if FF_PRED_REG
+  l->grid_pred_reg = std::min(kMaxCandBlocks, occupancy_grid((const void*)k_predict_reg<false>, l->nsm,
+                                                             kPredRegThreads));
+#endif
   if (cudaFuncSetAttribute((const void*)k_predict_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kPredWSmem) !=
       cudaSuccess) {
     delete l;
