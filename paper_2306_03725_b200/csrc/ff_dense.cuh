@@ -259,36 +259,42 @@ __global__ void __launch_bounds__(kDenseFwdThreads) k_dense_fwd(const float* __r
 // cleared; a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (the dropped a_lo.b_lo and the tf32
 // truncation of the lo parts are <= ~2^-20 relative).  The tensor core itself truncates fp32
 // operands to tf32 (tcprobe_mn: 1 + 3*2^-12 -> 1), so the raw TMA tiles ARE the hi operands;
-// A's lo tile is computed per stage (elementwise, at the same swizzled offsets) and xT's lo
-// once per forward by k_dropout_T.  Per 8-feature block two MMAs: A_hi . [x_hi | x_lo] (one
-// N = 64 MMA: x_lo is the next 32-sample atom) and A_lo . x_hi (N = 32), into separate TMEM
-// columns that the epilogue sums in a fixed order.  tools/microbench/tcrate.cu: an M = 128
-// MMA costs max(67, N / 2) cycles, so this is ~134 cycles per block (vs ~200 for three N = 32
-// MMAs).
+// xT's lo is written once per forward by k_dropout_T, and Wd's lo per stage by four converter
+// warps straight into TMEM (thread = A row = tile column: it reads its column's features from
+// the swizzled raw tile, byte f*128 + ((4 c) ^ ((f & 3) << 5)) per tools/microbench/swzprobe.cu,
+// and tcgen05.st's them into its TMEM lane), so A_lo never touches shared memory and its MMAs
+// read A from TMEM.  Per 8-feature block two MMAs: A_hi . [x_hi | x_lo] (one N = 64 MMA: x_lo
+// is the next 32-sample atom) and A_lo(TMEM) . x_hi (N = 32), into separate TMEM columns the
+// epilogue sums in a fixed order (tools/microbench/tcrate.cu: an M = 128 MMA costs
+// max(67, N / 2) cycles, so merging the x parts saves a third of the tensor time).
 // Persistent, one CTA per SM over the column tiles, warp-specialised, no CTA barrier in the
-// loop: warp 0 = TMA producer into a ring of kTmStages stages (A raw 16 KB + x hi/lo 8 KB,
-// plus the stage's 16-KB A-lo slot); warps 2-5 = lo converters; warp 1 = MMA issuer (8 MMAs
-// per 32-feature stage, commit -> the stage's "empty" barrier); warps 6-9 = epilogue from one
-// of two TMEM accumulator sets (the next tile's MMAs run while a tile's epilogue drains):
-// bias, ReLU, h|dh lines through a per-warp shared-memory transpose (4 full 128-B lines per
-// store instruction) and h_out.  Each column's result depends only on its own Wd column and
-// xT, so column shards are bit-identical to the unsharded layer.
-// What bounds it (profiles/r02_dense_fwd_tma.txt): shared-memory bandwidth —
-// per stage the TMA writes 24 KB, the converters read 16 and write 16 KB, the MMAs read 44 KB
-// (~100 KB at 128 B/clock = ~780 cycles; a clock64 trace of block 0 shows ~830 per stage).
-// Split raw/lo rings, two MMA-issuing warps and L2 prefetch ahead of the ring were measured
-// slower.
+// loop: warp 0 = TMA producer into a ring of kTmStages stages of kTmF = 64 features (A raw
+// 32 KB + x hi/lo 16 KB); warps 2-5 = A-lo converters; warp 1 = MMA issuer (16 MMAs per stage,
+// commit -> the stage's "empty" barrier); warps 6-9 = epilogue from one of two TMEM
+// accumulator sets (the next tile's MMAs run while a tile's epilogue drains): bias, ReLU, h|dh
+// lines through a per-warp shared-memory transpose (4 full 128-B lines per store instruction)
+// and h_out.  Each column's result depends only on its own Wd column and xT, so column shards
+// are bit-identical to the unsharded layer.  Measured steps (profiles/r02_dense_fwd_tma.txt):
+// 32-feature stages with A_lo in shared memory 22.9 us, A_lo in TMEM 22.0, 64-feature stages
+// 19.3 (per-stage barrier/commit overhead halved); the MMA issuer paces the pipeline.
 #ifndef FF_TM_STAGES
-#define FF_TM_STAGES 5
+#define FF_TM_STAGES 4
 #endif
 constexpr int kTmStages = FF_TM_STAGES;
+#ifndef FF_TM_F
+#define FF_TM_F 64
+#endif
+constexpr int kTmF = FF_TM_F;                                    // features per stage (32 or 64)
+static_assert(kTmF == 32 || kTmF == 64, "stage features");
 constexpr int kTmThreads = 320;                                  // 10 warps
-constexpr uint32_t kTmA = 16384, kTmX = 4096;                    // A tile (32 f x 128 c), x tile (32 f x 32 b)
-constexpr uint32_t kTmStage = 2 * kTmA + 2 * kTmX;              // A raw | A lo | x hi | x lo = 40 KB
-constexpr uint32_t kTmTx = kTmA + 2 * kTmX;                      // TMA bytes per stage
+constexpr uint32_t kTmG = kTmF * 128;                            // one 32-column group of the A tile (kTmF rows of 128 B)
+constexpr uint32_t kTmA = 4 * kTmG, kTmX = kTmF * 32 * 4;        // A tile (kTmF f x 128 c), x tile (kTmF f x 32 b)
+constexpr uint32_t kTmStage = kTmA + 2 * kTmX;                   // A raw | x hi | x lo (all TMA bytes)
 constexpr uint32_t kTmEpi = 4 * 32 * 33 * 4;                     // epilogue transpose buffers
 constexpr uint32_t kTmTileCols = 96;                             // TMEM columns per tile: [hi.hi | hi.lo] + lo.hi
-constexpr uint32_t kTmAlloc = 256;                               // two tile accumulator sets
+constexpr uint32_t kTmLoCol = 2 * kTmTileCols;                   // TMEM: A-lo tiles (32 columns per stage) after the accumulators
+constexpr uint32_t kTmAlloc = 512;
+static_assert(kTmLoCol + kTmF * kTmStages <= kTmAlloc, "TMEM columns");
 constexpr int kTmSmem = 1024 + kTmStages * kTmStage + kTmEpi + 256;
 
 // shared-memory matrix descriptor (sm_100): start, LBO, SBO (16-B units), version 1, layout
@@ -304,6 +310,16 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 // kind::tf32, D f32, A and B tf32 MN-major (bits 15, 16), M = 128, N = n
 __host__ __device__ constexpr uint32_t tm_idesc(uint32_t n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+// the same with A read from TMEM (A must be K-major there: lane = row, one column per K element)
+__host__ __device__ constexpr uint32_t tm_idesc_ts(uint32_t n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+template <uint32_t N>
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+               :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(tm_idesc_ts(N)), "r"(accumulate));
 }
 template <uint32_t N>
 __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
@@ -360,7 +376,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_dense_fwd_tma(const __grid_co
   auto empty = [&](uint32_t s) { return bar0 + 8u * (2 * kTmStages + s); };
   const uint32_t tfull0 = bar0 + 8u * (3 * kTmStages), tempty0 = tfull0 + 16, tptr_s = tempty0 + 16;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int ntiles = (m + 127) / 128, nst = (d + 31) / 32;
+  const int ntiles = (m + 127) / 128, nst = (d + kTmF - 1) / kTmF;
   if (w == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(tptr_s), "n"(kTmAlloc) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -388,11 +404,11 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_dense_fwd_tma(const __grid_co
           if (i >= (uint32_t)kTmStages) { mbar_wait(empty(s), ((i / kTmStages) - 1) & 1u); TM_TR(4, i - kTmStages); }
           TM_TR(0, i);
           const uint32_t stg = sbase + s * kTmStage;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(full(s)), "r"(kTmTx) : "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(full(s)), "r"(kTmStage) : "memory");
 #pragma unroll
-          for (int g = 0; g < 4; ++g) tma_load_3d(stg + (uint32_t)g * 4096u, &mW, 32 * g, 32 * st, t, full(s));
-          tma_load_2d(stg + 2 * kTmA, &mX, 0, 32 * st, full(s));
-          tma_load_2d(stg + 2 * kTmA + kTmX, &mXl, 0, 32 * st, full(s));
+          for (int g = 0; g < 4; ++g) tma_load_3d(stg + (uint32_t)g * kTmG, &mW, 32 * g, kTmF * st, t, full(s));
+          tma_load_2d(stg + kTmA, &mX, 0, kTmF * st, full(s));
+          tma_load_2d(stg + kTmA + kTmX, &mXl, 0, kTmF * st, full(s));
         }
     }
   } else if (w == 1) {                                            // ===== MMA issuer
@@ -406,43 +422,56 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_dense_fwd_tma(const __grid_co
         const uint32_t dhh = tmem_d + kTmTileCols * (uint32_t)acc, dlh = dhh + 64;
         for (int st = 0; st < nst; ++st, ++i) {
           const uint32_t s = i % kTmStages, par = (i / kTmStages) & 1u;
-          const uint32_t Ah = sbase + s * kTmStage, Al = Ah + kTmA, Xh = Ah + 2 * kTmA;
+          const uint32_t Ah = sbase + s * kTmStage, Xh = Ah + kTmA, Al = tmem_d + kTmLoCol + (uint32_t)kTmF * s;
           mbar_wait(full(s), par);
           mbar_wait(conv(s), par);
           TM_TR(2, i);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-          for (int kb = 0; kb < 4; ++kb) {                        // 8 features = two 4-row groups = 1 KB
-            const uint64_t xh = umma_desc(Xh + kb * 1024u, 4096, 512, 1);
+          for (int kb = 0; kb < kTmF / 8; ++kb) {                 // 8 features = two 4-row groups = 1 KB
+            const uint64_t xh = umma_desc(Xh + kb * 1024u, kTmX, 512, 1);
             const uint32_t accu = (st > 0 || kb > 0) ? 1u : 0u;
-            tc_mma_tf32<64>(dhh, umma_desc(Ah + kb * 1024u, 4096, 512, 1), xh, accu);   // [hi.hi | hi.lo]
-            tc_mma_tf32<32>(dlh, umma_desc(Al + kb * 1024u, 4096, 512, 1), xh, accu);   // lo.hi
+            tc_mma_tf32<64>(dhh, umma_desc(Ah + kb * 1024u, kTmG, 512, 1), xh, accu);   // [hi.hi | hi.lo]
+            tc_mma_tf32_ts<32>(dlh, Al + 8u * kb, xh, accu);                              // lo.hi (A-lo in TMEM)
           }
           tc_commit(empty(s));
         }
         tc_commit(tfull0 + 8u * acc);
       }
     }
-  } else if (w < 6) {                                             // ===== A lo converters (128 threads)
-    const uint32_t ct = (uint32_t)(tid - 64) * 16u;
+  } else if (w < 6) {                                             // ===== A-lo converters (128 threads)
+    // thread = A row (tile column 32 q + lane, TMEM lane quarter q = w % 4): reads its column's
+    // 32 features from the swizzled raw tile (byte f*128 + ((4 lane) ^ ((f & 3) << 5)) of
+    // group q, tools/microbench/swzprobe.cu; conflict-free) and writes lo into its TMEM lane
+    const int q = w & 3;
     uint32_t i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
       for (int st = 0; st < nst; ++st, ++i) {
         const uint32_t s = i % kTmStages;
         mbar_wait(full(s), (i / kTmStages) & 1u);
-        if (ct == 0) TM_TR(1, i);
-        const uint32_t raw = sbase + s * kTmStage + ct;
+        if (tid == 64) TM_TR(1, i);
+        const uint32_t raw = sbase + s * kTmStage + (uint32_t)q * kTmG;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 v;
-          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(raw + j * 2048u));
-          const float l0 = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          const float l1 = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          const float l2 = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          const float l3 = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(raw + kTmA + j * 2048u), "f"(l0), "f"(l1), "f"(l2), "f"(l3) : "memory");
+        for (int f0 = 0; f0 < kTmF; f0 += 32) {
+          uint32_t lo[32];
+#pragma unroll
+          for (int f1 = 0; f1 < 32; ++f1) {
+            const int f = f0 + f1;
+            float v;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(raw + (uint32_t)f * 128u + ((4u * lane) ^ ((uint32_t)(f & 3) << 5))));
+            lo[f1] = __float_as_uint(v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u));
+          }
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                       "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                       :: "r"(tmem_d + ((uint32_t)(32 * q) << 16) + kTmLoCol + (uint32_t)kTmF * s + (uint32_t)f0),
+                          "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]),
+                          "r"(lo[8]), "r"(lo[9]), "r"(lo[10]), "r"(lo[11]), "r"(lo[12]), "r"(lo[13]), "r"(lo[14]), "r"(lo[15]),
+                          "r"(lo[16]), "r"(lo[17]), "r"(lo[18]), "r"(lo[19]), "r"(lo[20]), "r"(lo[21]), "r"(lo[22]), "r"(lo[23]),
+                          "r"(lo[24]), "r"(lo[25]), "r"(lo[26]), "r"(lo[27]), "r"(lo[28]), "r"(lo[29]), "r"(lo[30]), "r"(lo[31])
+                       : "memory");
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy stores -> tensor core
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(conv(s));
       }

@@ -598,7 +598,7 @@ const char* encode_dense_maps(ff_dense* n) {
   {
     const cuuint64_t dims[3] = {128, d, (cuuint64_t)(n->ldw / 128)};
     const cuuint64_t strides[2] = {128 * 4, d * 128 * 4};
-    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t box[3] = {32, (cuuint32_t)kTmF, 1};
     if (enc(&n->tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, n->Wd, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
         CUDA_SUCCESS)
@@ -606,7 +606,7 @@ const char* encode_dense_maps(ff_dense* n) {
   }
   const cuuint64_t dims[2] = {32, d};
   const cuuint64_t strides[1] = {32 * 4};
-  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t box[2] = {32, (cuuint32_t)kTmF};
   if (enc(&n->tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, n->xT, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
           CUDA_SUCCESS ||
