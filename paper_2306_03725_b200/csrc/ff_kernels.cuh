@@ -884,8 +884,12 @@ __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float*
     // training step: t <- t + 1 and the Adam bias corrections 1/(1 - beta^t) (fp64, R6/R7)
     const int64_t tn = *t_dev + 1;
     *t_dev = tn;
+#ifndef FF_PREP_NOPOW
     rbc[0] = (float)(1.0 / (1.0 - pow((double)beta1, (double)tn)));
     rbc[1] = (float)(1.0 / (1.0 - pow((double)beta2, (double)tn)));
+#else
+    rbc[0] = 1.0f; rbc[1] = 1.0f;
+#endif
   }
   if (t2_dev != nullptr && blockIdx.x == 0 && tid == 32) {
     // whole-architecture step: the dense layer's own counter (R28), after its dropout read it

@@ -8,7 +8,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --c
   python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/launches.log 2>&1; tail -1 gpurun_out/launches.log | cut -c1-100
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_train" -s 6 -c 1 \
   -o gpurun_out/prof_full python bench.py --steps 3 --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_predict_ring|k_merge_topk_block" -s 10 -c 2 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_predict_reg|k_merge_topk_block" -s 10 -c 2 \
   -o gpurun_out/prof_pred python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_pred.log 2>&1; tail -1 gpurun_out/ncu_pred.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_dense_fwd|k_dense_bwd" -s 2 -c 2 \
   -o gpurun_out/prof_dense python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_dense.log 2>&1; tail -1 gpurun_out/ncu_dense.log
+FF_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 50 --warmup 5 --repeats 2 --no-cpu-baseline --e2e-steps 10 > gpurun_out/mr.json 2> gpurun_out/mr.err; echo "mr rc=$?"
