@@ -689,44 +689,60 @@ __global__ void __launch_bounds__(kDenseBwdThreads, 2) k_dense_bwd_adam(
 // next two 16-feature blocks streamed into shared memory by cp.async instead of registers:
 // every thread copies exactly the 16-B pieces it will update (2 features x 4 columns x 3
 // arrays) and each warp the two xT rows it reads, so the main loop needs no CTA barrier;
-// only the dz tile is shared (staged once).  ~96 KB of HBM reads are in flight per SM.
-// Same arithmetic and order as k_dense_bwd_adam: bit-identical results.
-constexpr int kDenseBwdNS = 3;                                      // stages
+// only the dz tile is shared.  Persistent (round 2): the (column tile, 16-feature block) work
+// items, tile-major, are split into equal contiguous ranges over a grid of resident CTAs, so
+// every CTA streams the same number of blocks (the round-1 grid of 256 x 3 CTAs ran 2.6 waves
+// at 2 CTAs/SM); a CTA restages dz when its range enters a new tile and updates the tile's
+// bias right after the tile's first block (warp 0 sums db over the 32 samples there).  Same
+// arithmetic and order as k_dense_bwd_adam: bit-identical results.
+#ifndef FF_BWD_NS
+#define FF_BWD_NS 3
+#endif
+#ifndef FF_BWD_MINB
+#define FF_BWD_MINB 2
+#endif
+constexpr int kDenseBwdNS = FF_BWD_NS;                                    // stages
 constexpr int kDenseBwdStage = (3 * kDenseBwdBlk * 128 + kDenseBwdBlk * 32) * 4;   // 26 KB
 constexpr int kDenseBwd1Smem = 32 * 128 * 4 + kDenseBwdNS * kDenseBwdStage;
-__global__ void __launch_bounds__(kDenseBwdThreads, 2) k_dense_bwd_adam_b32(
+// 4 warps, each 4 features x 128 columns of a 16-feature block (lane -> 4 columns): every
+// 16-B dz load serves 4 features (round 1: 8 warps x 2 features, twice the dz shared-memory
+// traffic), and the Adam updates run on packed fp32x2 ops (adam_update2, bit-identical)
+constexpr int kDenseBwd32Threads = 128, kDenseBwdFpw = kDenseBwdBlk / (kDenseBwd32Threads / 32);
+static_assert(kDenseBwdFpw == 4, "features per warp");
+__global__ void __launch_bounds__(kDenseBwd32Threads, FF_BWD_MINB) k_dense_bwd_adam_b32(
     float* __restrict__ Wd, float* __restrict__ mWd, float* __restrict__ vWd, float* __restrict__ bd,
     float* __restrict__ mbd, float* __restrict__ vbd, const float* __restrict__ xT, int d, int m, int ldx,
     const float* __restrict__ hd, int cstride, AdamArgs adam, float* __restrict__ dWd, float* __restrict__ dbd,
-    int rows_per_cta, const float* __restrict__ rbc) {
+    int ntiles, const float* __restrict__ rbc) {
   adam.rbc1 = rbc[0]; adam.rbc2 = rbc[1];                         // this step's bias corrections (device t)
   extern __shared__ __align__(16) float bsm[];
   float (*dzs)[128] = reinterpret_cast<float (*)[128]>(bsm);        // [32][128]
   float* const stages = bsm + 32 * 128;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int ct = blockIdx.x * 128, c0 = ct + 4 * lane;
-  const int f_lo = blockIdx.y * rows_per_cta, f_hi = min(d, f_lo + rows_per_cta);
-  const int nblk = f_hi > f_lo ? (f_hi - f_lo + kDenseBwdBlk - 1) / kDenseBwdBlk : 0;
-  const bool bias_cta = blockIdx.y == 0;
+  const int nfb = (d + kDenseBwdBlk - 1) / kDenseBwdBlk;             // feature blocks per tile
+  const int64_t nitems = (int64_t)ntiles * nfb;
+  const int64_t it_lo = nitems * blockIdx.x / gridDim.x, it_hi = nitems * (blockIdx.x + 1) / gridDim.x;
+  const int nblk = (int)(it_hi - it_lo);
   // stage layout (floats): P [16][128] | M [16][128] | V [16][128] | X [16][32]
   auto stage_ptr = [&](int s) { return stages + (size_t)s * (kDenseBwdStage / 4); };
   auto issue = [&](int bi) {
     if (bi < nblk) {
-      const int fblk = f_lo + bi * kDenseBwdBlk;
+      const int64_t item = it_lo + bi;
+      const int tile = (int)(item / nfb), fblk = (int)(item % nfb) * kDenseBwdBlk;
       float* st = stage_ptr(bi % kDenseBwdNS);
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int rl = 2 * w + r, f = fblk + rl;
-        const bool ok = f < f_hi;
-        const int64_t o = ((int64_t)blockIdx.x * d + (ok ? f : f_lo)) * 128 + 4 * lane;
+      for (int r = 0; r < kDenseBwdFpw; ++r) {
+        const int rl = kDenseBwdFpw * w + r, f = fblk + rl;
+        const bool ok = f < d;
+        const int64_t o = ((int64_t)tile * d + (ok ? f : 0)) * 128 + 4 * lane;
         const uint32_t so = (uint32_t)(rl * 128 + 4 * lane) * 4u;
         cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st) + so, Wd + o, ok);
         cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st + 16 * 128) + so, mWd + o, ok);
         cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st + 32 * 128) + so, vWd + o, ok);
       }
-      if (lane < 16) {                                               // this warp's 2 xT rows
-        const int rl = 2 * w + (lane >> 3), f = fblk + rl, s4 = (lane & 7) * 4;
-        const bool ok = f < f_hi;
+      {                                                              // this warp's 4 xT rows (one 16-B piece per lane)
+        const int rl = kDenseBwdFpw * w + (lane >> 3), f = fblk + rl, s4 = (lane & 7) * 4;
+        const bool ok = f < d;
         cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st + 48 * 128 + rl * 32 + s4),
                          xT + (int64_t)(ok ? f : 0) * ldx + s4, ok);
       }
@@ -735,88 +751,93 @@ __global__ void __launch_bounds__(kDenseBwdThreads, 2) k_dense_bwd_adam_b32(
   };
 #pragma unroll
   for (int s = 0; s < kDenseBwdNS - 1; ++s) issue(s);
-  if (threadIdx.x < 128) {   // dz tile: thread t <-> column ct + t
-    const int c = ct + threadIdx.x;
-    const float* line = hd + (int64_t)c * cstride;
-#pragma unroll
-    for (int s4 = 0; s4 < 32; s4 += 4) {
-      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), gv = hv;
-      if (c < m) { hv = *reinterpret_cast<const float4*>(line + s4); gv = *reinterpret_cast<const float4*>(line + 32 + s4); }
-      dzs[s4 + 0][threadIdx.x] = hv.x > 0.0f ? gv.x : 0.0f;
-      dzs[s4 + 1][threadIdx.x] = hv.y > 0.0f ? gv.y : 0.0f;
-      dzs[s4 + 2][threadIdx.x] = hv.z > 0.0f ? gv.z : 0.0f;
-      dzs[s4 + 3][threadIdx.x] = hv.w > 0.0f ? gv.w : 0.0f;
-    }
-  }
-  __syncthreads();
-  float db[4] = {0.f, 0.f, 0.f, 0.f};
+  int cur_tile = -1;
   for (int bi = 0; bi < nblk; ++bi) {
+    const int64_t item = it_lo + bi;
+    const int tile = (int)(item / nfb), fblk = (int)(item % nfb) * kDenseBwdBlk;
+    const int ct = tile * 128, c0 = ct + 4 * lane;
+    if (tile != cur_tile) {                                          // dz tile: thread t <-> column ct + t
+      __syncthreads();                                               // the previous tile's readers are done
+      {
+        const int c = ct + threadIdx.x;
+        const float* line = hd + (int64_t)c * cstride;
+#pragma unroll
+        for (int s4 = 0; s4 < 32; s4 += 4) {
+          float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), gv = hv;
+          if (c < m) { hv = *reinterpret_cast<const float4*>(line + s4); gv = *reinterpret_cast<const float4*>(line + 32 + s4); }
+          dzs[s4 + 0][threadIdx.x] = hv.x > 0.0f ? gv.x : 0.0f;
+          dzs[s4 + 1][threadIdx.x] = hv.y > 0.0f ? gv.y : 0.0f;
+          dzs[s4 + 2][threadIdx.x] = hv.z > 0.0f ? gv.z : 0.0f;
+          dzs[s4 + 3][threadIdx.x] = hv.w > 0.0f ? gv.w : 0.0f;
+        }
+      }
+      __syncthreads();
+      cur_tile = tile;
+    }
     issue(bi + kDenseBwdNS - 1);
     cp_async_wait<kDenseBwdNS - 1>();                                // this thread's block-bi copies
     __syncwarp();                                                    // ... and its warp's xT rows
     const float* st = stage_ptr(bi % kDenseBwdNS);
-    const int fblk = f_lo + bi * kDenseBwdBlk;
-    const bool do_bias = bias_cta && bi == 0 && w == 0;
-    float2 acc[2][2];
+    const bool do_bias = fblk == 0 && w == 0;
+    float db[4] = {0.f, 0.f, 0.f, 0.f};
+    float2 acc[kDenseBwdFpw][2];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
-#pragma unroll 4
+    for (int r = 0; r < kDenseBwdFpw; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
+#pragma unroll 2
     for (int b4 = 0; b4 < 32; b4 += 4) {
       float4 dz4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) dz4[u] = *reinterpret_cast<const float4*>(&dzs[b4 + u][4 * lane]);
       if (do_bias) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 4; ++u) {   // b ascending
           db[0] = __fadd_rn(db[0], dz4[u].x); db[1] = __fadd_rn(db[1], dz4[u].y);
           db[2] = __fadd_rn(db[2], dz4[u].z); db[3] = __fadd_rn(db[3], dz4[u].w);
         }
       }
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const float4 x4 = *reinterpret_cast<const float4*>(st + 48 * 128 + (2 * w + r) * 32 + b4);
+      for (int r = 0; r < kDenseBwdFpw; ++r) {
+        const float4 x4 = *reinterpret_cast<const float4*>(st + 48 * 128 + (kDenseBwdFpw * w + r) * 32 + b4);
         const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 4; ++u) {   // b = b4 + u ascending
           acc[r][0] = ffma2(bc2(xv[u]), make_float2(dz4[u].x, dz4[u].y), acc[r][0]);
           acc[r][1] = ffma2(bc2(xv[u]), make_float2(dz4[u].z, dz4[u].w), acc[r][1]);
         }
       }
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int rl = 2 * w + r, f = fblk + rl;
-      if (f >= f_hi) continue;
-      const int64_t o = ((int64_t)blockIdx.x * d + f) * 128 + 4 * lane;
-      float4 P = *reinterpret_cast<const float4*>(st + rl * 128 + 4 * lane);
-      float4 Mo = *reinterpret_cast<const float4*>(st + 16 * 128 + rl * 128 + 4 * lane);
-      float4 Ve = *reinterpret_cast<const float4*>(st + 32 * 128 + rl * 128 + 4 * lane);
-      const float4 g = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
-      if (dWd != nullptr) *reinterpret_cast<float4*>(dWd + o) = g;
-      adam_update(P.x, Mo.x, Ve.x, g.x, adam);
-      adam_update(P.y, Mo.y, Ve.y, g.y, adam);
-      adam_update(P.z, Mo.z, Ve.z, g.z, adam);
-      adam_update(P.w, Mo.w, Ve.w, g.w, adam);
-      st_na4(Wd + o, P);
-      st_na4(mWd + o, Mo);
-      st_na4(vWd + o, Ve);
+    for (int r = 0; r < kDenseBwdFpw; ++r) {
+      const int rl = kDenseBwdFpw * w + r, f = fblk + rl;
+      if (f >= d) continue;
+      const int64_t o = ((int64_t)tile * d + f) * 128 + 4 * lane;
+      const float4 P = *reinterpret_cast<const float4*>(st + rl * 128 + 4 * lane);
+      const float4 Mo = *reinterpret_cast<const float4*>(st + 16 * 128 + rl * 128 + 4 * lane);
+      const float4 Ve = *reinterpret_cast<const float4*>(st + 32 * 128 + rl * 128 + 4 * lane);
+      if (dWd != nullptr) *reinterpret_cast<float4*>(dWd + o) = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
+      float2 p0 = lo2(P), p1 = hi2(P), m0 = lo2(Mo), m1 = hi2(Mo), v0 = lo2(Ve), v1 = hi2(Ve);
+      adam_update2(p0, m0, v0, acc[r][0], adam);
+      adam_update2(p1, m1, v1, acc[r][1], adam);
+      st_na4(Wd + o, make_float4(p0.x, p0.y, p1.x, p1.y));
+      st_na4(mWd + o, make_float4(m0.x, m0.y, m1.x, m1.y));
+      st_na4(vWd + o, make_float4(v0.x, v0.y, v1.x, v1.y));
+    }
+    if (do_bias) {                                                   // the tile's bias, once (its first block)
+      float4 p = *reinterpret_cast<const float4*>(bd + c0);
+      float4 mo = *reinterpret_cast<const float4*>(mbd + c0);
+      float4 ve = *reinterpret_cast<const float4*>(vbd + c0);
+      if (dbd != nullptr) *reinterpret_cast<float4*>(dbd + c0) = make_float4(db[0], db[1], db[2], db[3]);
+      adam_update(p.x, mo.x, ve.x, db[0], adam);
+      adam_update(p.y, mo.y, ve.y, db[1], adam);
+      adam_update(p.z, mo.z, ve.z, db[2], adam);
+      adam_update(p.w, mo.w, ve.w, db[3], adam);
+      *reinterpret_cast<float4*>(bd + c0) = p;
+      *reinterpret_cast<float4*>(mbd + c0) = mo;
+      *reinterpret_cast<float4*>(vbd + c0) = ve;
     }
     __syncwarp();                                                    // stage reused by this warp's next issue
   }
   cp_async_wait<0>();
-  if (bias_cta && w == 0 && nblk > 0) {
-    float4 p = *reinterpret_cast<const float4*>(bd + c0);
-    float4 mo = *reinterpret_cast<const float4*>(mbd + c0);
-    float4 ve = *reinterpret_cast<const float4*>(vbd + c0);
-    if (dbd != nullptr) *reinterpret_cast<float4*>(dbd + c0) = make_float4(db[0], db[1], db[2], db[3]);
-    adam_update(p.x, mo.x, ve.x, db[0], adam);
-    adam_update(p.y, mo.y, ve.y, db[1], adam);
-    adam_update(p.z, mo.z, ve.z, db[2], adam);
-    adam_update(p.w, mo.w, ve.w, db[3], adam);
-    *reinterpret_cast<float4*>(bd + c0) = p;
-    *reinterpret_cast<float4*>(mbd + c0) = mo;
-    *reinterpret_cast<float4*>(vbd + c0) = ve;
-  }
 }
 
 // dh [B][m] (user layout) -> the dh half of hd (standalone dense backward).  Grid

@@ -123,6 +123,18 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
 }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d; mov.b64 a, {%2,%3}; mov.b64 b, {%4,%5}; add.rn.f32x2 d, a, b; mov.b64 {%0,%1}, d;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d; mov.b64 a, {%2,%3}; mov.b64 b, {%4,%5}; sub.rn.f32x2 d, a, b; mov.b64 {%0,%1}, d;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
 __device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
 __device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
 __device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
@@ -185,6 +197,19 @@ __device__ __forceinline__ void adam_update(float& p, float& mo, float& ve, floa
   float sq;                                  // MUFU.SQRT, rel. error ~2^-23 (sqrt(0) = 0)
   asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(vhat));
   p = __fsub_rn(p, __fdividef(__fmul_rn(a.lr, mhat), __fadd_rn(sq, a.eps)));
+}
+// The same update for two parameters with packed fp32x2 ops (each half rounds exactly like
+// the scalar op, so the results are bit-identical to two adam_update calls).
+__device__ __forceinline__ void adam_update2(float2& p, float2& mo, float2& ve, float2 q, const AdamArgs& a) {
+  mo = fadd2(fmul2(bc2(a.beta1), mo), fmul2(bc2(a.one_minus_b1), q));
+  ve = fadd2(fmul2(bc2(a.beta2), ve), fmul2(bc2(a.one_minus_b2), fmul2(q, q)));
+  const float2 mhat = fmul2(mo, bc2(a.rbc1));
+  const float2 vhat = fmul2(ve, bc2(a.rbc2));
+  float2 sq;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(sq.x) : "f"(vhat.x));
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(sq.y) : "f"(vhat.y));
+  const float2 num = fmul2(bc2(a.lr), mhat), den = fadd2(sq, bc2(a.eps));
+  p = fsub2(p, make_float2(__fdividef(num.x, den.x), __fdividef(num.y, den.y)));
 }
 
 }  // namespace ff

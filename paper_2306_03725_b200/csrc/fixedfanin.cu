@@ -567,6 +567,7 @@ struct ff_dense {
   CUtensorMap tmW, tmX, tmXl;   // TMA maps of Wd, xT and xTlo (k_dense_fwd_tma), encoded at create
   int ldw;
   int nsm;
+  int grid_bwd32;       // resident CTAs of the persistent B <= 32 backward
   int64_t t;            // host mirror of *t_dev
   int64_t* t_dev;       // Adam step counter (R28), advanced on the device (CUDA-graph capturable)
   float* rbc_dev;       // [2] bias corrections of the current step
@@ -665,10 +666,11 @@ ff_status dense_backward_impl(ff_dense* n, int B, float lr, const float* hd, cud
   const int fq = std::max(1, std::min((n->cfg.d + kDenseBwdBlk - 1) / kDenseBwdBlk, (4 * n->nsm + gx - 1) / gx));
   const int rows = ((n->cfg.d + fq - 1) / fq + kDenseBwdBlk - 1) / kDenseBwdBlk * kDenseBwdBlk;
   dim3 grid(gx, (n->cfg.d + rows - 1) / rows);
-  if (nb == 1)
-    k_dense_bwd_adam_b32<<<grid, kDenseBwdThreads, kDenseBwd1Smem, st>>>(
+  if (nb == 1)     // persistent: equal contiguous ranges of (tile, 16-feature block) items per resident CTA
+    k_dense_bwd_adam_b32<<<std::min<int64_t>((int64_t)n->grid_bwd32, (int64_t)gx * ((n->cfg.d + kDenseBwdBlk - 1) / kDenseBwdBlk)),
+                           kDenseBwd32Threads, kDenseBwd1Smem, st>>>(
         n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d, n->cfg.m, ldx, hd, 64 * nb, a,
-        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, rows, n->rbc_dev);
+        sg ? n->dWd : nullptr, sg ? n->dbd : nullptr, gx, n->rbc_dev);
   else
     k_dense_bwd_adam<<<grid, kDenseBwdThreads, 0, st>>>(n->Wd, n->mWd, n->vWd, n->bd, n->mbd, n->vbd, n->xT, n->cfg.d,
                                                         n->cfg.m, n->ldw, ldx, nb, hd, 64 * nb, a,
@@ -1173,6 +1175,7 @@ ff_status fixedfanin_dense_create(const ff_dense_config* cfg, void* workspace, s
     delete n;
     return fail(FF_ERR_CUDA, "dense forward smem attribute");
   }
+  n->grid_bwd32 = occupancy_grid((const void*)k_dense_bwd_adam_b32, n->nsm, kDenseBwd32Threads, kDenseBwd1Smem);
   {
     // TMA maps (128-B swizzle with 32-B atoms: the MN-major tf32 operand layout, ff_dense.cuh)
     const char* why = encode_dense_maps(n);

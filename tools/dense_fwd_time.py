@@ -36,3 +36,19 @@ with torch.cuda.stream(s):
     e1.record(s)
     e1.synchronize()
 print(f"m={m} graph-timed forward (dropout + dense): {e0.elapsed_time(e1) / 500 * 1e3:.2f} us per call", flush=True)
+# the same for forward + backward/Adam (the backward alone = the difference)
+with torch.cuda.stream(s):
+    n.forward(x, step=1, train=True, h=h); n.backward_adam(dh, 1e-3)
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2, stream=s):
+        for i in range(50):
+            n.forward(x, step=1, train=True, h=h)
+            n.backward_adam(dh, 1e-3)
+    g2.replay(); g2.replay()
+    e0.record(s)
+    for _ in range(10):
+        g2.replay()
+    e1.record(s)
+    e1.synchronize()
+fb = e0.elapsed_time(e1) / 500 * 1e3
+print(f"m={m} graph-timed forward + backward/Adam: {fb:.2f} us per call", flush=True)
