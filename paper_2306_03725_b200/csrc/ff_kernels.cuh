@@ -1451,7 +1451,8 @@ __global__ void __launch_bounds__(kPredRingThreads) k_predict_ring(const float* 
 // at 128 B/clock per SM); register gathers reach 19.9 TB/s vs 11-17.7 TB/s for LDGSTS
 // (profiles/r01_gatherbench.txt).  Latency is hidden by occupancy (24 warps/SM at 80
 // registers) with the next row's W/idx/bias prefetched.  Measured (profiles/r02_pred_reg.txt):
-// 0.197 vs 0.213 ms at B = 32; a variant that also keeps the next row's 8 lines in flight
+// 0.191 vs 0.213 ms at B = 32 (0.196 before the line address became one IMAD.WIDE.U32 of the
+// column by the line's byte stride, instead of IMAD.WIDE + LEA + LEA.HI.X); a variant that also keeps the next row's 8 lines in flight
 // (64 more registers, 16 warps/SM) took 0.27-0.30 ms, and one with the top-K lists in shared
 // memory (64 registers, 32 warps/SM) 0.21-0.23 ms.  Same score arithmetic (row_score_own):
 // bit-identical y.  Candidates go straight into the lane's register top-K list when they beat
@@ -1503,11 +1504,13 @@ __global__ void __launch_bounds__(kPredRegThreads, FF_PRED_REG_MINB) k_predict_r
   uint32_t j = (uint32_t)global_warp(), it = 0;
   float w = 0.f, bj = 0.f; int c = 0;
   if (j < nrows) { w = ld_na(W + j * 32u + lane); c = ld_na_ro(idx + j * 32u + lane); bj = ld_na(bias + j); }
+  const char* const hbb = reinterpret_cast<const char*>(hb);
+  const uint32_t cbytes = pin(4u * kColFloats);          // line address = one IMAD.WIDE.U32 per gather
   while (j < nrows) {
     float4 hv[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q)
-      hv[q] = ld_line4_plain(col_line(hb, (uint32_t)__shfl_sync(kFull, c, sl[q]), kColFloats));
+      hv[q] = ld_line4_plain(reinterpret_cast<const float*>(hbb + (uint64_t)(uint32_t)__shfl_sync(kFull, c, sl[q]) * cbytes));
     const uint32_t jn = j + nwarp;                       // the next row's state, in flight meanwhile
     float wn = 0.f, bjn = 0.f; int cn = 0;
     if (jn < nrows) { wn = ld_na(W + jn * 32u + lane); cn = ld_na_ro(idx + jn * 32u + lane); bjn = ld_na(bias + jn); }
