@@ -111,11 +111,13 @@ __device__ __forceinline__ void row_spread_k(const float (&w)[KPL], const int (&
   }
 }
 
+// (as a byte offset c * (4 cfloats): one IMAD.WIDE.U32 with the base, instead of a float-index
+// IMAD.WIDE followed by LEA + LEA.HI.X)
 __device__ __forceinline__ const float* col_line(const float* hb, uint32_t c, uint32_t cfloats) {
-  return hb + (size_t)c * cfloats;
+  return reinterpret_cast<const float*>(reinterpret_cast<const char*>(hb) + (uint64_t)c * (4u * cfloats));
 }
 __device__ __forceinline__ float* col_line(float* hb, uint32_t c, uint32_t cfloats) {
-  return hb + (size_t)c * cfloats;
+  return reinterpret_cast<float*>(reinterpret_cast<char*>(hb) + (uint64_t)c * (4u * cfloats));
 }
 
 // Gather this lane's 16-B segment of each connection's 128-B h line (hb = the lane's
