@@ -45,6 +45,10 @@ __device__ __forceinline__ void st_na4(float* a, float4 v) {
 __global__ void k_dropout_T(const float* __restrict__ x, int B, int d, int ldx, float p, float scale, int train,
                             uint32_t step, uint32_t key0, uint32_t key1, float* __restrict__ xT,
                             const int64_t* __restrict__ t_auto, float* __restrict__ xTlo) {
+  // the tensor-core forward is launched as this kernel's programmatic dependent: it may start
+  // (TMEM/barrier set-up, the first Wd stages) now and waits (griddepcontrol.wait) before it
+  // reads xT / xTlo
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // t_auto (FF_STEP_AUTO): the step key is the dense layer's device counter + 1, i.e. the
   // Adam step this forward belongs to (read before k_prep / k_step_t advance it)
   if (t_auto != nullptr) step = (uint32_t)(*t_auto + 1);
@@ -397,7 +401,12 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_dense_fwd_tma(const __grid_co
 
   if (w == 0) {                                                   // ===== TMA producer
     if (lane == 0) {
+      // launched as k_dropout_T's programmatic dependent: the Wd loads of the first ring fill
+      // are issued before griddepcontrol.wait (they do not depend on the dropout), the xT loads
+      // after it
       uint32_t i = 0;
+      bool x_ok = false;
+      const uint32_t nfill = (uint32_t)min(kTmStages, nst * ((ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1));
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
         for (int st = 0; st < nst; ++st, ++i) {
           const uint32_t s = i % kTmStages;
@@ -407,6 +416,16 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_dense_fwd_tma(const __grid_co
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(full(s)), "r"(kTmStage) : "memory");
 #pragma unroll
           for (int g = 0; g < 4; ++g) tma_load_3d(stg + (uint32_t)g * kTmG, &mW, 32 * g, kTmF * st, t, full(s));
+          if (!x_ok && i + 1 < nfill) continue;                   // x of the first nfill stages after the wait
+          if (!x_ok) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            x_ok = true;
+            for (uint32_t k = 0; k < i; ++k) {                     // the earlier stages of the fill (x depends on the stage only)
+              const uint32_t sk = k % kTmStages, stk = k % (uint32_t)nst;
+              tma_load_2d(sbase + sk * kTmStage + kTmA, &mX, 0, kTmF * (int)stk, full(sk));
+              tma_load_2d(sbase + sk * kTmStage + kTmA + kTmX, &mXl, 0, kTmF * (int)stk, full(sk));
+            }
+          }
           tma_load_2d(stg + kTmA, &mX, 0, kTmF * st, full(s));
           tma_load_2d(stg + kTmA + kTmX, &mXl, 0, kTmF * st, full(s));
         }

@@ -633,10 +633,22 @@ ff_status dense_forward_impl(ff_dense* n, const float* x, int B, uint64_t step, 
     FF_LAUNCHED();
   }
   if (nb == 1 && !(n->cfg.flags & FF_FLAG_DENSE_SIMT)) {          // tensor cores (tcgen05 + TMA, 3xTF32)
-    const int grid = std::min(n->ldw / 128, n->nsm);               // persistent: one CTA per SM
-    k_dense_fwd_tma<<<grid, kTmThreads, kTmSmem, st>>>(n->tmW, n->tmX, n->tmXl, n->bd, n->cfg.d, n->cfg.m, B, hd, 64,
-                                                       1, h_out);
-    FF_LAUNCHED();
+    // persistent, one CTA per SM; a programmatic dependent of k_dropout_T (PDL): its set-up and
+    // first Wd stages overlap the dropout kernel, its xT loads wait for it (griddepcontrol.wait)
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(std::min(n->ldw / 128, n->nsm));
+    lc.blockDim = dim3(kTmThreads);
+    lc.dynamicSmemBytes = kTmSmem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    const float* bdp = n->bd;
+    int dd = n->cfg.d, mm = n->cfg.m, BB = B, cs = 64, zd = 1;
+    FF_CUDA(cudaLaunchKernelEx(&lc, k_dense_fwd_tma, n->tmW, n->tmX, n->tmXl, bdp, dd, mm, BB, hd, cs, zd, h_out));
+    ++g_launches;
     if (train) n->fwd_B = B;
     return FF_OK;
   }
