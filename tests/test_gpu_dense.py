@@ -39,7 +39,8 @@ def dstate(dn):
     return {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in dn.get_params().items()}
 
 
-SHAPES = [(32, 512, 1000), (7, 37, 203), (70, 64, 300), (1, 5, 3), (32, 130, 4096)]
+SHAPES = [(32, 512, 1000), (7, 37, 203), (70, 64, 300), (1, 5, 3), (32, 130, 4096),
+          (32, 100, 37988)]   # > one column tile per SM (persistent TMA forward, backward ranges across tiles)
 
 
 @pytest.mark.parametrize("d,m,seed", [(512, 1000, 7), (37, 203, 3), (5, 3, 1), (768, 4096, 42)])
