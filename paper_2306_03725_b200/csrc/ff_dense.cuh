@@ -704,30 +704,32 @@ __global__ void __launch_bounds__(kDenseBwdThreads, 2) k_dense_bwd_adam(
   }
 }
 
-// The same backward + Adam for B <= 32 (one 32-sample chunk), with the Adam operands of the
-// next two 16-feature blocks streamed into shared memory by cp.async instead of registers:
-// every thread copies exactly the 16-B pieces it will update (2 features x 4 columns x 3
-// arrays) and each warp the two xT rows it reads, so the main loop needs no CTA barrier;
-// only the dz tile is shared.  Persistent (round 2): the (column tile, 16-feature block) work
-// items, tile-major, are split into equal contiguous ranges over a grid of resident CTAs, so
-// every CTA streams the same number of blocks (the round-1 grid of 256 x 3 CTAs ran 2.6 waves
-// at 2 CTAs/SM); a CTA restages dz when its range enters a new tile and updates the tile's
-// bias right after the tile's first block (warp 0 sums db over the 32 samples there).  Same
-// arithmetic and order as k_dense_bwd_adam: bit-identical results.
+// The same backward + Adam for B <= 32 (one 32-sample chunk).  Round 2: persistent — the
+// (column tile, 16-feature block) work items, tile-major, are split into equal contiguous
+// ranges over the resident CTAs (the round-1 grid of 256 x 3 CTAs ran 2.6 waves) — and fed by
+// the TMA engine: a producer warp streams each block's Wd / mWd / vWd rows (3 x 8 KB,
+// contiguous in the tiled layout) and its xT rows (2 KB) into a ring of kDenseBwdNS
+// shared-memory stages with cp.async.bulk (one mbarrier per stage, complete_tx), and four
+// compute warps — each 4 features x 128 columns, lane -> 4 columns, so every 16-B dz load
+// serves 4 features — release a stage by arriving on its "empty" barrier.  A CTA restages the
+// dz tile [32][128] when its range enters a new tile and updates the tile's bias right after
+// the tile's first block.  Adam runs on packed fp32x2 ops (adam_update2, bit-identical);
+// same arithmetic and order as k_dense_bwd_adam: bit-identical results.
 #ifndef FF_BWD_NS
 #define FF_BWD_NS 3
 #endif
 #ifndef FF_BWD_MINB
 #define FF_BWD_MINB 2
 #endif
-constexpr int kDenseBwdNS = FF_BWD_NS;                                    // stages
+constexpr int kDenseBwdNS = FF_BWD_NS;                               // stages
 constexpr int kDenseBwdStage = (3 * kDenseBwdBlk * 128 + kDenseBwdBlk * 32) * 4;   // 26 KB
-constexpr int kDenseBwd1Smem = 32 * 128 * 4 + kDenseBwdNS * kDenseBwdStage;
-// 4 warps, each 4 features x 128 columns of a 16-feature block (lane -> 4 columns): every
-// 16-B dz load serves 4 features (round 1: 8 warps x 2 features, twice the dz shared-memory
-// traffic), and the Adam updates run on packed fp32x2 ops (adam_update2, bit-identical)
-constexpr int kDenseBwd32Threads = 128, kDenseBwdFpw = kDenseBwdBlk / (kDenseBwd32Threads / 32);
-static_assert(kDenseBwdFpw == 4, "features per warp");
+constexpr int kDenseBwd1Smem = 32 * 128 * 4 + kDenseBwdNS * kDenseBwdStage + 16 * kDenseBwdNS;
+constexpr int kDenseBwd32Threads = 160, kDenseBwdFpw = 4;           // 4 compute warps + 1 TMA producer warp
+static_assert(kDenseBwdFpw * 4 == kDenseBwdBlk, "features per warp");
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
 __global__ void __launch_bounds__(kDenseBwd32Threads, FF_BWD_MINB) k_dense_bwd_adam_b32(
     float* __restrict__ Wd, float* __restrict__ mWd, float* __restrict__ vWd, float* __restrict__ bd,
     float* __restrict__ mbd, float* __restrict__ vbd, const float* __restrict__ xT, int d, int m, int ldx,
@@ -737,6 +739,9 @@ __global__ void __launch_bounds__(kDenseBwd32Threads, FF_BWD_MINB) k_dense_bwd_a
   extern __shared__ __align__(16) float bsm[];
   float (*dzs)[128] = reinterpret_cast<float (*)[128]>(bsm);        // [32][128]
   float* const stages = bsm + 32 * 128;
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(stages + kDenseBwdNS * (kDenseBwdStage / 4));
+  auto full = [&](int s) { return bar0 + 8u * (uint32_t)s; };
+  auto empty = [&](int s) { return bar0 + 8u * (uint32_t)(kDenseBwdNS + s); };
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nfb = (d + kDenseBwdBlk - 1) / kDenseBwdBlk;             // feature blocks per tile
   const int64_t nitems = (int64_t)ntiles * nfb;
@@ -744,39 +749,37 @@ __global__ void __launch_bounds__(kDenseBwd32Threads, FF_BWD_MINB) k_dense_bwd_a
   const int nblk = (int)(it_hi - it_lo);
   // stage layout (floats): P [16][128] | M [16][128] | V [16][128] | X [16][32]
   auto stage_ptr = [&](int s) { return stages + (size_t)s * (kDenseBwdStage / 4); };
-  auto issue = [&](int bi) {
-    if (bi < nblk) {
-      const int64_t item = it_lo + bi;
-      const int tile = (int)(item / nfb), fblk = (int)(item % nfb) * kDenseBwdBlk;
-      float* st = stage_ptr(bi % kDenseBwdNS);
-#pragma unroll
-      for (int r = 0; r < kDenseBwdFpw; ++r) {
-        const int rl = kDenseBwdFpw * w + r, f = fblk + rl;
-        const bool ok = f < d;
-        const int64_t o = ((int64_t)tile * d + (ok ? f : 0)) * 128 + 4 * lane;
-        const uint32_t so = (uint32_t)(rl * 128 + 4 * lane) * 4u;
-        cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st) + so, Wd + o, ok);
-        cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st + 16 * 128) + so, mWd + o, ok);
-        cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st + 32 * 128) + so, vWd + o, ok);
-      }
-      {                                                              // this warp's 4 xT rows (one 16-B piece per lane)
-        const int rl = kDenseBwdFpw * w + (lane >> 3), f = fblk + rl, s4 = (lane & 7) * 4;
-        const bool ok = f < d;
-        cp_async16_zfill((uint32_t)__cvta_generic_to_shared(st + 48 * 128 + rl * 32 + s4),
-                         xT + (int64_t)(ok ? f : 0) * ldx + s4, ok);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDenseBwdNS; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (w == 4) {                                                      // ===== TMA producer warp
+    if (lane == 0) {
+      for (int bi = 0; bi < nblk; ++bi) {
+        const int s = bi % kDenseBwdNS;
+        if (bi >= kDenseBwdNS) mbar_wait(empty(s), (uint32_t)(((bi / kDenseBwdNS) - 1) & 1));
+        const int64_t item = it_lo + bi;
+        const int tile = (int)(item / nfb), fblk = (int)(item % nfb) * kDenseBwdBlk;
+        const uint32_t rows = (uint32_t)min(kDenseBwdBlk, d - fblk);
+        const uint32_t st = (uint32_t)__cvta_generic_to_shared(stage_ptr(s));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(full(s)), "r"(rows * (3u * 512u + 128u)) : "memory");
+        const int64_t o = ((int64_t)tile * d + fblk) * 128;
+        bulk_g2s(st, Wd + o, rows * 512u, full(s));
+        bulk_g2s(st + 16u * 512u, mWd + o, rows * 512u, full(s));
+        bulk_g2s(st + 32u * 512u, vWd + o, rows * 512u, full(s));
+        bulk_g2s(st + 48u * 512u, xT + (int64_t)fblk * ldx, rows * 128u, full(s));
       }
     }
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int s = 0; s < kDenseBwdNS - 1; ++s) issue(s);
+    return;
+  }
   int cur_tile = -1;
   for (int bi = 0; bi < nblk; ++bi) {
     const int64_t item = it_lo + bi;
     const int tile = (int)(item / nfb), fblk = (int)(item % nfb) * kDenseBwdBlk;
     const int ct = tile * 128, c0 = ct + 4 * lane;
     if (tile != cur_tile) {                                          // dz tile: thread t <-> column ct + t
-      __syncthreads();                                               // the previous tile's readers are done
+      asm volatile("bar.sync 1, 128;" ::: "memory");                 // the previous tile's readers are done
       {
         const int c = ct + threadIdx.x;
         const float* line = hd + (int64_t)c * cstride;
@@ -790,13 +793,12 @@ __global__ void __launch_bounds__(kDenseBwd32Threads, FF_BWD_MINB) k_dense_bwd_a
           dzs[s4 + 3][threadIdx.x] = hv.w > 0.0f ? gv.w : 0.0f;
         }
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       cur_tile = tile;
     }
-    issue(bi + kDenseBwdNS - 1);
-    cp_async_wait<kDenseBwdNS - 1>();                                // this thread's block-bi copies
-    __syncwarp();                                                    // ... and its warp's xT rows
-    const float* st = stage_ptr(bi % kDenseBwdNS);
+    const int s = bi % kDenseBwdNS;
+    mbar_wait(full(s), (uint32_t)((bi / kDenseBwdNS) & 1));
+    const float* st = stage_ptr(s);
     const bool do_bias = fblk == 0 && w == 0;
     float db[4] = {0.f, 0.f, 0.f, 0.f};
     float2 acc[kDenseBwdFpw][2];
@@ -841,6 +843,8 @@ __global__ void __launch_bounds__(kDenseBwd32Threads, FF_BWD_MINB) k_dense_bwd_a
       st_na4(mWd + o, make_float4(m0.x, m0.y, m1.x, m1.y));
       st_na4(vWd + o, make_float4(v0.x, v0.y, v1.x, v1.y));
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty(s));                            // this warp is done with stage s
     if (do_bias) {                                                   // the tile's bias, once (its first block)
       float4 p = *reinterpret_cast<const float4*>(bd + c0);
       float4 mo = *reinterpret_cast<const float4*>(mbd + c0);
@@ -854,9 +858,7 @@ __global__ void __launch_bounds__(kDenseBwd32Threads, FF_BWD_MINB) k_dense_bwd_a
       *reinterpret_cast<float4*>(mbd + c0) = mo;
       *reinterpret_cast<float4*>(vbd + c0) = ve;
     }
-    __syncwarp();                                                    // stage reused by this warp's next issue
   }
-  cp_async_wait<0>();
 }
 
 // dh [B][m] (user layout) -> the dh half of hd (standalone dense backward).  Grid
