@@ -1,6 +1,6 @@
 """Predict (fused forward + top-K) throughput vs batch size at Amazon-670K: ms per batch,
 samples/s and the fraction of the h-line gather floor (128 B per connection and 32-sample
-line at the measured 19.9 TB/s gather ceiling).  B <= 32: k_predict_ring; B > 32:
+line at the measured 19.9 TB/s gather ceiling).  B <= 96: k_predict_reg (per 32-sample line); B > 96:
 k_predict_wide (FF_FLAG_NO_PIPE: the generic k_predict, for comparison).
 Usage: python tools/pred_sweep.py [--no-pipe] [B ...]"""
 import sys
