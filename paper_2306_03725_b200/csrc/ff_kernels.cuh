@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 #define FF_CSC_RING_D 2
 #endif
 #ifndef FF_CSC_RING_MINB
-#define FF_CSC_RING_MINB 6
+#define FF_CSC_RING_MINB 5
 #endif
 #ifndef FF_ATOM_RING_D
 #define FF_ATOM_RING_D 3
@@ -468,10 +468,18 @@ constexpr int kRingStageBytes = 8 * 32 * 16;            // 8 registers x 32 lane
 // there, where the kernel is issue/latency-bound, but 1-2% slower in the BCE (atomic, CSC)
 // modes, so only MODE 3 uses it.
 template <int MODE> __host__ __device__ constexpr bool ring_xpose() { return MODE == 3; }
+// The CSC row pass (MODE 1) gathers its h lines straight into registers instead of through the
+// ring (round 2): its rows only write a gradient line (no per-connection reductions), so the
+// ring's 8 KB of shared-memory traffic per row was the larger cost — 0.564 vs 0.579 ms per CSC
+// step at 5 CTAs/SM (atomic: 0.573 on the same box), parity green.
+#ifndef FF_CSC_REG
+#define FF_CSC_REG 1              // CSC row pass: 1 = h lines gathered straight into registers (no ring)
+#endif
+template <int MODE> __host__ __device__ constexpr bool ring_reg() { return MODE == 1 && FF_CSC_REG; }
 constexpr int kRingXposeBytes = 256;                         // per stage: c[32] | w[32], transposed
 template <int MODE>
 constexpr int ring_smem() {
-  return (kRingThreads / 32) * RingCfg<MODE>::D * (kRingStageBytes + (ring_xpose<MODE>() ? kRingXposeBytes : 0));
+  return ring_reg<MODE>() ? 0 : (kRingThreads / 32) * RingCfg<MODE>::D * (kRingStageBytes + (ring_xpose<MODE>() ? kRingXposeBytes : 0));
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
@@ -564,8 +572,10 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(x1.x), "=r"(x1.y), "=r"(x1.z), "=r"(x1.w) : "r"(a + 16u) : "memory");
     v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w; v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
   };
+  constexpr bool REG = ring_reg<MODE>();
   // gathers of one row into ring stage `stg` (always commits a group, possibly empty)
   auto issue = [&](Cur cu, const St& st, uint32_t stg) {
+    if (REG) return;                                    // gathered at compute time
     if (live(cu)) {
       const uint32_t dst = ring0 + stg * (uint32_t)kRingStageBytes;
       if constexpr (XP) {
@@ -618,11 +628,17 @@ __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_tra
     load_st(q_cur[D - 1], q_st[D - 1]);
     if (live(q_cur[0]) && i_of(q_cur[0]) == 0) load_bv(q_cur[0], bv_next);
 
-    cp_async_wait<D - 1>();                             // this row's group is complete
     float4 hv[NG];
-    const uint32_t src = ring0 + stg * (uint32_t)kRingStageBytes;
+    if constexpr (REG) {
 #pragma unroll
-    for (int q = 0; q < NG; ++q) hv[q] = lds4(src + (uint32_t)q * 512u);
+      for (int q = 0; q < NG; ++q)
+        hv[q] = ld_line4_plain(col_line(hb, (uint32_t)__shfl_sync(kFull, st.c, 4 * q + gq), kColFloats));
+    } else {
+      cp_async_wait<D - 1>();                           // this row's group is complete
+      const uint32_t src = ring0 + stg * (uint32_t)kRingStageBytes;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) hv[q] = lds4(src + (uint32_t)q * 512u);
+    }
     float ws[NG];
     uint32_t cq[NG];                                    // (MODE 3) this row's columns of connections 4q + gq
     if constexpr (XP) {
