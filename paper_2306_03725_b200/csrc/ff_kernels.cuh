@@ -262,8 +262,18 @@ __device__ __forceinline__ AdamArgs step_adam(const RowArgs& a) {
   return ad;
 }
 
+// Programmatic dependent launch (the training step's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): wait until the previous kernel of the
+// stream has completed and its memory is visible, then let the next one be scheduled so its
+// launch overlaps this kernel's tail.  Both are no-ops in a plain launch.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <int MODE, bool STORE_GRADS, int NG, bool CSC, bool FULL>
 __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_rows(RowArgs a) {
+  pdl_begin();
   const AdamArgs adam = step_adam(a);
   constexpr int KPL = (NG + 7) / 8;                 // slots per lane (k <= 32 * KPL)
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
@@ -504,6 +514,7 @@ __device__ __forceinline__ T* pin(T* p) { asm volatile("" : "+l"(p)); return p; 
 
 template <bool STORE_GRADS, int MODE>
 __global__ void __launch_bounds__(kRingThreads, RingCfg<MODE>::kMinBlocks) k_train_ring(RowArgs a) {
+  pdl_begin();
   const AdamArgs adam = step_adam(a);
   constexpr int NG = 8, D = RingCfg<MODE>::D;
   constexpr bool CSC = MODE == 1 || MODE == 2, HYB = MODE == 2;
@@ -755,6 +766,7 @@ template <bool NB1, bool SKIPZ>
 __global__ void __launch_bounds__(256) k_dh_csc(const int* __restrict__ col_ptr, const int* __restrict__ ent,
                                                 const float* __restrict__ gT, int rs, int m, int nb_rt, int tile,
                                                 float* __restrict__ hd, int c_begin) {
+  pdl_begin();
   const int nb = NB1 ? 1 : nb_rt;
   const int lane = threadIdx.x & 31, gq = lane >> 3, bq = lane & 7;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -896,6 +908,7 @@ __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float*
                        uint32_t* __restrict__ posmask, int64_t L_local, int64_t row_begin,
                        int64_t L_global, float* loss, int* err, int64_t* t_dev, float* rbc, float beta1,
                        float beta2, int64_t* t2_dev, float* rbc2, float beta1d, float beta2d) {
+  pdl_begin();
   __shared__ float t[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   if (t_dev != nullptr && blockIdx.x == 0 && tid == 0) {
@@ -968,6 +981,7 @@ __global__ void k_prep(const float* __restrict__ h, int B, int m, int nb, float*
 // in k_prep (16-B line loads and 16-B dh row stores).
 template <bool VEC>
 __global__ void k_dh_out(const float* __restrict__ hd, int B, int m, int nb, float* __restrict__ dh) {
+  pdl_begin();
   __shared__ float t[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int c0 = blockIdx.x * 32, q2 = blockIdx.y;

@@ -206,20 +206,38 @@ T* at(char* base, size_t off) { return reinterpret_cast<T*>(base + off); }
 // the dense layer's step counter, advanced by k_prep of a whole-architecture step
 struct DenseT { int64_t* t; float* rbc; float beta1, beta2; };
 
+#ifndef FF_STEP_PDL
+#define FF_STEP_PDL 1            // launch the step's kernels as programmatic dependents (pdl_begin() in each)
+#endif
+// launch configuration with programmatic stream serialization: the kernel may be scheduled
+// while its predecessor drains; it waits in pdl_begin() (griddepcontrol.wait) before touching
+// any data
+struct PdlCfg {
+  cudaLaunchConfig_t c;
+  cudaLaunchAttribute at[1];
+  PdlCfg(dim3 g, dim3 b, size_t smem, cudaStream_t st) {
+    c = {};
+    c.gridDim = g; c.blockDim = b; c.dynamicSmemBytes = smem; c.stream = st;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = FF_STEP_PDL;
+    c.attrs = at; c.numAttrs = 1;
+  }
+};
+
 ff_status launch_prep(ff_layer* l, const float* h, int B, bool zero_dh, const int* lbl_ptr,
                       const int* lbl_ids, float* loss, cudaStream_t st, bool step_t = false,
                       const DenseT* dt = nullptr) {
   const int nb = nb_of(B);
   dim3 grid((l->cfg.m + 31) / 32), block(32, 8);
   const bool vec = (l->cfg.m & 3) == 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0;
-  (vec ? k_prep<true> : k_prep<false>)<<<grid, block, 0, st>>>(h, B, l->cfg.m, nb, l->hd, zero_dh ? 1 : 0, lbl_ptr,
-                                                                lbl_ids, l->posmask, l->cfg.L_local, l->cfg.row_begin,
-                                                                l->cfg.L_global, loss, l->err,
-                                                                step_t ? l->t_dev : nullptr, l->rbc_dev,
-                                                                l->cfg.beta1, l->cfg.beta2, dt ? dt->t : nullptr,
-                                                                dt ? dt->rbc : nullptr, dt ? dt->beta1 : 0.0f,
-                                                                dt ? dt->beta2 : 0.0f);
-  FF_LAUNCHED();
+  PdlCfg pc(grid, block, 0, st);
+  int zd = zero_dh ? 1 : 0;
+  FF_CUDA(cudaLaunchKernelEx(&pc.c, vec ? k_prep<true> : k_prep<false>, h, B, l->cfg.m, nb, l->hd, zd, lbl_ptr, lbl_ids,
+                             l->posmask, l->cfg.L_local, l->cfg.row_begin, l->cfg.L_global, loss, l->err,
+                             step_t ? l->t_dev : (int64_t*)nullptr, l->rbc_dev, l->cfg.beta1, l->cfg.beta2,
+                             dt ? dt->t : (int64_t*)nullptr, dt ? dt->rbc : (float*)nullptr, dt ? dt->beta1 : 0.0f,
+                             dt ? dt->beta2 : 0.0f));
+  ++g_launches;
   return FF_OK;
 }
 
@@ -227,8 +245,10 @@ ff_status launch_dh_out(ff_layer* l, int B, float* dh, cudaStream_t st) {
   const int nb = nb_of(B);
   dim3 grid((l->cfg.m + 31) / 32, nb), block(32, 8);
   const bool vec = (l->cfg.m & 3) == 0 && (reinterpret_cast<uintptr_t>(dh) & 15) == 0;
-  (vec ? k_dh_out<true> : k_dh_out<false>)<<<grid, block, 0, st>>>(l->hd, B, l->cfg.m, nb, dh);
-  FF_LAUNCHED();
+  PdlCfg pc(grid, block, 0, st);
+  const float* hdp = l->hd;
+  FF_CUDA(cudaLaunchKernelEx(&pc.c, vec ? k_dh_out<true> : k_dh_out<false>, hdp, B, l->cfg.m, nb, dh));
+  ++g_launches;
   return FF_OK;
 }
 
@@ -297,7 +317,8 @@ int ring_smem_of(int mode) {
 
 ff_status launch_rows(const void* fn, int grid, RowArgs& a, cudaStream_t st, int threads = kRowThreads, int smem = 0) {
   void* args[] = {&a};
-  FF_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, (size_t)smem, st));
+  PdlCfg pc(dim3(grid), dim3(threads), (size_t)smem, st);
+  FF_CUDA(cudaLaunchKernelExC(&pc.c, fn, args));
   ++g_launches;
   return FF_OK;
 }
@@ -316,8 +337,11 @@ ff_status launch_dh_csc(ff_layer* l, int B, int tile, cudaStream_t st) {
   const bool skipz = l->cfg.loss == FF_LOSS_SQH;      // zero gradients are exact only for the squared hinge
   auto fn = B <= 32 ? (skipz ? k_dh_csc<true, true> : k_dh_csc<true, false>)
                     : (skipz ? k_dh_csc<false, true> : k_dh_csc<false, false>);
-  fn<<<l->grid_csc, 256, 0, st>>>(l->col_ptr, l->ent, l->gT, l->rs, l->cfg.m, nb_of(B), tile, l->hd, (int)l->split);
-  FF_LAUNCHED();
+  PdlCfg pc(dim3(l->grid_csc), dim3(256), 0, st);
+  const int* cp = l->col_ptr; const int* en = l->ent; const float* g = l->gT;
+  int nbB = nb_of(B), sp = (int)l->split;
+  FF_CUDA(cudaLaunchKernelEx(&pc.c, fn, cp, en, g, l->rs, l->cfg.m, nbB, tile, l->hd, sp));
+  ++g_launches;
   return FF_OK;
 }
 
