@@ -23,14 +23,16 @@ import torch
 import torch.distributed as dist
 sys.path.insert(0, os.environ["ROOT"])
 from paper_2306_03725_b200 import synth
-from paper_2306_03725_b200.layer import FixedFanInLayer, LayerConfig
+from paper_2306_03725_b200.layer import FF_DH_CSC, FixedFanInLayer, LayerConfig
 from paper_2306_03725_b200.sharded import GraphedSteps, ShardedLayer
 
 dist.init_process_group("nccl", init_method="tcp://127.0.0.1:" + os.environ["PORT"], rank=0, world_size=1)
 dev = torch.device("cuda:0")
 torch.cuda.set_device(dev)
 L, m, k, B, K, ROUNDS, lr = 20000, 1024, 32, 32, 3, 3, 1e-3
-mk = lambda: FixedFanInLayer(LayerConfig(L_global=L, m=m, k=k, max_batch=B, seed=7), device=dev)
+csc = os.environ["DH"] == "csc"
+mk = lambda: FixedFanInLayer(LayerConfig(L_global=L, m=m, k=k, max_batch=B, seed=7, dh_mode=FF_DH_CSC if csc else 0),
+                             device=dev)
 a, b = mk(), mk()
 h = [torch.from_numpy(synth.hidden_batch(B, m, step=j)).to(dev) for j in range(K)]
 lab = [synth.label_batch(B, L, 5.0, step=j) for j in range(K)]
@@ -51,6 +53,8 @@ for key in ("W", "idx", "bias", "mW", "vW", "mb", "vb"):
     assert torch.equal(pa[key], pb[key]), key
 assert pa["t"] == pb["t"] == ROUNDS * K, (pa["t"], pb["t"])
 for j in range(K):
+    if csc:                                          # the CSC pull sums in a fixed order: bit-identical
+        assert torch.equal(g.dh[j], dh_b[j]), j
     d = (g.dh[j] - dh_b[j]).abs().max().item()
     assert d <= 1e-5 * dh_b[j].abs().max().item(), (j, d)
 assert torch.equal(loss_a, loss_b) or abs(loss_a.item() - loss_b.item()) <= 1e-5 * abs(loss_b.item())
@@ -67,11 +71,12 @@ def _free_port():
     return p
 
 
-def test_graphed_sharded_steps_with_nccl_match_eager():
+@pytest.mark.parametrize("dh", ["atomic", "csc"])
+def test_graphed_sharded_steps_with_nccl_match_eager(dh):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     import __graft_entry__ as g
     g.build_lib()
-    env = dict(os.environ, ROOT=ROOT, PORT=str(_free_port()), MASTER_ADDR="127.0.0.1")
+    env = dict(os.environ, ROOT=ROOT, PORT=str(_free_port()), MASTER_ADDR="127.0.0.1", DH=dh)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "GRAPH_NCCL_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
