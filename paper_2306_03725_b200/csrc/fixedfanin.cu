@@ -779,7 +779,10 @@ ff_status fixedfanin_create(const ff_config* cfg, void* workspace, size_t bytes,
   l->grid_train = occupancy_grid(row_kernel<kModeTrain, false>(c.k, l->csc), l->nsm, kRowThreads);
   l->grid_fwd = occupancy_grid(row_kernel<kModeForward, false>(c.k, false), l->nsm, kRowThreads);
   l->grid_bwd = occupancy_grid(row_kernel<kModeBackward, false>(c.k, l->csc), l->nsm, kRowThreads);
-  l->grid_csc = occupancy_grid((const void*)k_dh_csc<true, false>, l->nsm, 256);
+#ifndef FF_CSC_COL_CTAS
+#define FF_CSC_COL_CTAS 0          // CSC column pass CTAs per SM (0: as many as fit)
+#endif
+  l->grid_csc = FF_CSC_COL_CTAS > 0 ? FF_CSC_COL_CTAS * l->nsm : occupancy_grid((const void*)k_dh_csc<true, false>, l->nsm, 256);
   for (int sg = 0; sg < 2; ++sg)
     for (int cs = 0; cs < 4; ++cs)
       if (cudaFuncSetAttribute(ring_kernel(sg, cs), cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem_of(cs)) !=
