@@ -83,7 +83,8 @@ typedef enum {
 
 /* ff_config.dh_mode */
 #define FF_DH_ATOMIC 0           /* dh by coalesced red.global.add (Alg. 2 with atomics) */
-#define FF_DH_CSC 1              /* dh by a transposed (CSC) index gather, rebuilt after redistribution */
+#define FF_DH_CSC 1              /* dh by a transposed (CSC) index gather, rebuilt after redistribution;
+                                    deterministic, and the faster BCE mode on B200       */
 #define FF_DH_HYBRID 2           /* columns c < hybrid_frac*m by red (the L1->L2 write path), the rest by
                                     the CSC gather (the read path): both paths busy at once */
 
@@ -97,7 +98,8 @@ typedef struct {
     int32_t max_batch;   /* largest B that will be passed, 1..FF_MAX_BATCH                      */
     int32_t max_topk;    /* largest K that will be passed to predict_topk, 1..FF_MAX_TOPK       */
     int32_t max_nnz;     /* largest lbl_ptr[B] for the *_host entry points (0 -> 64*max_batch)  */
-    int32_t dh_mode;     /* FF_DH_ATOMIC, FF_DH_CSC or FF_DH_HYBRID                             */
+    int32_t dh_mode;     /* FF_DH_ATOMIC (0, the default; best for FF_LOSS_SQH), FF_DH_CSC or     */
+                         /* FF_DH_HYBRID                                                         */
     uint64_t seed;       /* Philox key for init and redistribution (R13)                        */
     float init_scale;    /* W init U(-a, a); 0 -> a = fp32(1/sqrt(k)) (R17)                     */
     float beta1, beta2, eps;   /* Adam; 0 -> 0.9 / 0.999 / 1e-8 (R6)                            */
