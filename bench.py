@@ -61,10 +61,14 @@ def args_():
                         "margin (engineered-margin analog of a trained model, SURVEY §8(f) NEXT-1)")
     p.add_argument("--hybrid-frac", type=float, default=0.0,
                    help="--dh-mode hybrid: fraction of the columns reduced by red (0 -> library default 0.5)")
-    p.add_argument("--dh-mode", default="csc", choices=["atomic", "csc", "hybrid"],
-                   help="dh scatter: the deterministic CSC pull (default: measured 1.3-1.5%% faster than atomics "
-                        "since the row pass gathers into registers, DESIGN.md §6) or red.global atomics")
-    return p.parse_args()
+    p.add_argument("--dh-mode", default=None, choices=["atomic", "csc", "hybrid"],
+                   help="dh scatter: the deterministic CSC pull or red.global atomics; default: the mode measured "
+                        "faster for the loss (DESIGN.md §6) — CSC for BCE (1.3-1.5%% faster since the row pass "
+                        "gathers into registers), atomic for the squared hinge (its skipped reductions)")
+    a = p.parse_args()
+    if a.dh_mode is None:                       # the mode measured faster for this loss
+        a.dh_mode = "atomic" if a.loss == "sqh" else "csc"
+    return a
 
 
 def peaks():
