@@ -20,3 +20,15 @@ def test_reference_arm_prints_the_contract_line():
     assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["workload"] == "tiny"
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_dh_mode_defaults_to_the_mode_measured_faster_for_the_loss():
+    """CSC for BCE (register-gather row pass), atomic for the squared hinge."""
+    code = ("import sys; sys.argv = ['bench.py'] + sys.argv[1:]; import bench; a = bench.args_(); "
+            "print(a.dh_mode)")
+    out = lambda *extra: subprocess.run([sys.executable, "-c", code, *extra], capture_output=True, text=True,
+                                        timeout=120, cwd=ROOT).stdout.strip().splitlines()[-1]
+    assert out() == "csc"
+    assert out("--loss", "sqh") == "atomic"
+    assert out("--dh-mode", "atomic") == "atomic"
+    assert out("--loss", "sqh", "--dh-mode", "csc") == "csc"
