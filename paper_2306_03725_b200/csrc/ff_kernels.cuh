@@ -467,6 +467,7 @@ __global__ void __launch_bounds__(kRowThreads, NG > 8 ? 1 : kRowMinBlocks) k_row
 // most reductions skipped the kernel is latency-bound and prefers 2 stages at 5 CTAs/SM
 // (0.250 vs 0.265 ms at 100% skips), where the BCE step, bound by the reductions, does not care.
 template <int MODE> struct RingCfg {
+  static_assert((MODE == 1 ? FF_CSC_RING_D : MODE == 3 ? FF_SQH_RING_D : FF_ATOM_RING_D) >= 2, "ring depth D >= 2");
   static constexpr int D = MODE == 1 ? FF_CSC_RING_D : MODE == 3 ? FF_SQH_RING_D : FF_ATOM_RING_D;  // stages per warp
   static constexpr int kMinBlocks = MODE == 1 ? FF_CSC_RING_MINB : MODE == 3 ? FF_SQH_RING_MINB
                                                                               : FF_ATOM_RING_MINB;  // CTAs per SM
